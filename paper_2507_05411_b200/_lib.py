@@ -1,0 +1,84 @@
+"""ctypes binding of the C ABI in ``include/composer_b200.h``.
+
+The library is loaded from the package's ``_lib/`` directory (built by ``_build.py``).
+There is no fallback: if the shared object is missing or a symbol is absent the caller
+gets ``MissingExtensionError``.  Non-zero statuses become the matching ComposerError
+subclass (CB_ERR_SHAPE -> ShapeError, CB_ERR_UNSUPPORTED -> TypeMismatchError,
+otherwise KernelError) carrying the library's thread-local message.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+from .errors import KernelError, MissingExtensionError, ShapeError, TypeMismatchError
+
+_PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG_DIR, "_lib", "libcomposer_b200.so")
+HEADER_PATH = os.path.join(os.path.dirname(_PKG_DIR), "include", "composer_b200.h")
+
+CB_OK, CB_ERR_SHAPE, CB_ERR_ARG, CB_ERR_CUDA, CB_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
+DT_F32, DT_BF16 = 0, 1
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_L = ctypes.c_int64
+_F = ctypes.c_float
+_D = ctypes.c_double
+
+# name -> argtypes; the return type is always int (status) except where noted.
+SIGNATURES: dict[str, list] = {
+    "cb_abi_version": [],
+    "cb_gemm_set_path": [_I],
+    "cb_gemm": [_I, _I, _I, _I, _P, _L, _I, _P, _L, _I, _P, _L, _I, _P, _L, _I, _F, _I, _P],
+}
+
+_lib = None
+
+
+def declared_symbols() -> list[str]:
+    """Function names declared with CB_API in the public header."""
+    with open(HEADER_PATH, "r", encoding="utf-8") as fh:
+        text = fh.read()
+    return re.findall(r"CB_API\s+[\w\s\*]+?\b(cb_\w+)\s*\(", text)
+
+
+def load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise MissingExtensionError(
+            f"kernel library not built: {LIB_PATH} (run __graft_entry__.build() or python -m paper_2507_05411_b200._build)"
+        )
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, argtypes in SIGNATURES.items():
+        try:
+            fn = getattr(lib, name)
+        except AttributeError:
+            raise MissingExtensionError(f"kernel library lacks symbol {name}") from None
+        fn.argtypes = argtypes
+        fn.restype = ctypes.c_int
+    lib.cb_last_error.argtypes = []
+    lib.cb_last_error.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def check(status: int, what: str = "") -> None:
+    if status == CB_OK:
+        return
+    msg = (_lib.cb_last_error() or b"").decode("utf-8", "replace") if _lib is not None else ""
+    text = f"{what}: {msg}" if what else msg
+    if status == CB_ERR_SHAPE:
+        raise ShapeError(text)
+    if status == CB_ERR_UNSUPPORTED:
+        raise TypeMismatchError(text)
+    raise KernelError(f"status {status}: {text}")
+
+
+def call(name: str, *args) -> None:
+    lib = load()
+    check(getattr(lib, name)(*args), name)

@@ -1,0 +1,410 @@
+// GEMM for every contraction on the decoder step:  D = alpha * op(A) @ op(B) (+ D) (+ R)
+//
+// Replaces the reference's `x @ param(...)` products (reference layers.py:167, 340-348,
+// 412-416, 516, 597) and supplies the backward products the reference never runs.
+//
+// Two engines behind one entry point (cb_gemm):
+//   * gemm_tc   — bf16 operands, f32 accumulation in TMEM, tcgen05.mma issued by one
+//                 thread, operands staged by TMA into 128B-swizzled shared memory, a
+//                 persistent warp-specialised CTA per SM (TMA warp, MMA warp, 4 epilogue
+//                 warps) with a 2-deep TMEM accumulator so the epilogue of tile i overlaps
+//                 the MMAs of tile i+1.  Both K-major and MN-major operands are native
+//                 (UMMA descriptor major bits), so forward (x@W), dgrad (dY@W^T) and wgrad
+//                 (X^T@dY) all run on the reference's [in, out] weight layout with no
+//                 transposed copies.
+//   * gemm_simt — f32 FMA tiles; the fp32 parity mode (1e-5 contract) and shapes TMA
+//                 cannot describe (row strides not 16-byte aligned, e.g. hidden 341).
+#include <algorithm>
+
+#include "common.cuh"
+#include "composer_b200.h"
+
+namespace cb {
+
+struct Epi {
+  void* D;
+  int64_t ldd;
+  int d_f32;
+  const void* R;
+  int64_t ldr;
+  int r_f32;
+  float alpha;
+  int accumulate;
+  int M, N;
+};
+
+__device__ __forceinline__ float epi_load(const void* p, int64_t idx, int f32) {
+  return f32 ? reinterpret_cast<const float*>(p)[idx] : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[idx]);
+}
+
+__device__ __forceinline__ void epi_store1(const Epi& e, int r, int c, float v) {
+  v *= e.alpha;
+  const int64_t di = (int64_t)r * e.ldd + c;
+  if (e.accumulate) v += epi_load(e.D, di, e.d_f32);
+  if (e.R) v += epi_load(e.R, (int64_t)r * e.ldr + c, e.r_f32);
+  if (e.d_f32)
+    reinterpret_cast<float*>(e.D)[di] = v;
+  else
+    reinterpret_cast<__nv_bfloat16*>(e.D)[di] = __float2bfloat16_rn(v);
+}
+
+// ======================================================================================
+// tcgen05 engine
+// ======================================================================================
+namespace tc {
+constexpr int BM = 128;
+constexpr int BK = 64;  // one 128-byte swizzle atom of bf16 along K
+constexpr int kThreads = 256;
+constexpr int kGroupM = 16;  // raster: 16 M-tiles share each N column step (L2 reuse)
+
+template <int BN>
+struct Cfg {
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+  static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+};
+
+struct Args {
+  int M, N, K;
+  int a_mn, b_mn;
+  int tiles_m, tiles_n;
+  Epi e;
+};
+
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
+  const int per_group = kGroupM * tiles_n;
+  const int g = t / per_group;
+  const int r = t - g * per_group;
+  const int gm0 = g * kGroupM;
+  const int gsz = min(kGroupM, tiles_m - gm0);
+  tm = gm0 + r % gsz;
+  tn = r / gsz;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Args args) {
+  using C = Cfg<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::kStages * C::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_tiles = args.tiles_m * args.tiles_n;
+  const int nk = (args.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int tm, tn;
+        tile_coords(t, args.tiles_m, args.tiles_n, tm, tn);
+        const int m0 = tm * BM, n0 = tn * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], C::kStageBytes);
+          uint8_t* a_dst = sA + stage * C::kABytes;
+          uint8_t* b_dst = sB + stage * C::kBBytes;
+          const int k0 = kb * BK;
+          if (!args.a_mn) {
+            tma_load_2d(a_dst, &tmA, &full[stage], k0, m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d(a_dst + j * 8192, &tmA, &full[stage], m0 + 64 * j, k0);
+          }
+          if (!args.b_mn) {
+            tma_load_2d(b_dst, &tmB, &full[stage], k0, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b_dst + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0);
+          }
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16_f32(BM, BN, args.a_mn, args.b_mn);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * C::kABytes);
+          const uint32_t b_addr = smem_u32(sB + stage * C::kBBytes);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = args.a_mn ? sw128_desc(a_addr + kk * 2048, 8192, 1024) : sw128_desc(a_addr + kk * 32, 16, 1024);
+            const uint64_t bd = args.b_mn ? sw128_desc(b_addr + kk * 2048, 8192, 1024) : sw128_desc(b_addr + kk * 32, 16, 1024);
+            umma_f16_ss(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> registers -> global ----------------
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const Epi& e = args.e;
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      int tm, tn;
+      tile_coords(t, args.tiles_m, args.tiles_n, tm, tn);
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = tm * BM + q * 32 + lane;
+      const bool row_ok = row < e.M;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
+        tmem_ld_wait();
+        const int col0 = tn * BN + c * 32;
+        if (!row_ok || col0 >= e.N) continue;
+        const bool full_chunk = col0 + 32 <= e.N;
+        const bool fast = full_chunk && !e.accumulate && !e.R && e.alpha == 1.f && !e.d_f32 && ((e.ldd & 7) == 0) &&
+                          ((reinterpret_cast<uintptr_t>(e.D) & 15) == 0);
+        if (fast) {
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(e.D) + (int64_t)row * e.ldd + col0);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4 pk;
+            uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(v[j * 8 + 2 * h]), __uint_as_float(v[j * 8 + 2 * h + 1]));
+              w[h] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            dst[j] = pk;
+          }
+        } else {
+          const int lim = min(32, e.N - col0);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < lim) epi_store1(e, row, col0 + j, __uint_as_float(v[j]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::kTmemCols);
+  }
+}
+
+template <int BN>
+int launch(const Args& a, const void* A, int64_t lda, const void* B, int64_t ldb, cudaStream_t st) {
+  using C = Cfg<BN>;
+  CUtensorMap ta, tb;
+  int s;
+  // A: op(A) is MxK.  K-major -> stored [M][K]; MN-major -> stored [K][M].
+  if (!a.a_mn)
+    s = make_tmap_2d_bf16(&ta, A, a.M, a.K, lda, BM, BK);
+  else
+    s = make_tmap_2d_bf16(&ta, A, a.K, a.M, lda, BK, 64);
+  if (s) return s;
+  // B: op(B) is KxN.  K-major -> stored [N][K]; MN-major -> stored [K][N].
+  if (!a.b_mn)
+    s = make_tmap_2d_bf16(&tb, B, a.N, a.K, ldb, BN, BK);
+  else
+    s = make_tmap_2d_bf16(&tb, B, a.K, a.N, ldb, BK, 64);
+  if (s) return s;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    attr_set = true;
+  }
+  const int tiles = a.tiles_m * a.tiles_n;
+  const int grid = std::min(tiles, kNumSMs);
+  gemm_tc<BN><<<grid, kThreads, C::kSmem, st>>>(ta, tb, a);
+  return check_launch("gemm_tc");
+}
+}  // namespace tc
+
+// ======================================================================================
+// SIMT engine (f32 parity mode; unaligned bf16 shapes)
+// ======================================================================================
+namespace simt {
+constexpr int TM = 64, TN = 64, TK = 16;
+
+template <typename T>
+__global__ void __launch_bounds__(256) gemm_simt(int M, int N, int K, const T* __restrict__ A, int64_t sam, int64_t sak,
+                                                 const T* __restrict__ B, int64_t sbk, int64_t sbn, Epi e) {
+  __shared__ float As[TK][TM + 4];
+  __shared__ float Bs[TK][TN + 4];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += TK) {
+#pragma unroll
+    for (int i = 0; i < (TK * TM) / 256; ++i) {
+      const int idx = threadIdx.x + i * 256;
+      // walk the contiguous dimension with consecutive threads where possible
+      int kk, mm;
+      if (sak == 1) {
+        kk = idx % TK;
+        mm = idx / TK;
+      } else {
+        mm = idx % TM;
+        kk = idx / TM;
+      }
+      const int gm = m0 + mm, gk = k0 + kk;
+      As[kk][mm] = (gm < M && gk < K) ? to_f32(A[(int64_t)gm * sam + (int64_t)gk * sak]) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < (TK * TN) / 256; ++i) {
+      const int idx = threadIdx.x + i * 256;
+      int kk, nn;
+      if (sbn == 1) {
+        nn = idx % TN;
+        kk = idx / TN;
+      } else {
+        kk = idx % TK;
+        nn = idx / TK;
+      }
+      const int gn = n0 + nn, gk = k0 + kk;
+      Bs[kk][nn] = (gn < N && gk < K) ? to_f32(B[(int64_t)gk * sbk + (int64_t)gn * sbn]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = m0 + ty + 16 * i, c = n0 + tx + 16 * j;
+      if (r < M && c < N) epi_store1(e, r, c, acc[i][j]);
+    }
+}
+}  // namespace simt
+
+static int g_gemm_path = 0;  // 0 auto, 1 force SIMT, 2 force tcgen05
+
+}  // namespace cb
+
+using namespace cb;
+
+extern "C" int cb_gemm_set_path(int path) {
+  if (path < 0 || path > 2) return fail(CB_ERR_ARG, "gemm path must be 0 (auto), 1 (simt) or 2 (tcgen05)");
+  g_gemm_path = path;
+  return CB_OK;
+}
+
+// See include/composer_b200.h for the contract.
+extern "C" int cb_gemm(int M, int N, int K, int in_dtype, const void* A, int64_t lda, int trans_a, const void* B,
+                       int64_t ldb, int trans_b, void* D, int64_t ldd, int d_dtype, const void* R, int64_t ldr,
+                       int r_dtype, float alpha, int accumulate, void* stream) {
+  if (M < 0 || N < 0 || K < 0) return fail(CB_ERR_SHAPE, "gemm: negative extent (%d,%d,%d)", M, N, K);
+  if (!D) return fail(CB_ERR_ARG, "gemm: null output");
+  if (M == 0 || N == 0) return CB_OK;
+  if (in_dtype != CB_DT_F32 && in_dtype != CB_DT_BF16) return fail(CB_ERR_UNSUPPORTED, "gemm: input dtype %d", in_dtype);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Epi e{D, ldd, d_dtype == CB_DT_F32, R, ldr, r_dtype == CB_DT_F32, alpha, accumulate, M, N};
+  if (K == 0) {
+    // alpha*0 (+D) (+R): route through the SIMT epilogue with an empty reduction
+    dim3 grid((N + simt::TN - 1) / simt::TN, (M + simt::TM - 1) / simt::TM);
+    simt::gemm_simt<float><<<grid, 256, 0, st>>>(M, N, 0, nullptr, 0, 0, nullptr, 0, 0, e);
+    return check_launch("gemm_simt");
+  }
+  if (!A || !B) return fail(CB_ERR_ARG, "gemm: null operand");
+  const int64_t sam = trans_a ? 1 : lda, sak = trans_a ? lda : 1;
+  const int64_t sbk = trans_b ? 1 : ldb, sbn = trans_b ? ldb : 1;
+  if (in_dtype == CB_DT_BF16) {
+    const bool aligned = ((lda & 7) == 0) && ((ldb & 7) == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) &&
+                         ((reinterpret_cast<uintptr_t>(B) & 15) == 0);
+    const double work = (double)M * N * K;
+    bool use_tc = aligned && (g_gemm_path == 2 || (g_gemm_path == 0 && work >= (double)(1 << 22)));
+    if (g_gemm_path == 2 && !aligned) return fail(CB_ERR_UNSUPPORTED, "gemm: tcgen05 path needs 16-byte aligned operands");
+    if (use_tc) {
+      tc::Args a;
+      a.M = M;
+      a.N = N;
+      a.K = K;
+      a.a_mn = trans_a ? 1 : 0;
+      a.b_mn = trans_b ? 0 : 1;
+      a.e = e;
+      a.tiles_m = (M + tc::BM - 1) / tc::BM;
+      if (N > 128) {
+        a.tiles_n = (N + 255) / 256;
+        return tc::launch<256>(a, A, lda, B, ldb, st);
+      }
+      a.tiles_n = (N + 127) / 128;
+      return tc::launch<128>(a, A, lda, B, ldb, st);
+    }
+    dim3 grid((N + simt::TN - 1) / simt::TN, (M + simt::TM - 1) / simt::TM);
+    simt::gemm_simt<__nv_bfloat16><<<grid, 256, 0, st>>>(M, N, K, reinterpret_cast<const __nv_bfloat16*>(A), sam, sak,
+                                                         reinterpret_cast<const __nv_bfloat16*>(B), sbk, sbn, e);
+    return check_launch("gemm_simt_bf16");
+  }
+  dim3 grid((N + simt::TN - 1) / simt::TN, (M + simt::TM - 1) / simt::TM);
+  simt::gemm_simt<float><<<grid, 256, 0, st>>>(M, N, K, reinterpret_cast<const float*>(A), sam, sak,
+                                               reinterpret_cast<const float*>(B), sbk, sbn, e);
+  return check_launch("gemm_simt_f32");
+}
