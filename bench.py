@@ -1,0 +1,310 @@
+#!/usr/bin/env python
+"""Benchmark of the decoder training step (BASELINE.json metric: train tokens/s + MFU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1b] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one process per GPU, NCCL); every rank runs the same
+per-GPU batch (weak scaling) with FSDP-sharded state.  One step = forward + backward +
+AdamW over one synthetic batch of [batch, seq] tokens.  Timing: W warm-up
+steps, then K steps bracketed by barrier + synchronize, CUDA events on the compute
+stream, max over ranks.  Rank 0 prints one JSON line.
+
+--impl reference times the CPU restatement of the reference step (oracle/, float64,
+fwd+bwd+AdamW — the reference itself has no backward) on this host's cores, on a
+bounded sample of the same workload, and prints the same JSON line with
+"impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+NOMINAL_BF16_PFLOPS = 2.25e15
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            return json.load(fh), "measured"
+    return dict(FALLBACK_PEAKS), "fallback"
+
+
+def flops_per_token(module, batch, seq) -> float:
+    """3 x sum of the reference's own_flops (reference mesh.py:629,644) per token."""
+    total = 0
+    for _, m in module.walk():
+        total += m.behavior.own_flops(m.config, batch, seq)
+    return 3.0 * total / (batch * seq)
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sms.append(float(parts[1]))
+                    mx = float(parts[2])
+                except ValueError:
+                    continue
+                for n, v in zip(names, parts[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+        os.unlink(self.path)
+        loaded = [s for s in sms if mx and s > 0.3 * mx] or sms
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# --------------------------------------------------------------------------- CPU leg
+def cpu_sample(config: str, seconds_hint: float = 20.0) -> dict:
+    """Times the oracle (float64 fwd+bwd+AdamW) on a bounded sample of `config`.
+
+    Sample: the config's layer shape at 1 and 2 layers, batch 1, seq 256, full vocab;
+    per-token time extrapolated linearly in depth to the configured layer count.
+    """
+    import torch
+
+    from oracle import decoder_oracle as O
+    from paper_2507_05411_b200 import BENCH_CONFIGS, init_state, instantiate, root_key, synthetic_batch
+
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    seq = 256
+    full = BENCH_CONFIGS[config](batch=1, seq=seq, dtype="f32")
+    L = len(full.get("model.decoder.transformer.layer"))
+    times = {}
+    for nl in (1, 2):
+        cfg = BENCH_CONFIGS[config](batch=1, seq=seq, dtype="f32", layers=nl)
+        m = instantiate(cfg)
+        st = init_state(m, root_key(0))
+        spec = O.spec_from_config(m.config)
+        toks = synthetic_batch(0, 0, 1, seq, cfg.get("model.vocab_size"))["tokens"]
+        t0 = time.perf_counter()
+        O.train_step(st, toks, spec, O.AdamW(lr=1e-3))
+        times[nl] = time.perf_counter() - t0
+    per_layer = max(times[2] - times[1], 1e-9)
+    fixed = max(times[1] - per_layer, 0.0)
+    t_full = fixed + L * per_layer
+    return {"value": seq / t_full, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"oracle/ float64 fwd+bwd+AdamW of the {config} layer shape at 1 and 2 layers, batch 1, seq {seq}, "
+                      f"vocab {full.get('model.vocab_size')}; {times[1]:.2f}s/{times[2]:.2f}s, extrapolated linearly "
+                      f"to {L} layers ({t_full:.1f} s per {seq}-token step)"}
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2507_05411_b200 import BENCH_CONFIGS
+
+    for _ in range(args.warmup):
+        cpu_sample(args.config)
+    vals = [cpu_sample(args.config) for _ in range(args.steps)]
+    v = statistics.median(x["value"] for x in vals)
+    cfg = BENCH_CONFIGS[args.config](batch=args.batch, seq=args.seq)
+    line = {
+        "impl": "reference",
+        "metric": "train tokens/sec and MFU per B200, decoder step",
+        "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * args.batch * args.seq / v, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "global_batch": args.batch * args.gpus, "seq_len": args.seq,
+                   "d_model": cfg.get("model.dim"), "layers": len(cfg.get("model.decoder.transformer.layer"))},
+        "cpu_baseline": {**vals[-1], "value": v},
+        "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU leg
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="1b", choices=["tiny", "1b", "7b", "moe", "70b_layer"])
+    ap.add_argument("--batch", type=int, default=None, help="per-GPU batch (sequences)")
+    ap.add_argument("--seq", type=int, default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    defaults = {"tiny": (8, 256), "1b": (8, 4096), "7b": (2, 4096), "moe": (4, 4096), "70b_layer": (1, 4096)}
+    args.batch = args.batch or defaults[args.config][0]
+    args.seq = args.seq or defaults[args.config][1]
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_05411_b200 import BENCH_CONFIGS, TrainEngine, _lib, ops, synthetic_batch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    dtype = "f32" if args.config == "tiny" else "bf16"
+    cfg = BENCH_CONFIGS[args.config](batch=args.batch, seq=args.seq, dtype=dtype)
+    eng = TrainEngine(cfg, device=dev)
+    V = eng.cfg.get("model.vocab_size")
+    B, T = args.batch, args.seq
+    nsteps = args.warmup + args.steps
+    host = [synthetic_batch(rank, s, B, T, V)["tokens"] for s in range(nsteps)]
+    devtok = [eng.upload_tokens(h) for h in host]
+    torch.cuda.synchronize()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    stream = torch.cuda.current_stream()
+    for s in range(args.warmup):
+        eng.step(devtok[s])
+    barrier()
+    # ---- timed region: inputs resident in HBM
+    sampler = ClockSampler(local)
+    sampler.start()
+    n0 = _lib.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    loss = None
+    for s in range(args.steps):
+        loss, _ = eng.step(devtok[args.warmup + s])
+    ev1.record(stream)
+    barrier()
+    launches = _lib.launch_count() - n0
+    clocks = sampler.stop()
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    final_loss = float(loss.item())
+    tokens_step = world * B * T
+    value = tokens_step / (ms / 1e3)
+
+    # ---- kernel shares: the same steps again with CUDA events around GEMM / attention launches
+    prof = ops.KernelProfiler()
+    ops.set_profiler(prof)
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for s in range(min(args.steps, 3)):
+        eng.step(devtok[args.warmup + s])
+    p1.record(stream)
+    ops.set_profiler(None)
+    barrier()
+    kern = prof.summary()
+    prof_ms = p0.elapsed_time(p1)
+
+    # ---- end to end through the public API: host tokens in, loss out, every step
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for s in range(args.steps):
+        l_, _ = eng.step(host[args.warmup + s])
+        float(l_.item())
+    e1.record(stream)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    pk, pk_src = peaks()
+    fpt = flops_per_token(eng.module, B, T)
+    g = kern.get("gemm_bf16") or kern.get("gemm_f32") or {"flops": 0, "ms": 1.0, "launches": 0}
+    achieved = g["flops"] / (g["ms"] / 1e3) / 1e12
+    peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "gemm_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get("bytes_per_launch")
+    line = {
+        "metric": "train tokens/sec and MFU per B200, decoder step",
+        "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+        "data": "synthetic (reference synthetic_batch token stream; reference init_state weights)",
+        "config": {"workload": args.config, "global_batch": world * B, "per_gpu_batch": B, "seq_len": T,
+                   "d_model": eng.cfg.get("model.dim"), "layers": len(eng.cfg.get("model.decoder.transformer.layer")),
+                   "vocab": V, "params": eng.param_count(), "parallelism": f"fsdp{world}",
+                   "l2": "inputs larger than L2 (bf16 params + activations >> 126 MB)"},
+        "mfu": value * fpt / (world * NOMINAL_BF16_PFLOPS),
+        "model_flops_per_token": fpt,
+        "loss": final_loss,
+        "roofline": {"bound": "tensor", "kernel": "gemm_tc (tcgen05 persistent GEMM)", "achieved": achieved,
+                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "peak_source": f"{pk_src} bf16_tflops_sustained (kernel timed inside the step)",
+                     "traffic": traffic,
+                     "share_of_step": g["ms"] / prof_ms if prof_ms else None},
+        "kernels": {k: {"launches": v["launches"], "ms_per_step": v["ms"] / min(args.steps, 3),
+                        "tflops": v["flops"] / (v["ms"] / 1e3) / 1e12 if v["ms"] else None} for k, v in kern.items()},
+        "clocks": clocks,
+        "gpu_launches": launches,
+        "e2e": {"value": tokens_step / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": B * T * 8,
+                "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_sample(args.config)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -31,6 +31,8 @@ extern "C" {
 /* status / diagnostics */
 CB_API const char* cb_last_error(void);
 CB_API int cb_abi_version(void);
+/* Kernels launched by this library in this process so far (benchmark evidence). */
+CB_API long long cb_launch_count(void);
 
 /* ---------------------------------------------------------------------------------
  * GEMM:  D[M,N] = alpha * op(A) @ op(B)  (+ D if accumulate)  (+ R if R != NULL)
@@ -49,6 +51,114 @@ CB_API int cb_gemm(int M, int N, int K, int in_dtype, const void* A, int64_t lda
                    int r_dtype, float alpha, int accumulate, void* stream);
 /* 0 = automatic engine choice, 1 = force SIMT, 2 = force tcgen05 (tests only). */
 CB_API int cb_gemm_set_path(int path);
+
+/* ---------------------------------------------------------------------------------
+ * RMSNorm (layers.py:176-193): y = x / sqrt(mean(x^2) + eps) * scale, rstd[row] saved.
+ * Backward: dx = dres + d(norm)/dx . dy  (dres: the residual branch gradient, may be
+ * NULL); dscale += sum_rows dy * x * rstd (needs `workspace` of
+ * cb_rmsnorm_bwd_workspace bytes when dscale != NULL).  scale/rstd/dx/dscale are f32.
+ * ------------------------------------------------------------------------------- */
+CB_API int cb_rmsnorm_fwd(int rows, int dim, const void* x, int64_t ldx, int x_dtype, const float* scale, float eps,
+                          void* y, int64_t ldy, int y_dtype, float* rstd, void* stream);
+CB_API int cb_rmsnorm_bwd_workspace(int rows, int dim, int64_t* bytes);
+CB_API int cb_rmsnorm_bwd(int rows, int dim, const void* x, int64_t ldx, int x_dtype, const float* scale,
+                          const float* rstd, const void* dy, int64_t lddy, int dy_dtype, const float* dres,
+                          int64_t lddres, float* dx, int64_t lddx, float* dscale, float* workspace, void* stream);
+/* out[d] (+)= sum_p partial[p][d] in fixed order (deterministic). */
+CB_API int cb_col_reduce(int nparts, int dim, const float* partial, float* out, int accumulate, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * Embedding (layers.py:199-229): out[i] = table[ids[i]].  The backward is
+ * deterministic: cb_sort_ids groups positions by id (stable counting sort, one CTA;
+ * offsets int32[vocab+1], cursor int32[vocab] scratch, perm int32[n]), then
+ * cb_embedding_bwd adds each id's rows, in position order, into dtable (f32).
+ * ------------------------------------------------------------------------------- */
+CB_API int cb_embedding_fwd(int64_t n, int dim, const int64_t* ids, const void* table, int64_t ldt, int t_dtype,
+                            void* out, int64_t ldo, int o_dtype, void* stream);
+CB_API int cb_sort_ids(int n, int vocab, const int64_t* ids, int* offsets, int* cursor, int* perm, void* stream);
+CB_API int cb_embedding_bwd(int vocab, int dim, const int* offsets, const int* perm, const void* dout, int64_t ldo,
+                            int g_dtype, float* dtable, int64_t ldt, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * RoPE (layers.py:235-257, RoPEBehavior :267-276), in place on [rows = B*T] x heads x
+ * head_dim with row stride ld: interleaved pairs rotated by cos/sin tables f32
+ * [seq_len][head_dim/2]; inverse = 1 applies the transpose rotation (the backward).
+ * ------------------------------------------------------------------------------- */
+CB_API int cb_rope(int64_t rows, int seq_len, int heads, int head_dim, void* x, int64_t ld, int dtype,
+                   const float* cos_t, const float* sin_t, int inverse, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * Activations (layers.py:55-77, FFN :405-416).  ids: 0 linear, 1 relu, 2 silu,
+ * 3 sigmoid, 4 tanh.  out = act0(a) * act1(g) (g == NULL: out = act0(a)).
+ * ------------------------------------------------------------------------------- */
+CB_API int cb_act_fwd(int64_t rows, int cols, int act0, int act1, const void* a, int64_t lda, const void* g,
+                      int64_t ldg, void* out, int64_t ldo, int dtype, void* stream);
+CB_API int cb_act_bwd(int64_t rows, int cols, int act0, int act1, const void* a, int64_t lda, const void* g,
+                      int64_t ldg, const void* dout, int64_t lddo, void* da, int64_t ldda, void* dg, int64_t lddg,
+                      int dtype, void* stream);
+/* out (+)= alpha * in, 2-D strided, with dtype conversion. */
+CB_API int cb_copy2d(int64_t rows, int cols, const void* in, int64_t ldi, int in_dtype, void* out, int64_t ldo,
+                     int out_dtype, float alpha, int accumulate, void* stream);
+CB_API int cb_memset_zero(void* ptr, int64_t bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * Attention (layers.py:282-348), unmasked, flash-style (P never stored).  q/k/v/o
+ * rows are tokens (b*T + t), head h at columns [h*hd, (h+1)*hd).  lse/delta are f32
+ * [B][H][T].  kv_heads < heads is grouped-query attention (query head h reads kv head
+ * h / (heads/kv_heads)); kv_heads == heads is the reference's attention.
+ * ------------------------------------------------------------------------------- */
+CB_API int cb_attention_fwd(int batch, int seq_len, int heads, int kv_heads, int head_dim, int dtype, const void* q,
+                            int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv, void* o, int64_t ldo,
+                            float* lse, float scale, void* stream);
+CB_API int cb_attention_bwd(int batch, int seq_len, int heads, int kv_heads, int head_dim, int dtype, const void* q,
+                            int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv, const void* o,
+                            int64_t ldo, const float* lse, const void* dout, int64_t lddo, float* delta, void* dq,
+                            int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv, float scale, void* stream);
+/* 0 = automatic (tensor-core flash kernels when eligible), 1 = force SIMT (tests). */
+CB_API int cb_attention_set_path(int path);
+
+/* ---------------------------------------------------------------------------------
+ * Next-token cross-entropy (TrainerBehavior.forward, layers.py:638-651) fused with its
+ * gradient: row b*T+t of logits [B*T, V] predicts tokens[b, t+1]; rows t = T-1 get a
+ * zero gradient.  dlogits = (softmax - onehot) * grad_scale (may alias logits, or be
+ * NULL for forward-only).  row_loss f32[B*T] scratch; the mean over B*(T-1) rows goes
+ * to *loss64 / *loss32 (either may be NULL).
+ * ------------------------------------------------------------------------------- */
+CB_API int cb_xent_fwd_bwd(int batch, int seq_len, int vocab, const void* logits, int64_t ld, int l_dtype,
+                           const int64_t* tokens, float* row_loss, void* dlogits, int64_t ldg, int g_dtype,
+                           float grad_scale, double* loss64, float* loss32, void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * AdamW (the update the fn:adamw factory at layers.py:657-663,778-782 describes) over a
+ * flat f32 shard; optionally refreshes the bf16 working copy in the same pass.
+ * ------------------------------------------------------------------------------- */
+CB_API int cb_adamw(int64_t n, float* param, const float* grad, float* exp_avg, float* exp_avg_sq, void* param_bf16,
+                    float lr, float beta1, float beta2, float eps, float weight_decay, int step, float grad_scale,
+                    void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * MoE (layers.py:422-533).  cb_moe_route: probs = softmax(x @ router) in f64 per token,
+ * stable top-k (ties -> lowest expert id, layers.py:437), weights renormalized over the
+ * k picks (layers.py:440); idx int32[n][k], weights f32[n][k], probs f32[n][E].
+ * cb_moe_stats: out f64[1+2E] = [load_balance_loss, counts..., mean_probs...]
+ * (layers.py:441-449).  Dispatch/combine use cb_sort_ids on the expert ids.
+ * ------------------------------------------------------------------------------- */
+CB_API int cb_moe_route(int64_t n, int dim, int experts, int top_k, const void* x, int64_t ldx, int x_dtype,
+                        const float* router, int32_t* idx, float* weights, float* probs, void* stream);
+CB_API int cb_moe_stats(int64_t n, int experts, int top_k, const int32_t* idx, const float* probs, double* out,
+                        void* stream);
+CB_API int cb_gather_rows(int64_t n, int dim, const int32_t* perm, int div, const void* x, int64_t ldx, void* out,
+                          int64_t ldo, int dtype, void* stream);
+/* out[t] (+)= sum_j w[t,j] * y[inv[t*k+j]]  (weights == NULL -> 1), slot order (layers.py:529-531). */
+CB_API int cb_moe_combine(int64_t n, int dim, int top_k, const int32_t* inv, const float* weights, const void* y,
+                          int64_t ldy, int y_dtype, float* out, int64_t ldo, int accumulate, void* stream);
+CB_API int cb_moe_combine_bwd(int64_t n, int dim, int top_k, const int32_t* inv, const float* weights, const float* y,
+                              int64_t ldy, const float* dout, int64_t lddo, void* dy, int64_t lddy, int dy_dtype,
+                              float* dweights, void* stream);
+CB_API int cb_moe_router_bwd(int64_t n, int experts, int top_k, const float* probs, const int32_t* idx,
+                             const float* weights, const float* dweights, float* dlogits, void* stream);
+CB_API int cb_invert_perm(int64_t n, const int32_t* perm, int32_t* inv, void* stream);
+CB_API int cb_widen_i32(int64_t n, const int32_t* a, int64_t* b, void* stream);
 
 #ifdef __cplusplus
 }

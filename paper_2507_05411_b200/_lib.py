@@ -33,6 +33,32 @@ SIGNATURES: dict[str, list] = {
     "cb_abi_version": [],
     "cb_gemm_set_path": [_I],
     "cb_gemm": [_I, _I, _I, _I, _P, _L, _I, _P, _L, _I, _P, _L, _I, _P, _L, _I, _F, _I, _P],
+    "cb_rmsnorm_fwd": [_I, _I, _P, _L, _I, _P, _F, _P, _L, _I, _P, _P],
+    "cb_rmsnorm_bwd_workspace": [_I, _I, ctypes.POINTER(ctypes.c_int64)],
+    "cb_rmsnorm_bwd": [_I, _I, _P, _L, _I, _P, _P, _P, _L, _I, _P, _L, _P, _L, _P, _P, _P],
+    "cb_col_reduce": [_I, _I, _P, _P, _I, _P],
+    "cb_embedding_fwd": [_L, _I, _P, _P, _L, _I, _P, _L, _I, _P],
+    "cb_sort_ids": [_I, _I, _P, _P, _P, _P, _P],
+    "cb_embedding_bwd": [_I, _I, _P, _P, _P, _L, _I, _P, _L, _P],
+    "cb_rope": [_L, _I, _I, _I, _P, _L, _I, _P, _P, _I, _P],
+    "cb_act_fwd": [_L, _I, _I, _I, _P, _L, _P, _L, _P, _L, _I, _P],
+    "cb_act_bwd": [_L, _I, _I, _I, _P, _L, _P, _L, _P, _L, _P, _L, _P, _L, _I, _P],
+    "cb_copy2d": [_L, _I, _P, _L, _I, _P, _L, _I, _F, _I, _P],
+    "cb_memset_zero": [_P, _L, _P],
+    "cb_attention_fwd": [_I, _I, _I, _I, _I, _I, _P, _L, _P, _L, _P, _L, _P, _L, _P, _F, _P],
+    "cb_attention_bwd": [_I, _I, _I, _I, _I, _I, _P, _L, _P, _L, _P, _L, _P, _L, _P, _P, _L, _P, _P, _L, _P, _L,
+                         _P, _L, _F, _P],
+    "cb_attention_set_path": [_I],
+    "cb_xent_fwd_bwd": [_I, _I, _I, _P, _L, _I, _P, _P, _P, _L, _I, _F, _P, _P, _P],
+    "cb_adamw": [_L, _P, _P, _P, _P, _P, _F, _F, _F, _F, _F, _I, _F, _P],
+    "cb_moe_route": [_L, _I, _I, _I, _P, _L, _I, _P, _P, _P, _P, _P],
+    "cb_moe_stats": [_L, _I, _I, _P, _P, _P, _P],
+    "cb_gather_rows": [_L, _I, _P, _I, _P, _L, _P, _L, _I, _P],
+    "cb_moe_combine": [_L, _I, _I, _P, _P, _P, _L, _I, _P, _L, _I, _P],
+    "cb_moe_combine_bwd": [_L, _I, _I, _P, _P, _P, _L, _P, _L, _P, _L, _I, _P, _P],
+    "cb_moe_router_bwd": [_L, _I, _I, _P, _P, _P, _P, _P, _P],
+    "cb_invert_perm": [_L, _P, _P, _P],
+    "cb_widen_i32": [_L, _P, _P, _P],
 }
 
 _lib = None
@@ -63,8 +89,15 @@ def load():
         fn.restype = ctypes.c_int
     lib.cb_last_error.argtypes = []
     lib.cb_last_error.restype = ctypes.c_char_p
+    lib.cb_launch_count.argtypes = []
+    lib.cb_launch_count.restype = ctypes.c_longlong
     _lib = lib
     return lib
+
+
+def launch_count() -> int:
+    """Kernels launched through the library so far in this process."""
+    return int(load().cb_launch_count())
 
 
 def check(status: int, what: str = "") -> None:

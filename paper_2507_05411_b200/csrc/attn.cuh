@@ -1,0 +1,24 @@
+// Shared declarations of the attention engines (attn_simt.cu, attn_fa.cu, attn_api.cu).
+#pragma once
+#include "common.cuh"
+
+namespace cb {
+struct AttnGeom {
+  int B, T, H, KVH, hd;
+  int64_t ldq, ldk, ldv, ldo;
+  float scale;
+};
+int check_geom(const AttnGeom& g);
+int attn_fwd_simt(const AttnGeom& g, int dtype, const void* q, const void* k, const void* v, void* o, float* lse,
+                  cudaStream_t st);
+int attn_delta(const AttnGeom& g, int dtype, const void* o, const void* dout, int64_t lddo, float* delta,
+               cudaStream_t st);
+int attn_bwd_simt(const AttnGeom& g, int dtype, const void* q, const void* k, const void* v, const void* dout,
+                  int64_t lddo, const float* lse, const float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk,
+                  void* dv, int64_t lddv, cudaStream_t st);
+bool attn_fa_supported(const AttnGeom& g, int dtype, const void* q, const void* k, const void* v);
+int attn_fwd_fa(const AttnGeom& g, const void* q, const void* k, const void* v, void* o, float* lse, cudaStream_t st);
+int attn_bwd_fa(const AttnGeom& g, const void* q, const void* k, const void* v, const void* dout, int64_t lddo,
+                const float* lse, const float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
+                int64_t lddv, cudaStream_t st);
+}  // namespace cb

@@ -1,0 +1,40 @@
+// C-ABI entry points of the attention engines (dispatch: tensor-core flash kernels for
+// bf16 with a supported head_dim, SIMT engine otherwise).
+#include "attn.cuh"
+#include "composer_b200.h"
+
+namespace cb {
+static int g_attn_path = 0;  // 0 auto, 1 force SIMT
+}  // namespace cb
+
+using namespace cb;
+
+extern "C" int cb_attention_set_path(int path) {
+  if (path < 0 || path > 1) return fail(CB_ERR_ARG, "attention path must be 0 (auto) or 1 (simt)");
+  g_attn_path = path;
+  return CB_OK;
+}
+
+extern "C" int cb_attention_fwd(int batch, int seq_len, int heads, int kv_heads, int head_dim, int dtype,
+                                const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
+                                void* o, int64_t ldo, float* lse, float scale, void* stream) {
+  AttnGeom g{batch, seq_len, heads, kv_heads, head_dim, ldq, ldk, ldv, ldo, scale};
+  if (int s = check_geom(g)) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (g_attn_path == 0 && attn_fa_supported(g, dtype, q, k, v)) return attn_fwd_fa(g, q, k, v, o, lse, st);
+  return attn_fwd_simt(g, dtype, q, k, v, o, lse, st);
+}
+
+extern "C" int cb_attention_bwd(int batch, int seq_len, int heads, int kv_heads, int head_dim, int dtype,
+                                const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
+                                const void* o, int64_t ldo, const float* lse, const void* dout, int64_t lddo,
+                                float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv,
+                                float scale, void* stream) {
+  AttnGeom g{batch, seq_len, heads, kv_heads, head_dim, ldq, ldk, ldv, ldo, scale};
+  if (int s = check_geom(g)) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (int s = attn_delta(g, dtype, o, dout, lddo, delta, st)) return s;
+  if (g_attn_path == 0 && attn_fa_supported(g, dtype, q, k, v))
+    return attn_bwd_fa(g, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st);
+  return attn_bwd_simt(g, dtype, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st);
+}

@@ -23,7 +23,8 @@
 namespace cb {
 
 int fail(int code, const char* fmt, ...);
-int check_launch(const char* what);
+// Checks the launch status and counts `launches` kernels toward cb_launch_count().
+int check_launch(const char* what, int launches = 1);
 
 static constexpr int kNumSMs = 148;
 

@@ -1,0 +1,282 @@
+// Mixture-of-experts routing, dispatch and combine (reference layers.py:422-533).
+//
+//  cb_moe_route     probs = softmax(x @ router) computed in f64 per token (one warp per
+//                   token, lane e owns expert e), stable top-k by (prob desc, id asc) —
+//                   exactly argsort(-probs, kind="stable")[:k] (layers.py:437) — and the
+//                   renormalized gate weights picked/sum(picked) (layers.py:440).  Router
+//                   inputs that are bit-identical to the reference's give bit-identical
+//                   expert assignments (f64 logits).
+//  cb_moe_stats     load_balance_loss = E * sum_e f_e * mean_p_e (layers.py:441-449),
+//                   deterministic single-CTA reduction (summary only, not in the loss).
+//  cb_gather_rows   dispatch: rows of x into expert-sorted order (perm from cb_sort_ids).
+//  cb_moe_combine   out[t] = sum_slot w[t,slot] * y[pos(t,slot)] in slot order (layers.py:529-531).
+//  cb_moe_combine_bwd / cb_moe_router_bwd: the reverse of combine, renormalization and softmax.
+#include "common.cuh"
+#include "composer_b200.h"
+
+namespace cb {
+
+constexpr int kMaxExperts = 32;
+
+template <typename TX>
+__global__ void __launch_bounds__(128) moe_route_k(int64_t n, int d, int E, int k, const TX* __restrict__ x, int64_t ldx,
+                                                   const float* __restrict__ router, int32_t* __restrict__ idx,
+                                                   float* __restrict__ w, float* __restrict__ probs) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * 4 + warp;
+  if (t >= n) return;
+  const TX* xr = x + t * ldx;
+  double logit = -INFINITY;
+  if (lane < E) {
+    double acc = 0.0;
+    for (int c = 0; c < d; ++c) acc = fma((double)to_f32(xr[c]), (double)router[(int64_t)c * E + lane], acc);
+    logit = acc;
+  }
+  double mx = logit;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const double e = lane < E ? exp(logit - mx) : 0.0;
+  double s = e;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const double p = e / s;
+  if (lane < E) probs[t * E + lane] = (float)p;
+  // stable top-k: repeatedly take (max prob, lowest id)
+  bool taken = lane >= E;
+  double picked[kMaxExperts];
+  int pid[kMaxExperts];
+  double psum = 0.0;
+  for (int j = 0; j < k; ++j) {
+    double bv = taken ? -1.0 : p;
+    int bi = taken ? 1 << 30 : lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == bi) taken = true;
+    picked[j] = bv;
+    pid[j] = bi;
+    psum += bv;
+  }
+  if (lane == 0) {
+    for (int j = 0; j < k; ++j) {
+      idx[t * k + j] = pid[j];
+      w[t * k + j] = (float)(picked[j] / psum);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024) moe_stats_k(int64_t n, int E, int k, const int32_t* __restrict__ idx,
+                                                    const float* __restrict__ probs, double* __restrict__ out) {
+  __shared__ double psum[kMaxExperts][33];
+  __shared__ int cnt[kMaxExperts][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // each warp accumulates a strided subset of tokens in fixed order -> deterministic
+  double ps[kMaxExperts];
+  int cs[kMaxExperts];
+  for (int e = 0; e < E; ++e) {
+    ps[e] = 0.0;
+    cs[e] = 0;
+  }
+  for (int64_t t = threadIdx.x; t < n; t += blockDim.x) {
+    for (int e = 0; e < E; ++e) ps[e] += (double)probs[t * E + e];
+    for (int j = 0; j < k; ++j) cs[idx[t * k + j]] += 1;
+  }
+  for (int e = 0; e < E; ++e) {
+    double v = ps[e];
+    int c = cs[e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v += __shfl_xor_sync(0xffffffffu, v, o);
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    if (lane == 0) {
+      psum[e][warp] = v;
+      cnt[e][warp] = c;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nw = blockDim.x >> 5;
+    double lbl = 0.0;
+    for (int e = 0; e < E; ++e) {
+      double p = 0.0;
+      long long c = 0;
+      for (int w2 = 0; w2 < nw; ++w2) {
+        p += psum[e][w2];
+        c += cnt[e][w2];
+      }
+      const double f = (double)c / (double)(n * k);
+      lbl += f * (p / (double)n);
+      out[1 + e] = (double)c;
+      out[1 + E + e] = p / (double)n;
+    }
+    out[0] = (double)E * lbl;
+  }
+}
+
+template <typename T>
+__global__ void gather_rows_k(int64_t n, int d, const int32_t* __restrict__ perm, int div, const T* __restrict__ x,
+                              int64_t ldx, T* __restrict__ out, int64_t ldo) {
+  const int64_t r = blockIdx.x;
+  if (r >= n) return;
+  const int64_t src = perm[r] / div;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) out[r * ldo + c] = x[src * ldx + c];
+}
+
+// out[t] (+)= sum_j w[t,j] * y[inv[t*k+j]]  (w == NULL -> weights 1)
+template <typename TY>
+__global__ void combine_k(int64_t n, int d, int k, const int32_t* __restrict__ inv, const float* __restrict__ w,
+                          const TY* __restrict__ y, int64_t ldy, float* __restrict__ out, int64_t ldo, int accumulate) {
+  const int64_t t = blockIdx.x;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float acc = 0.f;
+    for (int j = 0; j < k; ++j) {
+      const float wj = w ? w[t * k + j] : 1.f;
+      acc += wj * to_f32(y[(int64_t)inv[t * k + j] * ldy + c]);
+    }
+    out[t * ldo + c] = accumulate ? out[t * ldo + c] + acc : acc;
+  }
+}
+
+// dy[inv[t*k+j]] = w[t,j] * dout[t] ;  dw[t,j] = dout[t] . y[inv[t*k+j]]
+template <typename TG>
+__global__ void __launch_bounds__(256) combine_bwd_k(int64_t n, int d, int k, const int32_t* __restrict__ inv,
+                                                     const float* __restrict__ w, const float* __restrict__ y,
+                                                     int64_t ldy, const float* __restrict__ dout, int64_t lddo,
+                                                     TG* __restrict__ dy, int64_t lddy, float* __restrict__ dw) {
+  __shared__ float red[32];
+  const int64_t t = blockIdx.x;
+  for (int j = 0; j < k; ++j) {
+    const int64_t r = inv[t * k + j];
+    const float wj = w[t * k + j];
+    float dot = 0.f;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+      const float g = dout[t * lddo + c];
+      dy[r * lddy + c] = from_f32<TG>(wj * g);
+      dot = fmaf(g, y[r * ldy + c], dot);
+    }
+    dot = block_sum(dot, red);
+    if (threadIdx.x == 0) dw[t * k + j] = dot;
+  }
+}
+
+// gradient of w = renorm(top-k(softmax(logits))) w.r.t. the logits
+__global__ void moe_router_bwd_k(int64_t n, int E, int k, const float* __restrict__ probs,
+                                 const int32_t* __restrict__ idx, const float* __restrict__ w,
+                                 const float* __restrict__ dw, float* __restrict__ dlogits) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  float dp[kMaxExperts];
+  for (int e = 0; e < E; ++e) dp[e] = 0.f;
+  float S = 0.f, wdw = 0.f;
+  for (int j = 0; j < k; ++j) {
+    S += probs[t * E + idx[t * k + j]];
+    wdw += w[t * k + j] * dw[t * k + j];
+  }
+  for (int j = 0; j < k; ++j) dp[idx[t * k + j]] += (dw[t * k + j] - wdw) / S;
+  float pdp = 0.f;
+  for (int e = 0; e < E; ++e) pdp += probs[t * E + e] * dp[e];
+  for (int e = 0; e < E; ++e) dlogits[t * E + e] = probs[t * E + e] * (dp[e] - pdp);
+}
+
+}  // namespace cb
+
+using namespace cb;
+
+extern "C" int cb_moe_route(int64_t n, int dim, int experts, int top_k, const void* x, int64_t ldx, int x_dtype,
+                            const float* router, int32_t* idx, float* weights, float* probs, void* stream) {
+  if (experts < 1 || experts > kMaxExperts) return fail(CB_ERR_UNSUPPORTED, "moe: experts must be in [1, %d]", kMaxExperts);
+  if (top_k < 1 || top_k > experts) return fail(CB_ERR_SHAPE, "top_k=%d must lie in [1, %d]", top_k, experts);
+  if (n <= 0) return CB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int blocks = (int)((n + 3) / 4);
+  if (x_dtype == CB_DT_F32)
+    moe_route_k<float><<<blocks, 128, 0, st>>>(n, dim, experts, top_k, (const float*)x, ldx, router, idx, weights, probs);
+  else
+    moe_route_k<__nv_bfloat16><<<blocks, 128, 0, st>>>(n, dim, experts, top_k, (const __nv_bfloat16*)x, ldx, router, idx,
+                                                       weights, probs);
+  return check_launch("moe_route");
+}
+
+// out f64[1 + 2E]: [load_balance_loss, counts_e..., mean_probs_e...]
+extern "C" int cb_moe_stats(int64_t n, int experts, int top_k, const int32_t* idx, const float* probs, double* out,
+                            void* stream) {
+  if (n <= 0) return CB_OK;
+  moe_stats_k<<<1, 1024, 0, (cudaStream_t)stream>>>(n, experts, top_k, idx, probs, out);
+  return check_launch("moe_stats");
+}
+
+extern "C" int cb_gather_rows(int64_t n, int dim, const int32_t* perm, int div, const void* x, int64_t ldx, void* out,
+                              int64_t ldo, int dtype, void* stream) {
+  if (n <= 0) return CB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == CB_DT_F32)
+    gather_rows_k<float><<<n, 256, 0, st>>>(n, dim, perm, div, (const float*)x, ldx, (float*)out, ldo);
+  else
+    gather_rows_k<__nv_bfloat16><<<n, 256, 0, st>>>(n, dim, perm, div, (const __nv_bfloat16*)x, ldx,
+                                                    (__nv_bfloat16*)out, ldo);
+  return check_launch("gather_rows");
+}
+
+extern "C" int cb_moe_combine(int64_t n, int dim, int top_k, const int32_t* inv, const float* weights, const void* y,
+                              int64_t ldy, int y_dtype, float* out, int64_t ldo, int accumulate, void* stream) {
+  if (n <= 0) return CB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (y_dtype == CB_DT_F32)
+    combine_k<float><<<n, 256, 0, st>>>(n, dim, top_k, inv, weights, (const float*)y, ldy, out, ldo, accumulate);
+  else
+    combine_k<__nv_bfloat16><<<n, 256, 0, st>>>(n, dim, top_k, inv, weights, (const __nv_bfloat16*)y, ldy, out, ldo,
+                                                accumulate);
+  return check_launch("moe_combine");
+}
+
+extern "C" int cb_moe_combine_bwd(int64_t n, int dim, int top_k, const int32_t* inv, const float* weights,
+                                  const float* y, int64_t ldy, const float* dout, int64_t lddo, void* dy, int64_t lddy,
+                                  int dy_dtype, float* dweights, void* stream) {
+  if (n <= 0) return CB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dy_dtype == CB_DT_F32)
+    combine_bwd_k<float><<<n, 256, 0, st>>>(n, dim, top_k, inv, weights, y, ldy, dout, lddo, (float*)dy, lddy, dweights);
+  else
+    combine_bwd_k<__nv_bfloat16><<<n, 256, 0, st>>>(n, dim, top_k, inv, weights, y, ldy, dout, lddo,
+                                                    (__nv_bfloat16*)dy, lddy, dweights);
+  return check_launch("moe_combine_bwd");
+}
+
+extern "C" int cb_moe_router_bwd(int64_t n, int experts, int top_k, const float* probs, const int32_t* idx,
+                                 const float* weights, const float* dweights, float* dlogits, void* stream) {
+  if (n <= 0) return CB_OK;
+  moe_router_bwd_k<<<(int)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, experts, top_k, probs, idx, weights,
+                                                                            dweights, dlogits);
+  return check_launch("moe_router_bwd");
+}
+
+// inv[perm[j]] = j
+__global__ void invert_perm_k(int64_t n, const int32_t* __restrict__ perm, int32_t* __restrict__ inv) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < n) inv[perm[j]] = (int32_t)j;
+}
+
+// int32 -> int64 widening (expert ids feed cb_sort_ids)
+__global__ void widen_k(int64_t n, const int32_t* __restrict__ a, int64_t* __restrict__ b) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j < n) b[j] = a[j];
+}
+
+extern "C" int cb_invert_perm(int64_t n, const int32_t* perm, int32_t* inv, void* stream) {
+  if (n <= 0) return CB_OK;
+  invert_perm_k<<<(int)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, perm, inv);
+  return check_launch("invert_perm");
+}
+
+extern "C" int cb_widen_i32(int64_t n, const int32_t* a, int64_t* b, void* stream) {
+  if (n <= 0) return CB_OK;
+  widen_k<<<(int)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, a, b);
+  return check_launch("widen_i32");
+}

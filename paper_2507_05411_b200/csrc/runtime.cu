@@ -3,6 +3,7 @@
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <atomic>
 #include <mutex>
 
 #include "common.cuh"
@@ -20,7 +21,10 @@ int fail(int code, const char* fmt, ...) {
   return code;
 }
 
-int check_launch(const char* what) {
+static std::atomic<long long> g_launches{0};
+
+int check_launch(const char* what, int launches) {
+  g_launches.fetch_add(launches, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(CB_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
   return CB_OK;
@@ -80,3 +84,5 @@ int make_tmap_3d_bf16(CUtensorMap* out, const void* base, uint64_t d0, uint64_t 
 
 extern "C" const char* cb_last_error(void) { return cb::g_last_error; }
 extern "C" int cb_abi_version(void) { return 1; }
+// Number of kernels this library has launched in this process (all threads).
+extern "C" long long cb_launch_count(void) { return cb::g_launches.load(std::memory_order_relaxed); }

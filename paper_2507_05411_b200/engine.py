@@ -1,0 +1,478 @@
+"""The training-step engine: parameter layout in HBM, FSDP, optimizer, step driver.
+
+``TrainEngine(cfg)`` instantiates a reference-style Trainer config and owns:
+
+* a **flat bucketed parameter layout** — one bucket per ``TransformerStack`` layer plus a
+  root bucket (embedding, final norm, ...) and a small replicated bucket for f32-pinned
+  tensors (norm scales, MoE router).  Inside a bucket an attention block's wq|wk|wv and a
+  gated FFN's w1|w1_gate are laid out as column slices of one matrix so the behaviors
+  issue one wide GEMM; every block is 64-element aligned (TMA needs 16 B).
+* per bucket: f32 master shard, bf16 (or f32) working copy of the full bucket, f32 grad
+  buffer, AdamW m/v shards.  With world size 1 the shard is the whole bucket.
+* **FSDP** (world size N > 1, one process per GPU, NCCL over NVLink): the working copy of
+  layer i+1 is all-gathered on a side stream while layer i computes; each layer's
+  gradient is reduce-scattered (mean over ranks) on the side stream right after that
+  layer's backward; AdamW runs on local shards and refreshes the local slice of the
+  working copy.  Sequences are independent, so the data path is plain data parallelism
+  over the batch and the loss is the all-reduced mean (reference SPEC.md:445: numerics
+  do not depend on partitioning).
+
+The step itself is ``module.value_and_grad`` over the behaviors in ``layers.py``: no
+PyTorch arithmetic, only C-ABI kernel launches.  PyTorch provides memory, streams and
+``torch.distributed``.
+"""
+
+from __future__ import annotations
+
+import math
+import re
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import ops
+from .config import ConfigNode, visit
+from .errors import ShapeError, TypeMismatchError
+from .module import Module, ParamProvider, instantiate, invoke, iter_param_specs, value_and_grad
+from .prng import child_key, root_key
+
+ALIGN = 64
+_F32_KINDS = {("RMSNorm", "scale"), ("MoE", "router")}
+_LAYER_RE = re.compile(r"^(.*\.transformer\.layer\[\d+\])(\.|$)")
+
+
+def model_precision(cfg: ConfigNode) -> str:
+    """The uniform compute dtype of every dtype-bearing node (the reference's DtypePolicy hook)."""
+    tags = set()
+
+    def enter(path, node):
+        if node.has_field("dtype"):
+            tags.add(node.get("dtype"))
+
+    visit(cfg, enter_fn=enter)
+    if not tags:
+        return "f32"
+    if len(tags) > 1:
+        raise TypeMismatchError(f"mixed dtype policies are not supported: {sorted(tags)}")
+    tag = tags.pop()
+    if tag not in ("f32", "bf16"):
+        raise TypeMismatchError(f"dtype {tag!r} has no B200 kernel path (supported: f32, bf16)")
+    return tag
+
+
+def set_dtype_policy(cfg: ConfigNode, tag: str) -> ConfigNode:
+    """Sets `dtype` on every matmul-bearing node (what the reference's DtypePolicyModifier does)."""
+    targets = []
+
+    def enter(path, node):
+        if node.has_field("dtype"):
+            targets.append(path)
+
+    visit(cfg, enter_fn=enter)
+    for p in targets:
+        cfg = cfg.set(f"{p}.dtype" if p else "dtype", tag)
+    return cfg
+
+
+def _align(n: int, a: int = ALIGN) -> int:
+    return (n + a - 1) // a * a
+
+
+@dataclass
+class Entry:
+    path: str  # module path ("model.decoder.emb")
+    name: str  # param name ("weight")
+    shape: tuple
+    offset: int  # element offset of the (group) block in the bucket
+    col0: int = 0  # column offset inside a fused group
+    ld: int = 0  # row stride inside a fused group (0 = contiguous)
+    module_kind: str = ""
+
+
+@dataclass
+class Bucket:
+    name: str
+    entries: list = field(default_factory=list)
+    numel: int = 0
+    replicated: bool = False
+
+
+def build_layout(module: Module) -> list[Bucket]:
+    root = Bucket("root")
+    rep = Bucket("replicated", replicated=True)
+    layers: dict[str, Bucket] = {}
+    order: list[Bucket] = []
+    grouped = {}
+    for path, mod, pname, shape in iter_param_specs(module):
+        if (mod.kind, pname) in _F32_KINDS:
+            b = rep
+        else:
+            m = _LAYER_RE.match(path)
+            if m:
+                key = m.group(1)
+                if key not in layers:
+                    layers[key] = Bucket(key)
+                    order.append(layers[key])
+                b = layers[key]
+            else:
+                b = root
+        grouped.setdefault((id(b), path), (b, mod, []))[2].append((pname, shape))
+    for (_, path), (b, mod, plist) in grouped.items():
+        names = dict(plist)
+        fuse = None
+        if mod.kind in ("Attention", "GroupedQueryAttention") and {"wq", "wk", "wv"} <= set(names):
+            fuse = ["wq", "wk", "wv"]
+        elif mod.kind == "FeedForward" and {"w1", "w1_gate"} <= set(names):
+            fuse = ["w1", "w1_gate"]
+        done = set()
+        if fuse:
+            rows = names[fuse[0]][0]
+            width = sum(names[n][1] for n in fuse)
+            off = b.numel
+            col = 0
+            for n in fuse:
+                b.entries.append(Entry(path, n, tuple(names[n]), off, col, width, mod.kind))
+                col += names[n][1]
+                done.add(n)
+            b.numel = _align(off + rows * width)
+        for pname, shape in plist:
+            if pname in done:
+                continue
+            b.entries.append(Entry(path, pname, tuple(shape), b.numel, 0, 0, mod.kind))
+            b.numel = _align(b.numel + int(np.prod(shape)))
+    out = [root] + order
+    if rep.entries:
+        out.append(rep)
+    return [b for b in out if b.entries]
+
+
+def _view(buf: torch.Tensor, e: Entry) -> torch.Tensor:
+    if e.ld:
+        rows, cols = e.shape
+        return buf.as_strided((rows, cols), (e.ld, 1), buf.storage_offset() + e.offset + e.col0)
+    n = int(np.prod(e.shape))
+    return buf[e.offset:e.offset + n].view(e.shape)
+
+
+def _tree_set(tree: dict, path: str, name: str, value):
+    from .module import state_segments
+
+    node = tree
+    for seg in state_segments(path) if path else []:
+        node = node.setdefault(seg, {})
+    node[name] = value
+
+
+def _tree_get(tree: dict, path: str, name: str):
+    from .module import state_segments
+
+    node = tree
+    for seg in state_segments(path) if path else []:
+        node = node[seg]
+    return node[name]
+
+
+def _skeleton(module: Module) -> dict:
+    """Empty nested dicts for every module path (so state/grads trees mirror the reference)."""
+    tree: dict = {}
+    for name, c in module.children.items():
+        tree[name] = _skeleton(c)
+    return tree
+
+
+class _Dist:
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.on = dist.is_available() and dist.is_initialized()
+        self.group = group
+        self.world = dist.get_world_size(group) if self.on else 1
+        self.rank = dist.get_rank(group) if self.on else 0
+
+
+class TrainEngine:
+    """Owns device state for one Trainer config and runs training steps on one GPU (rank)."""
+
+    def __init__(self, cfg: ConfigNode, device=None, precision: str | None = None, seed: int = 0,
+                 eps: float = 1e-8, weight_decay: float = 0.0, group=None, init: bool = True):
+        self.cfg = cfg
+        self.module = instantiate(cfg)
+        self.cfg = self.module.config
+        self.precision = precision or model_precision(self.cfg)
+        if self.precision not in ("f32", "bf16"):
+            raise TypeMismatchError(f"precision {self.precision!r} unsupported")
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.work_dtype = torch.bfloat16 if self.precision == "bf16" else torch.float32
+        learner = self.module.children.get("learner")
+        spec = learner.impl if learner is not None else None
+        self.lr = spec.lr if spec else 1e-3
+        self.beta1 = spec.beta1 if spec else 0.9
+        self.beta2 = spec.beta2 if spec else 0.999
+        self.eps, self.weight_decay = eps, weight_decay
+        self.seed = seed
+        self.step_count = 0
+        self.d = _Dist(group)
+        self.buckets = build_layout(self.module)
+        self._alloc()
+        self.options = {"precision": self.precision, "validate_ids": False}
+        if init:
+            self.init_params(root_key(seed))
+
+    # ------------------------------------------------------------------ memory
+    def _alloc(self):
+        N, dev = self.d.world, self.device
+        self.bufs = []
+        for b in self.buckets:
+            if b.replicated:
+                total = b.numel
+                master = torch.zeros(total, device=dev, dtype=torch.float32)
+                rec = dict(total=total, shard=total, master=master, work=master,
+                           grad=torch.zeros(total, device=dev, dtype=torch.float32))
+                rec["grad_shard"] = rec["grad"]
+            else:
+                total = _align(b.numel, ALIGN * N)
+                shard = total // N
+                master = torch.zeros(shard, device=dev, dtype=torch.float32)
+                if N == 1 and self.work_dtype == torch.float32:
+                    work = master
+                else:
+                    work = torch.zeros(total, device=dev, dtype=self.work_dtype)
+                grad = torch.zeros(total, device=dev, dtype=torch.float32)
+                grad_shard = grad if N == 1 else torch.zeros(shard, device=dev, dtype=torch.float32)
+                rec = dict(total=total, shard=shard, master=master, work=work, grad=grad, grad_shard=grad_shard)
+            rec["m"] = torch.zeros(rec["shard"], device=dev, dtype=torch.float32)
+            rec["v"] = torch.zeros(rec["shard"], device=dev, dtype=torch.float32)
+            self.bufs.append(rec)
+        self.state = _skeleton(self.module)
+        self.grads = _skeleton(self.module)
+        for b, rec in zip(self.buckets, self.bufs):
+            for e in b.entries:
+                _tree_set(self.state, e.path, e.name, _view(rec["work"], e))
+                _tree_set(self.grads, e.path, e.name, _view(rec["grad"], e))
+
+    def param_count(self) -> int:
+        return sum(int(np.prod(e.shape)) for b in self.buckets for e in b.entries)
+
+    # -------------------------------------------------------------- parameters
+    def _host_bucket(self, b: Bucket, rec, values) -> None:
+        """values(entry) -> np.ndarray; writes this rank's shard of the bucket's master + work."""
+        host = np.zeros(rec["total"], dtype=np.float32)
+        for e in b.entries:
+            arr = np.asarray(values(e), dtype=np.float64)
+            if tuple(arr.shape) != tuple(e.shape):
+                raise ShapeError(f"{e.path}.{e.name}: shape {arr.shape} != {e.shape}")
+            if e.ld:
+                rows, cols = e.shape
+                blk = host[e.offset:e.offset + rows * e.ld].reshape(rows, e.ld)
+                blk[:, e.col0:e.col0 + cols] = arr
+            else:
+                host[e.offset:e.offset + arr.size] = arr.reshape(-1)
+        r0 = 0 if b.replicated else self.d.rank * rec["shard"]
+        t = torch.from_numpy(host[r0:r0 + rec["shard"]]).to(self.device)
+        rec["master"].copy_(t)
+        if rec["work"] is not rec["master"]:
+            full = torch.from_numpy(host).to(self.device)
+            ops.copy2d(full.view(1, -1), rec["work"].view(1, -1))
+
+    def init_params(self, key) -> None:
+        """Reference-identical init (init_state semantics), generated tensor by tensor."""
+        from .module import param_key  # noqa: F401
+
+        cache: dict = {}
+
+        def values(e: Entry):
+            if e.path not in cache:
+                mod = self.module.child(e.path) if e.path else self.module
+                cache.clear()
+                cache[e.path] = mod.behavior.init_params(mod.config, self._module_key(key, e.path))
+            return cache[e.path][e.name]
+
+        for b, rec in zip(self.buckets, self.bufs):
+            self._host_bucket(b, rec, values)
+        torch.cuda.synchronize(self.device)
+
+    @staticmethod
+    def _module_key(key, path: str):
+        from .module import state_segments
+
+        for seg in state_segments(path) if path else []:
+            key = child_key(key, seg, 0)
+        return key
+
+    def load_state(self, state: dict) -> None:
+        """Loads a reference-layout numpy state tree (e.g. from the reference's init_state)."""
+        for b, rec in zip(self.buckets, self.bufs):
+            self._host_bucket(b, rec, lambda e: _tree_get(state, e.path, e.name))
+        torch.cuda.synchronize(self.device)
+
+    def _gather_full(self, buf: torch.Tensor, rec) -> torch.Tensor:
+        if self.d.world == 1 or buf.numel() == rec["total"]:
+            return buf
+        full = torch.empty(rec["total"], device=self.device, dtype=buf.dtype)
+        self.d.dist.all_gather_into_tensor(full, buf, group=self.d.group)
+        return full
+
+    def _export(self, which: str) -> dict:
+        out: dict = {}
+        for b, rec in zip(self.buckets, self.bufs):
+            src = rec["master"] if which == "master" else rec[which]
+            if which in ("master", "m", "v"):
+                src = self._gather_full(src, rec)
+            host = src.float().cpu().numpy().astype(np.float64)
+            for e in b.entries:
+                if e.ld:
+                    rows, cols = e.shape
+                    arr = host[e.offset:e.offset + rows * e.ld].reshape(rows, e.ld)[:, e.col0:e.col0 + cols].copy()
+                else:
+                    arr = host[e.offset:e.offset + int(np.prod(e.shape))].reshape(e.shape).copy()
+                _tree_set(out, e.path, e.name, arr)
+        return out
+
+    def state_numpy(self) -> dict:
+        return self._export("master")
+
+    def grads_numpy(self) -> dict:
+        """Full (all-reduced) gradients of the last compute_grads call."""
+        if self.d.world > 1:
+            for b, rec in zip(self.buckets, self.bufs):
+                if not b.replicated:
+                    self.d.dist.all_reduce(rec["grad"], op=self.d.dist.ReduceOp.AVG, group=self.d.group)
+        return self._export("grad")
+
+    # -------------------------------------------------------------------- step
+    def upload_tokens(self, tokens) -> torch.Tensor:
+        if isinstance(tokens, torch.Tensor) and tokens.is_cuda:
+            return tokens
+        arr = np.asarray(tokens)
+        if arr.ndim != 2 or arr.shape[1] < 2 or not np.issubdtype(arr.dtype, np.integer):
+            raise ShapeError("trainer expects integer tokens of shape [batch, seq>=2]")
+        vocab = self.cfg.get("model.vocab_size")
+        if arr.size and (arr.min() < 0 or arr.max() >= vocab):
+            raise ShapeError(f"token ids out of range [0, {vocab})")
+        host = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.int64)).pin_memory()
+        return host.to(self.device, non_blocking=True)
+
+    def step_key(self, step: int):
+        return child_key(root_key(self.seed), "step", step)
+
+    def loss(self, tokens, step: int | None = None) -> float:
+        """Forward-only loss (the reference's invoke(module, state, key, batch) result)."""
+        toks = self.upload_tokens(tokens)
+        provider = FSDPProvider(self) if self.d.world > 1 else None
+        if provider:
+            provider.start_step()
+        out, col = invoke(self.module, self.state, self.step_key(self.step_count if step is None else step),
+                          {"tokens": toks}, keep_outputs=False, provider=provider, options=self.options)
+        if self.d.world > 1:
+            t = torch.tensor([out], device=self.device, dtype=torch.float64)
+            self.d.dist.all_reduce(t, op=self.d.dist.ReduceOp.AVG, group=self.d.group)
+            return float(t.item())
+        return out
+
+    def compute_grads(self, tokens):
+        """Forward + backward; gradients land in the (sharded) grad buffers.  Returns (loss, collection)."""
+        toks = self.upload_tokens(tokens)
+        for rec in self.bufs:
+            ops.zero_(rec["grad"])
+        provider = FSDPProvider(self) if self.d.world > 1 else None
+        if provider:
+            provider.start_step()
+        loss, col, _ = value_and_grad(self.module, self.state, self.grads, self.step_key(self.step_count),
+                                      {"tokens": toks}, provider=provider, options=self.options)
+        if provider:
+            provider.finish_backward()
+            self.d.dist.all_reduce(loss, op=self.d.dist.ReduceOp.AVG, group=self.d.group)
+        return loss, col
+
+    def apply_update(self) -> None:
+        self.step_count += 1
+        for b, rec in zip(self.buckets, self.bufs):
+            if b.replicated or self.d.world == 1:
+                wshard = rec["work"]
+            else:
+                wshard = rec["work"][self.d.rank * rec["shard"]:(self.d.rank + 1) * rec["shard"]]
+            bf = wshard if (wshard.dtype == torch.bfloat16) else None
+            ops.adamw(rec["master"], rec["grad_shard"], rec["m"], rec["v"], bf, self.lr, self.beta1, self.beta2,
+                      self.eps, self.weight_decay, self.step_count)
+            if bf is None and wshard.data_ptr() != rec["master"].data_ptr():
+                ops.copy2d(rec["master"].view(1, -1), wshard.view(1, -1))
+
+    def step(self, tokens):
+        loss, col = self.compute_grads(tokens)
+        self.apply_update()
+        return loss, col
+
+
+class FSDPProvider(ParamProvider):
+    """Per-layer all-gather prefetch and reduce-scatter on a side stream (NCCL)."""
+
+    def __init__(self, eng: TrainEngine):
+        self.e = eng
+        self.dist = eng.d.dist
+        self.group = eng.d.group
+        self.compute = torch.cuda.current_stream(eng.device)
+        if not hasattr(eng, "_comm_stream"):
+            eng._comm_stream = torch.cuda.Stream(eng.device)
+        self.comm = eng._comm_stream
+        self.index = {b.name: i for i, b in enumerate(eng.buckets)}
+        self.layer_order = [i for i, b in enumerate(eng.buckets) if b.name != "root" and not b.replicated]
+        self.gathered: dict[int, torch.cuda.Event] = {}
+
+    def _ag(self, i: int) -> None:
+        if i in self.gathered:
+            return
+        rec, b = self.e.bufs[i], self.e.buckets[i]
+        if b.replicated:
+            return
+        ready = torch.cuda.Event()
+        ready.record(self.compute)
+        with torch.cuda.stream(self.comm):
+            self.comm.wait_event(ready)
+            r, s = self.e.d.rank, rec["shard"]
+            self.dist.all_gather_into_tensor(rec["work"], rec["work"][r * s:(r + 1) * s], group=self.group)
+            done = torch.cuda.Event()
+            done.record(self.comm)
+        self.gathered[i] = done
+
+    def _rs(self, i: int) -> None:
+        rec, b = self.e.bufs[i], self.e.buckets[i]
+        ready = torch.cuda.Event()
+        ready.record(self.compute)
+        with torch.cuda.stream(self.comm):
+            self.comm.wait_event(ready)
+            if b.replicated:
+                self.dist.all_reduce(rec["grad"], op=self.dist.ReduceOp.AVG, group=self.group)
+            else:
+                self.dist.reduce_scatter_tensor(rec["grad_shard"], rec["grad"], op=self.dist.ReduceOp.AVG,
+                                                group=self.group)
+
+    def start_step(self) -> None:
+        self._ag(0)
+        self.compute.wait_event(self.gathered[0])
+        if self.layer_order:
+            self._ag(self.layer_order[0])
+
+    def before_forward(self, path: str) -> None:
+        i = self.index.get(path)
+        if i is None:
+            return
+        self._ag(i)
+        self.compute.wait_event(self.gathered[i])
+        pos = self.layer_order.index(i)
+        if pos + 1 < len(self.layer_order):
+            self._ag(self.layer_order[pos + 1])
+
+    def after_backward(self, path: str) -> None:
+        i = self.index.get(path)
+        if i is not None:
+            self._rs(i)
+
+    def finish_backward(self) -> None:
+        for i, b in enumerate(self.e.buckets):
+            if b.name == "root" or b.replicated:
+                self._rs(i)
+        done = torch.cuda.Event()
+        done.record(self.comm)
+        self.compute.wait_event(done)

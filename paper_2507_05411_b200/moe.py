@@ -1,0 +1,194 @@
+"""MoE kind: token-choice top-k experts (reference layers.py:452-533), executed sparsely.
+
+The reference evaluates every expert on every token (dense einsum, layers.py:519-525)
+and then picks; the result only depends on the k selected experts, so the GPU path
+computes exactly those: route (f64 router, stable top-k, renorm) -> stable
+expert-sorted dispatch -> per-expert GEMMs on contiguous row blocks -> slot-order
+combine.  FLOPs match the reference's own accounting, which already counts only the k
+experts (layers.py:494-499).  ``load_balance_loss`` is recorded as a summary and, as in
+the reference, is not part of the loss (layers.py:532 vs 649-651).
+
+Per-expert row counts are read back to the host once per MoE layer invocation to size
+the expert GEMMs (E+1 ints).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib, ops
+from .errors import BadTopKError, ShapeError
+from .module import Behavior, RematTag, add_summary, param, param_grad, param_key, save, saved
+
+
+def _layers():
+    from . import layers
+
+    return layers
+
+
+class MoEBehavior(Behavior):
+    def validate(self, cfg):
+        L = _layers()
+        experts, top_k = cfg.get("num_experts"), cfg.get("top_k")
+        if experts < 1 or not 1 <= top_k <= experts:
+            raise BadTopKError(f"top_k={top_k} must lie in [1, {experts}]")
+        pair = L.activation_pair(cfg.get("activation"))
+        for n in pair if pair else (cfg.get("activation"),):
+            L.check_activation(n)
+
+    def param_shapes(self, cfg):
+        d, h, e = cfg.get("input_dim"), cfg.get("hidden_dim"), cfg.get("num_experts")
+        shapes = {"router": (d, e), "w1": (e, d, h), "w2": (e, h, d)}
+        if _layers().activation_pair(cfg.get("activation")):
+            shapes["w1_gate"] = (e, d, h)
+        return shapes
+
+    def param_specs(self, cfg):
+        spec = tuple(cfg.get("param_partition_spec"))
+        rev = tuple(reversed(spec))
+        specs = {"router": (spec[0], None), "w1": (None,) + spec, "w2": (None,) + rev}
+        if _layers().activation_pair(cfg.get("activation")):
+            specs["w1_gate"] = (None,) + spec
+        return specs
+
+    def init_params(self, cfg, key):
+        L = _layers()
+        d, h, e = cfg.get("input_dim"), cfg.get("hidden_dim"), cfg.get("num_experts")
+        out = {"router": L.fan_in_uniform(param_key(key, "router"), (d, e), d),
+               "w1": L.fan_in_uniform(param_key(key, "w1"), (e, d, h), d),
+               "w2": L.fan_in_uniform(param_key(key, "w2"), (e, h, d), h)}
+        if L.activation_pair(cfg.get("activation")):
+            out["w1_gate"] = L.fan_in_uniform(param_key(key, "w1_gate"), (e, d, h), d)
+        return out
+
+    def own_flops(self, cfg, batch, seq_len):
+        d, h, e, k = cfg.get("input_dim"), cfg.get("hidden_dim"), cfg.get("num_experts"), cfg.get("top_k")
+        rows = batch * seq_len
+        br = 2 if _layers().activation_pair(cfg.get("activation")) else 1
+        return 2 * rows * d * e + k * (br * 2 * rows * d * h + 2 * rows * h * d)
+
+    def remat_tags(self, cfg, batch, seq_len):
+        d, h, e, k = cfg.get("input_dim"), cfg.get("hidden_dim"), cfg.get("num_experts"), cfg.get("top_k")
+        rows = batch * seq_len
+        nb = _layers().DTYPE_BYTES[cfg.get("dtype")]
+        br = 2 if _layers().activation_pair(cfg.get("activation")) else 1
+        return [RematTag("router_logits", rows * e * nb, 2 * rows * d * e),
+                RematTag("expert_hidden", k * br * rows * h * nb, k * br * 2 * rows * d * h),
+                RematTag("expert_output", k * rows * d * nb, k * 2 * rows * h * d)]
+
+    # ------------------------------------------------------------------ execution
+    def forward(self, module, x):
+        L = _layers()
+        cfg = module.config
+        d, h, E, k = cfg.get("input_dim"), cfg.get("hidden_dim"), cfg.get("num_experts"), cfg.get("top_k")
+        B, T = L._checked_3d(x, d, "MoE")
+        adt = L.act_dtype()
+        dev = x.device
+        x2 = ops.cast(ops.rows2d(x), adt)
+        n = x2.shape[0]
+        router = L._f32(param("router"))
+        idx = torch.empty((n, k), device=dev, dtype=torch.int32)
+        w = torch.empty((n, k), device=dev, dtype=torch.float32)
+        probs = torch.empty((n, E), device=dev, dtype=torch.float32)
+        _lib.call("cb_moe_route", n, d, E, k, x2.data_ptr(), ops.ld(x2), ops.dt(x2), router.data_ptr(),
+                  idx.data_ptr(), w.data_ptr(), probs.data_ptr(), ops.stream_ptr())
+        stats = torch.empty((1 + 2 * E,), device=dev, dtype=torch.float64)
+        _lib.call("cb_moe_stats", n, E, k, idx.data_ptr(), probs.data_ptr(), stats.data_ptr(), ops.stream_ptr())
+        add_summary("load_balance_loss", stats[0:1] if L.is_recording() else float(stats[0].item()))
+        # stable expert-sorted dispatch of the n*k assignments
+        ids64 = torch.empty((n * k,), device=dev, dtype=torch.int64)
+        _lib.call("cb_widen_i32", n * k, idx.data_ptr(), ids64.data_ptr(), ops.stream_ptr())
+        offsets, perm = ops.sort_ids(ids64, E)
+        inv = torch.empty((n * k,), device=dev, dtype=torch.int32)
+        _lib.call("cb_invert_perm", n * k, perm.data_ptr(), inv.data_ptr(), ops.stream_ptr())
+        xe = torch.empty((n * k, d), device=dev, dtype=adt)
+        _lib.call("cb_gather_rows", n * k, d, perm.data_ptr(), k, x2.data_ptr(), ops.ld(x2), xe.data_ptr(),
+                  ops.ld(xe), ops.dt(xe), ops.stream_ptr())
+        off = offsets.cpu().numpy().astype(np.int64)  # E+1 ints: sizes the per-expert GEMMs
+        pair = L.activation_pair(cfg.get("activation"))
+        w1, w2 = param("w1"), param("w2")
+        wg = param("w1_gate") if pair else None
+        width = 2 * h if pair else h
+        pre = torch.empty((n * k, width), device=dev, dtype=adt)
+        hid = torch.empty((n * k, h), device=dev, dtype=adt)
+        ye = torch.empty((n * k, d), device=dev, dtype=torch.float32)
+        for e in range(E):
+            r0, r1 = int(off[e]), int(off[e + 1])
+            if r1 == r0:
+                continue
+            xs = xe[r0:r1]
+            ops.gemm(xs, w1[e], pre[r0:r1, :h])
+            if pair:
+                ops.gemm(xs, wg[e], pre[r0:r1, h:])
+        if pair:
+            hid = ops.act_fwd(pre[:, :h], pre[:, h:], pair[0], pair[1])
+        else:
+            hid = ops.act_fwd(pre, None, cfg.get("activation"))
+        for e in range(E):
+            r0, r1 = int(off[e]), int(off[e + 1])
+            if r1 > r0:
+                ops.gemm(hid[r0:r1], w2[e], ye[r0:r1])
+        out = torch.empty((n, d), device=dev, dtype=torch.float32)
+        _lib.call("cb_moe_combine", n, d, k, inv.data_ptr(), w.data_ptr(), ye.data_ptr(), ops.ld(ye), ops.dt(ye),
+                  out.data_ptr(), ops.ld(out), 0, ops.stream_ptr())
+        save(x2=x2, idx=idx, w=w, probs=probs, perm=perm, inv=inv, off=off, xe=xe, pre=pre, hid=hid, ye=ye,
+             geom=(B, T, d, h, E, k))
+        return out.view(B, T, d)
+
+    def backward(self, module, dout):
+        L = _layers()
+        cfg = module.config
+        s = saved()
+        B, T, d, h, E, k = s["geom"]
+        adt = L.act_dtype()
+        dev = dout.device
+        n = B * T
+        g = ops.rows2d(dout).contiguous() if dout.dtype == torch.float32 else ops.cast(ops.rows2d(dout), torch.float32)
+        dye = torch.empty((n * k, d), device=dev, dtype=adt)
+        dw = torch.empty((n, k), device=dev, dtype=torch.float32)
+        _lib.call("cb_moe_combine_bwd", n, d, k, s["inv"].data_ptr(), s["w"].data_ptr(), s["ye"].data_ptr(),
+                  ops.ld(s["ye"]), g.data_ptr(), ops.ld(g), dye.data_ptr(), ops.ld(dye), ops.dt(dye), dw.data_ptr(),
+                  ops.stream_ptr())
+        pair = L.activation_pair(cfg.get("activation"))
+        w1, w2 = param("w1"), param("w2")
+        gw1, gw2 = param_grad("w1"), param_grad("w2")
+        wg = param("w1_gate") if pair else None
+        gwg = param_grad("w1_gate") if pair else None
+        off, pre, hid, xe = s["off"], s["pre"], s["hid"], s["xe"]
+        dhid = torch.empty_like(hid)
+        for e in range(E):
+            r0, r1 = int(off[e]), int(off[e + 1])
+            if r1 == r0:
+                continue
+            ops.gemm(hid[r0:r1], dye[r0:r1], gw2[e], trans_a=True, accumulate=True)
+            ops.gemm(dye[r0:r1], w2[e], dhid[r0:r1], trans_b=True)
+        dpre = torch.empty_like(pre)
+        if pair:
+            ops.act_bwd(pre[:, :h], pre[:, h:], dhid, dpre[:, :h], dpre[:, h:], pair[0], pair[1])
+        else:
+            ops.act_bwd(pre, None, dhid, dpre, None, cfg.get("activation"))
+        dxe = torch.empty((n * k, d), device=dev, dtype=torch.float32)
+        for e in range(E):
+            r0, r1 = int(off[e]), int(off[e + 1])
+            if r1 == r0:
+                continue
+            xs = xe[r0:r1]
+            ops.gemm(xs, dpre[r0:r1, :h], gw1[e], trans_a=True, accumulate=True)
+            ops.gemm(dpre[r0:r1, :h], w1[e], dxe[r0:r1], trans_b=True)
+            if pair:
+                ops.gemm(xs, dpre[r0:r1, h:], gwg[e], trans_a=True, accumulate=True)
+                ops.gemm(dpre[r0:r1, h:], wg[e], dxe[r0:r1], trans_b=True, accumulate=True)
+        dx = torch.empty((n, d), device=dev, dtype=torch.float32)
+        _lib.call("cb_moe_combine", n, d, k, s["inv"].data_ptr(), None, dxe.data_ptr(), ops.ld(dxe), ops.dt(dxe),
+                  dx.data_ptr(), ops.ld(dx), 0, ops.stream_ptr())
+        # router: w = renorm(topk(softmax(x @ router)))
+        dlog = torch.empty((n, E), device=dev, dtype=torch.float32)
+        _lib.call("cb_moe_router_bwd", n, E, k, s["probs"].data_ptr(), s["idx"].data_ptr(), s["w"].data_ptr(),
+                  dw.data_ptr(), dlog.data_ptr(), ops.stream_ptr())
+        x32 = ops.cast(s["x2"], torch.float32)
+        router = L._f32(param("router"))
+        ops.gemm(x32, dlog, param_grad("router"), trans_a=True, accumulate=True)
+        ops.gemm(dlog, router, dx, trans_b=True, accumulate=True)
+        return dx.view(B, T, d)

@@ -2,10 +2,13 @@
 
 PyTorch is used only for device memory and streams: every arithmetic operation below
 is one call into ``libcomposer_b200.so``.  Shapes/dtypes are checked here, before the
-launch, and raise the reference's error classes.
+launch, and raise the reference's error classes.  All functions run on the current
+torch stream.
 """
 
 from __future__ import annotations
+
+import ctypes
 
 import torch
 
@@ -13,6 +16,7 @@ from . import _lib
 from .errors import ShapeError, TypeMismatchError
 
 _DT = {torch.float32: _lib.DT_F32, torch.bfloat16: _lib.DT_BF16}
+ACT_IDS = {"linear": 0, "relu": 1, "silu": 2, "sigmoid": 3, "tanh": 4}
 
 
 def dt(t: torch.Tensor) -> int:
@@ -30,12 +34,60 @@ def _ptr(t):
     return None if t is None else t.data_ptr()
 
 
-def _rowmajor_ld(t: torch.Tensor, what: str) -> int:
-    if t.dim() != 2 or t.stride(1) != 1:
-        raise ShapeError(f"{what} must be a 2-D row-major view (stride(1) == 1)")
+def ld(t: torch.Tensor, what: str = "tensor") -> int:
+    """Row stride of a 2-D row-major view (stride(1) == 1)."""
+    if t.dim() != 2 or (t.stride(1) != 1 and t.shape[1] > 1):
+        raise ShapeError(f"{what} must be a 2-D row-major view")
     return t.stride(0)
 
 
+def rows2d(t: torch.Tensor) -> torch.Tensor:
+    """[..., d] -> [rows, d] view (no copy; raises if not viewable)."""
+    return t.reshape(-1, t.shape[-1]) if t.dim() != 2 else t
+
+
+# ----------------------------------------------------------------- launch profiler
+class KernelProfiler:
+    """Records CUDA events around selected launches on the launching (current) stream.
+
+    Used by bench.py to measure the dominant kernels' achieved FLOP/s live inside the
+    timed step; records are (kind, algorithmic_flops, start_event, end_event).
+    """
+
+    def __init__(self):
+        self.records: list = []
+
+    def summary(self) -> dict:
+        torch.cuda.synchronize()
+        out: dict = {}
+        for kind, flops, s, e in self.records:
+            d = out.setdefault(kind, {"launches": 0, "flops": 0, "ms": 0.0})
+            d["launches"] += 1
+            d["flops"] += flops
+            d["ms"] += s.elapsed_time(e)
+        return out
+
+
+_PROFILER: KernelProfiler | None = None
+
+
+def set_profiler(p: KernelProfiler | None) -> None:
+    global _PROFILER
+    _PROFILER = p
+
+
+def _profiled(kind: str, flops: int, fn, *args):
+    if _PROFILER is None:
+        return fn(*args)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    out = fn(*args)
+    e.record()
+    _PROFILER.records.append((kind, flops, s, e))
+    return out
+
+
+# ----------------------------------------------------------------------------- GEMM
 def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, trans_a: bool = False, trans_b: bool = False,
          alpha: float = 1.0, accumulate: bool = False, residual: torch.Tensor | None = None) -> torch.Tensor:
     """out = alpha * op(a) @ op(b) (+ out) (+ residual); op(x) = x.T when trans_x."""
@@ -53,14 +105,162 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, trans_a: bool = Fa
     if residual is not None:
         if tuple(residual.shape) != (M, N):
             raise ShapeError("gemm: residual shape mismatch")
-        ldr = _rowmajor_ld(residual, "residual")
-    _lib.call(
-        "cb_gemm", M, N, K, dt(a), a.data_ptr(), _rowmajor_ld(a, "A"), int(trans_a), b.data_ptr(),
-        _rowmajor_ld(b, "B"), int(trans_b), out.data_ptr(), _rowmajor_ld(out, "out"), dt(out), _ptr(residual), ldr,
-        dt(residual) if residual is not None else 0, float(alpha), int(accumulate), stream_ptr(),
-    )
+        ldr = ld(residual, "residual")
+    kind = "gemm_bf16" if a.dtype == torch.bfloat16 else "gemm_f32"
+    _profiled(kind, 2 * M * N * K, _lib.call, "cb_gemm", M, N, K, dt(a), a.data_ptr(), ld(a, "A"), int(trans_a),
+              b.data_ptr(), ld(b, "B"), int(trans_b), out.data_ptr(), ld(out, "out"), dt(out), _ptr(residual), ldr,
+              dt(residual) if residual is not None else 0, float(alpha), int(accumulate), stream_ptr())
     return out
 
 
 def set_gemm_path(path: int) -> None:
     _lib.call("cb_gemm_set_path", int(path))
+
+
+def set_attention_path(path: int) -> None:
+    _lib.call("cb_attention_set_path", int(path))
+
+
+# -------------------------------------------------------------------------- RMSNorm
+def rmsnorm_fwd(x: torch.Tensor, scale: torch.Tensor, eps: float, out_dtype: torch.dtype):
+    x2 = rows2d(x)
+    rows, dim = x2.shape
+    y = torch.empty((rows, dim), device=x.device, dtype=out_dtype)
+    rstd = torch.empty((rows,), device=x.device, dtype=torch.float32)
+    _lib.call("cb_rmsnorm_fwd", rows, dim, x2.data_ptr(), ld(x2), dt(x2), scale.data_ptr(), float(eps), y.data_ptr(),
+              ld(y), dt(y), rstd.data_ptr(), stream_ptr())
+    return y.view(*x.shape[:-1], dim), rstd
+
+
+def rmsnorm_bwd(x, scale, rstd, dy, dres=None, dscale=None):
+    x2, g2 = rows2d(x), rows2d(dy)
+    rows, dim = x2.shape
+    dx = torch.empty((rows, dim), device=x.device, dtype=torch.float32)
+    ws = None
+    if dscale is not None:
+        nbytes = ctypes.c_int64(0)
+        _lib.call("cb_rmsnorm_bwd_workspace", rows, dim, ctypes.byref(nbytes))
+        ws = torch.empty((max(1, nbytes.value // 4),), device=x.device, dtype=torch.float32)
+    r2 = rows2d(dres) if dres is not None else None
+    _lib.call("cb_rmsnorm_bwd", rows, dim, x2.data_ptr(), ld(x2), dt(x2), scale.data_ptr(), rstd.data_ptr(),
+              g2.data_ptr(), ld(g2), dt(g2), _ptr(r2), ld(r2) if r2 is not None else 0, dx.data_ptr(), ld(dx),
+              _ptr(dscale), _ptr(ws), stream_ptr())
+    return dx.view(*x.shape[:-1], dim)
+
+
+# ------------------------------------------------------------------------ embedding
+def embedding_fwd(ids: torch.Tensor, table: torch.Tensor, out_dtype: torch.dtype):
+    flat = ids.reshape(-1)
+    n = flat.numel()
+    dim = table.shape[1]
+    out = torch.empty((n, dim), device=table.device, dtype=out_dtype)
+    _lib.call("cb_embedding_fwd", n, dim, flat.data_ptr(), table.data_ptr(), ld(table), dt(table), out.data_ptr(),
+              ld(out), dt(out), stream_ptr())
+    return out.view(*ids.shape, dim)
+
+
+def sort_ids(ids: torch.Tensor, vocab: int):
+    flat = ids.reshape(-1)
+    n = flat.numel()
+    offsets = torch.empty((vocab + 1,), device=ids.device, dtype=torch.int32)
+    cursor = torch.empty((vocab,), device=ids.device, dtype=torch.int32)
+    perm = torch.empty((max(n, 1),), device=ids.device, dtype=torch.int32)
+    _lib.call("cb_sort_ids", n, vocab, flat.data_ptr(), offsets.data_ptr(), cursor.data_ptr(), perm.data_ptr(),
+              stream_ptr())
+    return offsets, perm
+
+
+def embedding_bwd(offsets, perm, dout: torch.Tensor, dtable: torch.Tensor):
+    g2 = rows2d(dout)
+    vocab, dim = dtable.shape
+    _lib.call("cb_embedding_bwd", vocab, dim, offsets.data_ptr(), perm.data_ptr(), g2.data_ptr(), ld(g2), dt(g2),
+              dtable.data_ptr(), ld(dtable), stream_ptr())
+
+
+# ----------------------------------------------------------------------------- RoPE
+def rope_(x2d: torch.Tensor, seq_len: int, heads: int, head_dim: int, cos_t, sin_t, inverse: bool = False):
+    rows = x2d.shape[0]
+    _lib.call("cb_rope", rows, seq_len, heads, head_dim, x2d.data_ptr(), ld(x2d), dt(x2d), cos_t.data_ptr(),
+              sin_t.data_ptr(), int(inverse), stream_ptr())
+
+
+# ---------------------------------------------------------------------- activations
+def act_fwd(a: torch.Tensor, g: torch.Tensor | None, act0: str, act1: str = "linear"):
+    rows, cols = a.shape
+    out = torch.empty((rows, cols), device=a.device, dtype=a.dtype)
+    _lib.call("cb_act_fwd", rows, cols, ACT_IDS[act0], ACT_IDS[act1], a.data_ptr(), ld(a), _ptr(g),
+              ld(g) if g is not None else 0, out.data_ptr(), ld(out), dt(a), stream_ptr())
+    return out
+
+
+def act_bwd(a, g, dout, da, dg, act0: str, act1: str = "linear"):
+    rows, cols = a.shape
+    _lib.call("cb_act_bwd", rows, cols, ACT_IDS[act0], ACT_IDS[act1], a.data_ptr(), ld(a), _ptr(g),
+              ld(g) if g is not None else 0, dout.data_ptr(), ld(dout), da.data_ptr(), ld(da), _ptr(dg),
+              ld(dg) if dg is not None else 0, dt(a), stream_ptr())
+
+
+def copy2d(src: torch.Tensor, dst: torch.Tensor, alpha: float = 1.0, accumulate: bool = False):
+    s2, d2 = rows2d(src), rows2d(dst)
+    if s2.shape != d2.shape:
+        raise ShapeError("copy2d: shape mismatch")
+    _lib.call("cb_copy2d", s2.shape[0], s2.shape[1], s2.data_ptr(), ld(s2), dt(s2), d2.data_ptr(), ld(d2), dt(d2),
+              float(alpha), int(accumulate), stream_ptr())
+    return dst
+
+
+def cast(src: torch.Tensor, dtype: torch.dtype) -> torch.Tensor:
+    if src.dtype == dtype:
+        return src
+    out = torch.empty(src.shape, device=src.device, dtype=dtype)
+    return copy2d(src, out)
+
+
+def add_(dst: torch.Tensor, src: torch.Tensor, alpha: float = 1.0):
+    return copy2d(src, dst, alpha=alpha, accumulate=True)
+
+
+def zero_(t: torch.Tensor):
+    if not t.is_contiguous():
+        raise ShapeError("zero_: tensor must be contiguous")
+    _lib.call("cb_memset_zero", t.data_ptr(), t.numel() * t.element_size(), stream_ptr())
+    return t
+
+
+# ------------------------------------------------------------------------ attention
+def attention_fwd(q, k, v, B, T, H, KVH, hd, scale):
+    o = torch.empty((B * T, H * hd), device=q.device, dtype=q.dtype)
+    lse = torch.empty((B, H, T), device=q.device, dtype=torch.float32)
+    _profiled("attn_fwd", 4 * B * T * T * H * hd, _lib.call, "cb_attention_fwd", B, T, H, KVH, hd, dt(q),
+              q.data_ptr(), ld(q), k.data_ptr(), ld(k), v.data_ptr(), ld(v), o.data_ptr(), ld(o), lse.data_ptr(),
+              float(scale), stream_ptr())
+    return o, lse
+
+
+def attention_bwd(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, scale):
+    delta = torch.empty((B, H, T), device=q.device, dtype=torch.float32)
+    # algorithmic FLOPs: 2x forward (dP, dV, dQ, dK), the reference's backward_multiplier (mesh.py:644)
+    _profiled("attn_bwd", 8 * B * T * T * H * hd, _lib.call, "cb_attention_bwd", B, T, H, KVH, hd, dt(q),
+              q.data_ptr(), ld(q), k.data_ptr(), ld(k), v.data_ptr(), ld(v), o.data_ptr(), ld(o), lse.data_ptr(),
+              do.data_ptr(), ld(do), delta.data_ptr(), dq.data_ptr(), ld(dq), dk.data_ptr(), ld(dk), dv.data_ptr(),
+              ld(dv), float(scale), stream_ptr())
+
+
+# -------------------------------------------------------------------- cross-entropy
+def xent(logits2d: torch.Tensor, tokens: torch.Tensor, dlogits: torch.Tensor | None, grad_scale: float):
+    B, T = tokens.shape
+    V = logits2d.shape[1]
+    row_loss = torch.empty((B * T,), device=logits2d.device, dtype=torch.float32)
+    loss = torch.empty((1,), device=logits2d.device, dtype=torch.float64)
+    _lib.call("cb_xent_fwd_bwd", B, T, V, logits2d.data_ptr(), ld(logits2d), dt(logits2d), tokens.data_ptr(),
+              row_loss.data_ptr(), _ptr(dlogits), ld(dlogits) if dlogits is not None else 0,
+              dt(dlogits) if dlogits is not None else 0, float(grad_scale), loss.data_ptr(), None, stream_ptr())
+    return loss
+
+
+# ---------------------------------------------------------------------------- AdamW
+def adamw(param, grad, m, v, param_bf16, lr, beta1, beta2, eps, weight_decay, step, grad_scale=1.0):
+    n = param.numel()
+    _lib.call("cb_adamw", n, param.data_ptr(), grad.data_ptr(), m.data_ptr(), v.data_ptr(), _ptr(param_bf16),
+              float(lr), float(beta1), float(beta2), float(eps), float(weight_decay), int(step), float(grad_scale),
+              stream_ptr())
