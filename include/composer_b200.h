@@ -63,7 +63,8 @@ CB_API int cb_rmsnorm_fwd(int rows, int dim, const void* x, int64_t ldx, int x_d
 CB_API int cb_rmsnorm_bwd_workspace(int rows, int dim, int64_t* bytes);
 CB_API int cb_rmsnorm_bwd(int rows, int dim, const void* x, int64_t ldx, int x_dtype, const float* scale,
                           const float* rstd, const void* dy, int64_t lddy, int dy_dtype, const float* dres,
-                          int64_t lddres, float* dx, int64_t lddx, float* dscale, float* workspace, void* stream);
+                          int64_t lddres, float* dx, int64_t lddx, void* dx_bf16, int64_t lddxb, float* dscale,
+                          float* workspace, void* stream);
 /* out[d] (+)= sum_p partial[p][d] in fixed order (deterministic). */
 CB_API int cb_col_reduce(int nparts, int dim, const float* partial, float* out, int accumulate, void* stream);
 
@@ -116,6 +117,8 @@ CB_API int cb_attention_bwd(int batch, int seq_len, int heads, int kv_heads, int
                             int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv, float scale, void* stream);
 /* 0 = automatic (tensor-core flash kernels when eligible), 1 = force SIMT (tests). */
 CB_API int cb_attention_set_path(int path);
+/* 1 (default) = use the tcgen05/TMEM forward for head_dim 128; 0 = warp-MMA flash kernel (tests). */
+CB_API int cb_attention_set_tc(int enable);
 
 /* ---------------------------------------------------------------------------------
  * Next-token cross-entropy (TrainerBehavior.forward, layers.py:638-651) fused with its

@@ -35,7 +35,7 @@ SIGNATURES: dict[str, list] = {
     "cb_gemm": [_I, _I, _I, _I, _P, _L, _I, _P, _L, _I, _P, _L, _I, _P, _L, _I, _F, _I, _P],
     "cb_rmsnorm_fwd": [_I, _I, _P, _L, _I, _P, _F, _P, _L, _I, _P, _P],
     "cb_rmsnorm_bwd_workspace": [_I, _I, ctypes.POINTER(ctypes.c_int64)],
-    "cb_rmsnorm_bwd": [_I, _I, _P, _L, _I, _P, _P, _P, _L, _I, _P, _L, _P, _L, _P, _P, _P],
+    "cb_rmsnorm_bwd": [_I, _I, _P, _L, _I, _P, _P, _P, _L, _I, _P, _L, _P, _L, _P, _L, _P, _P, _P],
     "cb_col_reduce": [_I, _I, _P, _P, _I, _P],
     "cb_embedding_fwd": [_L, _I, _P, _P, _L, _I, _P, _L, _I, _P],
     "cb_sort_ids": [_I, _I, _P, _P, _P, _P, _P],
@@ -49,6 +49,7 @@ SIGNATURES: dict[str, list] = {
     "cb_attention_bwd": [_I, _I, _I, _I, _I, _I, _P, _L, _P, _L, _P, _L, _P, _L, _P, _P, _L, _P, _P, _L, _P, _L,
                          _P, _L, _F, _P],
     "cb_attention_set_path": [_I],
+    "cb_attention_set_tc": [_I],
     "cb_xent_fwd_bwd": [_I, _I, _I, _P, _L, _I, _P, _P, _P, _L, _I, _F, _P, _P, _P],
     "cb_adamw": [_L, _P, _P, _P, _P, _P, _F, _F, _F, _F, _F, _I, _F, _P],
     "cb_moe_route": [_L, _I, _I, _I, _P, _L, _I, _P, _P, _P, _P, _P],

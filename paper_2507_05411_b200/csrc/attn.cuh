@@ -16,6 +16,11 @@ int attn_delta(const AttnGeom& g, int dtype, const void* o, const void* dout, in
 int attn_bwd_simt(const AttnGeom& g, int dtype, const void* q, const void* k, const void* v, const void* dout,
                   int64_t lddo, const float* lse, const float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk,
                   void* dv, int64_t lddv, cudaStream_t st);
+bool attn_tc_supported(const AttnGeom& g, int dtype, const void* q, const void* k, const void* v);
+int attn_fwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, void* o, float* lse, cudaStream_t st);
+int attn_bwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, const void* dout, int64_t lddo,
+                const float* lse, const float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
+                int64_t lddv, cudaStream_t st);
 bool attn_fa_supported(const AttnGeom& g, int dtype, const void* q, const void* k, const void* v);
 int attn_fwd_fa(const AttnGeom& g, const void* q, const void* k, const void* v, void* o, float* lse, cudaStream_t st);
 int attn_bwd_fa(const AttnGeom& g, const void* q, const void* k, const void* v, const void* dout, int64_t lddo,

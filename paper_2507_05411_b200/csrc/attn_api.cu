@@ -21,6 +21,7 @@ extern "C" int cb_attention_fwd(int batch, int seq_len, int heads, int kv_heads,
   AttnGeom g{batch, seq_len, heads, kv_heads, head_dim, ldq, ldk, ldv, ldo, scale};
   if (int s = check_geom(g)) return s;
   cudaStream_t st = (cudaStream_t)stream;
+  if (g_attn_path == 0 && attn_tc_supported(g, dtype, q, k, v)) return attn_fwd_tc(g, q, k, v, o, lse, st);
   if (g_attn_path == 0 && attn_fa_supported(g, dtype, q, k, v)) return attn_fwd_fa(g, q, k, v, o, lse, st);
   return attn_fwd_simt(g, dtype, q, k, v, o, lse, st);
 }
@@ -34,6 +35,8 @@ extern "C" int cb_attention_bwd(int batch, int seq_len, int heads, int kv_heads,
   if (int s = check_geom(g)) return s;
   cudaStream_t st = (cudaStream_t)stream;
   if (int s = attn_delta(g, dtype, o, dout, lddo, delta, st)) return s;
+  if (g_attn_path == 0 && attn_tc_supported(g, dtype, q, k, v) && !((lddo | lddq | lddk | lddv) & 7))
+    return attn_bwd_tc(g, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st);
   if (g_attn_path == 0 && attn_fa_supported(g, dtype, q, k, v))
     return attn_bwd_fa(g, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st);
   return attn_bwd_simt(g, dtype, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st);

@@ -1,0 +1,290 @@
+// tcgen05 flash attention forward (bf16, head_dim 128), unmasked, GQA-aware.
+//
+// Reference op: AttentionBehavior.forward (reference layers.py:331-348): softmax over
+// all keys (no causal mask) of q k^T / sqrt(hd), then @ v.
+//
+// One CTA per (128-query tile, head, batch); 256 threads in four roles:
+//   warp 0      TMA producer: Q once, then K_j / V_j tiles into a 2-stage ring
+//   warp 1      MMA issuer (one thread): S_j = Q K_j^T into a double-buffered TMEM
+//               S tile, then O += P_j V_j with P read straight from TMEM (A operand
+//               in tensor memory) — S_{j+1} is issued before waiting for P_j so the
+//               tensor core computes the next scores while softmax runs
+//   warp 2      TMEM allocator (512 columns: S0 | S1 | O)
+//   warps 4-7   softmax: one thread owns one query row of S in TMEM (no shuffles),
+//               exp2-domain online softmax with lazy O rescaling (only when the row max
+//               grows by more than 2^8), P packed to bf16 pairs and stored back over S;
+//               then the epilogue (O / l, natural-log LSE).
+// K/V tiles stream through TMA with 128B swizzle; Q and K are K-major UMMA operands,
+// V is an MN-major operand (keys x hd, hd contiguous) — no transposes anywhere.
+#include "attn.cuh"
+#include "composer_b200.h"
+
+namespace cb {
+namespace tca {
+
+constexpr int HD = 128;
+constexpr int BM = 128, BN = 128;
+constexpr int kThreads = 256;
+constexpr int kTileBytes = 128 * 64 * 2;       // one [128 rows][64 cols] bf16 TMA box
+constexpr int kQBytes = 2 * kTileBytes;        // Q: two 64-column K-atoms
+constexpr int kStageBytes = 4 * kTileBytes;    // K (2 atoms) + V (2 MN-blocks)
+constexpr int kStages = 2;
+constexpr int kSmem = kQBytes + kStages * kStageBytes + 1024 + 256;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO = 256;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only if max grows by > 2^8
+
+struct Params {
+  int T, H, KVH, B;
+  float scale;
+  __nv_bfloat16* o;
+  int64_t ldo;
+  float* lse;
+};
+
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    fwd_tc_k(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+             const __grid_constant__ CUtensorMap tmV, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = smem + kQBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kQBytes + kStages * kStageBytes);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = bars + 3;
+  uint64_t* s_full = bars + 5;
+  uint64_t* p_ready = bars + 7;
+  uint64_t* o_done = bars + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int kvh = h / (p.H / p.KVH);
+  const int q0 = qt * BM;
+  const int nblk = (p.T + BN - 1) / BN;
+  const int row0 = b * p.T;  // first token row of this sequence
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_ready[s], 4);
+    }
+    mbar_init(o_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, kQBytes);
+      tma_load_2d(sQ, &tmQ, q_full, h * HD, row0 + q0);
+      tma_load_2d(sQ + kTileBytes, &tmQ, q_full, h * HD + 64, row0 + q0);
+      for (int j = 0; j < nblk; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[st], kStageBytes);
+        uint8_t* base = sKV + st * kStageBytes;
+        const int kr = row0 + j * BN;
+        tma_load_2d(base, &tmK, &kv_full[st], kvh * HD, kr);
+        tma_load_2d(base + kTileBytes, &tmK, &kv_full[st], kvh * HD + 64, kr);
+        tma_load_2d(base + 2 * kTileBytes, &tmV, &kv_full[st], kvh * HD, kr);
+        tma_load_2d(base + 3 * kTileBytes, &tmV, &kv_full[st], kvh * HD + 64, kr);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc_s = idesc_bf16_f32(BM, BN, 0, 0);
+      const uint32_t idesc_o = idesc_bf16_f32(BM, HD, 0, 1);
+      const uint32_t q_addr = smem_u32(sQ);
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        const uint32_t k_addr = smem_u32(sKV + st * kStageBytes);
+        const uint32_t d = tmem + (st ? kColS1 : kColS0);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * kTileBytes + (kk & 3) * 32;
+          umma_f16_ss(d, sw128_desc(q_addr + off, 16, 1024), sw128_desc(k_addr + off, 16, 1024), idesc_s, kk > 0);
+        }
+        umma_commit(&s_full[st]);
+      };
+      mbar_wait(q_full, 0);
+      mbar_wait(&kv_full[0], 0);
+      tc_fence_after();
+      issue_s(0);
+      for (int j = 0; j < nblk; ++j) {
+        const int st = j & 1;
+        if (j + 1 < nblk) {
+          mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+          tc_fence_after();
+          issue_s(j + 1);
+        }
+        mbar_wait(&p_ready[st], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(sKV + st * kStageBytes + 2 * kTileBytes);
+        const uint32_t pcol = tmem + (st ? kColS1 : kColS0);
+#pragma unroll
+        for (int k = 0; k < BN / 16; ++k)
+          umma_f16_ts(tmem + kColO, pcol + k * 8, sw128_desc(v_addr + k * 2048, 16384, 1024), idesc_o, (j | k) != 0);
+        umma_commit(o_done);
+        umma_commit(&kv_empty[st]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;  // TMEM lane == query row inside the tile
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const float c = p.scale * kLog2e;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < nblk; ++j) {
+      const int st = j & 1;
+      const uint32_t scol = tmem + lane_off + (st ? kColS1 : kColS0);
+      mbar_wait(&s_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t v[4][32];
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) tmem_ld32(scol + cc * 32, v[cc]);
+      tmem_ld_wait();
+      const int kbase = j * BN;
+      const int valid = min(BN, p.T - kbase);
+      float mx = -INFINITY;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          float s = __uint_as_float(v[cc][i]) * c;
+          if (cc * 32 + i >= valid) s = -INFINITY;
+          v[cc][i] = __float_as_uint(s);
+          mx = fmaxf(mx, s);
+        }
+      const bool need = mx > m_used + kRescaleThreshold;
+      const float m_new = need ? mx : m_used;
+      if (__any_sync(0xffffffffu, need)) {
+        const float corr = need ? exp2f(m_used - m_new) : 1.f;
+        if (j > 0) {
+          mbar_wait(o_done, (j - 1) & 1);  // PV_{j-1} has finished writing O
+          tc_fence_after();
+#pragma unroll 1
+          for (int cc = 0; cc < HD / 32; ++cc) {
+            uint32_t o[32];
+            tmem_ld32(tmem + lane_off + kColO + cc * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
+            tmem_st32(tmem + lane_off + kColO + cc * 32, o);
+          }
+          tmem_st_wait();
+        }
+        l *= corr;
+        m_used = m_new;
+      }
+      float rs = 0.f;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        uint32_t pk[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int cc = half * 2 + (i >> 4);
+          const int e = (i & 15) * 2;
+          const float p0 = exp2f(__uint_as_float(v[cc][e]) - m_used);
+          const float p1 = exp2f(__uint_as_float(v[cc][e + 1]) - m_used);
+          rs += p0 + p1;
+          pk[i] = pack2(p0, p1);
+        }
+        tmem_st32(scol + half * 32, pk);
+      }
+      l += rs;
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_ready[st]);
+    }
+    // epilogue
+    mbar_wait(o_done, (nblk - 1) & 1);
+    tc_fence_after();
+    const int qrow = q0 + row;
+    const float inv = 1.f / l;
+    __nv_bfloat16* orow = p.o + ((int64_t)row0 + qrow) * p.ldo + (int64_t)h * HD;
+#pragma unroll 1
+    for (int cc = 0; cc < HD / 32; ++cc) {
+      uint32_t o[32];
+      tmem_ld32(tmem + lane_off + kColO + cc * 32, o);
+      tmem_ld_wait();
+      if (qrow < p.T) {
+        uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          uint4 pkt;
+          pkt.x = pack2(__uint_as_float(o[w * 8 + 0]) * inv, __uint_as_float(o[w * 8 + 1]) * inv);
+          pkt.y = pack2(__uint_as_float(o[w * 8 + 2]) * inv, __uint_as_float(o[w * 8 + 3]) * inv);
+          pkt.z = pack2(__uint_as_float(o[w * 8 + 4]) * inv, __uint_as_float(o[w * 8 + 5]) * inv);
+          pkt.w = pack2(__uint_as_float(o[w * 8 + 6]) * inv, __uint_as_float(o[w * 8 + 7]) * inv);
+          dst[w] = pkt;
+        }
+      }
+    }
+    if (qrow < p.T) p.lse[((int64_t)b * p.H + h) * p.T + qrow] = (m_used + log2f(l)) * kLn2;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
+}  // namespace tca
+
+static int g_attn_tc = 1;
+
+bool attn_tc_supported(const AttnGeom& g, int dtype, const void* q, const void* k, const void* v) {
+  if (!g_attn_tc || dtype != CB_DT_BF16 || g.hd != 128) return false;
+  if ((g.ldq | g.ldk | g.ldv | g.ldo) & 7) return false;
+  return ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
+}
+
+int attn_fwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, void* o, float* lse,
+                cudaStream_t st) {
+  using namespace tca;
+  CUtensorMap mq, mk, mv;
+  const uint64_t rows = (uint64_t)g.B * g.T;
+  int s;
+  if ((s = make_tmap_2d_bf16(&mq, q, rows, (uint64_t)g.H * HD, g.ldq, 128, 64))) return s;
+  if ((s = make_tmap_2d_bf16(&mk, k, rows, (uint64_t)g.KVH * HD, g.ldk, 128, 64))) return s;
+  if ((s = make_tmap_2d_bf16(&mv, v, rows, (uint64_t)g.KVH * HD, g.ldv, 128, 64))) return s;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fwd_tc_k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    attr = true;
+  }
+  Params p{g.T, g.H, g.KVH, g.B, g.scale, (__nv_bfloat16*)o, g.ldo, lse};
+  dim3 grid((g.T + BM - 1) / BM, g.H, g.B);
+  fwd_tc_k<<<grid, kThreads, kSmem, st>>>(mq, mk, mv, p);
+  return check_launch("flash_fwd_tc");
+}
+
+}  // namespace cb
+
+extern "C" int cb_attention_set_tc(int enable) {
+  cb::g_attn_tc = enable ? 1 : 0;
+  return CB_OK;
+}

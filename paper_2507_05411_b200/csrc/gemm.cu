@@ -214,7 +214,62 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool full_chunk = col0 + 32 <= e.N;
         const bool fast = full_chunk && !e.accumulate && !e.R && e.alpha == 1.f && !e.d_f32 && ((e.ldd & 7) == 0) &&
                           ((reinterpret_cast<uintptr_t>(e.D) & 15) == 0);
-        if (fast) {
+        const bool vec = full_chunk && ((e.ldd & 7) == 0) && ((reinterpret_cast<uintptr_t>(e.D) & 31) == 0) &&
+                         (!e.R || (((e.ldr & 7) == 0) && ((reinterpret_cast<uintptr_t>(e.R) & 31) == 0)));
+        if (!fast && vec) {
+          // general epilogue, 8 columns (one 16/32-byte vector) at a time
+#pragma unroll
+          for (int g8 = 0; g8 < 4; ++g8) {
+            float o[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o[i] = __uint_as_float(v[g8 * 8 + i]) * e.alpha;
+            const int64_t di = (int64_t)row * e.ldd + col0 + g8 * 8;
+            if (e.accumulate) {
+              if (e.d_f32) {
+                const float4* s = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.D) + di);
+                const float4 a = s[0], b = s[1];
+                o[0] += a.x; o[1] += a.y; o[2] += a.z; o[3] += a.w; o[4] += b.x; o[5] += b.y; o[6] += b.z; o[7] += b.w;
+              } else {
+                const uint4 t = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(e.D) + di);
+                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&t);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const float2 f = __bfloat1622float2(h2[i]);
+                  o[2 * i] += f.x;
+                  o[2 * i + 1] += f.y;
+                }
+              }
+            }
+            if (e.R) {
+              const int64_t ri = (int64_t)row * e.ldr + col0 + g8 * 8;
+              if (e.r_f32) {
+                const float4* s = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.R) + ri);
+                const float4 a = s[0], b = s[1];
+                o[0] += a.x; o[1] += a.y; o[2] += a.z; o[3] += a.w; o[4] += b.x; o[5] += b.y; o[6] += b.z; o[7] += b.w;
+              } else {
+                const uint4 t = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(e.R) + ri);
+                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&t);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const float2 f = __bfloat1622float2(h2[i]);
+                  o[2 * i] += f.x;
+                  o[2 * i + 1] += f.y;
+                }
+              }
+            }
+            if (e.d_f32) {
+              float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.D) + di);
+              d[0] = make_float4(o[0], o[1], o[2], o[3]);
+              d[1] = make_float4(o[4], o[5], o[6], o[7]);
+            } else {
+              uint4 t;
+              __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&t);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) h2[i] = __floats2bfloat162_rn(o[2 * i], o[2 * i + 1]);
+              *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(e.D) + di) = t;
+            }
+          }
+        } else if (fast) {
           uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(e.D) + (int64_t)row * e.ldd + col0);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {

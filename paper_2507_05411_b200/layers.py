@@ -221,9 +221,20 @@ class RMSNormBehavior(Behavior):
         return y
 
     def backward(self, module, dy, dres=None):
-        """dres: gradient arriving on the residual branch of the same input (fused add)."""
+        """dres: gradient arriving on the residual branch of the same input (fused add).
+
+        In bf16 mode the same pass also writes the bf16 copy of dx that the next
+        backward GEMM consumes (attached as ``dx._bf16``; ``ops.cast`` picks it up).
+        """
         s = saved()
-        return ops.rmsnorm_bwd(s["x"], _f32(param("scale")), s["rstd"], dy, dres=dres, dscale=param_grad("scale"))
+        want = act_dtype() == torch.bfloat16
+        out = ops.rmsnorm_bwd(s["x"], _f32(param("scale")), s["rstd"], dy, dres=dres, dscale=param_grad("scale"),
+                              want_bf16=want)
+        if want:
+            dx, dxb = out
+            dx._bf16 = dxb
+            return dx
+        return out
 
 
 def _f32(t: torch.Tensor) -> torch.Tensor:
@@ -366,7 +377,9 @@ class AttentionBehavior(Behavior):
         return [RematTag("q_proj", nbytes, proj), RematTag("k_proj", nbytes, proj), RematTag("v_proj", nbytes, proj),
                 RematTag("context", nbytes, 4 * rows * seq_len * d), RematTag("o_proj", nbytes, proj)]
 
-    def forward(self, module, x):
+    fuses_residual = True  # forward(x, residual=r) returns r + attn(x) from the wo GEMM epilogue
+
+    def forward(self, module, x, residual=None):
         cfg = module.config
         d, H = cfg.get("input_dim"), cfg.get("num_heads")
         KVH = self.kv_heads(cfg)
@@ -387,7 +400,8 @@ class AttentionBehavior(Behavior):
         invoke_child("pos_emb", q, k, T)
         scale = 1.0 / math.sqrt(hd)
         o, lse = ops.attention_fwd(q, k, v, B, T, H, KVH, hd, scale)
-        out = _linear_fwd(o, wo, torch.float32)
+        out = torch.empty((o.shape[0], d), device=x.device, dtype=torch.float32)
+        ops.gemm(o, wo, out, residual=ops.rows2d(residual) if residual is not None else None)
         save(x2=x2, qkv=qkv, o=o, lse=lse, geom=(B, T, H, KVH, hd, d, kvd))
         return out.view(B, T, d)
 
@@ -395,7 +409,7 @@ class AttentionBehavior(Behavior):
         s = saved()
         B, T, H, KVH, hd, d, kvd = s["geom"]
         adt = act_dtype()
-        g = ops.cast(ops.rows2d(dout), adt)
+        g = ops.rows2d(ops.cast(dout, adt))
         do = _linear_bwd(s["o"], param("wo"), g, param_grad("wo"), adt)
         qkv = s["qkv"]
         dqkv = torch.empty_like(qkv)
@@ -489,7 +503,9 @@ class FeedForwardBehavior(Behavior):
         return [RematTag("hidden", br * rows * h * nb, br * 2 * rows * d * h),
                 RematTag("output", rows * d * nb, 2 * rows * h * d)]
 
-    def forward(self, module, x):
+    fuses_residual = True
+
+    def forward(self, module, x, residual=None):
         cfg = module.config
         if x.shape[-1] != cfg.get("input_dim"):
             raise ShapeError(f"FeedForward expects trailing dim {cfg.get('input_dim')}")
@@ -512,7 +528,8 @@ class FeedForwardBehavior(Behavior):
         else:
             pre = _linear_fwd(x2, param("w1"), adt)
             hidden = ops.act_fwd(pre, None, cfg.get("activation"))
-        out = _linear_fwd(hidden, param("w2"), torch.float32)
+        out = torch.empty((x2.shape[0], cfg.get("input_dim")), device=x.device, dtype=torch.float32)
+        ops.gemm(hidden, param("w2"), out, residual=ops.rows2d(residual) if residual is not None else None)
         save(x2=x2, pre=pre, hidden=hidden)
         return out.view(*lead, cfg.get("input_dim"))
 
@@ -521,7 +538,7 @@ class FeedForwardBehavior(Behavior):
         s = saved()
         adt = act_dtype()
         h = cfg.get("hidden_dim")
-        g = ops.cast(ops.rows2d(dout), adt)
+        g = ops.rows2d(ops.cast(dout, adt))
         dhidden = _linear_bwd(s["hidden"], param("w2"), g, param_grad("w2"), adt)
         pre = s["pre"]
         dpre = torch.empty_like(pre)
@@ -576,11 +593,16 @@ class TransformerLayerBehavior(Behavior):
                 cfg = cfg.set(f"{child}.input_dim", dim)
         return cfg
 
+    @staticmethod
+    def _branch(module, name: str, normed, residual):
+        """residual + child(normed); fused into the child's output GEMM when it supports it."""
+        if getattr(module.children[name].behavior, "fuses_residual", False):
+            return invoke_child(name, normed, residual=residual)
+        return ops.add_(invoke_child(name, normed), residual)
+
     def forward(self, module, x):
-        a = invoke_child("self_attention", invoke_child("self_attention_norm", x))
-        h = ops.add_(a, x)  # a := a + x (fresh buffer from the projection GEMM)
-        f = invoke_child("feed_forward", invoke_child("feed_forward_norm", h))
-        return ops.add_(f, h)
+        h = self._branch(module, "self_attention", invoke_child("self_attention_norm", x), x)
+        return self._branch(module, "feed_forward", invoke_child("feed_forward_norm", h), h)
 
     def backward(self, module, dout):
         dn2 = backward_child("feed_forward", dout)

@@ -132,10 +132,12 @@ def rmsnorm_fwd(x: torch.Tensor, scale: torch.Tensor, eps: float, out_dtype: tor
     return y.view(*x.shape[:-1], dim), rstd
 
 
-def rmsnorm_bwd(x, scale, rstd, dy, dres=None, dscale=None):
+def rmsnorm_bwd(x, scale, rstd, dy, dres=None, dscale=None, want_bf16=False):
+    """Returns dx (f32), or (dx, dx_bf16) when want_bf16 (the bf16 copy written in the same pass)."""
     x2, g2 = rows2d(x), rows2d(dy)
     rows, dim = x2.shape
     dx = torch.empty((rows, dim), device=x.device, dtype=torch.float32)
+    dxb = torch.empty((rows, dim), device=x.device, dtype=torch.bfloat16) if want_bf16 else None
     ws = None
     if dscale is not None:
         nbytes = ctypes.c_int64(0)
@@ -144,8 +146,11 @@ def rmsnorm_bwd(x, scale, rstd, dy, dres=None, dscale=None):
     r2 = rows2d(dres) if dres is not None else None
     _lib.call("cb_rmsnorm_bwd", rows, dim, x2.data_ptr(), ld(x2), dt(x2), scale.data_ptr(), rstd.data_ptr(),
               g2.data_ptr(), ld(g2), dt(g2), _ptr(r2), ld(r2) if r2 is not None else 0, dx.data_ptr(), ld(dx),
-              _ptr(dscale), _ptr(ws), stream_ptr())
-    return dx.view(*x.shape[:-1], dim)
+              _ptr(dxb), ld(dxb) if dxb is not None else 0, _ptr(dscale), _ptr(ws), stream_ptr())
+    dx = dx.view(*x.shape[:-1], dim)
+    if want_bf16:
+        return dx, dxb.view(*x.shape[:-1], dim)
+    return dx
 
 
 # ------------------------------------------------------------------------ embedding
@@ -210,8 +215,12 @@ def copy2d(src: torch.Tensor, dst: torch.Tensor, alpha: float = 1.0, accumulate:
 
 
 def cast(src: torch.Tensor, dtype: torch.dtype) -> torch.Tensor:
+    """dtype copy of `src`; reuses a copy a producing kernel already attached as `_bf16`."""
     if src.dtype == dtype:
         return src
+    cached = getattr(src, "_bf16", None)
+    if dtype == torch.bfloat16 and cached is not None:
+        return cached.reshape(src.shape)
     out = torch.empty(src.shape, device=src.device, dtype=dtype)
     return copy2d(src, out)
 

@@ -1,0 +1,157 @@
+"""C-ABI boundary and host-API tests that run without a GPU.
+
+* the shared library loads and exports every CB_API symbol include/composer_b200.h declares
+  (no compute calls: there is no device here);
+* the ctypes signature table covers exactly the declared API;
+* status codes map onto the reference's error classes;
+* the config / module API behaves like the reference's (reference tests test_config.py,
+  test_module.py): value semantics, REQUIRED, fn: resolution, errors, init determinism,
+  golden round trips.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_2507_05411_b200 as cb
+from paper_2507_05411_b200 import _lib
+from paper_2507_05411_b200.errors import (
+    BadPathError,
+    BadTopKError,
+    KernelError,
+    OddDimError,
+    ShapeError,
+    TypeMismatchError,
+    UnknownActivationError,
+    UnsetFieldError,
+)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    declared = _lib.declared_symbols()
+    assert len(declared) >= 30
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.cb_abi_version() == 1
+
+
+def test_signature_table_matches_header():
+    declared = set(_lib.declared_symbols())
+    special = {"cb_last_error", "cb_launch_count"}
+    assert set(_lib.SIGNATURES) | special == declared
+
+
+def test_status_mapping():
+    _lib.load()
+    with pytest.raises(ShapeError):
+        _lib.check(_lib.CB_ERR_SHAPE)
+    with pytest.raises(TypeMismatchError):
+        _lib.check(_lib.CB_ERR_UNSUPPORTED)
+    with pytest.raises(KernelError):
+        _lib.check(_lib.CB_ERR_CUDA)
+
+
+def test_shape_errors_raised_before_launch():
+    """Argument validation happens in the library before any device work (no GPU needed)."""
+    _lib.load()
+    with pytest.raises(ShapeError):
+        _lib.call("cb_gemm", -1, 4, 4, 1, None, 4, 0, None, 4, 0, 1, 4, 0, None, 0, 0, 1.0, 0, None)
+    with pytest.raises(ShapeError):
+        _lib.call("cb_rope", 4, 4, 1, 7, None, 7, 0, None, None, 0, None)
+    with pytest.raises(ShapeError):
+        _lib.call("cb_moe_route", 4, 8, 4, 5, None, 8, 0, None, None, None, None, None)
+    with pytest.raises(ShapeError):
+        _lib.call("cb_xent_fwd_bwd", 2, 1, 8, None, 8, 0, None, None, None, 0, 0, 1.0, None, None, None)
+
+
+# ----------------------------------------------------------------------- config API
+def test_value_semantics_and_paths():
+    base = cb.default_config("Trainer")
+    a = base.set("model.dim", 64)
+    assert base.get("model.dim") is cb.REQUIRED and a.get("model.dim") == 64
+    layer = cb.default_config("TransformerLayer").set("self_attention.num_heads", 4)
+    b = a.set("model.decoder.transformer.layer", (layer, layer))
+    c = b.set("model.decoder.transformer.layer[1].self_attention.num_heads", 8)
+    assert b.get("model.decoder.transformer.layer[1].self_attention.num_heads") == 4
+    assert c.get("model.decoder.transformer.layer[1].self_attention.num_heads") == 8
+    with pytest.raises(BadPathError):
+        a.set("model.nope", 1)
+    with pytest.raises(TypeMismatchError):
+        a.set("model.dim", "x")
+
+
+def test_instantiate_propagates_and_resolves():
+    cfg = cb.build_experiment("txf_rope")
+    m = cb.instantiate(cfg)
+    att = m.child("model.decoder.transformer.layer[0].self_attention")
+    assert att.config.get("input_dim") == 32
+    assert att.config.get("pos_emb.dim") == 8
+    ff = m.child("model.decoder.transformer.layer[0].feed_forward")
+    assert ff.config.get("hidden_dim") == 85  # floor(32 * 8/3 + 0.5)
+    with pytest.raises(UnsetFieldError):
+        cb.instantiate(cb.default_config("Trainer"))
+
+
+def test_layer_validation_errors():
+    with pytest.raises(ShapeError):
+        cb.instantiate(cb.build_experiment("txf_base").set("model.dim", 30))
+    with pytest.raises(OddDimError):
+        cb.instantiate(cb.experiments.transformer_trainer(48, 1, "relu", pos_kind="RoPE", heads=16))
+    with pytest.raises(UnknownActivationError):
+        cb.instantiate(cb.build_experiment("txf_base").set("model.decoder.transformer.layer[0].feed_forward.activation",
+                                                           "gelu"))
+    with pytest.raises(BadTopKError):
+        cb.instantiate(cb.build_experiment("txf_moe").set("model.decoder.transformer.layer[0].feed_forward.top_k", 9))
+
+
+def test_init_state_deterministic_and_path_local():
+    m = cb.instantiate(cb.build_experiment("txf_d16_l2_relu"))
+    s1 = cb.init_state(m, cb.root_key(0))
+    s2 = cb.init_state(m, cb.root_key(0))
+    l0a = s1["model"]["decoder"]["transformer"]["layer[0]"]["self_attention"]["wq"]
+    assert np.array_equal(l0a, s2["model"]["decoder"]["transformer"]["layer[0]"]["self_attention"]["wq"])
+    l1a = s1["model"]["decoder"]["transformer"]["layer[1]"]["self_attention"]["wq"]
+    assert not np.array_equal(l0a, l1a)
+
+
+def test_flops_and_remat_metadata_match_reference_formulas():
+    m = cb.instantiate(cb.build_experiment("txf_moe"))
+    att = m.child("model.decoder.transformer.layer[0].self_attention")
+    assert att.behavior.own_flops(att.config, 4, 8) == 8 * 32 * 32 * 32 + 4 * 32 * 8 * 32
+    moe = m.child("model.decoder.transformer.layer[0].feed_forward")
+    d, h, e, k, rows = 32, 85, 4, 2, 32
+    assert moe.behavior.own_flops(moe.config, 4, 8) == 2 * rows * d * e + k * (2 * 2 * rows * d * h + 2 * rows * h * d)
+    assert [t.name for t in moe.behavior.remat_tags(moe.config, 4, 8)] == ["router_logits", "expert_hidden",
+                                                                             "expert_output"]
+
+
+REF_GOLDENS = "/root/reference/pkg/tests/goldens"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_GOLDENS), reason="reference goldens not present (GPU box)")
+def test_reference_golden_configs_round_trip_and_instantiate():
+    for f in sorted(os.listdir(REF_GOLDENS)):
+        text = open(os.path.join(REF_GOLDENS, f)).read()
+        cfg = cb.parse_golden(text)
+        assert cb.serialize_golden(cfg) == text, f
+        cb.instantiate(cfg)
+
+
+def test_engine_layout_fuses_and_aligns():
+    from paper_2507_05411_b200.engine import ALIGN, build_layout
+
+    m = cb.instantiate(cb.BENCH_CONFIGS["1b"](batch=1, seq=128, layers=2))
+    buckets = build_layout(m)
+    names = [b.name for b in buckets]
+    assert names[0] == "root" and names[-1] == "replicated"
+    assert names[1] == "model.decoder.transformer.layer[0]"
+    layer = buckets[1]
+    att = {e.name: e for e in layer.entries if e.path.endswith("self_attention")}
+    assert att["wq"].ld == att["wk"].ld == 3 * 2048 and att["wk"].col0 == 2048
+    for b in buckets:
+        for e in b.entries:
+            assert e.offset % ALIGN == 0
+    rep = buckets[-1]
+    assert all(e.name == "scale" for e in rep.entries)

