@@ -51,6 +51,12 @@ CB_API int cb_gemm(int M, int N, int K, int in_dtype, const void* A, int64_t lda
                    int r_dtype, float alpha, int accumulate, void* stream);
 /* 0 = automatic engine choice, 1 = force SIMT, 2 = force tcgen05 (tests only). */
 CB_API int cb_gemm_set_path(int path);
+/* D = op(A) @ op(B) with RoPE (layers.py:235-257; positions = row % seq_len) applied to
+ * output columns [0, rope_cols) — the q|k part of the fused QKV projection (layers.py:340-343).
+ * Rotated in the tcgen05 epilogue (no extra HBM pass); other engines rotate afterwards. */
+CB_API int cb_gemm_rope(int M, int N, int K, int in_dtype, const void* A, int64_t lda, int trans_a, const void* B,
+                        int64_t ldb, int trans_b, void* D, int64_t ldd, int d_dtype, int seq_len, int head_dim,
+                        int rope_cols, const float* cos_t, const float* sin_t, void* stream);
 
 /* ---------------------------------------------------------------------------------
  * RMSNorm (layers.py:176-193): y = x / sqrt(mean(x^2) + eps) * scale, rstd[row] saved.
@@ -115,6 +121,12 @@ CB_API int cb_attention_bwd(int batch, int seq_len, int heads, int kv_heads, int
                             int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv, const void* o,
                             int64_t ldo, const float* lse, const void* dout, int64_t lddo, float* delta, void* dq,
                             int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv, float scale, void* stream);
+/* Backward for q/k rotated by cb_gemm_rope: dq/dk are returned un-rotated (the RoPE backward). */
+CB_API int cb_attention_bwd_rope(int batch, int seq_len, int heads, int kv_heads, int head_dim, int dtype,
+                                 const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
+                                 const void* o, int64_t ldo, const float* lse, const void* dout, int64_t lddo,
+                                 float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv,
+                                 float scale, const float* cos_t, const float* sin_t, void* stream);
 /* 0 = automatic (tensor-core flash kernels when eligible), 1 = force SIMT (tests). */
 CB_API int cb_attention_set_path(int path);
 /* 1 (default) = use the tcgen05/TMEM forward for head_dim 128; 0 = warp-MMA flash kernel (tests). */

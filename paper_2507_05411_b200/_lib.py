@@ -49,6 +49,9 @@ SIGNATURES: dict[str, list] = {
     "cb_attention_bwd": [_I, _I, _I, _I, _I, _I, _P, _L, _P, _L, _P, _L, _P, _L, _P, _P, _L, _P, _P, _L, _P, _L,
                          _P, _L, _F, _P],
     "cb_attention_set_path": [_I],
+    "cb_gemm_rope": [_I, _I, _I, _I, _P, _L, _I, _P, _L, _I, _P, _L, _I, _I, _I, _I, _P, _P, _P],
+    "cb_attention_bwd_rope": [_I, _I, _I, _I, _I, _I, _P, _L, _P, _L, _P, _L, _P, _L, _P, _P, _L, _P, _P, _L, _P,
+                              _L, _P, _L, _F, _P, _P, _P],
     "cb_attention_set_tc": [_I],
     "cb_xent_fwd_bwd": [_I, _I, _I, _P, _L, _I, _P, _P, _P, _L, _I, _F, _P, _P, _P],
     "cb_adamw": [_L, _P, _P, _P, _P, _P, _F, _F, _F, _F, _F, _I, _F, _P],

@@ -20,7 +20,7 @@ bool attn_tc_supported(const AttnGeom& g, int dtype, const void* q, const void* 
 int attn_fwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, void* o, float* lse, cudaStream_t st);
 int attn_bwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, const void* dout, int64_t lddo,
                 const float* lse, const float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
-                int64_t lddv, cudaStream_t st);
+                int64_t lddv, cudaStream_t st, const float* rope_cos = nullptr, const float* rope_sin = nullptr);
 bool attn_fa_supported(const AttnGeom& g, int dtype, const void* q, const void* k, const void* v);
 int attn_fwd_fa(const AttnGeom& g, const void* q, const void* k, const void* v, void* o, float* lse, cudaStream_t st);
 int attn_bwd_fa(const AttnGeom& g, const void* q, const void* k, const void* v, const void* dout, int64_t lddo,

@@ -41,3 +41,28 @@ extern "C" int cb_attention_bwd(int batch, int seq_len, int heads, int kv_heads,
     return attn_bwd_fa(g, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st);
   return attn_bwd_simt(g, dtype, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st);
 }
+
+// Backward of attention whose q/k were rotated by RoPE in the projection epilogue
+// (cb_gemm_rope): dq / dk come back un-rotated (inverse rotation, reference
+// layers.py:235-257).  The tcgen05 kernels fuse the rotation into their dQ / dK stores;
+// other engines run cb_rope(inverse) afterwards.
+extern "C" int cb_attention_bwd_rope(int batch, int seq_len, int heads, int kv_heads, int head_dim, int dtype,
+                                     const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
+                                     int64_t ldv, const void* o, int64_t ldo, const float* lse, const void* dout,
+                                     int64_t lddo, float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk,
+                                     void* dv, int64_t lddv, float scale, const float* cos_t, const float* sin_t,
+                                     void* stream) {
+  AttnGeom g{batch, seq_len, heads, kv_heads, head_dim, ldq, ldk, ldv, ldo, scale};
+  if (int s = check_geom(g)) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (g_attn_path == 0 && attn_tc_supported(g, dtype, q, k, v) && !((lddo | lddq | lddk | lddv) & 7)) {
+    if (int s = attn_delta(g, dtype, o, dout, lddo, delta, st)) return s;
+    return attn_bwd_tc(g, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st, cos_t, sin_t);
+  }
+  if (int s = cb_attention_bwd(batch, seq_len, heads, kv_heads, head_dim, dtype, q, ldq, k, ldk, v, ldv, o, ldo, lse,
+                               dout, lddo, delta, dq, lddq, dk, lddk, dv, lddv, scale, stream))
+    return s;
+  const int64_t rows = (int64_t)batch * seq_len;
+  if (int s = cb_rope(rows, seq_len, heads, head_dim, dq, lddq, dtype, cos_t, sin_t, 1, stream)) return s;
+  return cb_rope(rows, seq_len, kv_heads, head_dim, dk, lddk, dtype, cos_t, sin_t, 1, stream);
+}

@@ -3,19 +3,18 @@
 // Reference op: AttentionBehavior.forward (reference layers.py:331-348): softmax over
 // all keys (no causal mask) of q k^T / sqrt(hd), then @ v.
 //
-// One CTA per (128-query tile, head, batch); 256 threads in four roles:
-//   warp 0      TMA producer: Q once, then K_j / V_j tiles into a 2-stage ring
-//   warp 1      MMA issuer (one thread): S_j = Q K_j^T into a double-buffered TMEM
-//               S tile, then O += P_j V_j with P read straight from TMEM (A operand
-//               in tensor memory) — S_{j+1} is issued before waiting for P_j so the
-//               tensor core computes the next scores while softmax runs
-//   warp 2      TMEM allocator (512 columns: S0 | S1 | O)
-//   warps 4-7   softmax: one thread owns one query row of S in TMEM (no shuffles),
-//               exp2-domain online softmax with lazy O rescaling (only when the row max
-//               grows by more than 2^8), P packed to bf16 pairs and stored back over S;
-//               then the epilogue (O / l, natural-log LSE).
-// K/V tiles stream through TMA with 128B swizzle; Q and K are K-major UMMA operands,
-// V is an MN-major operand (keys x hd, hd contiguous) — no transposes anywhere.
+// One CTA per (256-query block, head, batch) = two 128-row query tiles A and B that share
+// every K/V tile (half the K/V shared-memory traffic per FLOP).  384 threads:
+//   warp 0       TMA producer: Q_A, Q_B once, then K_j / V_j into a 2-stage ring
+//   warp 1       MMA issuer (one thread), ping-pong between the tiles so the tensor core
+//                always has work while one softmax group runs:
+//                  S_A(j) S_B(j) | PV_A(j) S_A(j+1) | PV_B(j) S_B(j+1) | ...
+//                S = Q K^T lands in TMEM; P (bf16) is written back over S and consumed as
+//                the TMEM A operand of O += P V (V is an MN-major smem operand)
+//   warp 2       TMEM allocator (512 columns: S_A | S_B | O_A | O_B)
+//   warps 4-7    softmax of tile A, warps 8-11 softmax of tile B: one thread owns one
+//                query row (no shuffles), exp2 domain, lazy O rescale (only when the row
+//                max grows by more than 2^8), then the epilogue (O / l, natural-log LSE).
 #include "attn.cuh"
 #include "composer_b200.h"
 
@@ -24,17 +23,16 @@ namespace tca {
 
 constexpr int HD = 128;
 constexpr int BM = 128, BN = 128;
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;
 constexpr int kTileBytes = 128 * 64 * 2;       // one [128 rows][64 cols] bf16 TMA box
-constexpr int kQBytes = 2 * kTileBytes;        // Q: two 64-column K-atoms
+constexpr int kQBytes = 2 * kTileBytes;        // one Q tile: two 64-column K-atoms
 constexpr int kStageBytes = 4 * kTileBytes;    // K (2 atoms) + V (2 MN-blocks)
 constexpr int kStages = 2;
-constexpr int kSmem = kQBytes + kStages * kStageBytes + 1024 + 256;
+constexpr int kSmem = 2 * kQBytes + kStages * kStageBytes + 1024 + 256;
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO = 256;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
-constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only if max grows by > 2^8
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
 struct Params {
   int T, H, KVH, B;
@@ -48,29 +46,34 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_tc_k(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
              const __grid_constant__ CUtensorMap tmV, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sKV = smem + kQBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kQBytes + kStages * kStageBytes);
+  uint8_t* sQ = smem;  // [2 tiles][kQBytes]
+  uint8_t* sKV = smem + 2 * kQBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kQBytes + kStages * kStageBytes);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;
-  uint64_t* kv_empty = bars + 3;
-  uint64_t* s_full = bars + 5;
-  uint64_t* p_ready = bars + 7;
-  uint64_t* o_done = bars + 9;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* kv_full = bars + 1;   // [2] stages
+  uint64_t* kv_empty = bars + 3;  // [2] stages
+  uint64_t* s_full = bars + 5;    // [2] tiles
+  uint64_t* p_ready = bars + 7;   // [2] tiles
+  uint64_t* o_done = bars + 9;    // [2] tiles
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int kvh = h / (p.H / p.KVH);
-  const int q0 = qt * BM;
+  const int q0 = qb * 2 * BM;
   const int nblk = (p.T + BN - 1) / BN;
-  const int row0 = b * p.T;  // first token row of this sequence
+  const int row0 = b * p.T;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
@@ -82,8 +85,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&kv_empty[s], 1);
       mbar_init(&s_full[s], 1);
       mbar_init(&p_ready[s], 4);
+      mbar_init(&o_done[s], 1);
     }
-    mbar_init(o_done, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
@@ -94,9 +97,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(q_full, kQBytes);
-      tma_load_2d(sQ, &tmQ, q_full, h * HD, row0 + q0);
-      tma_load_2d(sQ + kTileBytes, &tmQ, q_full, h * HD + 64, row0 + q0);
+      mbar_expect_tx(q_full, 2 * kQBytes);
+      for (int x = 0; x < 2; ++x) {
+        tma_load_2d(sQ + x * kQBytes, &tmQ, q_full, h * HD, row0 + q0 + x * BM);
+        tma_load_2d(sQ + x * kQBytes + kTileBytes, &tmQ, q_full, h * HD + 64, row0 + q0 + x * BM);
+      }
       for (int j = 0; j < nblk; ++j) {
         const int st = j & 1;
         mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
@@ -114,120 +119,132 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       const uint32_t idesc_s = idesc_bf16_f32(BM, BN, 0, 0);
       const uint32_t idesc_o = idesc_bf16_f32(BM, HD, 0, 1);
-      const uint32_t q_addr = smem_u32(sQ);
-      auto issue_s = [&](int j) {
-        const int st = j & 1;
-        const uint32_t k_addr = smem_u32(sKV + st * kStageBytes);
-        const uint32_t d = tmem + (st ? kColS1 : kColS0);
+      auto issue_s = [&](int x, int j) {
+        const uint32_t q_addr = smem_u32(sQ + x * kQBytes);
+        const uint32_t k_addr = smem_u32(sKV + (j & 1) * kStageBytes);
+        const uint32_t d = tmem + x * 128u;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * kTileBytes + (kk & 3) * 32;
           umma_f16_ss(d, sw128_desc(q_addr + off, 16, 1024), sw128_desc(k_addr + off, 16, 1024), idesc_s, kk > 0);
         }
-        umma_commit(&s_full[st]);
+        umma_commit(&s_full[x]);
+      };
+      auto issue_pv = [&](int x, int j) {
+        mbar_wait(&p_ready[x], j & 1);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(sKV + (j & 1) * kStageBytes + 2 * kTileBytes);
+#pragma unroll
+        for (int k = 0; k < BN / 16; ++k)
+          umma_f16_ts(tmem + 256u + x * 128u, tmem + x * 128u + k * 8, sw128_desc(v_addr + k * 2048, 16384, 1024),
+                      idesc_o, (j | k) != 0);
+        umma_commit(&o_done[x]);
       };
       mbar_wait(q_full, 0);
       mbar_wait(&kv_full[0], 0);
       tc_fence_after();
-      issue_s(0);
+      issue_s(0, 0);
+      issue_s(1, 0);
       for (int j = 0; j < nblk; ++j) {
-        const int st = j & 1;
+        issue_pv(0, j);
         if (j + 1 < nblk) {
           mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
           tc_fence_after();
-          issue_s(j + 1);
+          issue_s(0, j + 1);
         }
-        mbar_wait(&p_ready[st], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t v_addr = smem_u32(sKV + st * kStageBytes + 2 * kTileBytes);
-        const uint32_t pcol = tmem + (st ? kColS1 : kColS0);
-#pragma unroll
-        for (int k = 0; k < BN / 16; ++k)
-          umma_f16_ts(tmem + kColO, pcol + k * 8, sw128_desc(v_addr + k * 2048, 16384, 1024), idesc_o, (j | k) != 0);
-        umma_commit(o_done);
-        umma_commit(&kv_empty[st]);
+        issue_pv(1, j);
+        umma_commit(&kv_empty[j & 1]);
+        if (j + 1 < nblk) issue_s(1, j + 1);
       }
     }
     __syncwarp();
   } else if (warp >= 4) {
-    const int q = warp & 3;
-    const int row = q * 32 + lane;  // TMEM lane == query row inside the tile
+    const int x = (warp - 4) >> 2;  // query tile
+    const int q = warp & 3;         // TMEM lane quadrant
+    const int row = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const uint32_t scol = tmem + lane_off + x * 128u;
+    const uint32_t ocol = tmem + lane_off + 256u + x * 128u;
     const float c = p.scale * kLog2e;
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < nblk; ++j) {
-      const int st = j & 1;
-      const uint32_t scol = tmem + lane_off + (st ? kColS1 : kColS0);
-      mbar_wait(&s_full[st], (j >> 1) & 1);
+      mbar_wait(&s_full[x], j & 1);
       tc_fence_after();
-      uint32_t v[4][32];
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) tmem_ld32(scol + cc * 32, v[cc]);
-      tmem_ld_wait();
-      const int kbase = j * BN;
-      const int valid = min(BN, p.T - kbase);
+      // pass 1 over the S row in TMEM: row max (keeps only 32 values live)
+      const int valid = min(BN, p.T - j * BN);
       float mx = -INFINITY;
+#pragma unroll 1
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(scol + cc * 32, v);
+        tmem_ld_wait();
+        if (valid >= BN) {
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc)
+          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
+        } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          float s = __uint_as_float(v[cc][i]) * c;
-          if (cc * 32 + i >= valid) s = -INFINITY;
-          v[cc][i] = __float_as_uint(s);
-          mx = fmaxf(mx, s);
+          for (int i = 0; i < 32; ++i)
+            if (cc * 32 + i < valid) mx = fmaxf(mx, __uint_as_float(v[i]));
         }
+      }
+      mx *= c;
       const bool need = mx > m_used + kRescaleThreshold;
       const float m_new = need ? mx : m_used;
       if (__any_sync(0xffffffffu, need)) {
-        const float corr = need ? exp2f(m_used - m_new) : 1.f;
+        const float corr = need ? fast_exp2(m_used - m_new) : 1.f;
         if (j > 0) {
-          mbar_wait(o_done, (j - 1) & 1);  // PV_{j-1} has finished writing O
+          mbar_wait(&o_done[x], (j - 1) & 1);  // PV_{j-1} has finished writing O
           tc_fence_after();
 #pragma unroll 1
           for (int cc = 0; cc < HD / 32; ++cc) {
             uint32_t o[32];
-            tmem_ld32(tmem + lane_off + kColO + cc * 32, o);
+            tmem_ld32(ocol + cc * 32, o);
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
-            tmem_st32(tmem + lane_off + kColO + cc * 32, o);
+            tmem_st32(ocol + cc * 32, o);
           }
           tmem_st_wait();
         }
         l *= corr;
         m_used = m_new;
       }
+      // pass 2: P = exp2(S c - m) packed to bf16 pairs over the first 64 columns of S.
+      // Chunk cc's packed output (columns [16cc, 16cc+16)) only overwrites S columns that
+      // earlier chunks already consumed.
       float rs = 0.f;
+#pragma unroll 1
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(scol + cc * 32, v);
+        tmem_ld_wait();
+        uint32_t pk[16];
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        uint32_t pk[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int cc = half * 2 + (i >> 4);
-          const int e = (i & 15) * 2;
-          const float p0 = exp2f(__uint_as_float(v[cc][e]) - m_used);
-          const float p1 = exp2f(__uint_as_float(v[cc][e + 1]) - m_used);
+        for (int i = 0; i < 16; ++i) {
+          const bool ok0 = cc * 32 + 2 * i < valid, ok1 = cc * 32 + 2 * i + 1 < valid;
+          const float p0 = ok0 ? fast_exp2(fmaf(__uint_as_float(v[2 * i]), c, -m_used)) : 0.f;
+          const float p1 = ok1 ? fast_exp2(fmaf(__uint_as_float(v[2 * i + 1]), c, -m_used)) : 0.f;
           rs += p0 + p1;
           pk[i] = pack2(p0, p1);
         }
-        tmem_st32(scol + half * 32, pk);
+        tmem_st16(scol + cc * 16, pk);
       }
       l += rs;
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_ready[st]);
+      if (lane == 0) mbar_arrive(&p_ready[x]);
     }
     // epilogue
-    mbar_wait(o_done, (nblk - 1) & 1);
+    mbar_wait(&o_done[x], (nblk - 1) & 1);
     tc_fence_after();
-    const int qrow = q0 + row;
+    const int qrow = q0 + x * BM + row;
     const float inv = 1.f / l;
     __nv_bfloat16* orow = p.o + ((int64_t)row0 + qrow) * p.ldo + (int64_t)h * HD;
 #pragma unroll 1
     for (int cc = 0; cc < HD / 32; ++cc) {
       uint32_t o[32];
-      tmem_ld32(tmem + lane_off + kColO + cc * 32, o);
+      tmem_ld32(ocol + cc * 32, o);
       tmem_ld_wait();
       if (qrow < p.T) {
         uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
@@ -277,7 +294,7 @@ int attn_fwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, 
     attr = true;
   }
   Params p{g.T, g.H, g.KVH, g.B, g.scale, (__nv_bfloat16*)o, g.ldo, lse};
-  dim3 grid((g.T + BM - 1) / BM, g.H, g.B);
+  dim3 grid((g.T + 2 * BM - 1) / (2 * BM), g.H, g.B);
   fwd_tc_k<<<grid, kThreads, kSmem, st>>>(mq, mk, mv, p);
   return check_launch("flash_fwd_tc");
 }

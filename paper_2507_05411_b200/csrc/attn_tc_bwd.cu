@@ -1,16 +1,19 @@
 // tcgen05 flash attention backward (bf16, head_dim 128), unmasked, GQA-aware.
 //
 // Deterministic two-kernel split (no atomics), both recomputing P = exp(S - LSE):
-//   dkdv: one CTA per (128-key tile, kv head, batch); sweeps every 128-query tile of every
-//         query head in the kv group:
-//           S^T  = K Q^T          (A = K   smem K-major, B = Q  smem K-major)  -> TMEM
-//           dP^T = V dO^T         (A = V   smem K-major, B = dO smem K-major)  -> TMEM
-//           P^T  = exp2(S^T c - lse2), dS^T = P^T (dP^T - delta)   [1 thread = 1 key row]
-//           dV  += P^T dO         (A = P^T from TMEM, B = dO smem MN-major)
-//           dK  += dS^T Q         (A = dS^T from TMEM, B = Q  smem MN-major)
-//   dq:   one CTA per (128-query tile, head, batch); sweeps every 128-key tile:
-//           S = Q K^T, dP = dO V^T, dS = P (dP - delta), dQ += dS K (B = K MN-major)
-// TMEM (512 columns): dkdv = S^T | dP^T | dV | dK;  dq = S | dP | dQ.
+//   dkdv: one CTA per (128-key tile, kv head, batch); sweeps every query tile of every
+//         query head in the kv group in 64-query sub-tiles u:
+//           S^T_u  = K Q_u^T      (A = K  smem K-major, B = Q_u  smem K-major)  -> TMEM
+//           dP^T_u = V dO_u^T     (A = V  smem K-major, B = dO_u smem K-major)  -> TMEM
+//           P^T = exp2(S^T c - lse2), dS^T = P^T (dP^T - delta)    [1 thread = 1 key row]
+//           dV += P^T dO_u        (A = P^T from TMEM, B = dO_u smem MN-major)
+//           dK += dS^T Q_u        (A = dS^T from TMEM, B = Q_u  smem MN-major)
+//         S^T / dP^T are double-buffered (2 x 64 columns each), so the MMAs of sub-tile
+//         u+1 and the accumulations of u-1 run while the CUDA cores handle sub-tile u.
+//   dq:   one CTA per (128-query tile, head, batch); sweeps every 128-key tile j:
+//           S_j = Q K_j^T (double-buffered), dP_j = dO V_j^T, dS = P (dP - delta),
+//           dQ += dS K_j (B = K_j MN-major); S_{j+1} is issued before dQ_j.
+// TMEM (512 columns): dkdv = S^T[2] | dP^T[2] | dV | dK;  dq = S[2] | dP | dQ.
 // Warp roles as in the forward: 0 TMA, 1 MMA (single thread), 2 TMEM alloc, 4-7 compute.
 #include "attn.cuh"
 #include "composer_b200.h"
@@ -20,9 +23,9 @@ namespace tcb {
 
 constexpr int HD = 128;
 constexpr int BT = 128;  // tile rows (keys or queries)
-constexpr int kThreads = 256;
-constexpr int kBox = 128 * 64 * 2;    // one [128][64] bf16 TMA box (16 KB)
-constexpr int kTile = 2 * kBox;       // one [128][128] tile (two 64-column atoms)
+constexpr int kThreads = 384;  // warps 0-3: TMA, MMA, TMEM alloc, idle; 4-11: compute
+constexpr int kBox = 128 * 64 * 2;  // one [128][64] bf16 TMA box (16 KB)
+constexpr int kTile = 2 * kBox;     // one [128][128] tile (two 64-column atoms)
 constexpr int kSmem = 6 * kTile + 1024 + 4096;
 constexpr uint32_t kCols = 512;
 constexpr float kLog2e = 1.4426950408889634f;
@@ -36,6 +39,8 @@ struct Params {
   int64_t ld0;
   __nv_bfloat16* o1;  // dv (dkdv)
   int64_t ld1;
+  const float* rope_cos;  // optional [T][HD/2]: un-rotate dK / dQ on store
+  const float* rope_sin;
 };
 
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
@@ -44,20 +49,38 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-// K-major operand descriptor of a [128][128] tile for the kk-th K=16 step
+// K-major operand descriptor for the kk-th K=16 step of a tile whose rows start at `base`
 __device__ __forceinline__ uint64_t kdesc(uint32_t base, int kk) {
   return sw128_desc(base + (kk >> 2) * kBox + (kk & 3) * 32, 16, 1024);
 }
 // MN-major operand descriptor (rows = K dim, 128 columns = N) for the k-th K=16 step
 __device__ __forceinline__ uint64_t mndesc(uint32_t base, int k) { return sw128_desc(base + k * 2048, kBox, 1024); }
 
-// store one thread's 128-column f32 TMEM row as bf16 (times `mul`) to global
-__device__ __forceinline__ void store_row(uint32_t taddr, __nv_bfloat16* dst, float mul, bool ok) {
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// store one thread's 128-column f32 TMEM row as bf16 (times `mul`) to global; when `rc`
+// is given, first apply the inverse RoPE rotation of this row's position (rc/rs = cos/sin
+// table row, HD/2 entries) — the backward of the forward's fused rotation
+__device__ __forceinline__ void store_row(uint32_t taddr, __nv_bfloat16* dst, float mul, bool ok,
+                                          const float* rc = nullptr, const float* rs = nullptr, int nchunks = HD / 32) {
 #pragma unroll 1
-  for (int cc = 0; cc < HD / 32; ++cc) {
+  for (int cc = 0; cc < nchunks; ++cc) {
     uint32_t o[32];
     tmem_ld32(taddr + cc * 32, o);
     tmem_ld_wait();
+    if (ok && rc) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float c = rc[cc * 16 + i], s = rs[cc * 16 + i];
+        const float e = __uint_as_float(o[2 * i]), d = __uint_as_float(o[2 * i + 1]);
+        o[2 * i] = __float_as_uint(e * c + d * s);
+        o[2 * i + 1] = __float_as_uint(d * c - e * s);
+      }
+    }
     if (ok) {
       uint4* d = reinterpret_cast<uint4*>(dst + cc * 32);
 #pragma unroll
@@ -73,6 +96,11 @@ __device__ __forceinline__ void store_row(uint32_t taddr, __nv_bfloat16* dst, fl
   }
 }
 
+__device__ __forceinline__ void store_row_half(uint32_t taddr, __nv_bfloat16* dst, float mul, bool ok, const float* rc,
+                                               const float* rs) {
+  store_row(taddr, dst, mul, ok, rc, rs, HD / 64);
+}
+
 // ====================================================================== dK / dV
 __global__ void __launch_bounds__(kThreads, 1)
     dkdv_k(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -86,20 +114,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* sD = sL + 256;                                   // [2][128] delta
   uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 256);
   uint64_t* kv_full = bars;
-  uint64_t* qd_full = bars + 1;   // [2]
-  uint64_t* qd_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* dp_full = bars + 6;
-  uint64_t* p_ready = bars + 7;
-  uint64_t* ds_ready = bars + 8;
-  uint64_t* mma_done = bars + 9;
-  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* qd_full = bars + 1;    // [2]
+  uint64_t* qd_empty = bars + 3;   // [2]
+  uint64_t* s_full = bars + 5;     // [2]
+  uint64_t* dp_full = bars + 7;    // [2]
+  uint64_t* p_ready = bars + 9;    // [2]
+  uint64_t* ds_ready = bars + 11;  // [2]
+  uint64_t* mma_done = bars + 13;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 14);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kt = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
   const int group = p.H / p.KVH;
   const int nq = (p.T + BT - 1) / BT;
-  const int total = group * nq;
+  const int total = group * nq;  // 128-query tiles
+  const int U = 2 * total;       // 64-query sub-tiles
   const int row0 = b * p.T, k0 = kt * BT;
 
   if (warp == 0 && lane == 0) {
@@ -111,11 +140,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&qd_full[s], 1);
       mbar_init(&qd_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&dp_full[s], 1);
+      mbar_init(&p_ready[s], 8);
+      mbar_init(&ds_ready[s], 8);
     }
-    mbar_init(s_full, 1);
-    mbar_init(dp_full, 1);
-    mbar_init(p_ready, 4);
-    mbar_init(ds_ready, 4);
     mbar_init(mma_done, 1);
     fence_mbar_init();
   }
@@ -124,7 +153,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *slot;
-  const uint32_t cS = 0, cP = 128, cV = 256, cK = 384;
+  // TMEM columns: S^T sub-tiles at half*64, dP^T sub-tiles at 128 + half*64
+  const uint32_t cV = 256, cK = 384;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -148,114 +178,121 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t id_s = idesc_bf16_f32(128, 128, 0, 0);   // K-major x K-major
+      const uint32_t id_s = idesc_bf16_f32(128, 64, 0, 0);    // K-major x K-major, 64 queries
       const uint32_t id_acc = idesc_bf16_f32(128, 128, 0, 1); // TMEM A x MN-major B
       const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
+      auto issue_sp = [&](int u) {
+        const int it = u >> 1, half = u & 1, st = it & 1;
+        if (half == 0) {
+          mbar_wait(&qd_full[st], (it >> 1) & 1);
+          tc_fence_after();
+        }
+        const uint32_t aQ = smem_u32(ring + st * 2 * kTile) + half * 8192, aG = aQ + kTile;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + (half * 64u), kdesc(aK, kk), kdesc(aQ, kk), id_s, kk > 0);
+        umma_commit(&s_full[half]);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + (128u + half * 64u), kdesc(aV, kk), kdesc(aG, kk), id_s, kk > 0);
+        umma_commit(&dp_full[half]);
+      };
       mbar_wait(kv_full, 0);
-      for (int it = 0; it < total; ++it) {
-        const int st = it & 1;
-        const uint32_t aQ = smem_u32(ring + st * 2 * kTile), aG = aQ + kTile;
-        mbar_wait(&qd_full[st], (it >> 1) & 1);
+      tc_fence_after();
+      issue_sp(0);
+      for (int u = 0; u < U; ++u) {
+        if (u + 1 < U) issue_sp(u + 1);
+        const int it = u >> 1, half = u & 1, st = it & 1;
+        const uint32_t aQ = smem_u32(ring + st * 2 * kTile) + half * 8192, aG = aQ + kTile;
+        mbar_wait(&p_ready[half], (u >> 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + cS, kdesc(aK, kk), kdesc(aQ, kk), id_s, kk > 0);
-        umma_commit(s_full);
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + cP, kdesc(aV, kk), kdesc(aG, kk), id_s, kk > 0);
-        umma_commit(dp_full);
-        mbar_wait(p_ready, it & 1);
+        for (int k = 0; k < 4; ++k) umma_f16_ts(tmem + cV, tmem + (half * 64u) + k * 8, mndesc(aG, k), id_acc, (u | k) != 0);
+        mbar_wait(&ds_ready[half], (u >> 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < BT / 16; ++k) umma_f16_ts(tmem + cV, tmem + cS + k * 8, mndesc(aG, k), id_acc, (it | k) != 0);
-        mbar_wait(ds_ready, it & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int k = 0; k < BT / 16; ++k) umma_f16_ts(tmem + cK, tmem + cP + k * 8, mndesc(aQ, k), id_acc, (it | k) != 0);
-        umma_commit(&qd_empty[st]);
-        umma_commit(mma_done);
+        for (int k = 0; k < 4; ++k) umma_f16_ts(tmem + cK, tmem + (128u + half * 64u) + k * 8, mndesc(aQ, k), id_acc, (u | k) != 0);
+        if (half == 1) umma_commit(&qd_empty[st]);
       }
+      umma_commit(mma_done);
     }
     __syncwarp();
   } else if (warp >= 4) {
+    // 8 compute warps: warps w and w+4 share TMEM lane quadrant w%4 (key rows) and split
+    // each 64-query sub-tile into two 32-column halves (ch)
     const int q = warp & 3;
-    const int t = threadIdx.x - 128;  // 0..127: key row inside the tile
+    const int ch = (warp - 4) >> 2;
+    const int t = q * 32 + lane;       // key row inside the tile
+    const int tt = threadIdx.x - 128;  // 0..255
     const uint32_t lo = (uint32_t)(q * 32) << 16;
     const float c = p.scale * kLog2e;
-    for (int it = 0; it < total; ++it) {
+    for (int u = 0; u < U; ++u) {
+      const int it = u >> 1, half = u & 1;
       const int h = kvh * group + it / nq, q0 = (it % nq) * BT;
-      float* L = sL + (it & 1) * 128;
-      float* D = sD + (it & 1) * 128;
-      {
-        const int qi = q0 + t;
-        const int64_t li = ((int64_t)b * p.H + h) * p.T + qi;
-        L[t] = qi < p.T ? p.lse[li] * kLog2e : 0.f;
-        D[t] = qi < p.T ? p.delta[li] : 0.f;
+      const float* L = sL + (it & 1) * 128 + half * 64 + ch * 32;
+      const float* D = sD + (it & 1) * 128 + half * 64 + ch * 32;
+      if (half == 0) {
+        if (tt < 128) {
+          const int qi = q0 + tt;
+          const int64_t li = ((int64_t)b * p.H + h) * p.T + qi;
+          sL[(it & 1) * 128 + tt] = qi < p.T ? p.lse[li] * kLog2e : 0.f;
+          sD[(it & 1) * 128 + tt] = qi < p.T ? p.delta[li] : 0.f;
+        }
+        named_sync(1, 256);
       }
-      named_sync(1, 128);
-      const int valid = min(BT, p.T - q0);
-      mbar_wait(s_full, it & 1);
+      const int valid = min(64, p.T - (q0 + half * 64)) - ch * 32;
+      mbar_wait(&s_full[half], (u >> 1) & 1);
       tc_fence_after();
-      float pr[128];
+      float pr[32];
       {
         uint32_t v[32];
+        tmem_ld32(tmem + lo + half * 64u + ch * 32, v);
+        tmem_ld_wait();
+        if (valid >= 32) {
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          tmem_ld32(tmem + lo + cS + cc * 32, v);
-          tmem_ld_wait();
+          for (int i = 0; i < 32; ++i) pr[i] = fast_exp2(fmaf(__uint_as_float(v[i]), c, -L[i]));
+        } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int col = cc * 32 + i;
-            pr[col] = col < valid ? exp2f(__uint_as_float(v[i]) * c - L[col]) : 0.f;
-          }
+          for (int i = 0; i < 32; ++i) pr[i] = i < valid ? fast_exp2(fmaf(__uint_as_float(v[i]), c, -L[i])) : 0.f;
         }
-        uint32_t pk[32];
+        uint32_t pk[16];
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) pk[i] = pack2(pr[hh * 64 + 2 * i], pr[hh * 64 + 2 * i + 1]);
-          tmem_st32(tmem + lo + cS + hh * 32, pk);
-        }
+        for (int i = 0; i < 16; ++i) pk[i] = pack2(pr[2 * i], pr[2 * i + 1]);
+        named_sync(2 + q, 64);  // the partner warp has read its raw S columns
+        tmem_st16(tmem + lo + half * 64u + ch * 16, pk);
         tmem_st_wait();
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_ready);
-      mbar_wait(dp_full, it & 1);
+      if (lane == 0) mbar_arrive(&p_ready[half]);
+      mbar_wait(&dp_full[half], (u >> 1) & 1);
       tc_fence_after();
       {
         uint32_t v[32];
         uint32_t pk[16];
+        tmem_ld32(tmem + lo + 128u + half * 64u + ch * 32, v);
+        tmem_ld_wait();
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          tmem_ld32(tmem + lo + cP + cc * 32, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int col = cc * 32 + 2 * i;
-            const float d0 = pr[col] * (__uint_as_float(v[2 * i]) - D[col]);
-            const float d1 = pr[col + 1] * (__uint_as_float(v[2 * i + 1]) - D[col + 1]);
-            pk[i] = pack2(d0, d1);
-          }
-          // dS^T chunk cc covers keys' columns [32cc, 32cc+32) -> packed columns [16cc, 16cc+16)
-          asm volatile(
-              "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-              "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(tmem + lo + cP + cc * 16),
-              "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3]), "r"(pk[4]), "r"(pk[5]), "r"(pk[6]), "r"(pk[7]),
-              "r"(pk[8]), "r"(pk[9]), "r"(pk[10]), "r"(pk[11]), "r"(pk[12]), "r"(pk[13]), "r"(pk[14]), "r"(pk[15])
-              : "memory");
-        }
+        for (int i = 0; i < 16; ++i)
+          pk[i] = pack2(pr[2 * i] * (__uint_as_float(v[2 * i]) - D[2 * i]),
+                        pr[2 * i + 1] * (__uint_as_float(v[2 * i + 1]) - D[2 * i + 1]));
+        named_sync(2 + q, 64);
+        tmem_st16(tmem + lo + 128u + half * 64u + ch * 16, pk);
         tmem_st_wait();
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(ds_ready);
+      if (lane == 0) mbar_arrive(&ds_ready[half]);
     }
-    mbar_wait(mma_done, (total - 1) & 1);
+    mbar_wait(mma_done, 0);
     tc_fence_after();
     const int krow = k0 + t;
     const bool ok = krow < p.T;
-    store_row(tmem + lo + cK, p.o0 + ((int64_t)row0 + krow) * p.ld0 + (int64_t)kvh * HD, p.scale, ok);
-    store_row(tmem + lo + cV, p.o1 + ((int64_t)row0 + krow) * p.ld1 + (int64_t)kvh * HD, 1.f, ok);
+    if (ch == 0) {
+      const float* rc = p.rope_cos ? p.rope_cos + (int64_t)(ok ? krow : 0) * (HD / 2) : nullptr;
+      const float* rs = p.rope_sin ? p.rope_sin + (int64_t)(ok ? krow : 0) * (HD / 2) : nullptr;
+      store_row(tmem + lo + cK, p.o0 + ((int64_t)row0 + krow) * p.ld0 + (int64_t)kvh * HD, p.scale, ok, rc, rs);
+    } else {
+      store_row(tmem + lo + cV, p.o1 + ((int64_t)row0 + krow) * p.ld1 + (int64_t)kvh * HD, 1.f, ok);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -278,10 +315,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;   // [2]
   uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* dp_full = bars + 6;
-  uint64_t* ds_ready = bars + 7;
-  uint64_t* mma_done = bars + 8;
+  uint64_t* s_full = bars + 5;    // [2]
+  uint64_t* dp_full = bars + 7;
+  uint64_t* ds_ready = bars + 8;
+  uint64_t* mma_done = bars + 9;
   uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 10);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -299,10 +336,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
+      mbar_init(&s_full[s], 1);
     }
-    mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
-    mbar_init(ds_ready, 4);
+    mbar_init(ds_ready, 8);
     mbar_init(mma_done, 1);
     fence_mbar_init();
   }
@@ -311,7 +348,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *slot;
-  const uint32_t cS = 0, cP = 128, cQ = 256;
+  // TMEM columns: S buffers at st*128
+  const uint32_t cP = 256, cQ = 384;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -338,30 +376,44 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t id_s = idesc_bf16_f32(128, 128, 0, 0);
       const uint32_t id_acc = idesc_bf16_f32(128, 128, 0, 1);
       const uint32_t aQ = smem_u32(sQ), aG = smem_u32(sG);
-      mbar_wait(q_full, 0);
-      for (int j = 0; j < nk; ++j) {
+      auto issue_s = [&](int j) {
         const int st = j & 1;
-        const uint32_t aK = smem_u32(ring + st * 2 * kTile), aV = aK + kTile;
         mbar_wait(&kv_full[st], (j >> 1) & 1);
         tc_fence_after();
+        const uint32_t aK = smem_u32(ring + st * 2 * kTile);
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + cS, kdesc(aQ, kk), kdesc(aK, kk), id_s, kk > 0);
-        umma_commit(s_full);
+        for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + (st * 128u), kdesc(aQ, kk), kdesc(aK, kk), id_s, kk > 0);
+        umma_commit(&s_full[st]);
+      };
+      auto issue_dp = [&](int j) {
+        const uint32_t aV = smem_u32(ring + (j & 1) * 2 * kTile) + kTile;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + cP, kdesc(aG, kk), kdesc(aV, kk), id_s, kk > 0);
         umma_commit(dp_full);
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      issue_dp(0);
+      for (int j = 0; j < nk; ++j) {
+        const int st = j & 1;
+        if (j + 1 < nk) issue_s(j + 1);
         mbar_wait(ds_ready, j & 1);
         tc_fence_after();
+        const uint32_t aK = smem_u32(ring + st * 2 * kTile);
 #pragma unroll
-        for (int k = 0; k < BT / 16; ++k) umma_f16_ts(tmem + cQ, tmem + cS + k * 8, mndesc(aK, k), id_acc, (j | k) != 0);
+        for (int k = 0; k < BT / 16; ++k) umma_f16_ts(tmem + cQ, tmem + (st * 128u) + k * 8, mndesc(aK, k), id_acc, (j | k) != 0);
         umma_commit(&kv_empty[st]);
-        umma_commit(mma_done);
+        if (j + 1 < nk) issue_dp(j + 1);
       }
+      umma_commit(mma_done);
     }
     __syncwarp();
   } else if (warp >= 4) {
+    // 8 compute warps: warps w and w+4 share lane quadrant w%4 (query rows) and split each
+    // 128-key tile into two 64-column halves (ch)
     const int q = warp & 3;
-    const int t = threadIdx.x - 128;
+    const int ch = (warp - 4) >> 2;
+    const int t = q * 32 + lane;
     const uint32_t lo = (uint32_t)(q * 32) << 16;
     const float c = p.scale * kLog2e;
     const int qrow = q0 + t;
@@ -370,20 +422,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float L = ok ? p.lse[li] * kLog2e : 0.f;
     const float D = ok ? p.delta[li] : 0.f;
     for (int j = 0; j < nk; ++j) {
-      const int valid = min(BT, p.T - j * BT);
-      mbar_wait(s_full, j & 1);
+      const int st = j & 1;
+      const int valid = min(BT, p.T - j * BT) - ch * 64;
+      mbar_wait(&s_full[st], (j >> 1) & 1);
       tc_fence_after();
-      float pr[128];
+      float pr[64];
       {
         uint32_t v[32];
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          tmem_ld32(tmem + lo + cS + cc * 32, v);
+        for (int cc = 0; cc < 2; ++cc) {
+          tmem_ld32(tmem + lo + st * 128u + ch * 64 + cc * 32, v);
           tmem_ld_wait();
+          if (valid >= 64) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int col = cc * 32 + i;
-            pr[col] = col < valid ? exp2f(__uint_as_float(v[i]) * c - L) : 0.f;
+            for (int i = 0; i < 32; ++i) pr[cc * 32 + i] = fast_exp2(fmaf(__uint_as_float(v[i]), c, -L));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              pr[cc * 32 + i] = cc * 32 + i < valid ? fast_exp2(fmaf(__uint_as_float(v[i]), c, -L)) : 0.f;
           }
         }
       }
@@ -391,32 +447,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       {
         uint32_t v[32];
-        uint32_t pk[16];
+        uint32_t pk[2][16];
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          tmem_ld32(tmem + lo + cP + cc * 32, v);
+        for (int cc = 0; cc < 2; ++cc) {
+          tmem_ld32(tmem + lo + cP + ch * 64 + cc * 32, v);
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int col = cc * 32 + 2 * i;
-            pk[i] = pack2(pr[col] * (__uint_as_float(v[2 * i]) - D), pr[col + 1] * (__uint_as_float(v[2 * i + 1]) - D));
+            pk[cc][i] = pack2(pr[col] * (__uint_as_float(v[2 * i]) - D), pr[col + 1] * (__uint_as_float(v[2 * i + 1]) - D));
           }
-          asm volatile(
-              "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-              "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(tmem + lo + cS + cc * 16),
-              "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3]), "r"(pk[4]), "r"(pk[5]), "r"(pk[6]), "r"(pk[7]),
-              "r"(pk[8]), "r"(pk[9]), "r"(pk[10]), "r"(pk[11]), "r"(pk[12]), "r"(pk[13]), "r"(pk[14]), "r"(pk[15])
-              : "memory");
         }
+        named_sync(2 + q, 64);  // both halves have read their raw S columns
+        tmem_st16(tmem + lo + st * 128u + ch * 32, pk[0]);
+        tmem_st16(tmem + lo + st * 128u + ch * 32 + 16, pk[1]);
         tmem_st_wait();
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_ready);
     }
-    mbar_wait(mma_done, (nk - 1) & 1);
+    mbar_wait(mma_done, 0);
     tc_fence_after();
-    store_row(tmem + lo + cQ, p.o0 + ((int64_t)row0 + qrow) * p.ld0 + (int64_t)h * HD, p.scale, ok);
+    const float* rc = p.rope_cos ? p.rope_cos + (int64_t)(ok ? qrow : 0) * (HD / 2) : nullptr;
+    const float* rs = p.rope_sin ? p.rope_sin + (int64_t)(ok ? qrow : 0) * (HD / 2) : nullptr;
+    store_row_half(tmem + lo + cQ + ch * 64, p.o0 + ((int64_t)row0 + qrow) * p.ld0 + (int64_t)h * HD + ch * 64,
+                   p.scale, ok, rc ? rc + ch * 32 : nullptr, rs ? rs + ch * 32 : nullptr);
   }
   tc_fence_before();
   __syncthreads();
@@ -430,7 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 int attn_bwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, const void* dout, int64_t lddo,
                 const float* lse, const float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
-                int64_t lddv, cudaStream_t st) {
+                int64_t lddv, cudaStream_t st, const float* rope_cos, const float* rope_sin) {
   using namespace tcb;
   if ((lddo | lddq | lddk | lddv) & 7) return fail(CB_ERR_ARG, "tc attention bwd: strides must be 16-byte aligned");
   CUtensorMap mq, mk, mv, mg;
@@ -446,10 +502,11 @@ int attn_bwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, 
     cudaFuncSetAttribute(dq_k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     attr = true;
   }
-  Params pk{g.T, g.H, g.KVH, g.B, g.scale, lse, delta, (__nv_bfloat16*)dk, lddk, (__nv_bfloat16*)dv, lddv};
+  Params pk{g.T, g.H, g.KVH, g.B, g.scale, lse, delta, (__nv_bfloat16*)dk, lddk, (__nv_bfloat16*)dv, lddv,
+            rope_cos, rope_sin};
   dkdv_k<<<dim3((g.T + BT - 1) / BT, g.KVH, g.B), kThreads, kSmem, st>>>(mq, mk, mv, mg, pk);
   if (int e = check_launch("flash_bwd_dkdv_tc")) return e;
-  Params pq{g.T, g.H, g.KVH, g.B, g.scale, lse, delta, (__nv_bfloat16*)dq, lddq, nullptr, 0};
+  Params pq{g.T, g.H, g.KVH, g.B, g.scale, lse, delta, (__nv_bfloat16*)dq, lddq, nullptr, 0, rope_cos, rope_sin};
   dq_k<<<dim3((g.T + BT - 1) / BT, g.H, g.B), kThreads, kSmem, st>>>(mq, mk, mv, mg, pq);
   return check_launch("flash_bwd_dq_tc");
 }

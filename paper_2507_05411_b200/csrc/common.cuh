@@ -66,9 +66,10 @@ template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(flo
 // Overflow-safe logistic, the same two-branch form as the reference _sigmoid
 // (reference layers.py:55-61).
 __device__ __forceinline__ float stable_sigmoid(float x) {
-  if (x >= 0.f) return 1.f / (1.f + __expf(-x));
-  const float e = __expf(x);
-  return e / (1.f + e);
+  // e = exp(-|x|) never overflows; x >= 0 -> 1/(1+e), x < 0 -> e/(1+e)
+  const float e = __expf(-fabsf(x));
+  const float r = __fdividef(1.f, 1.f + e);
+  return x >= 0.f ? r : e * r;
 }
 
 // ------------------------------------------------------------------------------------
@@ -191,6 +192,14 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
       : "memory");
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&p)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3]), "r"(p[4]), "r"(p[5]), "r"(p[6]), "r"(p[7]), "r"(p[8]), "r"(p[9]),
+      "r"(p[10]), "r"(p[11]), "r"(p[12]), "r"(p[13]), "r"(p[14]), "r"(p[15])
+      : "memory");
+}
 
 // UMMA shared-memory matrix descriptor, 128-byte swizzle, sm_100 layout version 1.
 //   bits [0,14)  start address >> 4

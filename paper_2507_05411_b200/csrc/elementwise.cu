@@ -129,13 +129,24 @@ __global__ void __launch_bounds__(256) gated_bwd_k(int cols, int cb, int a0, int
     d[0] = to_f32(dout[r * lddo + c]);
     if (g) y[0] = to_f32(g[r * ldg + c]);
   }
+  if (g && a0 == ACT_LINEAR && a1 == ACT_SILU) {
+    // SwiGLU: one sigmoid per element serves silu(g) and silu'(g)
 #pragma unroll
-  for (int i = 0; i < W; ++i) {
-    if (g) {
-      ra[i] = d[i] * act_f(a1, y[i]) * act_df(a0, x[i]);
-      rg[i] = d[i] * act_f(a0, x[i]) * act_df(a1, y[i]);
-    } else {
-      ra[i] = d[i] * act_df(a0, x[i]);
+    for (int i = 0; i < W; ++i) {
+      const float s = stable_sigmoid(y[i]);
+      const float sg = y[i] * s;
+      ra[i] = d[i] * sg;
+      rg[i] = d[i] * x[i] * (s + sg * (1.f - s));
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      if (g) {
+        ra[i] = d[i] * act_f(a1, y[i]) * act_df(a0, x[i]);
+        rg[i] = d[i] * act_f(a0, x[i]) * act_df(a1, y[i]);
+      } else {
+        ra[i] = d[i] * act_df(a0, x[i]);
+      }
     }
   }
   if constexpr (VEC) {

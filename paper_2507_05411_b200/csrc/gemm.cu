@@ -31,6 +31,11 @@ struct Epi {
   float alpha;
   int accumulate;
   int M, N;
+  // optional RoPE on output columns [0, rope_cols): rows are tokens (position = row % rope_T),
+  // interleaved pairs inside heads of rope_hd columns (reference layers.py:235-257)
+  const float* rope_cos = nullptr;
+  const float* rope_sin = nullptr;
+  int rope_T = 0, rope_hd = 0, rope_cols = 0;
 };
 
 __device__ __forceinline__ float epi_load(const void* p, int64_t idx, int f32) {
@@ -211,6 +216,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_wait();
         const int col0 = tn * BN + c * 32;
         if (!row_ok || col0 >= e.N) continue;
+        if (e.rope_cos && col0 < e.rope_cols) {
+          // 32 columns = 16 pairs of one head (rope_hd % 32 == 0 is required on this path)
+          const int half = e.rope_hd >> 1;
+          const int p0 = (col0 % e.rope_hd) >> 1;
+          const int64_t tb = (int64_t)(row % e.rope_T) * half + p0;
+          const float4* cs4 = reinterpret_cast<const float4*>(e.rope_cos + tb);
+          const float4* sn4 = reinterpret_cast<const float4*>(e.rope_sin + tb);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 cq = cs4[j], sq = sn4[j];
+            const float cc[4] = {cq.x, cq.y, cq.z, cq.w}, ss[4] = {sq.x, sq.y, sq.z, sq.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int k = (j * 4 + i) * 2;
+              const float ev = __uint_as_float(v[k]), od = __uint_as_float(v[k + 1]);
+              v[k] = __float_as_uint(ev * cc[i] - od * ss[i]);
+              v[k + 1] = __float_as_uint(ev * ss[i] + od * cc[i]);
+            }
+          }
+        }
         const bool full_chunk = col0 + 32 <= e.N;
         const bool fast = full_chunk && !e.accumulate && !e.R && e.alpha == 1.f && !e.d_f32 && ((e.ldd & 7) == 0) &&
                           ((reinterpret_cast<uintptr_t>(e.D) & 15) == 0);
@@ -401,6 +426,7 @@ __global__ void __launch_bounds__(256) gemm_simt(int M, int N, int K, const T* _
 }  // namespace simt
 
 static int g_gemm_path = 0;  // 0 auto, 1 force SIMT, 2 force tcgen05
+static thread_local int g_last_gemm_tc = 0;  // did the last gemm_impl call run on tcgen05?
 
 }  // namespace cb
 
@@ -412,16 +438,52 @@ extern "C" int cb_gemm_set_path(int path) {
   return CB_OK;
 }
 
+static int gemm_impl(int M, int N, int K, int in_dtype, const void* A, int64_t lda, int trans_a, const void* B,
+                     int64_t ldb, int trans_b, void* D, int64_t ldd, int d_dtype, const void* R, int64_t ldr,
+                     int r_dtype, float alpha, int accumulate, cudaStream_t st, Epi e);
+
 // See include/composer_b200.h for the contract.
 extern "C" int cb_gemm(int M, int N, int K, int in_dtype, const void* A, int64_t lda, int trans_a, const void* B,
                        int64_t ldb, int trans_b, void* D, int64_t ldd, int d_dtype, const void* R, int64_t ldr,
                        int r_dtype, float alpha, int accumulate, void* stream) {
+  Epi e{D, ldd, d_dtype == CB_DT_F32, R, ldr, r_dtype == CB_DT_F32, alpha, accumulate, M, N};
+  return gemm_impl(M, N, K, in_dtype, A, lda, trans_a, B, ldb, trans_b, D, ldd, d_dtype, R, ldr, r_dtype, alpha,
+                   accumulate, reinterpret_cast<cudaStream_t>(stream), e);
+}
+
+// D = op(A) @ op(B) with RoPE applied to output columns [0, rope_cols) (the q|k part of a
+// fused QKV projection) inside the tcgen05 epilogue; other engines rotate in a second pass.
+extern "C" int cb_gemm_rope(int M, int N, int K, int in_dtype, const void* A, int64_t lda, int trans_a, const void* B,
+                            int64_t ldb, int trans_b, void* D, int64_t ldd, int d_dtype, int seq_len, int head_dim,
+                            int rope_cols, const float* cos_t, const float* sin_t, void* stream) {
+  if (head_dim <= 0 || head_dim % 2 || rope_cols % head_dim || rope_cols > N)
+    return fail(CB_ERR_SHAPE, "gemm_rope: bad head_dim %d / rope_cols %d", head_dim, rope_cols);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Epi e{D, ldd, d_dtype == CB_DT_F32, nullptr, 0, 0, 1.f, 0, M, N};
+  const bool fuse = in_dtype == CB_DT_BF16 && head_dim % 32 == 0 && seq_len > 0 &&
+                    !(reinterpret_cast<uintptr_t>(cos_t) & 15) && !(reinterpret_cast<uintptr_t>(sin_t) & 15);
+  if (fuse) {
+    e.rope_cos = cos_t;
+    e.rope_sin = sin_t;
+    e.rope_T = seq_len;
+    e.rope_hd = head_dim;
+    e.rope_cols = rope_cols;
+  }
+  int s = gemm_impl(M, N, K, in_dtype, A, lda, trans_a, B, ldb, trans_b, D, ldd, d_dtype, nullptr, 0, 0, 1.f, 0, st, e);
+  if (s) return s;
+  if (fuse && g_last_gemm_tc) return CB_OK;
+  // the SIMT engine ignores the rope fields: rotate in a separate pass
+  return cb_rope(M, seq_len, rope_cols / head_dim, head_dim, D, ldd, d_dtype, cos_t, sin_t, 0, stream);
+}
+
+static int gemm_impl(int M, int N, int K, int in_dtype, const void* A, int64_t lda, int trans_a, const void* B,
+                     int64_t ldb, int trans_b, void* D, int64_t ldd, int d_dtype, const void* R, int64_t ldr,
+                     int r_dtype, float alpha, int accumulate, cudaStream_t st, Epi e) {
+  g_last_gemm_tc = 0;
   if (M < 0 || N < 0 || K < 0) return fail(CB_ERR_SHAPE, "gemm: negative extent (%d,%d,%d)", M, N, K);
   if (!D) return fail(CB_ERR_ARG, "gemm: null output");
   if (M == 0 || N == 0) return CB_OK;
   if (in_dtype != CB_DT_F32 && in_dtype != CB_DT_BF16) return fail(CB_ERR_UNSUPPORTED, "gemm: input dtype %d", in_dtype);
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  Epi e{D, ldd, d_dtype == CB_DT_F32, R, ldr, r_dtype == CB_DT_F32, alpha, accumulate, M, N};
   if (K == 0) {
     // alpha*0 (+D) (+R): route through the SIMT epilogue with an empty reduction
     dim3 grid((N + simt::TN - 1) / simt::TN, (M + simt::TM - 1) / simt::TM);
@@ -446,6 +508,7 @@ extern "C" int cb_gemm(int M, int N, int K, int in_dtype, const void* A, int64_t
       a.b_mn = trans_b ? 0 : 1;
       a.e = e;
       a.tiles_m = (M + tc::BM - 1) / tc::BM;
+      g_last_gemm_tc = 1;
       if (N > 128) {
         a.tiles_n = (N + 255) / 256;
         return tc::launch<256>(a, A, lda, B, ldb, st);

@@ -175,13 +175,24 @@ __global__ void __launch_bounds__(256) rmsnorm_dscale_partial_k(int rows, int di
   partial[(int64_t)chunk * dim + col] = acc;
 }
 
-__global__ void col_reduce_k(int nparts, int dim, const float* __restrict__ partial, float* __restrict__ out,
-                             int accumulate) {
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= dim) return;
+// 256 threads = 32 columns x 8 row lanes; lane r sums parts r, r+8, ... in order, then
+// lane 0 adds the 8 lane sums in order: a fixed summation order (deterministic).
+__global__ void __launch_bounds__(256) col_reduce_k(int nparts, int dim, const float* __restrict__ partial,
+                                                    float* __restrict__ out, int accumulate) {
+  __shared__ float red[8][33];
+  const int c = threadIdx.x & 31, r = threadIdx.x >> 5;
+  const int col = blockIdx.x * 32 + c;
   float acc = 0.f;
-  for (int p = 0; p < nparts; ++p) acc += partial[(int64_t)p * dim + col];
-  out[col] = accumulate ? out[col] + acc : acc;
+  if (col < dim)
+    for (int p = r; p < nparts; p += 8) acc += partial[(int64_t)p * dim + col];
+  red[r][c] = acc;
+  __syncthreads();
+  if (r == 0 && col < dim) {
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += red[i][c];
+    out[col] = accumulate ? out[col] + s : s;
+  }
 }
 
 static bool vec_ok(int dim, const void* const* ptrs, const int64_t* lds, int n, int elem_align = 8) {
@@ -237,7 +248,7 @@ static int launch_bwd(int rows, int dim, const void* x, int64_t ldx, const float
                                                     dscale ? workspace : nullptr);
     if (int s = check_launch("rmsnorm_bwd")) return s;
     if (dscale) {
-      col_reduce_k<<<(dim + 255) / 256, 256, 0, st>>>(P, dim, workspace, dscale, 1);
+      col_reduce_k<<<(dim + 31) / 32, 256, 0, st>>>(P, dim, workspace, dscale, 1);
       return check_launch("rmsnorm_dscale_reduce");
     }
     return CB_OK;
@@ -252,7 +263,7 @@ static int launch_bwd(int rows, int dim, const void* x, int64_t ldx, const float
     rmsnorm_dscale_partial_k<TX, TG><<<grid, 256, 0, st>>>(rows, dim, rpc, (const TX*)x, ldx, rstd, (const TG*)dy,
                                                           lddy, workspace);
     if (int s = check_launch("rmsnorm_dscale_partial")) return s;
-    col_reduce_k<<<(dim + 255) / 256, 256, 0, st>>>(chunks, dim, workspace, dscale, 1);
+    col_reduce_k<<<(dim + 31) / 32, 256, 0, st>>>(chunks, dim, workspace, dscale, 1);
     return check_launch("rmsnorm_dscale_reduce");
   }
   return CB_OK;
@@ -278,6 +289,6 @@ extern "C" int cb_rmsnorm_bwd(int rows, int dim, const void* x, int64_t ldx, int
 
 extern "C" int cb_col_reduce(int nparts, int dim, const float* partial, float* out, int accumulate, void* stream) {
   if (nparts <= 0 || dim <= 0) return CB_OK;
-  col_reduce_k<<<(dim + 255) / 256, 256, 0, (cudaStream_t)stream>>>(nparts, dim, partial, out, accumulate);
+  col_reduce_k<<<(dim + 31) / 32, 256, 0, (cudaStream_t)stream>>>(nparts, dim, partial, out, accumulate);
   return check_launch("col_reduce");
 }

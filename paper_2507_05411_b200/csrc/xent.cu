@@ -86,6 +86,82 @@ __global__ void __launch_bounds__(512) xent_k(int T, int V, const TL* __restrict
   }
 }
 
+// Single-HBM-pass variant for f32 logits: the row lives in registers (NV4 float4 per thread,
+// V <= NV4 * 4 * 1024), so logits are read once and dlogits written once.
+__device__ __forceinline__ void combine_ms(float& m, float& s, float m2, float s2) {
+  const float mm = fmaxf(m, m2);
+  s = (m == -INFINITY ? 0.f : s * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
+  m = mm;
+}
+
+template <int NV4, typename TG>
+__global__ void __launch_bounds__(1024) xent_reg_k(int T, int V, const float* __restrict__ logits, int64_t ld,
+                                                   const int64_t* __restrict__ tokens, float* __restrict__ row_loss,
+                                                   TG* __restrict__ dlogits, int64_t ldg, float grad_scale) {
+  __shared__ float sm[32], ss[32];
+  const int64_t row = blockIdx.x;
+  const int t = (int)(row % T);
+  const float* lr = logits + row * ld;
+  TG* gr = dlogits ? dlogits + row * ldg : nullptr;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int V4 = V >> 2;
+  if (t == T - 1) {
+    if (gr)
+      for (int i = tid; i < V; i += blockDim.x) gr[i] = from_f32<TG>(0.f);
+    if (tid == 0) row_loss[row] = 0.f;
+    return;
+  }
+  const int64_t target = tokens[row + 1];
+  const float target_logit = tid == 0 ? lr[target] : 0.f;
+  float4 r[NV4];
+  float m = -INFINITY, s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV4; ++i) {
+    const int j = i * 1024 + tid;
+    if (j < V4) {
+      r[i] = reinterpret_cast<const float4*>(lr)[j];
+      const float mx = fmaxf(fmaxf(r[i].x, r[i].y), fmaxf(r[i].z, r[i].w));
+      const float sub = __expf(r[i].x - mx) + __expf(r[i].y - mx) + __expf(r[i].z - mx) + __expf(r[i].w - mx);
+      combine_ms(m, s, mx, sub);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) combine_ms(m, s, __shfl_xor_sync(0xffffffffu, m, o), __shfl_xor_sync(0xffffffffu, s, o));
+  if (lane == 0) {
+    sm[wid] = m;
+    ss[wid] = s;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    m = lane < (int)(blockDim.x >> 5) ? sm[lane] : -INFINITY;
+    s = lane < (int)(blockDim.x >> 5) ? ss[lane] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) combine_ms(m, s, __shfl_xor_sync(0xffffffffu, m, o), __shfl_xor_sync(0xffffffffu, s, o));
+    if (lane == 0) {
+      sm[0] = m;
+      ss[0] = s;
+    }
+  }
+  __syncthreads();
+  m = sm[0];
+  s = ss[0];
+  if (tid == 0) row_loss[row] = m + logf(s) - target_logit;
+  if (!gr) return;
+  const float inv = grad_scale / s;
+#pragma unroll
+  for (int i = 0; i < NV4; ++i) {
+    const int j = i * 1024 + tid;
+    if (j < V4) {
+      float p[4] = {__expf(r[i].x - m) * inv, __expf(r[i].y - m) * inv, __expf(r[i].z - m) * inv,
+                    __expf(r[i].w - m) * inv};
+      const int base = j * 4;
+      if (target >= base && target < base + 4) p[target - base] -= grad_scale;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) gr[base + e] = from_f32<TG>(p[e]);
+    }
+  }
+}
+
 // Deterministic mean of row losses (rows with t == T-1 are zero and excluded from the count).
 __global__ void __launch_bounds__(1024) loss_reduce_k(int64_t rows, int64_t count, const float* __restrict__ row_loss,
                                                       double* __restrict__ out64, float* __restrict__ out32) {
@@ -119,7 +195,16 @@ extern "C" int cb_xent_fwd_bwd(int batch, int seq_len, int vocab, const void* lo
   if (vocab <= 0) return fail(CB_ERR_SHAPE, "xent: vocab must be positive");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t rows = (int64_t)batch * seq_len;
-  if (l_dtype == CB_DT_F32 && g_dtype == CB_DT_F32)
+  const bool reg_ok = l_dtype == CB_DT_F32 && vocab % 4 == 0 && vocab <= 8 * 4 * 1024 && (ld % 4) == 0 &&
+                      !(reinterpret_cast<uintptr_t>(logits) & 15) && (!dlogits || dlogits != logits);
+  if (reg_ok) {
+    if (g_dtype == CB_DT_F32)
+      xent_reg_k<8, float><<<rows, 1024, 0, st>>>(seq_len, vocab, (const float*)logits, ld, tokens, row_loss,
+                                                  (float*)dlogits, ldg, grad_scale);
+    else
+      xent_reg_k<8, __nv_bfloat16><<<rows, 1024, 0, st>>>(seq_len, vocab, (const float*)logits, ld, tokens, row_loss,
+                                                          (__nv_bfloat16*)dlogits, ldg, grad_scale);
+  } else if (l_dtype == CB_DT_F32 && g_dtype == CB_DT_F32)
     xent_k<float, float><<<rows, 512, 0, st>>>(seq_len, vocab, (const float*)logits, ld, tokens, row_loss,
                                                (float*)dlogits, ldg, grad_scale);
   else if (l_dtype == CB_DT_F32)

@@ -390,19 +390,30 @@ class AttentionBehavior(Behavior):
         x2 = ops.cast(ops.rows2d(x), adt)
         wq, wk, wv, wo = param("wq"), param("wk"), param("wv"), param("wo")
         wqkv = fused_columns(wq, wk, wv)
+        pos = module.children["pos_emb"]
+        # RoPE folded into the QKV GEMM epilogue (and its inverse into the attention
+        # backward's dQ/dK stores) when the positional child is the stock RoPE kind
+        rope = None
+        if wqkv is not None and pos.kind == "RoPE" and option("fuse_rope", True):
+            rope = rope_tables(T, hd, pos.config.get("base"), x.device)
         if wqkv is not None:
-            qkv = _linear_fwd(x2, wqkv, adt)
+            qkv = torch.empty((x2.shape[0], wqkv.shape[1]), device=x.device, dtype=adt)
+            if rope is not None:
+                ops.gemm_rope(x2, wqkv, qkv, T, hd, d + kvd, rope[0], rope[1])
+            else:
+                ops.gemm(x2, wqkv, qkv)
         else:
             qkv = torch.empty((x2.shape[0], d + 2 * kvd), device=x.device, dtype=adt)
             for w, c0, c1 in ((wq, 0, d), (wk, d, d + kvd), (wv, d + kvd, d + 2 * kvd)):
                 ops.gemm(x2, w, qkv[:, c0:c1])
         q, k, v = qkv[:, :d], qkv[:, d:d + kvd], qkv[:, d + kvd:]
-        invoke_child("pos_emb", q, k, T)
+        if rope is None:
+            invoke_child("pos_emb", q, k, T)
         scale = 1.0 / math.sqrt(hd)
         o, lse = ops.attention_fwd(q, k, v, B, T, H, KVH, hd, scale)
         out = torch.empty((o.shape[0], d), device=x.device, dtype=torch.float32)
         ops.gemm(o, wo, out, residual=ops.rows2d(residual) if residual is not None else None)
-        save(x2=x2, qkv=qkv, o=o, lse=lse, geom=(B, T, H, KVH, hd, d, kvd))
+        save(x2=x2, qkv=qkv, o=o, lse=lse, rope=rope, geom=(B, T, H, KVH, hd, d, kvd))
         return out.view(B, T, d)
 
     def backward(self, module, dout):
@@ -415,8 +426,12 @@ class AttentionBehavior(Behavior):
         dqkv = torch.empty_like(qkv)
         q, k, v = qkv[:, :d], qkv[:, d:d + kvd], qkv[:, d + kvd:]
         dq, dk, dv = dqkv[:, :d], dqkv[:, d:d + kvd], dqkv[:, d + kvd:]
-        ops.attention_bwd(q, k, v, s["o"], s["lse"], do, dq, dk, dv, B, T, H, KVH, hd, 1.0 / math.sqrt(hd))
-        backward_child("pos_emb", dq, dk)
+        if s["rope"] is not None:
+            ops.attention_bwd_rope(q, k, v, s["o"], s["lse"], do, dq, dk, dv, B, T, H, KVH, hd,
+                                   1.0 / math.sqrt(hd), s["rope"][0], s["rope"][1])
+        else:
+            ops.attention_bwd(q, k, v, s["o"], s["lse"], do, dq, dk, dv, B, T, H, KVH, hd, 1.0 / math.sqrt(hd))
+            backward_child("pos_emb", dq, dk)
         wq, wk, wv = param("wq"), param("wk"), param("wv")
         wqkv = fused_columns(wq, wk, wv)
         gq, gk, gv = param_grad("wq"), param_grad("wk"), param_grad("wv")

@@ -113,6 +113,20 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, trans_a: bool = Fa
     return out
 
 
+def gemm_rope(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, seq_len: int, head_dim: int, rope_cols: int,
+              cos_t: torch.Tensor, sin_t: torch.Tensor) -> torch.Tensor:
+    """out = a @ b with RoPE applied to out[:, :rope_cols] (fused into the tcgen05 epilogue)."""
+    M, K = a.shape
+    N = b.shape[1]
+    if b.shape[0] != K or tuple(out.shape) != (M, N):
+        raise ShapeError("gemm_rope: shape mismatch")
+    _profiled("gemm_bf16" if a.dtype == torch.bfloat16 else "gemm_f32", 2 * M * N * K, _lib.call, "cb_gemm_rope",
+              M, N, K, dt(a), a.data_ptr(), ld(a, "A"), 0, b.data_ptr(), ld(b, "B"), 0, out.data_ptr(),
+              ld(out, "out"), dt(out), int(seq_len), int(head_dim), int(rope_cols), cos_t.data_ptr(),
+              sin_t.data_ptr(), stream_ptr())
+    return out
+
+
 def set_gemm_path(path: int) -> None:
     _lib.call("cb_gemm_set_path", int(path))
 
@@ -244,6 +258,15 @@ def attention_fwd(q, k, v, B, T, H, KVH, hd, scale):
               q.data_ptr(), ld(q), k.data_ptr(), ld(k), v.data_ptr(), ld(v), o.data_ptr(), ld(o), lse.data_ptr(),
               float(scale), stream_ptr())
     return o, lse
+
+
+def attention_bwd_rope(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, scale, cos_t, sin_t):
+    """Backward for q/k rotated in the projection epilogue: dq/dk come back un-rotated."""
+    delta = torch.empty((B, H, T), device=q.device, dtype=torch.float32)
+    _profiled("attn_bwd", 8 * B * T * T * H * hd, _lib.call, "cb_attention_bwd_rope", B, T, H, KVH, hd, dt(q),
+              q.data_ptr(), ld(q), k.data_ptr(), ld(k), v.data_ptr(), ld(v), o.data_ptr(), ld(o), lse.data_ptr(),
+              do.data_ptr(), ld(do), delta.data_ptr(), dq.data_ptr(), ld(dq), dk.data_ptr(), ld(dk), dv.data_ptr(),
+              ld(dv), float(scale), cos_t.data_ptr(), sin_t.data_ptr(), stream_ptr())
 
 
 def attention_bwd(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, scale):

@@ -1,0 +1,95 @@
+"""Multi-GPU FSDP parity: run under torchrun with N ranks.
+
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 --master-port 29511 \
+        scripts/fsdp_check.py [--precision f32|bf16] [--config txf_rope|mid] [--steps 2]
+
+Each rank trains on its slice of one global batch; the all-reduced loss, the gathered
+gradients and the updated parameters must match the single-process oracle on the whole
+global batch (parity across N).  Rank 0 prints one JSON line.
+"""
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--precision", default="f32")
+    ap.add_argument("--config", default="txf_rope")
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--batch", type=int, default=8, help="global batch")
+    ap.add_argument("--seq", type=int, default=8)
+    args = ap.parse_args()
+
+    import torch
+    import torch.distributed as dist
+
+    from oracle import decoder_oracle as O
+    from paper_2507_05411_b200 import (TrainEngine, build_experiment, init_state, instantiate, root_key,
+                                       set_dtype_policy, synthetic_batch)
+    from paper_2507_05411_b200.experiments import transformer_trainer
+
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    if args.config == "mid":
+        cfg = transformer_trainer(256, 2, ("linear", "silu"), pos_kind="RoPE", heads=2, vocab=512)
+        for i in range(2):
+            cfg = cfg.set(f"model.decoder.transformer.layer[{i}].feed_forward.hidden_dim", 768)
+    else:
+        cfg = build_experiment(args.config)
+    cfg = set_dtype_policy(cfg, args.precision)
+    eng = TrainEngine(cfg, device=dev)
+    V = eng.cfg.get("model.vocab_size")
+    B, T = args.batch, args.seq
+    assert B % world == 0
+    per = B // world
+
+    m = instantiate(cfg)
+    st = init_state(m, root_key(0))
+    spec = O.spec_from_config(m.config)
+    mm = vv = None
+    out = {"world": world, "precision": args.precision, "config": args.config, "steps": []}
+    tol = 1e-5 if args.precision == "f32" else 2e-2
+    ok = True
+    for step in range(args.steps):
+        toks = synthetic_batch(0, step, B, T, V)["tokens"]
+        mine = toks[rank * per:(rank + 1) * per]
+        loss, _ = eng.compute_grads(mine)
+        loss = float(loss.item())
+        grads = eng.grads_numpy() if step == 0 else None
+        eng.apply_update()
+        lo, go, st, mm, vv, _ = O.train_step(st, toks, spec, O.AdamW(lr=eng.lr), mm, vv, step + 1)
+        rec = {"loss": loss, "oracle": lo, "loss_rel": abs(loss - lo) / lo}
+        ok &= rec["loss_rel"] < tol
+        if grads is not None:
+            worst = 0.0
+            for (k, a), (_, b) in zip(O.leaves(grads), O.leaves(go)):
+                worst = max(worst, float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)))
+            rec["grad_rel_max"] = worst
+            ok &= worst < tol
+        out["steps"].append(rec)
+    params = eng.state_numpy()
+    worst = 0.0
+    for (k, a), (_, b) in zip(O.leaves(params), O.leaves(st)):
+        worst = max(worst, float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)))
+    out["param_rel_max"] = worst
+    ok &= worst < tol
+    out["ok"] = bool(ok)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()

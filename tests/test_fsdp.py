@@ -1,0 +1,103 @@
+"""Multi-process tests of the data-parallel / FSDP path.
+
+CPU (gloo, world size 2, runs here): the invariants FSDP relies on —
+  * the global-batch loss is the mean of equal-size per-rank losses and the global
+    gradient is the mean of per-rank gradients (what reduce-scatter(AVG) computes),
+    checked with the oracle and a real gloo all_reduce;
+  * the flat bucket layout shards into equal, aligned slices whose all-gather
+    reconstructs every parameter view.
+GPU (NCCL, needs >= 2 devices): scripts/fsdp_check.py under torchrun compares the
+engine at N=2 with the single-process oracle on the whole batch.
+"""
+
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    sys.path.insert(0, REPO)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import decoder_oracle as O
+    from paper_2507_05411_b200 import build_experiment, init_state, instantiate, root_key, synthetic_batch
+    from paper_2507_05411_b200.engine import ALIGN, _view, build_layout
+
+    m = instantiate(build_experiment("txf_rope"))
+    st = init_state(m, root_key(0))
+    spec = O.spec_from_config(m.config)
+    toks = synthetic_batch(0, 0, 8, 8)["tokens"]
+    per = 8 // world
+    loss, grads, _ = O.value_and_grad(st, toks[rank * per:(rank + 1) * per], spec)
+    t = torch.tensor([loss], dtype=torch.float64)
+    dist.all_reduce(t)
+    flat = torch.tensor(np.concatenate([g.ravel() for _, g in O.leaves(grads)]), dtype=torch.float64)
+    dist.all_reduce(flat)
+    # bucket sharding: each rank owns an equal aligned slice; all_gather rebuilds the bucket
+    buckets = build_layout(m)
+    ok_views = True
+    for b in buckets:
+        total = (b.numel + ALIGN * world - 1) // (ALIGN * world) * (ALIGN * world)
+        shard = total // world
+        full = torch.arange(total, dtype=torch.float32)
+        mine = full[rank * shard:(rank + 1) * shard].clone()
+        parts = [torch.empty(shard) for _ in range(world)]
+        dist.all_gather(parts, mine)
+        rebuilt = torch.cat(parts)
+        ok_views &= bool(torch.equal(rebuilt, full))
+        for e in b.entries:
+            ok_views &= bool(torch.equal(_view(rebuilt, e), _view(full, e)))
+    if rank == 0:
+        gl, gg, _ = O.value_and_grad(st, toks, spec)
+        gflat = np.concatenate([g.ravel() for _, g in O.leaves(gg)])
+        q.put((float(t.item()) / world, gl, (flat.numpy() / world), gflat, ok_views))
+    dist.destroy_process_group()
+
+
+def test_data_parallel_invariants_gloo():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    mean_loss, global_loss, mean_grad, global_grad, ok_views = res
+    assert abs(mean_loss - global_loss) < 1e-12
+    assert np.linalg.norm(mean_grad - global_grad) / np.linalg.norm(global_grad) < 1e-12
+    assert ok_views
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["f32", "bf16"])
+def test_fsdp_two_gpus_matches_oracle(precision):
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs (run with gpurun --gpus 2)")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(REPO, "scripts", "fsdp_check.py"),
+           "--precision", precision, "--config", "txf_rope" if precision == "f32" else "mid", "--seq",
+           "8" if precision == "f32" else "128"]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
