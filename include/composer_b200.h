@@ -175,6 +175,21 @@ CB_API int cb_moe_router_bwd(int64_t n, int experts, int top_k, const float* pro
 CB_API int cb_invert_perm(int64_t n, const int32_t* perm, int32_t* inv, void* stream);
 CB_API int cb_widen_i32(int64_t n, const int32_t* a, int64_t* b, void* stream);
 
+/* ---------------------------------------------------------------------------------
+ * Parameter init on the device, bit-identical to init_state (prng.py:61-69,
+ * layers.py:114-116): numpy PCG64 stream from (state, inc) (the host derives them from
+ * the key with SeedSequence), uniform(low, high) in C order.  Element i of a tensor with
+ * `cols` columns lands at bucket position offset + (i/cols)*ld + col0 + i%cols (ld = 0:
+ * offset + i).  master (f32) receives positions [master_begin, master_end) (this rank's
+ * shard, indexed from master_begin); work (the full working copy) receives all.
+ * ------------------------------------------------------------------------------- */
+CB_API int cb_init_uniform(uint64_t state_lo, uint64_t state_hi, uint64_t inc_lo, uint64_t inc_hi, int64_t n,
+                           double low, double high, int64_t cols, int64_t ld, int64_t col0, int64_t offset,
+                           float* master, int64_t master_begin, int64_t master_end, void* work, int work_dtype,
+                           void* stream);
+CB_API int cb_init_const(int64_t n, float value, int64_t cols, int64_t ld, int64_t col0, int64_t offset, float* master,
+                         int64_t master_begin, int64_t master_end, void* work, int work_dtype, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -181,9 +181,17 @@ def route_tokens(probs: torch.Tensor, top_k: int):
     return idx, w, dispatch, mean_probs
 
 
-def moe(x, p, ls: LayerSpec):
+def moe(x, p, ls: LayerSpec, forced_idx=None):
+    """forced_idx [B, T, k]: use these expert choices instead of the top-k (the reference's
+    own forced-routing oracle, tests/test_layers.py:352-359); weights still renormalize the
+    router probabilities of the chosen experts."""
     probs = torch.softmax(x @ p["router"], dim=-1)
     idx, w, dispatch, mean_probs = route_tokens(probs, ls.top_k)
+    if forced_idx is not None:
+        idx = torch.as_tensor(np.asarray(forced_idx), dtype=torch.long)
+        picked = torch.gather(probs, -1, idx)
+        w = picked / picked.sum(dim=-1, keepdim=True)
+        dispatch = torch.bincount(idx.reshape(-1), minlength=probs.shape[-1]).to(F64) / idx.numel()
     pair = _act_pair(ls.activation)
     hidden = torch.einsum("btd,edh->ebth", x, p["w1"])
     if pair:
@@ -202,7 +210,8 @@ def moe(x, p, ls: LayerSpec):
     return out, lbl, idx
 
 
-def forward_loss(params: dict, tokens: np.ndarray, spec: ModelSpec, summaries: dict | None = None):
+def forward_loss(params: dict, tokens: np.ndarray, spec: ModelSpec, summaries: dict | None = None,
+                 forced_routing: dict | None = None):
     """params: nested dict of float64 torch tensors in the reference state layout."""
     dec = params["model"]["decoder"]
     tok = torch.as_tensor(np.asarray(tokens), dtype=torch.long)
@@ -214,7 +223,7 @@ def forward_loss(params: dict, tokens: np.ndarray, spec: ModelSpec, summaries: d
         h = x + attention(rmsnorm(x, lp["self_attention_norm"]["scale"], ls.eps1), lp["self_attention"], ls)
         n2 = rmsnorm(h, lp["feed_forward_norm"]["scale"], ls.eps2)
         if ls.ffn == "MoE":
-            f, lbl, _ = moe(n2, lp["feed_forward"], ls)
+            f, lbl, _ = moe(n2, lp["feed_forward"], ls, (forced_routing or {}).get(i))
             if summaries is not None:
                 summaries[f"model.decoder.transformer.layer[{i}].feed_forward/load_balance_loss"] = lbl
         else:
@@ -253,10 +262,10 @@ def leaves(tree, prefix=""):
         yield prefix, tree
 
 
-def value_and_grad(state_np: dict, tokens: np.ndarray, spec: ModelSpec):
+def value_and_grad(state_np: dict, tokens: np.ndarray, spec: ModelSpec, forced_routing: dict | None = None):
     params = to_torch(state_np, requires_grad=True)
     summaries: dict = {}
-    loss = forward_loss(params, tokens, spec, summaries)
+    loss = forward_loss(params, tokens, spec, summaries, forced_routing)
     loss.backward()
 
     def grads(t):
@@ -286,9 +295,10 @@ def adamw_update(p, g, m, v, step: int, opt: AdamW):
     return p, m, v
 
 
-def train_step(state_np: dict, tokens: np.ndarray, spec: ModelSpec, opt: AdamW, m=None, v=None, step: int = 1):
-    """Returns loss, grads, new_state, new_m, new_v (nested numpy dicts)."""
-    loss, grads, summaries = value_and_grad(state_np, tokens, spec)
+def train_step(state_np: dict, tokens: np.ndarray, spec: ModelSpec, opt: AdamW, m=None, v=None, step: int = 1,
+               forced_routing: dict | None = None):
+    """Returns loss, grads, new_state, new_m, new_v, summaries (nested numpy dicts)."""
+    loss, grads, summaries = value_and_grad(state_np, tokens, spec, forced_routing)
 
     def walk(p, g, mm, vv):
         if isinstance(p, dict):

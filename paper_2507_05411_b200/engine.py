@@ -277,7 +277,46 @@ class TrainEngine:
             ops.copy2d(full.view(1, -1), rec["work"].view(1, -1))
 
     def init_params(self, key) -> None:
-        """Reference-identical init (init_state semantics), generated tensor by tensor."""
+        """Reference-identical init, generated on the device (init.cu: numpy's PCG64 stream
+        reproduced bit-exactly from each tensor's key).  Kinds without a declarative
+        ``param_init`` fall back to their host ``init_params``."""
+        from . import _lib
+        from .module import param_key
+        from .prng import pcg64_state
+
+        fallback = False
+        for b, rec in zip(self.buckets, self.bufs):
+            if b.replicated:
+                m0, m1 = 0, rec["total"]
+            else:
+                m0, m1 = self.d.rank * rec["shard"], (self.d.rank + 1) * rec["shard"]
+            work = None if rec["work"] is rec["master"] else rec["work"]
+            wdt = ops.dt(rec["work"])
+            for e in b.entries:
+                mod = self.module.child(e.path) if e.path else self.module
+                spec = mod.behavior.param_init(mod.config)
+                if spec is None or e.name not in spec:
+                    fallback = True
+                    continue
+                n = int(np.prod(e.shape))
+                cols = e.shape[-1] if e.ld else 0
+                kind = spec[e.name]
+                if kind[0] == "uniform":
+                    st, inc = pcg64_state(param_key(self._module_key(key, e.path), e.name))
+                    mask = (1 << 64) - 1
+                    _lib.call("cb_init_uniform", st & mask, st >> 64, inc & mask, inc >> 64, n, float(kind[1]),
+                              float(kind[2]), cols, e.ld, e.col0, e.offset, rec["master"].data_ptr(), m0, m1,
+                              work.data_ptr() if work is not None else None, wdt, ops.stream_ptr())
+                else:
+                    _lib.call("cb_init_const", n, float(kind[1]), cols, e.ld, e.col0, e.offset,
+                              rec["master"].data_ptr(), m0, m1, work.data_ptr() if work is not None else None, wdt,
+                              ops.stream_ptr())
+        torch.cuda.synchronize(self.device)
+        if fallback:
+            self.init_params_host(key)
+
+    def init_params_host(self, key) -> None:
+        """Reference-identical init (init_state semantics) generated on the host, tensor by tensor."""
         from .module import param_key  # noqa: F401
 
         cache: dict = {}

@@ -42,12 +42,14 @@ from .module import (
     param,
     param_grad,
     param_key,
+    recording,
     register_behavior,
     register_spec_function,
     save,
     saved,
 )
 from .prng import RngKey, uniform
+from .remat import decide_tag, resolve_policy
 
 DTYPE_BYTES = {"f32": 4, "bf16": 2, "int8": 1, "fp8": 1}
 ACTIVATION_NAMES = ("linear", "relu", "silu", "sigmoid", "tanh")
@@ -88,6 +90,12 @@ def scaled_hidden_dim(fields, scale: float) -> int:
 def fan_in_uniform(key: RngKey, shape, fan_in: int) -> np.ndarray:
     bound = 1.0 / math.sqrt(fan_in)
     return uniform(key, -bound, bound, tuple(shape))
+
+
+def uniform_spec(fan_in: int) -> tuple:
+    """param_init entry equivalent to fan_in_uniform (layers.py:114-116)."""
+    bound = 1.0 / math.sqrt(fan_in)
+    return ("uniform", -bound, bound)
 
 
 def _pspec(cfg):
@@ -168,6 +176,12 @@ class LinearBehavior(Behavior):
             out["bias"] = np.zeros((cfg.get("output_dim"),), dtype=np.float64)
         return out
 
+    def param_init(self, cfg):
+        out = {"weight": uniform_spec(cfg.get("input_dim"))}
+        if cfg.get("bias"):
+            out["bias"] = ("const", 0.0)
+        return out
+
     def own_flops(self, cfg, batch, seq_len):
         return 2 * batch * seq_len * cfg.get("input_dim") * cfg.get("output_dim")
 
@@ -211,6 +225,9 @@ class RMSNormBehavior(Behavior):
     def init_params(self, cfg, key):
         return {"scale": np.ones((cfg.get("input_dim"),), dtype=np.float64)}
 
+    def param_init(self, cfg):
+        return {"scale": ("const", 1.0)}
+
     def forward(self, module, x):
         cfg = module.config
         if x.shape[-1] != cfg.get("input_dim"):
@@ -253,6 +270,9 @@ class EmbeddingBehavior(Behavior):
 
     def init_params(self, cfg, key):
         return {"weight": fan_in_uniform(param_key(key, "weight"), self.param_shapes(cfg)["weight"], cfg.get("dim"))}
+
+    def param_init(self, cfg):
+        return {"weight": uniform_spec(cfg.get("dim"))}
 
     def remat_tags(self, cfg, batch, seq_len):
         return [RematTag("output", batch * seq_len * cfg.get("dim") * _dbytes(cfg), 0)]
@@ -363,6 +383,9 @@ class AttentionBehavior(Behavior):
     def init_params(self, cfg, key):
         d = cfg.get("input_dim")
         return {n: fan_in_uniform(param_key(key, n), s, d) for n, s in self.param_shapes(cfg).items()}
+
+    def param_init(self, cfg):
+        return {n: uniform_spec(cfg.get("input_dim")) for n in self.param_shapes(cfg)}
 
     def own_flops(self, cfg, batch, seq_len):
         d = cfg.get("input_dim")
@@ -504,6 +527,13 @@ class FeedForwardBehavior(Behavior):
             out["w1_gate"] = fan_in_uniform(param_key(key, "w1_gate"), (d, h), d)
         return out
 
+    def param_init(self, cfg):
+        d, h = cfg.get("input_dim"), cfg.get("hidden_dim")
+        out = {"w1": uniform_spec(d), "w2": uniform_spec(h)}
+        if activation_pair(cfg.get("activation")):
+            out["w1_gate"] = uniform_spec(d)
+        return out
+
     def own_flops(self, cfg, batch, seq_len):
         d, h = cfg.get("input_dim"), cfg.get("hidden_dim")
         rows = batch * seq_len
@@ -615,13 +645,52 @@ class TransformerLayerBehavior(Behavior):
             return invoke_child(name, normed, residual=residual)
         return ops.add_(invoke_child(name, normed), residual)
 
-    def forward(self, module, x):
-        h = self._branch(module, "self_attention", invoke_child("self_attention_norm", x), x)
+    # --- rematerialisation (the layer's remat_policy, reference mesh.py:204-252) -------
+    @staticmethod
+    def _recompute(module, child: str) -> bool:
+        """True if the policy recomputes any remat tag of `child` (tag decisions as the
+        reference's decide_tag: exact key, then the longest matching glob, default save;
+        'offload' is executed as save)."""
+        policy = module.config.get("remat_policy")
+        if not policy:
+            return False
+        policy = resolve_policy(policy)
+        c = module.children[child]
+        tags = [t.name for t in c.behavior.remat_tags(c.config, 1, 1)]
+        return any(decide_tag(t, policy) == "recompute" for t in tags)
+
+    def _attn_block(self, module, x):
+        return self._branch(module, "self_attention", invoke_child("self_attention_norm", x), x)
+
+    def _ffn_block(self, module, h):
         return self._branch(module, "feed_forward", invoke_child("feed_forward_norm", h), h)
 
+    def forward(self, module, x):
+        ra = is_recording() and self._recompute(module, "self_attention")
+        rf = is_recording() and self._recompute(module, "feed_forward")
+        if ra:
+            with recording(False):  # activations of this block are recomputed in backward
+                h = self._attn_block(module, x)
+        else:
+            h = self._attn_block(module, x)
+        if rf:
+            with recording(False):
+                out = self._ffn_block(module, h)
+        else:
+            out = self._ffn_block(module, h)
+        save(x=x if ra else None, h=h if rf else None)
+        return out
+
     def backward(self, module, dout):
+        s = saved()
+        if s.get("h") is not None:
+            with recording(True):
+                self._ffn_block(module, s["h"])
         dn2 = backward_child("feed_forward", dout)
         dh = backward_child("feed_forward_norm", dn2, dres=dout)
+        if s.get("x") is not None:
+            with recording(True):
+                self._attn_block(module, s["x"])
         dn1 = backward_child("self_attention", dh)
         return backward_child("self_attention_norm", dn1, dres=dh)
 

@@ -63,6 +63,14 @@ class MoEBehavior(Behavior):
             out["w1_gate"] = L.fan_in_uniform(param_key(key, "w1_gate"), (e, d, h), d)
         return out
 
+    def param_init(self, cfg):
+        L = _layers()
+        d, h = cfg.get("input_dim"), cfg.get("hidden_dim")
+        out = {"router": L.uniform_spec(d), "w1": L.uniform_spec(d), "w2": L.uniform_spec(h)}
+        if L.activation_pair(cfg.get("activation")):
+            out["w1_gate"] = L.uniform_spec(d)
+        return out
+
     def own_flops(self, cfg, batch, seq_len):
         d, h, e, k = cfg.get("input_dim"), cfg.get("hidden_dim"), cfg.get("num_experts"), cfg.get("top_k")
         rows = batch * seq_len
@@ -97,6 +105,8 @@ class MoEBehavior(Behavior):
         stats = torch.empty((1 + 2 * E,), device=dev, dtype=torch.float64)
         _lib.call("cb_moe_stats", n, E, k, idx.data_ptr(), probs.data_ptr(), stats.data_ptr(), ops.stream_ptr())
         add_summary("load_balance_loss", stats[0:1] if L.is_recording() else float(stats[0].item()))
+        if L.option("record_routing", False):  # debug summary: the chosen experts per token
+            add_summary("route_indices", idx.view(B, T, k))
         # stable expert-sorted dispatch of the n*k assignments
         ids64 = torch.empty((n * k,), device=dev, dtype=torch.int64)
         _lib.call("cb_widen_i32", n * k, idx.data_ptr(), ids64.data_ptr(), ops.stream_ptr())

@@ -60,6 +60,9 @@ def test_xent_matches_torch(cuda):
     (2, 128, 4, 4, 64, torch.bfloat16, 0),
     (2, 200, 4, 2, 128, torch.bfloat16, 0),  # ragged T: masked key tiles + rows crossing into the next sequence
     (2, 200, 4, 2, 128, torch.bfloat16, 2),  # same, warp-MMA flash forward instead of tcgen05
+    (4, 128, 2, 2, 128, torch.bfloat16, 0),  # single key tile; second query tile of the CTA is padding
+    (4, 128, 2, 2, 128, torch.bfloat16, 2),
+    (3, 64, 2, 1, 128, torch.bfloat16, 0),   # T < tile
 ])
 def test_attention_fwd_bwd(cuda, B, T, H, KVH, hd, dt, path):
     from paper_2507_05411_b200 import _lib, ops
@@ -95,6 +98,53 @@ def test_attention_fwd_bwd(cuda, B, T, H, KVH, hd, dt, path):
     assert _rel(dqkv[:, :d].view(B, T, H, hd).transpose(1, 2), Q.grad) < tol
     assert _rel(dqkv[:, d:d + kvd].view(B, T, KVH, hd).transpose(1, 2), K.grad) < tol
     assert _rel(dqkv[:, d + kvd:].view(B, T, KVH, hd).transpose(1, 2), Vv.grad) < tol
+
+
+@pytest.mark.parametrize("B,T,H,KVH", [(2, 256, 2, 2), (4, 128, 2, 1), (1, 200, 4, 2)])
+def test_fused_rope_projection_and_backward(cuda, B, T, H, KVH):
+    """cb_gemm_rope == gemm then rope; cb_attention_bwd_rope == attention bwd then inverse rope."""
+    from paper_2507_05411_b200 import ops
+    from paper_2507_05411_b200.layers import rope_tables
+
+    hd = 128
+    d, kvd = H * hd, KVH * hd
+    g = torch.Generator().manual_seed(B * T)
+    x = torch.randn(B * T, 256, generator=g).to(cuda, torch.bfloat16)
+    w = (0.05 * torch.randn(256, d + 2 * kvd, generator=g)).to(cuda, torch.bfloat16)
+    cs, sn = rope_tables(T, hd, 10000.0, cuda)
+    fused = torch.empty(B * T, d + 2 * kvd, device=cuda, dtype=torch.bfloat16)
+    ops.gemm_rope(x, w, fused, T, hd, d + kvd, cs, sn)
+    plain = torch.empty_like(fused)
+    ops.gemm(x, w, plain)
+    ops.rope_(plain[:, :d], T, H, hd, cs, sn)
+    ops.rope_(plain[:, d:d + kvd], T, KVH, hd, cs, sn)
+    assert _rel(fused.float(), plain.float()) < 1e-2
+    q, k, v = fused[:, :d], fused[:, d:d + kvd], fused[:, d + kvd:]
+    scale = 1 / math.sqrt(hd)
+    o, lse = ops.attention_fwd(q, k, v, B, T, H, KVH, hd, scale)
+    do = torch.randn(B * T, d, generator=g).to(cuda, torch.bfloat16)
+    d1, d2 = torch.empty_like(fused), torch.empty_like(fused)
+    ops.attention_bwd_rope(q, k, v, o, lse, do, d1[:, :d], d1[:, d:d + kvd], d1[:, d + kvd:], B, T, H, KVH, hd, scale,
+                           cs, sn)
+    ops.attention_bwd(q, k, v, o, lse, do, d2[:, :d], d2[:, d:d + kvd], d2[:, d + kvd:], B, T, H, KVH, hd, scale)
+    ops.rope_(d2[:, :d], T, H, hd, cs, sn, inverse=True)
+    ops.rope_(d2[:, d:d + kvd], T, KVH, hd, cs, sn, inverse=True)
+    assert _rel(d1.float(), d2.float()) < 1e-2
+
+
+@pytest.mark.parametrize("name", ["txf_moe", "txf_rope", "txf_d48_l3_relu"])
+def test_device_init_bit_exact(cuda, name):
+    """The device PCG64 initialiser reproduces the reference init_state bit for bit (as f32)."""
+    from oracle import decoder_oracle as O
+    from paper_2507_05411_b200 import TrainEngine, build_experiment, init_state, instantiate, root_key
+
+    cfg = build_experiment(name)
+    eng = TrainEngine(cfg, device=cuda, seed=3)
+    ref = dict(O.leaves(init_state(instantiate(cfg), root_key(3))))
+    got = dict(O.leaves(eng.state_numpy()))
+    assert set(ref) == set(got)
+    for k in ref:
+        assert np.array_equal(got[k], ref[k].astype(np.float32).astype(np.float64)), k
 
 
 def test_embedding_bwd_deterministic(cuda):

@@ -47,8 +47,14 @@ def run_parity(cfg, precision, B, T, tol, seed=0, check_update=True, decomposed=
     eng = TrainEngine(cfg, device="cuda:0", seed=seed)
     V = eng.cfg.get("model.vocab_size")
     toks = synthetic_batch(seed, 0, B, T, V)["tokens"]
+    if precision == "bf16":
+        eng.options["record_routing"] = True
     loss, col = eng.compute_grads(toks)
     loss = float(loss.item())
+    forced = {}
+    for key, vals in col.flat_summaries().items():
+        if key.endswith("/route_indices"):  # bf16: compare at the GPU's routing decisions
+            forced[int(key.split("layer[")[1].split("]")[0])] = np.asarray(vals[0]).astype(np.int64)
     grads = dict(_leaves(eng.grads_numpy()))
     eng.apply_update()
     params = dict(_leaves(eng.state_numpy()))
@@ -56,7 +62,8 @@ def run_parity(cfg, precision, B, T, tol, seed=0, check_update=True, decomposed=
     m = instantiate(cfg)
     st = init_state(m, root_key(seed))
     spec = O.spec_from_config(m.config)
-    lo, go, po, _, _, summ = O.train_step(st, toks, spec, O.AdamW(lr=eng.lr, beta1=eng.beta1, beta2=eng.beta2))
+    lo, go, po, _, _, summ = O.train_step(st, toks, spec, O.AdamW(lr=eng.lr, beta1=eng.beta1, beta2=eng.beta2),
+                                          forced_routing=forced or None)
     go, po = dict(_leaves(go)), dict(_leaves(po))
     assert set(grads) == set(go)
     assert abs(loss - lo) / abs(lo) < tol, (loss, lo)
@@ -138,12 +145,13 @@ def test_fast_path_shape_f32(cuda, hd):
 
 
 def test_fast_path_moe_bf16(cuda):
-    """bf16 router inputs flip the top-2 choice of ~0.5% of tokens relative to the f64
-    oracle, which moves the router-weight gradient by ~8%; every other
-    tensor holds 2e-2.  Bit-exact routing on identical inputs is tested in
-    test_kernels_gpu.py::test_moe_router_topk_bit_exact.  The flipped tokens also move
-    between experts, so the MoE block's expert/norm gradients sit at ~2.2%."""
-    run_parity(_mid(128, "MoE"), "bf16", 4, 128, 2e-2, loose={"router": 0.15, "feed_forward": 0.05})
+    """bf16 router *inputs* flip the top-2 choice of ~0.5% of tokens relative to the f64
+    oracle — a discontinuity, not an arithmetic error.  The bf16 parity run
+    therefore records the GPU's expert choices (debug summary ``route_indices``) and the
+    oracle evaluates the step at those choices (the reference's own forced-routing oracle,
+    tests/test_layers.py:352-359); every tensor is then held to 2e-2.  Bit-exact routing on
+    identical inputs is tested in test_kernels_gpu.py::test_moe_router_topk_bit_exact."""
+    run_parity(_mid(128, "MoE"), "bf16", 4, 128, 2e-2)
 
 
 def test_tiny_bench_config_bf16(cuda):
@@ -160,6 +168,27 @@ def test_forward_loss_matches_reference_invoke(cuda):
         eng = TrainEngine(build_experiment(name), device="cuda:0")
         got = eng.loss(np.array(rec["tokens"], dtype=np.int64))
         assert abs(got - rec["loss"]) / rec["loss"] < 1e-5, (name, got, rec["loss"])
+
+
+@pytest.mark.parametrize("policy", ["recompute_all", "save_qkvo_flash"])
+def test_remat_policies_are_exact(cuda, policy):
+    """Rematerialised blocks rerun the same deterministic kernels: gradients are bit-identical."""
+    from paper_2507_05411_b200 import TrainEngine, set_dtype_policy, synthetic_batch
+    from paper_2507_05411_b200.remat import POLICY_ALIASES
+
+    base = set_dtype_policy(_mid(128), "bf16")
+    remat = base
+    for i in range(2):
+        remat = remat.set(f"model.decoder.transformer.layer[{i}].remat_policy", POLICY_ALIASES[policy])
+    toks = synthetic_batch(0, 0, 2, 256, 512)["tokens"]
+    outs = []
+    for cfg in (base, remat):
+        eng = TrainEngine(cfg, device="cuda:0")
+        loss, _ = eng.compute_grads(toks)
+        outs.append((float(loss.item()), dict(_leaves(eng.grads_numpy()))))
+    assert outs[0][0] == outs[1][0]
+    for k in outs[0][1]:
+        assert np.array_equal(outs[0][1][k], outs[1][1][k]), k
 
 
 def test_two_steps_train(cuda):
