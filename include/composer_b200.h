@@ -172,6 +172,12 @@ CB_API int cb_moe_combine_bwd(int64_t n, int dim, int top_k, const int32_t* inv,
                               float* dweights, void* stream);
 CB_API int cb_moe_router_bwd(int64_t n, int experts, int top_k, const float* probs, const int32_t* idx,
                              const float* weights, const float* dweights, float* dlogits, void* stream);
+/* Router backward products (x @ router, layers.py:516): drouter (+)= x^T dlogits (fixed token
+ * blocks + ordered reduction; workspace ceil(n/512)*dim*experts floats) and
+ * dx += dlogits router^T. */
+CB_API int cb_moe_router_bwd_gemms(int64_t n, int dim, int experts, const void* x, int64_t ldx, int x_dtype,
+                                   const float* dlogits, const float* router, float* drouter, float* dx,
+                                   int64_t lddx, float* workspace, void* stream);
 CB_API int cb_invert_perm(int64_t n, const int32_t* perm, int32_t* inv, void* stream);
 CB_API int cb_widen_i32(int64_t n, const int32_t* a, int64_t* b, void* stream);
 

@@ -62,6 +62,7 @@ SIGNATURES: dict[str, list] = {
     "cb_moe_combine_bwd": [_L, _I, _I, _P, _P, _P, _L, _P, _L, _P, _L, _I, _P, _P],
     "cb_moe_router_bwd": [_L, _I, _I, _P, _P, _P, _P, _P, _P],
     "cb_invert_perm": [_L, _P, _P, _P],
+    "cb_moe_router_bwd_gemms": [_L, _I, _I, _P, _L, _I, _P, _P, _P, _P, _L, _P, _P],
     "cb_widen_i32": [_L, _P, _P, _P],
     "cb_init_uniform": [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _L, _D, _D, _L, _L, _L,
                         _L, _P, _L, _L, _P, _I, _P],

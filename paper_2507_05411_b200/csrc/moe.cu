@@ -257,6 +257,53 @@ extern "C" int cb_moe_router_bwd(int64_t n, int experts, int top_k, const float*
   return check_launch("moe_router_bwd");
 }
 
+// Router backward products, E <= 32 experts (tiny N/K that GEMM tiles waste):
+//   partial[blk][c*E + e] = sum_{t in blk's tokens} x[t][c] * dlog[t][e]   (then col-reduce)
+//   dx[t][c] += sum_e dlog[t][e] * router[c][e]
+template <typename TX>
+__global__ void __launch_bounds__(256) router_wgrad_k(int64_t n, int d, int E, int tok_per_blk,
+                                                      const TX* __restrict__ x, int64_t ldx,
+                                                      const float* __restrict__ dlog, float* __restrict__ partial) {
+  __shared__ float sg[64][kMaxExperts];
+  const int64_t t0 = (int64_t)blockIdx.x * tok_per_blk;
+  const int64_t t1 = min(n, t0 + tok_per_blk);
+  const int c0 = blockIdx.y * 256 + threadIdx.x;  // this thread's column
+  float acc[kMaxExperts];
+#pragma unroll
+  for (int e = 0; e < kMaxExperts; ++e) acc[e] = 0.f;
+  for (int64_t tb = t0; tb < t1; tb += 64) {
+    const int cnt = (int)min<int64_t>(64, t1 - tb);
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt * E; i += blockDim.x) sg[i / E][i % E] = dlog[(tb + i / E) * E + i % E];
+    __syncthreads();
+    if (c0 < d) {
+      for (int j = 0; j < cnt; ++j) {
+        const float xv = to_f32(x[(tb + j) * ldx + c0]);
+#pragma unroll
+        for (int e = 0; e < kMaxExperts; ++e)
+          if (e < E) acc[e] = fmaf(xv, sg[j][e], acc[e]);
+      }
+    }
+  }
+  if (c0 < d) {
+    float* pr = partial + (int64_t)blockIdx.x * d * E + (int64_t)c0 * E;
+    for (int e = 0; e < E; ++e) pr[e] = acc[e];
+  }
+}
+
+__global__ void __launch_bounds__(256) router_dx_k(int64_t n, int d, int E, const float* __restrict__ dlog,
+                                                   const float* __restrict__ router, float* __restrict__ dx,
+                                                   int64_t lddx) {
+  const int64_t t = blockIdx.x;
+  float g[kMaxExperts];
+  for (int e = 0; e < E; ++e) g[e] = dlog[t * E + e];
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float s = 0.f;
+    for (int e = 0; e < E; ++e) s = fmaf(g[e], router[(int64_t)c * E + e], s);
+    dx[t * lddx + c] += s;
+  }
+}
+
 // inv[perm[j]] = j
 __global__ void invert_perm_k(int64_t n, const int32_t* __restrict__ perm, int32_t* __restrict__ inv) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -279,4 +326,26 @@ extern "C" int cb_widen_i32(int64_t n, const int32_t* a, int64_t* b, void* strea
   if (n <= 0) return CB_OK;
   widen_k<<<(int)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, a, b);
   return check_launch("widen_i32");
+}
+
+// drouter (+)= x^T dlog (deterministic: fixed token blocks + ordered column reduction);
+// dx += dlog router^T.  workspace: ceil(n / 512) * dim * experts floats.
+extern "C" int cb_moe_router_bwd_gemms(int64_t n, int dim, int experts, const void* x, int64_t ldx, int x_dtype,
+                                       const float* dlogits, const float* router, float* drouter, float* dx,
+                                       int64_t lddx, float* workspace, void* stream) {
+  if (experts < 1 || experts > kMaxExperts) return fail(CB_ERR_UNSUPPORTED, "moe: experts must be in [1, %d]", kMaxExperts);
+  if (n <= 0) return CB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int tpb = 512;
+  const int nblk = (int)((n + tpb - 1) / tpb);
+  dim3 grid(nblk, (dim + 255) / 256);
+  if (x_dtype == CB_DT_F32)
+    router_wgrad_k<float><<<grid, 256, 0, st>>>(n, dim, experts, tpb, (const float*)x, ldx, dlogits, workspace);
+  else
+    router_wgrad_k<__nv_bfloat16><<<grid, 256, 0, st>>>(n, dim, experts, tpb, (const __nv_bfloat16*)x, ldx, dlogits,
+                                                        workspace);
+  if (int s = check_launch("moe_router_wgrad")) return s;
+  if (int s = cb_col_reduce(nblk, dim * experts, workspace, drouter, 1, stream)) return s;
+  router_dx_k<<<(int)n, 256, 0, st>>>(n, dim, experts, dlogits, router, dx, lddx);
+  return check_launch("moe_router_dx");
 }

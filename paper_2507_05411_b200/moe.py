@@ -197,8 +197,10 @@ class MoEBehavior(Behavior):
         dlog = torch.empty((n, E), device=dev, dtype=torch.float32)
         _lib.call("cb_moe_router_bwd", n, E, k, s["probs"].data_ptr(), s["idx"].data_ptr(), s["w"].data_ptr(),
                   dw.data_ptr(), dlog.data_ptr(), ops.stream_ptr())
-        x32 = ops.cast(s["x2"], torch.float32)
         router = L._f32(param("router"))
-        ops.gemm(x32, dlog, param_grad("router"), trans_a=True, accumulate=True)
-        ops.gemm(dlog, router, dx, trans_b=True, accumulate=True)
+        x2 = s["x2"]
+        ws = torch.empty(((n + 511) // 512) * d * E, device=dev, dtype=torch.float32)
+        _lib.call("cb_moe_router_bwd_gemms", n, d, E, x2.data_ptr(), ops.ld(x2), ops.dt(x2), dlog.data_ptr(),
+                  router.data_ptr(), param_grad("router").data_ptr(), dx.data_ptr(), ops.ld(dx), ws.data_ptr(),
+                  ops.stream_ptr())
         return dx.view(B, T, d)
