@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(256) router_wgrad_k(int64_t n, int d, int E, i
 #pragma unroll
   for (int e = 0; e < kMaxExperts; ++e) acc[e] = 0.f;
   for (int64_t tb = t0; tb < t1; tb += 64) {
-    const int cnt = (int)min<int64_t>(64, t1 - tb);
+    const int cnt = (int)(t1 - tb < 64 ? t1 - tb : 64);
     __syncthreads();
     for (int i = threadIdx.x; i < cnt * E; i += blockDim.x) sg[i / E][i % E] = dlog[(tb + i / E) * E + i % E];
     __syncthreads();
