@@ -1,20 +1,22 @@
 // tcgen05 flash attention backward (bf16, head_dim 128), unmasked, GQA-aware.
 //
 // Deterministic two-kernel split (no atomics), both recomputing P = exp(S - LSE):
-//   dkdv: one CTA per (128-key tile, kv head, batch); sweeps every query tile of every
-//         query head in the kv group in 64-query sub-tiles u:
+//   dkdv: one CTA per (128-key tile, kv head, batch); sweeps every 128-query tile u of
+//         every query head in the kv group:
 //           S^T_u  = K Q_u^T      (A = K  smem K-major, B = Q_u  smem K-major)  -> TMEM
 //           dP^T_u = V dO_u^T     (A = V  smem K-major, B = dO_u smem K-major)  -> TMEM
-//           P^T = exp2(S^T c - lse2), dS^T = P^T (dP^T - delta)    [1 thread = 1 key row]
+//           P^T = exp2(S^T c - lse2), dS^T = P^T (dP^T - delta)   [CUDA cores, per key row]
 //           dV += P^T dO_u        (A = P^T from TMEM, B = dO_u smem MN-major)
 //           dK += dS^T Q_u        (A = dS^T from TMEM, B = Q_u  smem MN-major)
-//         S^T / dP^T are double-buffered (2 x 64 columns each), so the MMAs of sub-tile
-//         u+1 and the accumulations of u-1 run while the CUDA cores handle sub-tile u.
+//         MMA issue order  dV(u) S(u+1) | dK(u) dP(u+1)  lets the exp pass of tile u+1
+//         overlap dK(u)/dP(u+1) and the dS pass overlap dV(u+1)/S(u+2) with single-buffered
+//         TMEM (S^T | dP^T | dV | dK = 512 columns).
 //   dq:   one CTA per (128-query tile, head, batch); sweeps every 128-key tile j:
 //           S_j = Q K_j^T (double-buffered), dP_j = dO V_j^T, dS = P (dP - delta),
 //           dQ += dS K_j (B = K_j MN-major); S_{j+1} is issued before dQ_j.
-// TMEM (512 columns): dkdv = S^T[2] | dP^T[2] | dV | dK;  dq = S[2] | dP | dQ.
-// Warp roles as in the forward: 0 TMA, 1 MMA (single thread), 2 TMEM alloc, 4-7 compute.
+//           TMEM: S[2] | dP | dQ.
+// Roles: warp 0 TMA, warp 1 MMA (single thread), warp 2 TMEM alloc, warps 4-11 compute
+// (warps w and w+4 share TMEM lane quadrant w%4 and split each tile's columns in halves).
 #include "attn.cuh"
 #include "composer_b200.h"
 
@@ -23,7 +25,7 @@ namespace tcb {
 
 constexpr int HD = 128;
 constexpr int BT = 128;  // tile rows (keys or queries)
-constexpr int kThreads = 384;  // warps 0-3: TMA, MMA, TMEM alloc, idle; 4-11: compute
+constexpr int kThreads = 384;
 constexpr int kBox = 128 * 64 * 2;  // one [128][64] bf16 TMA box (16 KB)
 constexpr int kTile = 2 * kBox;     // one [128][128] tile (two 64-column atoms)
 constexpr int kSmem = 6 * kTile + 1024 + 4096;
@@ -48,6 +50,11 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 // K-major operand descriptor for the kk-th K=16 step of a tile whose rows start at `base`
 __device__ __forceinline__ uint64_t kdesc(uint32_t base, int kk) {
@@ -56,17 +63,11 @@ __device__ __forceinline__ uint64_t kdesc(uint32_t base, int kk) {
 // MN-major operand descriptor (rows = K dim, 128 columns = N) for the k-th K=16 step
 __device__ __forceinline__ uint64_t mndesc(uint32_t base, int k) { return sw128_desc(base + k * 2048, kBox, 1024); }
 
-__device__ __forceinline__ float fast_exp2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-// store one thread's 128-column f32 TMEM row as bf16 (times `mul`) to global; when `rc`
-// is given, first apply the inverse RoPE rotation of this row's position (rc/rs = cos/sin
-// table row, HD/2 entries) — the backward of the forward's fused rotation
-__device__ __forceinline__ void store_row(uint32_t taddr, __nv_bfloat16* dst, float mul, bool ok,
-                                          const float* rc = nullptr, const float* rs = nullptr, int nchunks = HD / 32) {
+// Store `nchunks` x 32 f32 TMEM columns of this thread's row as bf16 (times `mul`); with
+// rc/rs (cos/sin of this row's position) first apply the inverse RoPE rotation — the
+// backward of the rotation fused into the QKV projection.
+__device__ __forceinline__ void store_row(uint32_t taddr, __nv_bfloat16* dst, float mul, bool ok, const float* rc,
+                                          const float* rs, int nchunks) {
 #pragma unroll 1
   for (int cc = 0; cc < nchunks; ++cc) {
     uint32_t o[32];
@@ -96,9 +97,17 @@ __device__ __forceinline__ void store_row(uint32_t taddr, __nv_bfloat16* dst, fl
   }
 }
 
-__device__ __forceinline__ void store_row_half(uint32_t taddr, __nv_bfloat16* dst, float mul, bool ok, const float* rc,
-                                               const float* rs) {
-  store_row(taddr, dst, mul, ok, rc, rs, HD / 64);
+// Packs 64 f32 values (two 32-column TMEM loads at src) through `f` into 32 bf16 pairs.
+template <typename F>
+__device__ __forceinline__ void load64(uint32_t src, float (&out)[64], F f) {
+#pragma unroll
+  for (int cc = 0; cc < 2; ++cc) {
+    uint32_t v[32];
+    tmem_ld32(src + cc * 32, v);
+    tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) out[cc * 32 + i] = f(cc * 32 + i, __uint_as_float(v[i]));
+  }
 }
 
 // ====================================================================== dK / dV
@@ -109,26 +118,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = smem;
   uint8_t* sV = smem + kTile;
-  uint8_t* ring = smem + 2 * kTile;  // [2] x {Q tile, dO tile}
+  uint8_t* ring = smem + 2 * kTile;                        // [2] x {Q tile, dO tile}
   float* sL = reinterpret_cast<float*>(smem + 6 * kTile);  // [2][128] lse * log2e
-  float* sD = sL + 256;                                   // [2][128] delta
+  float* sD = sL + 256;                                    // [2][128] delta
   uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 256);
   uint64_t* kv_full = bars;
-  uint64_t* qd_full = bars + 1;    // [2]
-  uint64_t* qd_empty = bars + 3;   // [2]
-  uint64_t* s_full = bars + 5;     // [2]
-  uint64_t* dp_full = bars + 7;    // [2]
-  uint64_t* p_ready = bars + 9;    // [2]
-  uint64_t* ds_ready = bars + 11;  // [2]
-  uint64_t* mma_done = bars + 13;
-  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* qd_full = bars + 1;   // [2]
+  uint64_t* qd_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* dp_full = bars + 6;
+  uint64_t* p_ready = bars + 7;
+  uint64_t* ds_ready = bars + 8;
+  uint64_t* mma_done = bars + 9;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 10);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kt = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
   const int group = p.H / p.KVH;
   const int nq = (p.T + BT - 1) / BT;
-  const int total = group * nq;  // 128-query tiles
-  const int U = 2 * total;       // 64-query sub-tiles
+  const int total = group * nq;  // 128-query tiles to sweep
   const int row0 = b * p.T, k0 = kt * BT;
 
   if (warp == 0 && lane == 0) {
@@ -140,11 +148,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&qd_full[s], 1);
       mbar_init(&qd_empty[s], 1);
-      mbar_init(&s_full[s], 1);
-      mbar_init(&dp_full[s], 1);
-      mbar_init(&p_ready[s], 8);
-      mbar_init(&ds_ready[s], 8);
     }
+    mbar_init(s_full, 1);
+    mbar_init(dp_full, 1);
+    mbar_init(p_ready, 8);
+    mbar_init(ds_ready, 8);
     mbar_init(mma_done, 1);
     fence_mbar_init();
   }
@@ -153,8 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *slot;
-  // TMEM columns: S^T sub-tiles at half*64, dP^T sub-tiles at 128 + half*64
-  const uint32_t cV = 256, cK = 384;
+  const uint32_t cS = 0, cP = 128, cV = 256, cK = 384;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -178,109 +185,106 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t id_s = idesc_bf16_f32(128, 64, 0, 0);    // K-major x K-major, 64 queries
-      const uint32_t id_acc = idesc_bf16_f32(128, 128, 0, 1); // TMEM A x MN-major B
+      const uint32_t id_s = idesc_bf16_f32(128, 128, 0, 0);    // K-major x K-major
+      const uint32_t id_acc = idesc_bf16_f32(128, 128, 0, 1);  // TMEM A x MN-major B
       const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-      auto issue_sp = [&](int u) {
-        const int it = u >> 1, half = u & 1, st = it & 1;
-        if (half == 0) {
-          mbar_wait(&qd_full[st], (it >> 1) & 1);
-          tc_fence_after();
-        }
-        const uint32_t aQ = smem_u32(ring + st * 2 * kTile) + half * 8192, aG = aQ + kTile;
+      auto tileQ = [&](int u) { return smem_u32(ring + (u & 1) * 2 * kTile); };
+      auto issue_s = [&](int u) {
+        mbar_wait(&qd_full[u & 1], (u >> 1) & 1);
+        tc_fence_after();
+        const uint32_t aQ = tileQ(u);
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + (half * 64u), kdesc(aK, kk), kdesc(aQ, kk), id_s, kk > 0);
-        umma_commit(&s_full[half]);
+        for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + cS, kdesc(aK, kk), kdesc(aQ, kk), id_s, kk > 0);
+        umma_commit(s_full);
+      };
+      auto issue_dp = [&](int u) {
+        const uint32_t aG = tileQ(u) + kTile;
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + (128u + half * 64u), kdesc(aV, kk), kdesc(aG, kk), id_s, kk > 0);
-        umma_commit(&dp_full[half]);
+        for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + cP, kdesc(aV, kk), kdesc(aG, kk), id_s, kk > 0);
+        umma_commit(dp_full);
       };
       mbar_wait(kv_full, 0);
       tc_fence_after();
-      issue_sp(0);
-      for (int u = 0; u < U; ++u) {
-        if (u + 1 < U) issue_sp(u + 1);
-        const int it = u >> 1, half = u & 1, st = it & 1;
-        const uint32_t aQ = smem_u32(ring + st * 2 * kTile) + half * 8192, aG = aQ + kTile;
-        mbar_wait(&p_ready[half], (u >> 1) & 1);
+      issue_s(0);
+      issue_dp(0);
+      for (int u = 0; u < total; ++u) {
+        const uint32_t aQ = tileQ(u), aG = aQ + kTile;
+        mbar_wait(p_ready, u & 1);
         tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < 4; ++k) umma_f16_ts(tmem + cV, tmem + (half * 64u) + k * 8, mndesc(aG, k), id_acc, (u | k) != 0);
-        mbar_wait(&ds_ready[half], (u >> 1) & 1);
+        for (int k = 0; k < BT / 16; ++k) umma_f16_ts(tmem + cV, tmem + cS + k * 8, mndesc(aG, k), id_acc, (u | k) != 0);
+        if (u + 1 < total) issue_s(u + 1);  // S^T region: P^T(u) already consumed (in-order)
+        mbar_wait(ds_ready, u & 1);
         tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < 4; ++k) umma_f16_ts(tmem + cK, tmem + (128u + half * 64u) + k * 8, mndesc(aQ, k), id_acc, (u | k) != 0);
-        if (half == 1) umma_commit(&qd_empty[st]);
+        for (int k = 0; k < BT / 16; ++k) umma_f16_ts(tmem + cK, tmem + cP + k * 8, mndesc(aQ, k), id_acc, (u | k) != 0);
+        umma_commit(&qd_empty[u & 1]);
+        if (u + 1 < total) issue_dp(u + 1);  // dP^T region: dS^T(u) already consumed
       }
       umma_commit(mma_done);
     }
     __syncwarp();
   } else if (warp >= 4) {
-    // 8 compute warps: warps w and w+4 share TMEM lane quadrant w%4 (key rows) and split
-    // each 64-query sub-tile into two 32-column halves (ch)
     const int q = warp & 3;
-    const int ch = (warp - 4) >> 2;
+    const int ch = (warp - 4) >> 2;    // query-column half of each tile
     const int t = q * 32 + lane;       // key row inside the tile
     const int tt = threadIdx.x - 128;  // 0..255
     const uint32_t lo = (uint32_t)(q * 32) << 16;
     const float c = p.scale * kLog2e;
-    for (int u = 0; u < U; ++u) {
-      const int it = u >> 1, half = u & 1;
-      const int h = kvh * group + it / nq, q0 = (it % nq) * BT;
-      const float* L = sL + (it & 1) * 128 + half * 64 + ch * 32;
-      const float* D = sD + (it & 1) * 128 + half * 64 + ch * 32;
-      if (half == 0) {
-        if (tt < 128) {
-          const int qi = q0 + tt;
-          const int64_t li = ((int64_t)b * p.H + h) * p.T + qi;
-          sL[(it & 1) * 128 + tt] = qi < p.T ? p.lse[li] * kLog2e : 0.f;
-          sD[(it & 1) * 128 + tt] = qi < p.T ? p.delta[li] : 0.f;
-        }
-        named_sync(1, 256);
+    for (int u = 0; u < total; ++u) {
+      const int h = kvh * group + u / nq, q0 = (u % nq) * BT;
+      if (tt < 128) {
+        const int qi = q0 + tt;
+        const int64_t li = ((int64_t)b * p.H + h) * p.T + qi;
+        sL[(u & 1) * 128 + tt] = qi < p.T ? p.lse[li] * kLog2e : 0.f;
+        sD[(u & 1) * 128 + tt] = qi < p.T ? p.delta[li] : 0.f;
       }
-      const int valid = min(64, p.T - (q0 + half * 64)) - ch * 32;
-      mbar_wait(&s_full[half], (u >> 1) & 1);
+      named_sync(1, 256);
+      const float* L = sL + (u & 1) * 128 + ch * 64;
+      const float* D = sD + (u & 1) * 128 + ch * 64;
+      const int valid = min(BT, p.T - q0) - ch * 64;
+      mbar_wait(s_full, u & 1);
       tc_fence_after();
-      float pr[32];
+      float pr[64];
+      if (valid >= 64)
+        load64(tmem + lo + cS + ch * 64, pr, [&](int i, float s) { return fast_exp2(fmaf(s, c, -L[i])); });
+      else
+        load64(tmem + lo + cS + ch * 64, pr,
+               [&](int i, float s) { return i < valid ? fast_exp2(fmaf(s, c, -L[i])) : 0.f; });
       {
-        uint32_t v[32];
-        tmem_ld32(tmem + lo + half * 64u + ch * 32, v);
-        tmem_ld_wait();
-        if (valid >= 32) {
+        uint32_t pk[2][16];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) pr[i] = fast_exp2(fmaf(__uint_as_float(v[i]), c, -L[i]));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) pr[i] = i < valid ? fast_exp2(fmaf(__uint_as_float(v[i]), c, -L[i])) : 0.f;
+        for (int i = 0; i < 16; ++i) {
+          pk[0][i] = pack2(pr[2 * i], pr[2 * i + 1]);
+          pk[1][i] = pack2(pr[32 + 2 * i], pr[33 + 2 * i]);
         }
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) pk[i] = pack2(pr[2 * i], pr[2 * i + 1]);
-        named_sync(2 + q, 64);  // the partner warp has read its raw S columns
-        tmem_st16(tmem + lo + half * 64u + ch * 16, pk);
+        named_sync(2 + q, 64);  // the partner warp has read its raw S^T columns
+        tmem_st16(tmem + lo + cS + ch * 32, pk[0]);
+        tmem_st16(tmem + lo + cS + ch * 32 + 16, pk[1]);
         tmem_st_wait();
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_ready[half]);
-      mbar_wait(&dp_full[half], (u >> 1) & 1);
+      if (lane == 0) mbar_arrive(p_ready);
+      mbar_wait(dp_full, u & 1);
       tc_fence_after();
       {
-        uint32_t v[32];
-        uint32_t pk[16];
-        tmem_ld32(tmem + lo + 128u + half * 64u + ch * 32, v);
-        tmem_ld_wait();
+        float ds[64];
+        load64(tmem + lo + cP + ch * 64, ds, [&](int i, float dp) { return pr[i] * (dp - D[i]); });
+        uint32_t pk[2][16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          pk[i] = pack2(pr[2 * i] * (__uint_as_float(v[2 * i]) - D[2 * i]),
-                        pr[2 * i + 1] * (__uint_as_float(v[2 * i + 1]) - D[2 * i + 1]));
+        for (int i = 0; i < 16; ++i) {
+          pk[0][i] = pack2(ds[2 * i], ds[2 * i + 1]);
+          pk[1][i] = pack2(ds[32 + 2 * i], ds[33 + 2 * i]);
+        }
         named_sync(2 + q, 64);
-        tmem_st16(tmem + lo + 128u + half * 64u + ch * 16, pk);
+        tmem_st16(tmem + lo + cP + ch * 32, pk[0]);
+        tmem_st16(tmem + lo + cP + ch * 32 + 16, pk[1]);
         tmem_st_wait();
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&ds_ready[half]);
+      if (lane == 0) mbar_arrive(ds_ready);
     }
     mbar_wait(mma_done, 0);
     tc_fence_after();
@@ -289,9 +293,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (ch == 0) {
       const float* rc = p.rope_cos ? p.rope_cos + (int64_t)(ok ? krow : 0) * (HD / 2) : nullptr;
       const float* rs = p.rope_sin ? p.rope_sin + (int64_t)(ok ? krow : 0) * (HD / 2) : nullptr;
-      store_row(tmem + lo + cK, p.o0 + ((int64_t)row0 + krow) * p.ld0 + (int64_t)kvh * HD, p.scale, ok, rc, rs);
+      store_row(tmem + lo + cK, p.o0 + ((int64_t)row0 + krow) * p.ld0 + (int64_t)kvh * HD, p.scale, ok, rc, rs, 4);
     } else {
-      store_row(tmem + lo + cV, p.o1 + ((int64_t)row0 + krow) * p.ld1 + (int64_t)kvh * HD, 1.f, ok);
+      store_row(tmem + lo + cV, p.o1 + ((int64_t)row0 + krow) * p.ld1 + (int64_t)kvh * HD, 1.f, ok, nullptr,
+                nullptr, 4);
     }
   }
   tc_fence_before();
@@ -348,8 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *slot;
-  // TMEM columns: S buffers at st*128
-  const uint32_t cP = 256, cQ = 384;
+  const uint32_t cP = 256, cQ = 384;  // S buffers at st * 128
 
   if (warp == 0) {
     if (lane == 0) {
@@ -382,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t aK = smem_u32(ring + st * 2 * kTile);
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + (st * 128u), kdesc(aQ, kk), kdesc(aK, kk), id_s, kk > 0);
+        for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + st * 128u, kdesc(aQ, kk), kdesc(aK, kk), id_s, kk > 0);
         umma_commit(&s_full[st]);
       };
       auto issue_dp = [&](int j) {
@@ -401,7 +405,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t aK = smem_u32(ring + st * 2 * kTile);
 #pragma unroll
-        for (int k = 0; k < BT / 16; ++k) umma_f16_ts(tmem + cQ, tmem + (st * 128u) + k * 8, mndesc(aK, k), id_acc, (j | k) != 0);
+        for (int k = 0; k < BT / 16; ++k)
+          umma_f16_ts(tmem + cQ, tmem + st * 128u + k * 8, mndesc(aK, k), id_acc, (j | k) != 0);
         umma_commit(&kv_empty[st]);
         if (j + 1 < nk) issue_dp(j + 1);
       }
@@ -409,10 +414,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else if (warp >= 4) {
-    // 8 compute warps: warps w and w+4 share lane quadrant w%4 (query rows) and split each
-    // 128-key tile into two 64-column halves (ch)
     const int q = warp & 3;
-    const int ch = (warp - 4) >> 2;
+    const int ch = (warp - 4) >> 2;  // key-column half of each tile
     const int t = q * 32 + lane;
     const uint32_t lo = (uint32_t)(q * 32) << 16;
     const float c = p.scale * kLog2e;
@@ -427,36 +430,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&s_full[st], (j >> 1) & 1);
       tc_fence_after();
       float pr[64];
-      {
-        uint32_t v[32];
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          tmem_ld32(tmem + lo + st * 128u + ch * 64 + cc * 32, v);
-          tmem_ld_wait();
-          if (valid >= 64) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) pr[cc * 32 + i] = fast_exp2(fmaf(__uint_as_float(v[i]), c, -L));
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              pr[cc * 32 + i] = cc * 32 + i < valid ? fast_exp2(fmaf(__uint_as_float(v[i]), c, -L)) : 0.f;
-          }
-        }
-      }
+      if (valid >= 64)
+        load64(tmem + lo + st * 128u + ch * 64, pr, [&](int, float s) { return fast_exp2(fmaf(s, c, -L)); });
+      else
+        load64(tmem + lo + st * 128u + ch * 64, pr,
+               [&](int i, float s) { return i < valid ? fast_exp2(fmaf(s, c, -L)) : 0.f; });
       mbar_wait(dp_full, j & 1);
       tc_fence_after();
       {
-        uint32_t v[32];
+        float ds[64];
+        load64(tmem + lo + cP + ch * 64, ds, [&](int i, float dp) { return pr[i] * (dp - D); });
         uint32_t pk[2][16];
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          tmem_ld32(tmem + lo + cP + ch * 64 + cc * 32, v);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int col = cc * 32 + 2 * i;
-            pk[cc][i] = pack2(pr[col] * (__uint_as_float(v[2 * i]) - D), pr[col + 1] * (__uint_as_float(v[2 * i + 1]) - D));
-          }
+        for (int i = 0; i < 16; ++i) {
+          pk[0][i] = pack2(ds[2 * i], ds[2 * i + 1]);
+          pk[1][i] = pack2(ds[32 + 2 * i], ds[33 + 2 * i]);
         }
         named_sync(2 + q, 64);  // both halves have read their raw S columns
         tmem_st16(tmem + lo + st * 128u + ch * 32, pk[0]);
@@ -469,10 +457,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_wait(mma_done, 0);
     tc_fence_after();
-    const float* rc = p.rope_cos ? p.rope_cos + (int64_t)(ok ? qrow : 0) * (HD / 2) : nullptr;
-    const float* rs = p.rope_sin ? p.rope_sin + (int64_t)(ok ? qrow : 0) * (HD / 2) : nullptr;
-    store_row_half(tmem + lo + cQ + ch * 64, p.o0 + ((int64_t)row0 + qrow) * p.ld0 + (int64_t)h * HD + ch * 64,
-                   p.scale, ok, rc ? rc + ch * 32 : nullptr, rs ? rs + ch * 32 : nullptr);
+    const float* rc = p.rope_cos ? p.rope_cos + (int64_t)(ok ? qrow : 0) * (HD / 2) + ch * 32 : nullptr;
+    const float* rs = p.rope_sin ? p.rope_sin + (int64_t)(ok ? qrow : 0) * (HD / 2) + ch * 32 : nullptr;
+    store_row(tmem + lo + cQ + ch * 64, p.o0 + ((int64_t)row0 + qrow) * p.ld0 + (int64_t)h * HD + ch * 64, p.scale,
+              ok, rc, rs, 2);
   }
   tc_fence_before();
   __syncthreads();
