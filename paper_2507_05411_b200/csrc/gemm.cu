@@ -89,7 +89,11 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   tn = r / gsz;
 }
 
-template <int BN>
+// MC = 1: one CTA per 128 x BN tile.  MC = 2: a cluster of two CTAs computes two vertically
+// adjacent tiles that share the B (weight) tile; each CTA loads half of B and multicasts it
+// to both, so the L2->SM operand traffic per FLOP drops by a third (the kernel is L2-
+// bandwidth-limited at 1-CTA: ~96 B/cycle/SM needed at peak MMA rate).
+template <int BN, int MC>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Args args) {
   using C = Cfg<BN>;
@@ -104,15 +108,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int num_tiles = args.tiles_m * args.tiles_n;
+  const int rank = MC == 2 ? (int)cluster_ctarank() : 0;
+  const int tiles_mg = (args.tiles_m + MC - 1) / MC;  // M-tile groups (pairs when MC == 2)
+  const int num_units = tiles_mg * args.tiles_n;
+  const int unit0 = MC == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int unit_stride = MC == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int nk = (args.K + BK - 1) / BK;
+  auto coords = [&](int u, int& tm, int& tn) {
+    int tg;
+    tile_coords(u, tiles_mg, args.tiles_n, tg, tn);
+    tm = tg * MC + rank;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC);  // both CTAs' MMAs must release a stage (multicast B lands in both)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -122,7 +135,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
   tc_fence_before();
-  __syncthreads();
+  if (MC == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -131,9 +147,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int u = unit0; u < num_units; u += unit_stride) {
         int tm, tn;
-        tile_coords(t, args.tiles_m, args.tiles_n, tm, tn);
+        coords(u, tm, tn);
         const int m0 = tm * BM, n0 = tn * BN;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -147,11 +163,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j) tma_load_2d(a_dst + j * 8192, &tmA, &full[stage], m0 + 64 * j, k0);
           }
-          if (!args.b_mn) {
-            tma_load_2d(b_dst, &tmB, &full[stage], k0, n0);
-          } else {
+          if (MC == 1) {
+            if (!args.b_mn) {
+              tma_load_2d(b_dst, &tmB, &full[stage], k0, n0);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b_dst + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0);
+              for (int j = 0; j < BN / 64; ++j) tma_load_2d(b_dst + j * 8192, &tmB, &full[stage], n0 + 64 * j, k0);
+            }
+          } else {
+            // this CTA's half of B (rows [rank*BN/2, (rank+1)*BN/2) of the tile), to both CTAs
+            constexpr int kHalf = BN / 2;
+            uint8_t* hb = b_dst + rank * (kHalf * BK * 2);
+            if (!args.b_mn) {
+              tma_load_2d_mc(hb, &tmB, &full[stage], k0, n0 + rank * kHalf, 0x3);
+            } else {
+#pragma unroll
+              for (int j = 0; j < kHalf / 64; ++j)
+                tma_load_2d_mc(hb + j * 8192, &tmB, &full[stage], n0 + rank * kHalf + 64 * j, k0, 0x3);
+            }
           }
           if (++stage == C::kStages) {
             stage = 0;
@@ -168,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      for (int u = unit0; u < num_units; u += unit_stride, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -185,7 +214,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t bd = args.b_mn ? sw128_desc(b_addr + kk * 2048, 8192, 1024) : sw128_desc(b_addr + kk * 32, 16, 1024);
             umma_f16_ss(d_tmem, ad, bd, idesc, (kb | kk) != 0);
           }
-          umma_commit(&empty[stage]);
+          if (MC == 2)
+            umma_commit_mc(&empty[stage], 0x3);  // release the stage in both CTAs (B is shared)
+          else
+            umma_commit(&empty[stage]);
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
@@ -200,9 +232,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const Epi& e = args.e;
     int it = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+    for (int u = unit0; u < num_units; u += unit_stride, ++it) {
       int tm, tn;
-      tile_coords(t, args.tiles_m, args.tiles_n, tm, tn);
+      coords(u, tm, tn);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
@@ -320,16 +352,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (MC == 2)
+    cluster_sync();  // no CTA leaves while its peer may still multicast into / commit to it
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::kTmemCols);
   }
 }
 
+static int g_gemm_mc = 2;  // B-multicast cluster pairs (1 disables; tests compare both)
+
 template <int BN>
 int launch(const Args& a, const void* A, int64_t lda, const void* B, int64_t ldb, cudaStream_t st) {
   using C = Cfg<BN>;
+  const int mc = (g_gemm_mc == 2 && a.tiles_m >= 2) ? 2 : 1;
   CUtensorMap ta, tb;
   int s;
   // A: op(A) is MxK.  K-major -> stored [M][K]; MN-major -> stored [K][M].
@@ -338,21 +376,41 @@ int launch(const Args& a, const void* A, int64_t lda, const void* B, int64_t ldb
   else
     s = make_tmap_2d_bf16(&ta, A, a.K, a.M, lda, BK, 64);
   if (s) return s;
-  // B: op(B) is KxN.  K-major -> stored [N][K]; MN-major -> stored [K][N].
+  // B: op(B) is KxN.  K-major -> stored [N][K] (box rows = the BN/mc rows one CTA loads);
+  // MN-major -> stored [K][N].
   if (!a.b_mn)
-    s = make_tmap_2d_bf16(&tb, B, a.N, a.K, ldb, BN, BK);
+    s = make_tmap_2d_bf16(&tb, B, a.N, a.K, ldb, BN / mc, BK);
   else
     s = make_tmap_2d_bf16(&tb, B, a.K, a.N, ldb, BK, 64);
   if (s) return s;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    cudaFuncSetAttribute(gemm_tc<BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    cudaFuncSetAttribute(gemm_tc<BN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     attr_set = true;
   }
-  const int tiles = a.tiles_m * a.tiles_n;
-  const int grid = std::min(tiles, kNumSMs);
-  gemm_tc<BN><<<grid, kThreads, C::kSmem, st>>>(ta, tb, a);
-  return check_launch("gemm_tc");
+  if (mc == 1) {
+    const int grid = std::min(a.tiles_m * a.tiles_n, kNumSMs);
+    gemm_tc<BN, 1><<<grid, kThreads, C::kSmem, st>>>(ta, tb, a);
+    return check_launch("gemm_tc");
+  }
+  const int pairs = ((a.tiles_m + 1) / 2) * a.tiles_n;
+  const int grid = 2 * std::min(pairs, kNumSMs / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc<BN, 2>, ta, tb, a);
+  if (e != cudaSuccess) return fail(CB_ERR_CUDA, "gemm_tc cluster launch: %s", cudaGetErrorString(e));
+  return check_launch("gemm_tc_mc");
 }
 }  // namespace tc
 
@@ -431,6 +489,11 @@ static thread_local int g_last_gemm_tc = 0;  // did the last gemm_impl call run 
 }  // namespace cb
 
 using namespace cb;
+
+extern "C" int cb_gemm_set_multicast(int enable) {
+  tc::g_gemm_mc = enable ? 2 : 1;
+  return CB_OK;
+}
 
 extern "C" int cb_gemm_set_path(int path) {
   if (path < 0 || path > 2) return fail(CB_ERR_ARG, "gemm path must be 0 (auto), 1 (simt) or 2 (tcgen05)");

@@ -28,18 +28,21 @@ def _operands(M, N, K, ta, tb, dtype, dev):
     return a, b
 
 
-@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("M,N,K", SHAPES + [(384, 768, 512), (640, 256, 128)])  # odd tile-pair counts
 @pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
-def test_gemm_tcgen05_bf16(cuda, M, N, K, ta, tb):
-    from paper_2507_05411_b200 import ops
+@pytest.mark.parametrize("mc", [1, 0])
+def test_gemm_tcgen05_bf16(cuda, M, N, K, ta, tb, mc):
+    from paper_2507_05411_b200 import _lib, ops
 
     a, b = _operands(M, N, K, ta, tb, torch.bfloat16, cuda)
     out = torch.empty(M, N, device=cuda, dtype=torch.float32)
     ops.set_gemm_path(2)
+    _lib.call("cb_gemm_set_multicast", mc)
     try:
         ops.gemm(a, b, out, trans_a=ta, trans_b=tb)
     finally:
         ops.set_gemm_path(0)
+        _lib.call("cb_gemm_set_multicast", 1)
     torch.cuda.synchronize()
     ref = _ref(a, b, ta, tb)
     rel = (out - ref).norm() / ref.norm()
