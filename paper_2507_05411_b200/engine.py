@@ -410,45 +410,62 @@ class TrainEngine:
             return float(t.item())
         return out
 
-    def compute_grads(self, tokens):
-        """Forward + backward; gradients land in the (sharded) grad buffers.  Returns (loss, collection)."""
+    def compute_grads(self, tokens, update: bool = False):
+        """Forward + backward; gradients land in the (sharded) grad buffers.  Returns (loss, collection).
+
+        update=True also applies AdamW (step counter advanced first): each layer bucket is
+        updated on a side stream as soon as its gradient is final (right after that layer's
+        backward, or its reduce-scatter under FSDP), overlapping the HBM-bound optimizer with
+        the backward GEMMs of earlier layers.
+        """
         toks = self.upload_tokens(tokens)
+        key = self.step_key(self.step_count)
+        if update:
+            self.step_count += 1
         for rec in self.bufs:
             ops.zero_(rec["grad"])
-        provider = FSDPProvider(self) if self.d.world > 1 else None
+        if self.d.world > 1:
+            provider = FSDPProvider(self, update=update)
+        else:
+            provider = LocalUpdateProvider(self) if update else None
         if provider:
             provider.start_step()
-        loss, col, _ = value_and_grad(self.module, self.state, self.grads, self.step_key(self.step_count),
-                                      {"tokens": toks}, provider=provider, options=self.options)
+        loss, col, _ = value_and_grad(self.module, self.state, self.grads, key, {"tokens": toks}, provider=provider,
+                                      options=self.options)
         if provider:
             provider.finish_backward()
+        if self.d.world > 1:
             self.d.dist.all_reduce(loss, op=self.d.dist.ReduceOp.AVG, group=self.d.group)
         return loss, col
 
+    def _adamw_bucket(self, i: int) -> None:
+        b, rec = self.buckets[i], self.bufs[i]
+        if b.replicated or self.d.world == 1:
+            wshard = rec["work"]
+        else:
+            wshard = rec["work"][self.d.rank * rec["shard"]:(self.d.rank + 1) * rec["shard"]]
+        bf = wshard if (wshard.dtype == torch.bfloat16) else None
+        ops.adamw(rec["master"], rec["grad_shard"], rec["m"], rec["v"], bf, self.lr, self.beta1, self.beta2,
+                  self.eps, self.weight_decay, self.step_count)
+        if bf is None and wshard.data_ptr() != rec["master"].data_ptr():
+            ops.copy2d(rec["master"].view(1, -1), wshard.view(1, -1))
+
     def apply_update(self) -> None:
         self.step_count += 1
-        for b, rec in zip(self.buckets, self.bufs):
-            if b.replicated or self.d.world == 1:
-                wshard = rec["work"]
-            else:
-                wshard = rec["work"][self.d.rank * rec["shard"]:(self.d.rank + 1) * rec["shard"]]
-            bf = wshard if (wshard.dtype == torch.bfloat16) else None
-            ops.adamw(rec["master"], rec["grad_shard"], rec["m"], rec["v"], bf, self.lr, self.beta1, self.beta2,
-                      self.eps, self.weight_decay, self.step_count)
-            if bf is None and wshard.data_ptr() != rec["master"].data_ptr():
-                ops.copy2d(rec["master"].view(1, -1), wshard.view(1, -1))
+        for i in range(len(self.buckets)):
+            self._adamw_bucket(i)
 
     def step(self, tokens):
-        loss, col = self.compute_grads(tokens)
-        self.apply_update()
-        return loss, col
+        """One training step: forward, backward and the AdamW update (overlapped with backward)."""
+        return self.compute_grads(tokens, update=True)
 
 
 class FSDPProvider(ParamProvider):
     """Per-layer all-gather prefetch and reduce-scatter on a side stream (NCCL)."""
 
-    def __init__(self, eng: TrainEngine):
+    def __init__(self, eng: TrainEngine, update: bool = False):
         self.e = eng
+        self.update = update  # run AdamW on each bucket right after its reduce-scatter (comm stream)
         self.dist = eng.d.dist
         self.group = eng.d.group
         self.compute = torch.cuda.current_stream(eng.device)
@@ -486,6 +503,8 @@ class FSDPProvider(ParamProvider):
             else:
                 self.dist.reduce_scatter_tensor(rec["grad_shard"], rec["grad"], op=self.dist.ReduceOp.AVG,
                                                 group=self.group)
+            if self.update:
+                self.e._adamw_bucket(i)
 
     def start_step(self) -> None:
         self._ag(0)
@@ -515,3 +534,38 @@ class FSDPProvider(ParamProvider):
         done = torch.cuda.Event()
         done.record(self.comm)
         self.compute.wait_event(done)
+
+
+class LocalUpdateProvider(ParamProvider):
+    """Single-GPU step: AdamW of each layer bucket on a side stream right after that layer's
+    backward (the root and replicated buckets, whose gradients complete last, at the end)."""
+
+    def __init__(self, eng: TrainEngine):
+        self.e = eng
+        self.compute = torch.cuda.current_stream(eng.device)
+        if not hasattr(eng, "_opt_stream"):
+            eng._opt_stream = torch.cuda.Stream(eng.device)
+        self.side = eng._opt_stream
+        self.index = {b.name: i for i, b in enumerate(eng.buckets)}
+        self.done: set[int] = set()
+
+    def _update(self, i: int) -> None:
+        ready = torch.cuda.Event()
+        ready.record(self.compute)
+        with torch.cuda.stream(self.side):
+            self.side.wait_event(ready)
+            self.e._adamw_bucket(i)
+        self.done.add(i)
+
+    def after_backward(self, path: str) -> None:
+        i = self.index.get(path)
+        if i is not None:
+            self._update(i)
+
+    def finish_backward(self) -> None:
+        for i in range(len(self.e.buckets)):
+            if i not in self.done:
+                self._update(i)
+        fin = torch.cuda.Event()
+        fin.record(self.side)
+        self.compute.wait_event(fin)

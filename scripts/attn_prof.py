@@ -1,0 +1,23 @@
+"""Runs the attention kernels once at the 1B step shape (for ncu captures)."""
+import math
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+from paper_2507_05411_b200 import ops
+
+B, T, H, KVH, hd = 8, 4096, 16, 16, 128
+d, kvd = H * hd, KVH * hd
+dev = torch.device("cuda")
+qkv = torch.randn(B * T, d + 2 * kvd, device=dev).bfloat16()
+q, k, v = qkv[:, :d], qkv[:, d:d + kvd], qkv[:, d + kvd:]
+do = torch.randn(B * T, d, device=dev).bfloat16()
+dqkv = torch.empty_like(qkv)
+scale = 1 / math.sqrt(hd)
+for _ in range(2):
+    o, lse = ops.attention_fwd(q, k, v, B, T, H, KVH, hd, scale)
+    ops.attention_bwd(q, k, v, o, lse, do, dqkv[:, :d], dqkv[:, d:d + kvd], dqkv[:, d + kvd:], B, T, H, KVH, hd, scale)
+torch.cuda.synchronize()
+print("ok")
