@@ -9,6 +9,15 @@ static int g_attn_path = 0;  // 0 auto, 1 force SIMT
 
 using namespace cb;
 
+// tcgen05 backward: bf16 hd 128, 16-byte strides, and lse / delta rows the producer warp can
+// bulk-copy (16-byte aligned rows: T % 4 == 0)
+static bool tc_bwd_ok(const AttnGeom& g, int dtype, const void* q, const void* k, const void* v, const float* lse,
+                      const float* delta, int64_t lddo, int64_t lddq, int64_t lddk, int64_t lddv) {
+  if (g_attn_path != 0 || !attn_tc_supported(g, dtype, q, k, v)) return false;
+  if ((lddo | lddq | lddk | lddv) & 7) return false;
+  return g.T % 4 == 0 && ((reinterpret_cast<uintptr_t>(lse) | reinterpret_cast<uintptr_t>(delta)) & 15) == 0;
+}
+
 extern "C" int cb_attention_set_path(int path) {
   if (path < 0 || path > 1) return fail(CB_ERR_ARG, "attention path must be 0 (auto) or 1 (simt)");
   g_attn_path = path;
@@ -35,7 +44,7 @@ extern "C" int cb_attention_bwd(int batch, int seq_len, int heads, int kv_heads,
   if (int s = check_geom(g)) return s;
   cudaStream_t st = (cudaStream_t)stream;
   if (int s = attn_delta(g, dtype, o, dout, lddo, delta, st)) return s;
-  if (g_attn_path == 0 && attn_tc_supported(g, dtype, q, k, v) && !((lddo | lddq | lddk | lddv) & 7))
+  if (tc_bwd_ok(g, dtype, q, k, v, lse, delta, lddo, lddq, lddk, lddv))
     return attn_bwd_tc(g, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st);
   if (g_attn_path == 0 && attn_fa_supported(g, dtype, q, k, v))
     return attn_bwd_fa(g, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st);
@@ -55,7 +64,7 @@ extern "C" int cb_attention_bwd_rope(int batch, int seq_len, int heads, int kv_h
   AttnGeom g{batch, seq_len, heads, kv_heads, head_dim, ldq, ldk, ldv, ldo, scale};
   if (int s = check_geom(g)) return s;
   cudaStream_t st = (cudaStream_t)stream;
-  if (g_attn_path == 0 && attn_tc_supported(g, dtype, q, k, v) && !((lddo | lddq | lddk | lddv) & 7)) {
+  if (tc_bwd_ok(g, dtype, q, k, v, lse, delta, lddo, lddq, lddk, lddv)) {
     if (int s = attn_delta(g, dtype, o, dout, lddo, delta, st)) return s;
     return attn_bwd_tc(g, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st, cos_t, sin_t);
   }

@@ -5,7 +5,8 @@
 //
 // One CTA per (256-query block, head, batch) = two 128-row query tiles A and B that share
 // every K/V tile (half the K/V shared-memory traffic per FLOP).  384 threads:
-//   warp 0       TMA producer: Q_A, Q_B once, then K_j / V_j into a 2-stage ring
+//   warp 0       TMA producer: Q_A, Q_B once, then K_j into a 3-slot ring (a slot frees
+//                as soon as S_B(j) has read it); warp 3 streams V_j into a 2-slot ring
 //   warp 1       MMA issuer (one thread), ping-pong between the tiles so the tensor core
 //                always has work while one softmax group runs:
 //                  S_A(j) S_B(j) | PV_A(j) S_A(j+1) | PV_B(j) S_B(j+1) | ...
@@ -21,18 +22,32 @@
 namespace cb {
 namespace tca {
 
+// Optional per-iteration clock64 trace of CTA (0,0,0) for pipeline analysis
+// (scripts/attn_trace.cu builds this file with CB_ATTN_TRACE; the library never does).
+#ifdef CB_ATTN_TRACE
+__device__ unsigned long long g_trace[16][64];
+#define ATTN_TRACE(ev, j) \
+  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 64 && (threadIdx.x & 31) == 0) g_trace[ev][j] = clock64()
+#else
+#define ATTN_TRACE(ev, j)
+#endif
+
 constexpr int HD = 128;
 constexpr int BM = 128, BN = 128;
 constexpr int kThreads = 384;
 constexpr int kTileBytes = 128 * 64 * 2;       // one [128 rows][64 cols] bf16 TMA box
 constexpr int kQBytes = 2 * kTileBytes;        // one Q tile: two 64-column K-atoms
-constexpr int kStageBytes = 4 * kTileBytes;    // K (2 atoms) + V (2 MN-blocks)
-constexpr int kStages = 2;
-constexpr int kSmem = 2 * kQBytes + kStages * kStageBytes + 1024 + 256;
+constexpr int kKVBytes = 2 * kTileBytes;       // one K or V tile (two 64-column boxes)
+constexpr int kKSlots = 3, kVSlots = 2;        // K frees after S_B(j), V after PV_B(j)
+constexpr int kSmem = 2 * kQBytes + (kKSlots + kVSlots) * kKVBytes + 1024 + 256;
 constexpr uint32_t kTmemCols = 512;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+#ifndef CB_ATTN_EMU
+#define CB_ATTN_EMU 3
+#endif
+constexpr int kEmuPairs = CB_ATTN_EMU;  // of every 8 exp2 pairs, this many on the FMA pipe
 
 struct Params {
   int T, H, KVH, B;
@@ -58,15 +73,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;  // [2 tiles][kQBytes]
-  uint8_t* sKV = smem + 2 * kQBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kQBytes + kStages * kStageBytes);
+  uint8_t* sK = smem + 2 * kQBytes;    // [kKSlots]
+  uint8_t* sV = sK + kKSlots * kKVBytes;  // [kVSlots]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kVSlots * kKVBytes);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;   // [2] stages
-  uint64_t* kv_empty = bars + 3;  // [2] stages
-  uint64_t* s_full = bars + 5;    // [2] tiles
-  uint64_t* p_ready = bars + 7;   // [2] tiles
-  uint64_t* o_done = bars + 9;    // [2] tiles
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+  uint64_t* k_full = bars + 1;    // [3]
+  uint64_t* k_empty = bars + 4;   // [3]
+  uint64_t* v_full = bars + 7;    // [2]
+  uint64_t* v_empty = bars + 9;   // [2]
+  uint64_t* s_full = bars + 11;   // [2] tiles
+  uint64_t* p_ready = bars + 13;  // [2] tiles
+  uint64_t* o_done = bars + 15;   // [2] tiles
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -80,9 +98,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
     mbar_init(q_full, 1);
+    for (int s = 0; s < kKSlots; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
       mbar_init(&s_full[s], 1);
       mbar_init(&p_ready[s], 4);
       mbar_init(&o_done[s], 1);
@@ -103,61 +125,88 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(sQ + x * kQBytes + kTileBytes, &tmQ, q_full, h * HD + 64, row0 + q0 + x * BM);
       }
       for (int j = 0; j < nblk; ++j) {
+        const int st = j % kKSlots;
+        mbar_wait(&k_empty[st], ((j / kKSlots) & 1) ^ 1);
+        ATTN_TRACE(12, j);
+        mbar_expect_tx(&k_full[st], kKVBytes);
+        tma_load_2d(sK + st * kKVBytes, &tmK, &k_full[st], kvh * HD, row0 + j * BN);
+        tma_load_2d(sK + st * kKVBytes + kTileBytes, &tmK, &k_full[st], kvh * HD + 64, row0 + j * BN);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 3) {
+    // second producer: V_j, independent of the K ring
+    if (lane == 0) {
+      for (int j = 0; j < nblk; ++j) {
         const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], kStageBytes);
-        uint8_t* base = sKV + st * kStageBytes;
-        const int kr = row0 + j * BN;
-        tma_load_2d(base, &tmK, &kv_full[st], kvh * HD, kr);
-        tma_load_2d(base + kTileBytes, &tmK, &kv_full[st], kvh * HD + 64, kr);
-        tma_load_2d(base + 2 * kTileBytes, &tmV, &kv_full[st], kvh * HD, kr);
-        tma_load_2d(base + 3 * kTileBytes, &tmV, &kv_full[st], kvh * HD + 64, kr);
+        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        ATTN_TRACE(13, j);
+        mbar_expect_tx(&v_full[st], kKVBytes);
+        tma_load_2d(sV + st * kKVBytes, &tmV, &v_full[st], kvh * HD, row0 + j * BN);
+        tma_load_2d(sV + st * kKVBytes + kTileBytes, &tmV, &v_full[st], kvh * HD + 64, row0 + j * BN);
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc_s = idesc_bf16_f32(BM, BN, 0, 0);
-      const uint32_t idesc_o = idesc_bf16_f32(BM, HD, 0, 1);
-      auto issue_s = [&](int x, int j) {
-        const uint32_t q_addr = smem_u32(sQ + x * kQBytes);
-        const uint32_t k_addr = smem_u32(sKV + (j & 1) * kStageBytes);
-        const uint32_t d = tmem + x * 128u;
+    // MMA issuer: the whole warp walks the schedule (so descriptors stay warp-uniform, in
+    // uniform registers) and one elected lane issues each group of tcgen05.mma
+    const uint32_t idesc_s = idesc_bf16_f32(BM, BN, 0, 0);
+    const uint32_t idesc_o = idesc_bf16_f32(BM, HD, 0, 1);
+    auto issue_s = [&](int x, int j) {
+      ATTN_TRACE(x, j);
+      const uint64_t qd = sw128_desc(smem_u32(sQ + x * kQBytes), 16, 1024);
+      const uint64_t kd = sw128_desc(smem_u32(sK + (j % kKSlots) * kKVBytes), 16, 1024);
+      const uint32_t d = tmem + x * 128u;
+      if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * kTileBytes + (kk & 3) * 32;
-          umma_f16_ss(d, sw128_desc(q_addr + off, 16, 1024), sw128_desc(k_addr + off, 16, 1024), idesc_s, kk > 0);
+          const uint64_t off = (uint64_t)(((kk >> 2) * kTileBytes + (kk & 3) * 32) >> 4);
+          umma_f16_ss(d, qd + off, kd + off, idesc_s, kk > 0);
         }
         umma_commit(&s_full[x]);
-      };
-      auto issue_pv = [&](int x, int j) {
-        mbar_wait(&p_ready[x], j & 1);
-        tc_fence_after();
-        const uint32_t v_addr = smem_u32(sKV + (j & 1) * kStageBytes + 2 * kTileBytes);
-#pragma unroll
-        for (int k = 0; k < BN / 16; ++k)
-          umma_f16_ts(tmem + 256u + x * 128u, tmem + x * 128u + k * 8, sw128_desc(v_addr + k * 2048, 16384, 1024),
-                      idesc_o, (j | k) != 0);
-        umma_commit(&o_done[x]);
-      };
-      mbar_wait(q_full, 0);
-      mbar_wait(&kv_full[0], 0);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int x, int j) {
+      if (x == 0) ATTN_TRACE(14, j);
+      mbar_wait(&p_ready[x], j & 1);
+      if (x == 0) mbar_wait(&v_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
-      issue_s(0, 0);
-      issue_s(1, 0);
-      for (int j = 0; j < nblk; ++j) {
-        issue_pv(0, j);
-        if (j + 1 < nblk) {
-          mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
-          tc_fence_after();
-          issue_s(0, j + 1);
-        }
-        issue_pv(1, j);
-        umma_commit(&kv_empty[j & 1]);
-        if (j + 1 < nblk) issue_s(1, j + 1);
+      ATTN_TRACE(2 + x, j);
+      const uint64_t vd = sw128_desc(smem_u32(sV + (j & 1) * kKVBytes), 16384, 1024);
+      const uint32_t o = tmem + 256u + x * 128u, pa = tmem + x * 128u;
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < BN / 16; ++k) umma_f16_ts(o, pa + k * 8, vd + (uint64_t)(k * 128), idesc_o, (j | k) != 0);
+        umma_commit(&o_done[x]);
+      }
+      __syncwarp();
+      ATTN_TRACE(10 + 5 * x, j);
+    };
+    auto commit = [&](uint64_t* bar) {
+      if (elect_one()) umma_commit(bar);
+      __syncwarp();
+    };
+    mbar_wait(q_full, 0);
+    mbar_wait(&k_full[0], 0);
+    tc_fence_after();
+    issue_s(0, 0);
+    issue_s(1, 0);
+    commit(&k_empty[0]);
+    for (int j = 0; j < nblk; ++j) {
+      issue_pv(0, j);
+      if (j + 1 < nblk) {
+        mbar_wait(&k_full[(j + 1) % kKSlots], ((j + 1) / kKSlots) & 1);
+        tc_fence_after();
+        issue_s(0, j + 1);
+      }
+      issue_pv(1, j);
+      commit(&v_empty[j & 1]);
+      if (j + 1 < nblk) {
+        issue_s(1, j + 1);
+        commit(&k_empty[(j + 1) % kKSlots]);
       }
     }
-    __syncwarp();
   } else if (warp >= 4) {
     const int x = (warp - 4) >> 2;  // query tile
     const int q = warp & 3;         // TMEM lane quadrant
@@ -170,28 +219,67 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < nblk; ++j) {
       mbar_wait(&s_full[x], j & 1);
       tc_fence_after();
-      // pass 1 over the S row in TMEM: row max (keeps only 32 values live)
+      if (q == 0 && lane == 0) ATTN_TRACE(4 + 3 * x, j);
+      // the whole S row (128 f32) in registers: four loads in flight, one wait
       const int valid = min(BN, p.T - j * BN);
-      float mx = -INFINITY;
-#pragma unroll 1
-      for (int cc = 0; cc < 4; ++cc) {
-        uint32_t v[32];
-        tmem_ld32(scol + cc * 32, v);
-        tmem_ld_wait();
-        if (valid >= BN) {
+      uint32_t sv[4][32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
-        } else {
+      for (int cc = 0; cc < 4; ++cc) tmem_ld32(scol + cc * 32, sv[cc]);
+      tmem_ld_wait_regs(sv[0]);
+      reg_fence(sv[1]);
+      reg_fence(sv[2]);
+      reg_fence(sv[3]);
+      if (valid < BN) {  // ragged last block: columns past T take no part
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc)
 #pragma unroll
           for (int i = 0; i < 32; ++i)
-            if (cc * 32 + i < valid) mx = fmaxf(mx, __uint_as_float(v[i]));
-        }
+            if (cc * 32 + i >= valid) sv[cc][i] = __float_as_uint(-INFINITY);
       }
-      mx *= c;
+      float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          mx0 = fmaxf(mx0, fmaxf(__uint_as_float(sv[cc][i]), __uint_as_float(sv[cc][i + 1])));
+          mx1 = fmaxf(mx1, fmaxf(__uint_as_float(sv[cc][i + 2]), __uint_as_float(sv[cc][i + 3])));
+        }
+      const float mx = fmaxf(mx0, mx1) * c;
+      if (q == 0 && lane == 0) ATTN_TRACE(5 + 3 * x, j);
       const bool need = mx > m_used + kRescaleThreshold;
-      const float m_new = need ? mx : m_used;
+      const float m_prev = m_used;
+      if (need) m_used = mx;
+      // P = exp2(S c - m) packed to bf16 pairs into the first 64 columns of S.  Pair
+      // arithmetic (FFMA2/FADD2); kEmuPairs of every 8 pairs take the polynomial exp2 on the
+      // FMA pipe so the MUFU (16 ex2/clk/SM) stops being the bound.
+      const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_used, -m_used);
+      float2 rsa = make_float2(0.f, 0.f), rsb = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float2 a = ffma2(make_float2(__uint_as_float(sv[cc][2 * i]), __uint_as_float(sv[cc][2 * i + 1])), c2, nm2);
+          float2 e;
+          if ((i & 7) < kEmuPairs) {
+            e = exp2_poly2(a);
+          } else {
+            e.x = fast_exp2(a.x);
+            e.y = fast_exp2(a.y);
+          }
+          if (i & 1)
+            rsb = fadd2(rsb, e);
+          else
+            rsa = fadd2(rsa, e);
+          pk[i] = pack2(e.x, e.y);
+        }
+        tmem_st16(scol + cc * 16, pk);
+      }
+      const float rs = (rsa.x + rsa.y) + (rsb.x + rsb.y);
+      // lazy rescale of O (after the exponentials, when the S row is no longer live): only
+      // when some row's max grew past the threshold; PV_j has not been issued yet
       if (__any_sync(0xffffffffu, need)) {
-        const float corr = need ? fast_exp2(m_used - m_new) : 1.f;
+        const float corr = need ? fast_exp2(m_prev - m_used) : 1.f;
         if (j > 0) {
           mbar_wait(&o_done[x], (j - 1) & 1);  // PV_{j-1} has finished writing O
           tc_fence_after();
@@ -199,40 +287,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int cc = 0; cc < HD / 32; ++cc) {
             uint32_t o[32];
             tmem_ld32(ocol + cc * 32, o);
-            tmem_ld_wait();
+            tmem_ld_wait_regs(o);
 #pragma unroll
             for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
             tmem_st32(ocol + cc * 32, o);
           }
-          tmem_st_wait();
         }
         l *= corr;
-        m_used = m_new;
-      }
-      // pass 2: P = exp2(S c - m) packed to bf16 pairs over the first 64 columns of S.
-      // Chunk cc's packed output (columns [16cc, 16cc+16)) only overwrites S columns that
-      // earlier chunks already consumed.
-      float rs = 0.f;
-#pragma unroll 1
-      for (int cc = 0; cc < 4; ++cc) {
-        uint32_t v[32];
-        tmem_ld32(scol + cc * 32, v);
-        tmem_ld_wait();
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const bool ok0 = cc * 32 + 2 * i < valid, ok1 = cc * 32 + 2 * i + 1 < valid;
-          const float p0 = ok0 ? fast_exp2(fmaf(__uint_as_float(v[2 * i]), c, -m_used)) : 0.f;
-          const float p1 = ok1 ? fast_exp2(fmaf(__uint_as_float(v[2 * i + 1]), c, -m_used)) : 0.f;
-          rs += p0 + p1;
-          pk[i] = pack2(p0, p1);
-        }
-        tmem_st16(scol + cc * 16, pk);
       }
       l += rs;
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
+      if (q == 0 && lane == 0) ATTN_TRACE(6 + 3 * x, j);
       if (lane == 0) mbar_arrive(&p_ready[x]);
     }
     // epilogue

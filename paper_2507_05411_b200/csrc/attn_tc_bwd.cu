@@ -28,7 +28,9 @@ constexpr int BT = 128;  // tile rows (keys or queries)
 constexpr int kThreads = 384;
 constexpr int kBox = 128 * 64 * 2;  // one [128][64] bf16 TMA box (16 KB)
 constexpr int kTile = 2 * kBox;     // one [128][128] tile (two 64-column atoms)
-constexpr int kSmem = 6 * kTile + 1024 + 4096;
+// dq: Q, dO, K ring [3], V ring [2] = 224 KB (+ alignment slack)
+constexpr int kKSlots = 3, kVSlots = 2;
+constexpr int kSmemDq = (2 + kKSlots + kVSlots) * kTile + 1024 + 256;
 constexpr uint32_t kCols = 512;
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -56,12 +58,18 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
-// K-major operand descriptor for the kk-th K=16 step of a tile whose rows start at `base`
-__device__ __forceinline__ uint64_t kdesc(uint32_t base, int kk) {
-  return sw128_desc(base + (kk >> 2) * kBox + (kk & 3) * 32, 16, 1024);
-}
-// MN-major operand descriptor (rows = K dim, 128 columns = N) for the k-th K=16 step
-__device__ __forceinline__ uint64_t mndesc(uint32_t base, int k) { return sw128_desc(base + k * 2048, kBox, 1024); }
+// descriptor start-address offset (16-byte units) of the kk-th K=16 step of a K-major
+// [128][128] tile (two 64-column swizzle atoms)
+__device__ __forceinline__ uint64_t koff(int kk) { return (uint64_t)(((kk >> 2) * kBox + (kk & 3) * 32) >> 4); }
+
+#ifdef CB_ATTN_TRACE
+__device__ unsigned long long g_btrace[16][64];
+#define BWD_TRACE(ev, j) \
+  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 64 && (threadIdx.x & 31) == 0) g_btrace[ev][j] = clock64()
+#else
+#define BWD_TRACE(ev, j)
+#endif
+
 
 // Store `nchunks` x 32 f32 TMEM columns of this thread's row as bf16 (times `mul`); with
 // rc/rs (cos/sin of this row's position) first apply the inverse RoPE rotation — the
@@ -97,40 +105,82 @@ __device__ __forceinline__ void store_row(uint32_t taddr, __nv_bfloat16* dst, fl
   }
 }
 
-// Packs 64 f32 values (two 32-column TMEM loads at src) through `f` into 32 bf16 pairs.
-template <typename F>
-__device__ __forceinline__ void load64(uint32_t src, float (&out)[64], F f) {
+#ifndef CB_ATTN_EMU_BWD
+#define CB_ATTN_EMU_BWD 2
+#endif
+constexpr int kEmuPairs = CB_ATTN_EMU_BWD;  // of every 8 exp2 pairs, this many on the FMA pipe
+
+// 64 f32 TMEM columns of this thread's row: both loads in flight, one wait
+__device__ __forceinline__ void ld64(uint32_t src, uint32_t (&v)[2][32]) {
+  tmem_ld32(src, v[0]);
+  tmem_ld32(src + 32, v[1]);
+  tmem_ld_wait_regs(v[0]);
+  reg_fence(v[1]);
+}
+__device__ __forceinline__ float4 lds4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float2 col2(const uint32_t (&v)[2][32], int i) {  // columns 2i, 2i+1
+  return make_float2(__uint_as_float(v[i >> 4][2 * (i & 15)]), __uint_as_float(v[i >> 4][2 * (i & 15) + 1]));
+}
+__device__ __forceinline__ float2 exp2_pair(float2 a, int i) {
+  if ((i & 7) < kEmuPairs) return exp2_poly2(a);
+  return make_float2(fast_exp2(a.x), fast_exp2(a.y));
+}
+// pack 32 pairs to bf16 and store them as 32 TMEM columns at dst
+__device__ __forceinline__ void pack_store(uint32_t dst, const float2 (&v)[32]) {
+  uint32_t pk[2][16];
 #pragma unroll
-  for (int cc = 0; cc < 2; ++cc) {
-    uint32_t v[32];
-    tmem_ld32(src + cc * 32, v);
-    tmem_ld_wait();
-#pragma unroll
-    for (int i = 0; i < 32; ++i) out[cc * 32 + i] = f(cc * 32 + i, __uint_as_float(v[i]));
+  for (int i = 0; i < 16; ++i) {
+    pk[0][i] = pack2(v[i].x, v[i].y);
+    pk[1][i] = pack2(v[16 + i].x, v[16 + i].y);
   }
+  tmem_st16(dst, pk[0]);
+  tmem_st16(dst + 16, pk[1]);
+  tmem_st_wait();
 }
 
 // ====================================================================== dK / dV
+// 128-query tiles.  TMEM: S^T | dP^T | dV | dK (128 columns each).  Compute warps w and w+4
+// share TMEM lane quadrant w%4: half ch takes query columns [64 ch, 64 ch + 64) and writes
+// its bf16 pairs to columns [64 ch, 64 ch + 32) of the same region, so the halves never
+// touch each other's inputs; the dV / dK MMAs read the packed A operand from both halves.
+// MMA order per tile u:  [p_ready(u)] dV(u) S(u+1) | [ds_ready(u)] dK(u) dP(u+1).
+// smem: K, V, Q ring [3], dO ring [2], lse/delta ring [2] = 226 KB: this needs the dynamic
+// shared-memory base to be 1024-aligned already (checked).
+constexpr int kQSlots = 3, kGSlots = 2;
+constexpr int kSmemDkdv = (2 + kQSlots + kGSlots) * kTile + 2 * 1024 + 8 * 24;
+
+// TMEM column of the k-th K=16 step of a packed bf16 A operand written by the two halves
+__device__ __forceinline__ uint32_t packed_col(int k) { return (uint32_t)((k >> 2) * 64 + (k & 3) * 8); }
+
 __global__ void __launch_bounds__(kThreads, 1)
     dkdv_k(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmG, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw;
+  if (smem_u32(smem) & 1023) __trap();  // see kSmemDkdv
   uint8_t* sK = smem;
   uint8_t* sV = smem + kTile;
-  uint8_t* ring = smem + 2 * kTile;                        // [2] x {Q tile, dO tile}
-  float* sL = reinterpret_cast<float*>(smem + 6 * kTile);  // [2][128] lse * log2e
-  float* sD = sL + 256;                                    // [2][128] delta
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 256);
+  uint8_t* sQ = smem + 2 * kTile;                               // [kQSlots]
+  uint8_t* sG = sQ + kQSlots * kTile;                           // [kGSlots]
+  float* sLD = reinterpret_cast<float*>(sG + kGSlots * kTile);  // [2] x {lse[128], delta[128]}
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sG + kGSlots * kTile + 2048);
   uint64_t* kv_full = bars;
-  uint64_t* qd_full = bars + 1;   // [2]
-  uint64_t* qd_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* dp_full = bars + 6;
-  uint64_t* p_ready = bars + 7;
-  uint64_t* ds_ready = bars + 8;
-  uint64_t* mma_done = bars + 9;
-  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* q_full = bars + 1;     // [3]
+  uint64_t* q_empty = bars + 4;    // [3]
+  uint64_t* g_full = bars + 7;     // [2]
+  uint64_t* g_empty = bars + 9;    // [2]
+  uint64_t* ld_full = bars + 11;   // [2]
+  uint64_t* ld_empty = bars + 13;  // [2]
+  uint64_t* s_full = bars + 15;
+  uint64_t* dp_full = bars + 16;
+  uint64_t* p_ready = bars + 17;
+  uint64_t* ds_ready = bars + 18;
+  uint64_t* mma_done = bars + 19;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 20);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kt = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
@@ -145,9 +195,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmV);
     tma_prefetch_desc(&tmG);
     mbar_init(kv_full, 1);
+    for (int s = 0; s < kQSlots; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_empty[s], 1);
+    }
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&qd_full[s], 1);
-      mbar_init(&qd_empty[s], 1);
+      mbar_init(&g_full[s], 1);
+      mbar_init(&g_empty[s], 1);
+      mbar_init(&ld_full[s], 1);
+      mbar_init(&ld_empty[s], 8);
     }
     mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
@@ -164,6 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t cS = 0, cP = 128, cV = 256, cK = 384;
 
   if (warp == 0) {
+    // producer A: K, V once, then the Q tiles (3-slot ring; a slot frees after dK(u))
     if (lane == 0) {
       mbar_expect_tx(kv_full, 2 * kTile);
       tma_load_2d(sK, &tmK, kv_full, kvh * HD, row0 + k0);
@@ -171,120 +228,160 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_load_2d(sV, &tmV, kv_full, kvh * HD, row0 + k0);
       tma_load_2d(sV + kBox, &tmV, kv_full, kvh * HD + 64, row0 + k0);
       for (int it = 0; it < total; ++it) {
-        const int st = it & 1;
+        const int st = it % kQSlots;
         const int h = kvh * group + it / nq, q0 = (it % nq) * BT;
-        mbar_wait(&qd_empty[st], ((it >> 1) & 1) ^ 1);
-        mbar_expect_tx(&qd_full[st], 2 * kTile);
-        uint8_t* base = ring + st * 2 * kTile;
-        tma_load_2d(base, &tmQ, &qd_full[st], h * HD, row0 + q0);
-        tma_load_2d(base + kBox, &tmQ, &qd_full[st], h * HD + 64, row0 + q0);
-        tma_load_2d(base + kTile, &tmG, &qd_full[st], h * HD, row0 + q0);
-        tma_load_2d(base + kTile + kBox, &tmG, &qd_full[st], h * HD + 64, row0 + q0);
+        mbar_wait(&q_empty[st], ((it / kQSlots) & 1) ^ 1);
+        BWD_TRACE(8, it);
+        mbar_expect_tx(&q_full[st], kTile);
+        tma_load_2d(sQ + st * kTile, &tmQ, &q_full[st], h * HD, row0 + q0);
+        tma_load_2d(sQ + st * kTile + kBox, &tmQ, &q_full[st], h * HD + 64, row0 + q0);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 3) {
+    // producer B: dO tiles (a slot frees after dV(u)) and the lse / delta rows of each tile
+    // (bulk copies; a slot frees once the compute warps finished the dS pass)
+    if (lane == 0) {
+      for (int it = 0; it < total; ++it) {
+        const int st = it & 1;
+        const uint32_t ph = ((it >> 1) & 1) ^ 1;
+        const int h = kvh * group + it / nq, q0 = (it % nq) * BT;
+        mbar_wait(&g_empty[st], ph);
+        BWD_TRACE(9, it);
+        mbar_expect_tx(&g_full[st], kTile);
+        tma_load_2d(sG + st * kTile, &tmG, &g_full[st], h * HD, row0 + q0);
+        tma_load_2d(sG + st * kTile + kBox, &tmG, &g_full[st], h * HD + 64, row0 + q0);
+        const int nvalid = min(BT, p.T - q0);
+        const uint32_t bytes = (uint32_t)nvalid * 4u;
+        const int64_t li = ((int64_t)b * p.H + h) * p.T + q0;
+        mbar_wait(&ld_empty[st], ph);
+        // ragged last tile: lse = +inf makes P (hence dS) vanish for query columns past T,
+        // so the compute warps need no masking
+        for (int i = nvalid; i < BT; ++i) {
+          sLD[st * 256 + i] = INFINITY;
+          sLD[st * 256 + 128 + i] = 0.f;
+        }
+        mbar_expect_tx(&ld_full[st], 2 * bytes);
+        bulk_load(sLD + st * 256, p.lse + li, bytes, &ld_full[st]);
+        bulk_load(sLD + st * 256 + 128, p.delta + li, bytes, &ld_full[st]);
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t id_s = idesc_bf16_f32(128, 128, 0, 0);    // K-major x K-major
-      const uint32_t id_acc = idesc_bf16_f32(128, 128, 0, 1);  // TMEM A x MN-major B
-      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-      auto tileQ = [&](int u) { return smem_u32(ring + (u & 1) * 2 * kTile); };
-      auto issue_s = [&](int u) {
-        mbar_wait(&qd_full[u & 1], (u >> 1) & 1);
-        tc_fence_after();
-        const uint32_t aQ = tileQ(u);
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + cS, kdesc(aK, kk), kdesc(aQ, kk), id_s, kk > 0);
-        umma_commit(s_full);
-      };
-      auto issue_dp = [&](int u) {
-        const uint32_t aG = tileQ(u) + kTile;
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + cP, kdesc(aV, kk), kdesc(aG, kk), id_s, kk > 0);
-        umma_commit(dp_full);
-      };
-      mbar_wait(kv_full, 0);
+    // MMA issuer: the whole warp walks the schedule (warp-uniform descriptors in uniform
+    // registers); one elected lane issues each MMA group
+    const uint32_t id_s = idesc_bf16_f32(128, 128, 0, 0);    // K-major x K-major
+    const uint32_t id_acc = idesc_bf16_f32(128, 128, 0, 1);  // TMEM A x MN-major B
+    const uint64_t dK = sw128_desc(smem_u32(sK), 16, 1024), dV = sw128_desc(smem_u32(sV), 16, 1024);
+    auto tileQ = [&](int u) { return smem_u32(sQ + (u % kQSlots) * kTile); };
+    auto tileG = [&](int u) { return smem_u32(sG + (u & 1) * kTile); };
+    auto issue_s = [&](int u) {
+      mbar_wait(&q_full[u % kQSlots], (u / kQSlots) & 1);
       tc_fence_after();
-      issue_s(0);
-      issue_dp(0);
-      for (int u = 0; u < total; ++u) {
-        const uint32_t aQ = tileQ(u), aG = aQ + kTile;
-        mbar_wait(p_ready, u & 1);
-        tc_fence_after();
+      BWD_TRACE(1, u);
+      const uint64_t dQ = sw128_desc(tileQ(u), 16, 1024);
+      if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < BT / 16; ++k) umma_f16_ts(tmem + cV, tmem + cS + k * 8, mndesc(aG, k), id_acc, (u | k) != 0);
-        if (u + 1 < total) issue_s(u + 1);  // S^T region: P^T(u) already consumed (in-order)
-        mbar_wait(ds_ready, u & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int k = 0; k < BT / 16; ++k) umma_f16_ts(tmem + cK, tmem + cP + k * 8, mndesc(aQ, k), id_acc, (u | k) != 0);
-        umma_commit(&qd_empty[u & 1]);
-        if (u + 1 < total) issue_dp(u + 1);  // dP^T region: dS^T(u) already consumed
+        for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + cS, dK + koff(kk), dQ + koff(kk), id_s, kk > 0);
+        umma_commit(s_full);
       }
-      umma_commit(mma_done);
+      __syncwarp();
+    };
+    auto issue_dp = [&](int u) {
+      mbar_wait(&g_full[u & 1], (u >> 1) & 1);
+      tc_fence_after();
+      BWD_TRACE(3, u);
+      const uint64_t dG = sw128_desc(tileG(u), 16, 1024);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + cP, dV + koff(kk), dG + koff(kk), id_s, kk > 0);
+        umma_commit(dp_full);
+      }
+      __syncwarp();
+    };
+    mbar_wait(kv_full, 0);
+    tc_fence_after();
+    issue_s(0);
+    issue_dp(0);
+    for (int u = 0; u < total; ++u) {
+      const uint64_t mQ = sw128_desc(tileQ(u), kBox, 1024), mG = sw128_desc(tileG(u), kBox, 1024);
+      mbar_wait(p_ready, u & 1);
+      tc_fence_after();
+      BWD_TRACE(0, u);
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < BT / 16; ++k)
+          umma_f16_ts(tmem + cV, tmem + cS + packed_col(k), mG + (uint64_t)(k * 128), id_acc, (u | k) != 0);
+        umma_commit(&g_empty[u & 1]);  // dO(u) is done (dP(u) and dV(u))
+      }
+      __syncwarp();
+      if (u + 1 < total) issue_s(u + 1);  // S^T region: P^T(u) already consumed (in-order)
+      mbar_wait(ds_ready, u & 1);
+      tc_fence_after();
+      BWD_TRACE(2, u);
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < BT / 16; ++k)
+          umma_f16_ts(tmem + cK, tmem + cP + packed_col(k), mQ + (uint64_t)(k * 128), id_acc, (u | k) != 0);
+        umma_commit(&q_empty[u % kQSlots]);
+      }
+      __syncwarp();
+      if (u + 1 < total) issue_dp(u + 1);  // dP^T region: dS^T(u) already consumed
     }
+    if (elect_one()) umma_commit(mma_done);
     __syncwarp();
   } else if (warp >= 4) {
     const int q = warp & 3;
-    const int ch = (warp - 4) >> 2;    // query-column half of each tile
-    const int t = q * 32 + lane;       // key row inside the tile
-    const int tt = threadIdx.x - 128;  // 0..255
+    const int ch = (warp - 4) >> 2;  // query-column half of each tile
+    const int t = q * 32 + lane;     // key row inside the tile
     const uint32_t lo = (uint32_t)(q * 32) << 16;
+    const uint32_t half = (uint32_t)ch * 64u;
     const float c = p.scale * kLog2e;
+    const float2 c2 = make_float2(c, c), nlog2e = make_float2(-kLog2e, -kLog2e);
     for (int u = 0; u < total; ++u) {
-      const int h = kvh * group + u / nq, q0 = (u % nq) * BT;
-      if (tt < 128) {
-        const int qi = q0 + tt;
-        const int64_t li = ((int64_t)b * p.H + h) * p.T + qi;
-        sL[(u & 1) * 128 + tt] = qi < p.T ? p.lse[li] * kLog2e : 0.f;
-        sD[(u & 1) * 128 + tt] = qi < p.T ? p.delta[li] : 0.f;
-      }
-      named_sync(1, 256);
-      const float* L = sL + (u & 1) * 128 + ch * 64;
-      const float* D = sD + (u & 1) * 128 + ch * 64;
-      const int valid = min(BT, p.T - q0) - ch * 64;
+      mbar_wait(&ld_full[u & 1], (u >> 1) & 1);
+      const uint32_t sL = smem_u32(sLD + (u & 1) * 256 + ch * 64);  // lse; delta at +128 floats
       mbar_wait(s_full, u & 1);
       tc_fence_after();
-      float pr[64];
-      if (valid >= 64)
-        load64(tmem + lo + cS + ch * 64, pr, [&](int i, float s) { return fast_exp2(fmaf(s, c, -L[i])); });
-      else
-        load64(tmem + lo + cS + ch * 64, pr,
-               [&](int i, float s) { return i < valid ? fast_exp2(fmaf(s, c, -L[i])) : 0.f; });
+      if (warp == 4) BWD_TRACE(4, u);
+      float2 pr[32];
       {
-        uint32_t pk[2][16];
+        uint32_t sv[2][32];
+        ld64(tmem + lo + cS + half, sv);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          pk[0][i] = pack2(pr[2 * i], pr[2 * i + 1]);
-          pk[1][i] = pack2(pr[32 + 2 * i], pr[33 + 2 * i]);
+        for (int i = 0; i < 32; i += 2) {
+          const float4 l4 = lds4(sL + 8 * i);
+          pr[i] = exp2_pair(ffma2(col2(sv, i), c2, fmul2(make_float2(l4.x, l4.y), nlog2e)), i);
+          pr[i + 1] = exp2_pair(ffma2(col2(sv, i + 1), c2, fmul2(make_float2(l4.z, l4.w), nlog2e)), i + 1);
         }
-        named_sync(2 + q, 64);  // the partner warp has read its raw S^T columns
-        tmem_st16(tmem + lo + cS + ch * 32, pk[0]);
-        tmem_st16(tmem + lo + cS + ch * 32 + 16, pk[1]);
-        tmem_st_wait();
+        pack_store(tmem + lo + cS + half, pr);  // over this half's own S^T columns
       }
       tc_fence_before();
       __syncwarp();
+      if (warp == 4) BWD_TRACE(5, u);
       if (lane == 0) mbar_arrive(p_ready);
       mbar_wait(dp_full, u & 1);
       tc_fence_after();
+      if (warp == 4) BWD_TRACE(6, u);
       {
-        float ds[64];
-        load64(tmem + lo + cP + ch * 64, ds, [&](int i, float dp) { return pr[i] * (dp - D[i]); });
-        uint32_t pk[2][16];
+        uint32_t dv[2][32];
+        ld64(tmem + lo + cP + half, dv);
+        float2 ds[32];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          pk[0][i] = pack2(ds[2 * i], ds[2 * i + 1]);
-          pk[1][i] = pack2(ds[32 + 2 * i], ds[33 + 2 * i]);
+        for (int i = 0; i < 32; i += 2) {
+          const float4 d4 = lds4(sL + 512 + 8 * i);
+          ds[i] = fmul2(pr[i], ffma2(make_float2(d4.x, d4.y), make_float2(-1.f, -1.f), col2(dv, i)));
+          ds[i + 1] = fmul2(pr[i + 1], ffma2(make_float2(d4.z, d4.w), make_float2(-1.f, -1.f), col2(dv, i + 1)));
         }
-        named_sync(2 + q, 64);
-        tmem_st16(tmem + lo + cP + ch * 32, pk[0]);
-        tmem_st16(tmem + lo + cP + ch * 32 + 16, pk[1]);
-        tmem_st_wait();
+        pack_store(tmem + lo + cP + half, ds);
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(ds_ready);
+      if (warp == 4) BWD_TRACE(7, u);
+      if (lane == 0) {
+        mbar_arrive(ds_ready);
+        mbar_arrive(&ld_empty[u & 1]);
+      }
     }
     mbar_wait(mma_done, 0);
     tc_fence_after();
@@ -315,16 +412,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
   uint8_t* sG = smem + kTile;
-  uint8_t* ring = smem + 2 * kTile;  // [2] x {K tile, V tile}
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * kTile + 2048);
+  uint8_t* sK = smem + 2 * kTile;      // [kKSlots]
+  uint8_t* sV = sK + kKSlots * kTile;  // [kVSlots]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kVSlots * kTile);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* dp_full = bars + 7;
-  uint64_t* ds_ready = bars + 8;
-  uint64_t* mma_done = bars + 9;
-  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* k_full = bars + 1;   // [3]
+  uint64_t* k_empty = bars + 4;  // [3]
+  uint64_t* v_full = bars + 7;   // [2]
+  uint64_t* v_empty = bars + 9;  // [2]
+  uint64_t* s_full = bars + 11;  // [2]
+  uint64_t* dp_full = bars + 13;
+  uint64_t* ds_ready = bars + 14;
+  uint64_t* mma_done = bars + 15;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -338,9 +438,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmV);
     tma_prefetch_desc(&tmG);
     mbar_init(q_full, 1);
+    for (int s = 0; s < kKSlots; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
       mbar_init(&s_full[s], 1);
     }
     mbar_init(dp_full, 1);
@@ -353,9 +457,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *slot;
-  const uint32_t cP = 256, cQ = 384;  // S buffers at st * 128
+  const uint32_t cP = 256, cQ = 384;  // S buffers at (j & 1) * 128
 
   if (warp == 0) {
+    // producer A: Q, dO once, then K_j (3-deep ring; a slot frees after dQ(j))
     if (lane == 0) {
       mbar_expect_tx(q_full, 2 * kTile);
       tma_load_2d(sQ, &tmQ, q_full, h * HD, row0 + q0);
@@ -363,55 +468,74 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_load_2d(sG, &tmG, q_full, h * HD, row0 + q0);
       tma_load_2d(sG + kBox, &tmG, q_full, h * HD + 64, row0 + q0);
       for (int j = 0; j < nk; ++j) {
+        const int st = j % kKSlots;
+        mbar_wait(&k_empty[st], ((j / kKSlots) & 1) ^ 1);
+        mbar_expect_tx(&k_full[st], kTile);
+        tma_load_2d(sK + st * kTile, &tmK, &k_full[st], kvh * HD, row0 + j * BT);
+        tma_load_2d(sK + st * kTile + kBox, &tmK, &k_full[st], kvh * HD + 64, row0 + j * BT);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 3) {
+    // producer B: V_j (a slot frees after dP(j))
+    if (lane == 0) {
+      for (int j = 0; j < nk; ++j) {
         const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], 2 * kTile);
-        uint8_t* base = ring + st * 2 * kTile;
-        const int kr = row0 + j * BT;
-        tma_load_2d(base, &tmK, &kv_full[st], kvh * HD, kr);
-        tma_load_2d(base + kBox, &tmK, &kv_full[st], kvh * HD + 64, kr);
-        tma_load_2d(base + kTile, &tmV, &kv_full[st], kvh * HD, kr);
-        tma_load_2d(base + kTile + kBox, &tmV, &kv_full[st], kvh * HD + 64, kr);
+        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&v_full[st], kTile);
+        tma_load_2d(sV + st * kTile, &tmV, &v_full[st], kvh * HD, row0 + j * BT);
+        tma_load_2d(sV + st * kTile + kBox, &tmV, &v_full[st], kvh * HD + 64, row0 + j * BT);
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t id_s = idesc_bf16_f32(128, 128, 0, 0);
-      const uint32_t id_acc = idesc_bf16_f32(128, 128, 0, 1);
-      const uint32_t aQ = smem_u32(sQ), aG = smem_u32(sG);
-      auto issue_s = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t aK = smem_u32(ring + st * 2 * kTile);
+    const uint32_t id_s = idesc_bf16_f32(128, 128, 0, 0);
+    const uint32_t id_acc = idesc_bf16_f32(128, 128, 0, 1);
+    const uint64_t dQ = sw128_desc(smem_u32(sQ), 16, 1024), dG = sw128_desc(smem_u32(sG), 16, 1024);
+    auto issue_s = [&](int j) {
+      const int ks = j % kKSlots;
+      mbar_wait(&k_full[ks], (j / kKSlots) & 1);
+      tc_fence_after();
+      const uint64_t dKj = sw128_desc(smem_u32(sK + ks * kTile), 16, 1024);
+      if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + st * 128u, kdesc(aQ, kk), kdesc(aK, kk), id_s, kk > 0);
-        umma_commit(&s_full[st]);
-      };
-      auto issue_dp = [&](int j) {
-        const uint32_t aV = smem_u32(ring + (j & 1) * 2 * kTile) + kTile;
+        for (int kk = 0; kk < HD / 16; ++kk)
+          umma_f16_ss(tmem + (j & 1) * 128u, dQ + koff(kk), dKj + koff(kk), id_s, kk > 0);
+        umma_commit(&s_full[j & 1]);
+      }
+      __syncwarp();
+    };
+    auto issue_dp = [&](int j) {
+      mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      const uint64_t dVj = sw128_desc(smem_u32(sV + (j & 1) * kTile), 16, 1024);
+      if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + cP, kdesc(aG, kk), kdesc(aV, kk), id_s, kk > 0);
+        for (int kk = 0; kk < HD / 16; ++kk) umma_f16_ss(tmem + cP, dG + koff(kk), dVj + koff(kk), id_s, kk > 0);
         umma_commit(dp_full);
-      };
-      mbar_wait(q_full, 0);
-      issue_s(0);
-      issue_dp(0);
-      for (int j = 0; j < nk; ++j) {
-        const int st = j & 1;
-        if (j + 1 < nk) issue_s(j + 1);
-        mbar_wait(ds_ready, j & 1);
-        tc_fence_after();
-        const uint32_t aK = smem_u32(ring + st * 2 * kTile);
+        umma_commit(&v_empty[j & 1]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(q_full, 0);
+    issue_s(0);
+    issue_dp(0);
+    for (int j = 0; j < nk; ++j) {
+      const int st = j & 1;
+      if (j + 1 < nk) issue_s(j + 1);
+      mbar_wait(ds_ready, j & 1);
+      tc_fence_after();
+      const uint64_t mK = sw128_desc(smem_u32(sK + (j % kKSlots) * kTile), kBox, 1024);
+      if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < BT / 16; ++k)
-          umma_f16_ts(tmem + cQ, tmem + st * 128u + k * 8, mndesc(aK, k), id_acc, (j | k) != 0);
-        umma_commit(&kv_empty[st]);
-        if (j + 1 < nk) issue_dp(j + 1);
+          umma_f16_ts(tmem + cQ, tmem + st * 128u + packed_col(k), mK + (uint64_t)(k * 128), id_acc, (j | k) != 0);
+        umma_commit(&k_empty[j % kKSlots]);
       }
-      umma_commit(mma_done);
+      __syncwarp();
+      if (j + 1 < nk) issue_dp(j + 1);
     }
+    if (elect_one()) umma_commit(mma_done);
     __syncwarp();
   } else if (warp >= 4) {
     const int q = warp & 3;
@@ -424,32 +548,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t li = ((int64_t)b * p.H + h) * p.T + qrow;
     const float L = ok ? p.lse[li] * kLog2e : 0.f;
     const float D = ok ? p.delta[li] : 0.f;
+    const float2 c2 = make_float2(c, c), nl2 = make_float2(-L, -L), nd2 = make_float2(-D, -D);
     for (int j = 0; j < nk; ++j) {
       const int st = j & 1;
       const int valid = min(BT, p.T - j * BT) - ch * 64;
       mbar_wait(&s_full[st], (j >> 1) & 1);
       tc_fence_after();
-      float pr[64];
-      if (valid >= 64)
-        load64(tmem + lo + st * 128u + ch * 64, pr, [&](int, float s) { return fast_exp2(fmaf(s, c, -L)); });
-      else
-        load64(tmem + lo + st * 128u + ch * 64, pr,
-               [&](int i, float s) { return i < valid ? fast_exp2(fmaf(s, c, -L)) : 0.f; });
+      float2 pr[32];
+      {
+        uint32_t sv[2][32];
+        ld64(tmem + lo + st * 128u + ch * 64, sv);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pr[i] = exp2_pair(ffma2(col2(sv, i), c2, nl2), i);
+        if (valid < 64) {  // key columns past T
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if (2 * i >= valid) pr[i].x = 0.f;
+            if (2 * i + 1 >= valid) pr[i].y = 0.f;
+          }
+        }
+      }
       mbar_wait(dp_full, j & 1);
       tc_fence_after();
       {
-        float ds[64];
-        load64(tmem + lo + cP + ch * 64, ds, [&](int i, float dp) { return pr[i] * (dp - D); });
-        uint32_t pk[2][16];
+        uint32_t dv[2][32];
+        ld64(tmem + lo + cP + ch * 64, dv);
+        float2 ds[32];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          pk[0][i] = pack2(ds[2 * i], ds[2 * i + 1]);
-          pk[1][i] = pack2(ds[32 + 2 * i], ds[33 + 2 * i]);
-        }
-        named_sync(2 + q, 64);  // both halves have read their raw S columns
-        tmem_st16(tmem + lo + st * 128u + ch * 32, pk[0]);
-        tmem_st16(tmem + lo + st * 128u + ch * 32 + 16, pk[1]);
-        tmem_st_wait();
+        for (int i = 0; i < 32; ++i) ds[i] = fmul2(pr[i], fadd2(col2(dv, i), nd2));
+        pack_store(tmem + lo + st * 128u + ch * 64, ds);  // over this half's own S columns
       }
       tc_fence_before();
       __syncwarp();
@@ -486,16 +613,16 @@ int attn_bwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, 
   if ((s = make_tmap_2d_bf16(&mg, dout, rows, (uint64_t)g.H * HD, lddo, 128, 64))) return s;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(dkdv_k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    cudaFuncSetAttribute(dq_k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(dkdv_k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDkdv);
+    cudaFuncSetAttribute(dq_k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDq);
     attr = true;
   }
   Params pk{g.T, g.H, g.KVH, g.B, g.scale, lse, delta, (__nv_bfloat16*)dk, lddk, (__nv_bfloat16*)dv, lddv,
             rope_cos, rope_sin};
-  dkdv_k<<<dim3((g.T + BT - 1) / BT, g.KVH, g.B), kThreads, kSmem, st>>>(mq, mk, mv, mg, pk);
+  dkdv_k<<<dim3((g.T + BT - 1) / BT, g.KVH, g.B), kThreads, kSmemDkdv, st>>>(mq, mk, mv, mg, pk);
   if (int e = check_launch("flash_bwd_dkdv_tc")) return e;
   Params pq{g.T, g.H, g.KVH, g.B, g.scale, lse, delta, (__nv_bfloat16*)dq, lddq, nullptr, 0, rope_cos, rope_sin};
-  dq_k<<<dim3((g.T + BT - 1) / BT, g.H, g.B), kThreads, kSmem, st>>>(mq, mk, mv, mg, pq);
+  dq_k<<<dim3((g.T + BT - 1) / BT, g.H, g.B), kThreads, kSmemDq, st>>>(mq, mk, mv, mg, pq);
   return check_launch("flash_bwd_dq_tc");
 }
 

@@ -1,0 +1,66 @@
+// Pipeline trace + timing of the tcgen05 attention backward kernels (CB_ATTN_TRACE build),
+// 1B step shape.  Build (from the repo root):
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DCB_ATTN_TRACE \
+//     -I paper_2507_05411_b200/csrc -I include scripts/attn_bwd_trace.cu \
+//     paper_2507_05411_b200/csrc/runtime.cu -o scripts/bin/attn_bwd_trace -lcuda
+#include <cstdio>
+#include <vector>
+
+#include "../paper_2507_05411_b200/csrc/attn_tc.cu"
+#include "../paper_2507_05411_b200/csrc/attn_tc_bwd.cu"
+
+int main() {
+  const int B = 8, T = 4096, H = 16, hd = 128;
+  const size_t n = (size_t)B * T * H * hd;
+  std::vector<__nv_bfloat16> h(n);
+  uint32_t x = 12345;
+  for (size_t i = 0; i < n; ++i) {
+    x = x * 1664525u + 1013904223u;
+    h[i] = __float2bfloat16(((x >> 8) & 0xffff) / 65536.f - 0.5f);
+  }
+  void *q, *k, *v, *o, *g, *dq, *dk, *dv;
+  float *lse, *delta;
+  for (void** p : {&q, &k, &v, &o, &g, &dq, &dk, &dv}) cudaMalloc(p, n * 2);
+  cudaMalloc(&lse, (size_t)B * H * T * 4);
+  cudaMalloc(&delta, (size_t)B * H * T * 4);
+  cudaMemset(delta, 0, (size_t)B * H * T * 4);
+  for (void* p : {q, k, v, g}) cudaMemcpy(p, h.data(), n * 2, cudaMemcpyHostToDevice);
+  cb::AttnGeom geo{B, T, H, H, hd, H * hd, H * hd, H * hd, H * hd, 0.08838834764831845f};
+  cb::attn_fwd_tc(geo, q, k, v, o, lse, 0);
+  auto bwd = [&]() {
+    return cb::attn_bwd_tc(geo, q, k, v, g, H * hd, lse, delta, dq, H * hd, dk, H * hd, dv, H * hd, 0);
+  };
+  for (int it = 0; it < 3; ++it)
+    if (int s = bwd()) {
+      printf("launch failed %d\n", s);
+      return 1;
+    }
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    printf("kernel failed\n");
+    return 1;
+  }
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int it = 0; it < 10; ++it) bwd();
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  ms /= 10;
+  printf("bwd %.3f ms  %.1f TFLOP/s (5 GEMMs algorithmic)\n", ms, 10.0 * B * T * (double)T * H * hd / ms / 1e9);
+  unsigned long long tr[16][64];
+  cudaMemcpyFromSymbol(tr, cb::tcb::g_btrace, sizeof(tr));
+  const unsigned long long t0 = tr[1][0];
+  const char* names[10] = {"dV", "S+1", "dK", "dP+1", "c.S", "c.P", "c.dP", "c.dS", "ld.Q", "ld.dO"};
+  printf("  u");
+  for (int e = 0; e < 10; ++e) printf(" %7s", names[e]);
+  printf("\n");
+  for (int j = 0; j < 16; ++j) {
+    printf("%3d", j);
+    for (int e = 0; e < 10; ++e) printf(" %7lld", (long long)(tr[e][j] - t0));
+    printf("\n");
+  }
+  return 0;
+}
