@@ -51,8 +51,10 @@ CB_API int cb_gemm(int M, int N, int K, int in_dtype, const void* A, int64_t lda
                    int r_dtype, float alpha, int accumulate, void* stream);
 /* 0 = automatic engine choice, 1 = force SIMT, 2 = force tcgen05 (tests only). */
 CB_API int cb_gemm_set_path(int path);
-/* 1 (default) = cluster pairs share the B tile via TMA multicast; 0 = one CTA per tile. */
-CB_API int cb_gemm_set_multicast(int enable);
+/* Cluster mode of the tcgen05 engine: 1 (default) = CTA-pair MMA (cta_group::2, 256x256
+   tiles); 2 = cluster pairs sharing the B tile via TMA multicast; 3 = CTA pair; 0 = one CTA
+   per 128-row tile. */
+CB_API int cb_gemm_set_multicast(int mode);
 /* D = op(A) @ op(B) with RoPE (layers.py:235-257; positions = row % seq_len) applied to
  * output columns [0, rope_cols) — the q|k part of the fused QKV projection (layers.py:340-343).
  * Rotated in the tcgen05 epilogue (no extra HBM pass); other engines rotate afterwards. */

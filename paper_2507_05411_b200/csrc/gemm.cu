@@ -89,6 +89,108 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   tn = r / gsz;
 }
 
+// One 32-column accumulator chunk of one output row through the epilogue: optional RoPE
+// rotation of the columns [0, rope_cols), then alpha / accumulate / residual and the store.
+__device__ __forceinline__ void epi_chunk(const Epi& e, uint32_t (&v)[32], int row, int col0) {
+  if (e.rope_cos && col0 < e.rope_cols) {
+    // 32 columns = 16 pairs of one head (rope_hd % 32 == 0 is required on this path)
+    const int half = e.rope_hd >> 1;
+    const int p0 = (col0 % e.rope_hd) >> 1;
+    const int64_t tb = (int64_t)(row % e.rope_T) * half + p0;
+    const float4* cs4 = reinterpret_cast<const float4*>(e.rope_cos + tb);
+    const float4* sn4 = reinterpret_cast<const float4*>(e.rope_sin + tb);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 cq = cs4[j], sq = sn4[j];
+      const float cc[4] = {cq.x, cq.y, cq.z, cq.w}, ss[4] = {sq.x, sq.y, sq.z, sq.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int k = (j * 4 + i) * 2;
+        const float ev = __uint_as_float(v[k]), od = __uint_as_float(v[k + 1]);
+        v[k] = __float_as_uint(ev * cc[i] - od * ss[i]);
+        v[k + 1] = __float_as_uint(ev * ss[i] + od * cc[i]);
+      }
+    }
+  }
+  const bool full_chunk = col0 + 32 <= e.N;
+  const bool fast = full_chunk && !e.accumulate && !e.R && e.alpha == 1.f && !e.d_f32 && ((e.ldd & 7) == 0) &&
+                    ((reinterpret_cast<uintptr_t>(e.D) & 15) == 0);
+  const bool vec = full_chunk && ((e.ldd & 7) == 0) && ((reinterpret_cast<uintptr_t>(e.D) & 31) == 0) &&
+                   (!e.R || (((e.ldr & 7) == 0) && ((reinterpret_cast<uintptr_t>(e.R) & 31) == 0)));
+  if (!fast && vec) {
+    // general epilogue, 8 columns (one 16/32-byte vector) at a time
+#pragma unroll
+    for (int g8 = 0; g8 < 4; ++g8) {
+      float o[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = __uint_as_float(v[g8 * 8 + i]) * e.alpha;
+      const int64_t di = (int64_t)row * e.ldd + col0 + g8 * 8;
+      if (e.accumulate) {
+        if (e.d_f32) {
+          const float4* s = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.D) + di);
+          const float4 a = s[0], b = s[1];
+          o[0] += a.x; o[1] += a.y; o[2] += a.z; o[3] += a.w; o[4] += b.x; o[5] += b.y; o[6] += b.z; o[7] += b.w;
+        } else {
+          const uint4 t = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(e.D) + di);
+          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&t);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 f = __bfloat1622float2(h2[i]);
+            o[2 * i] += f.x;
+            o[2 * i + 1] += f.y;
+          }
+        }
+      }
+      if (e.R) {
+        const int64_t ri = (int64_t)row * e.ldr + col0 + g8 * 8;
+        if (e.r_f32) {
+          const float4* s = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.R) + ri);
+          const float4 a = s[0], b = s[1];
+          o[0] += a.x; o[1] += a.y; o[2] += a.z; o[3] += a.w; o[4] += b.x; o[5] += b.y; o[6] += b.z; o[7] += b.w;
+        } else {
+          const uint4 t = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(e.R) + ri);
+          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&t);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 f = __bfloat1622float2(h2[i]);
+            o[2 * i] += f.x;
+            o[2 * i + 1] += f.y;
+          }
+        }
+      }
+      if (e.d_f32) {
+        float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.D) + di);
+        d[0] = make_float4(o[0], o[1], o[2], o[3]);
+        d[1] = make_float4(o[4], o[5], o[6], o[7]);
+      } else {
+        uint4 t;
+        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&t);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h2[i] = __floats2bfloat162_rn(o[2 * i], o[2 * i + 1]);
+        *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(e.D) + di) = t;
+      }
+    }
+  } else if (fast) {
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(e.D) + (int64_t)row * e.ldd + col0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint4 pk;
+      uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(v[j * 8 + 2 * h]), __uint_as_float(v[j * 8 + 2 * h + 1]));
+        w[h] = *reinterpret_cast<uint32_t*>(&b2);
+      }
+      dst[j] = pk;
+    }
+  } else {
+    const int lim = min(32, e.N - col0);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < lim) epi_store1(e, row, col0 + j, __uint_as_float(v[j]));
+  }
+}
+
 // MC = 1: one CTA per 128 x BN tile.  MC = 2: a cluster of two CTAs computes two vertically
 // adjacent tiles that share the B (weight) tile; each CTA loads half of B and multicasts it
 // to both, so the L2->SM operand traffic per FLOP drops by a third (the kernel is L2-
@@ -143,20 +245,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ---------------- TMA producer ----------------
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = unit0; u < num_units; u += unit_stride) {
-        int tm, tn;
-        coords(u, tm, tn);
-        const int m0 = tm * BM, n0 = tn * BN;
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+    // ---------------- TMA producer (whole warp, one elected lane issues) ----------------
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = unit0; u < num_units; u += unit_stride) {
+      int tm, tn;
+      coords(u, tm, tn);
+      const int m0 = tm * BM, n0 = tn * BN;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* a_dst = sA + stage * C::kABytes;
+        uint8_t* b_dst = sB + stage * C::kBBytes;
+        const int k0 = kb * BK;
+        if (elect_one()) {
           mbar_expect_tx(&full[stage], C::kStageBytes);
-          uint8_t* a_dst = sA + stage * C::kABytes;
-          uint8_t* b_dst = sB + stage * C::kBBytes;
-          const int k0 = kb * BK;
           if (!args.a_mn) {
             tma_load_2d(a_dst, &tmA, &full[stage], k0, m0);
           } else {
@@ -182,51 +284,55 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tma_load_2d_mc(hb + j * 8192, &tmB, &full[stage], n0 + rank * kHalf + 64 * j, k0, 0x3);
             }
           }
-          if (++stage == C::kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
+        }
+        __syncwarp();
+        if (++stage == C::kStages) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
-    __syncwarp();
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {
-      const uint32_t idesc = idesc_bf16_f32(BM, BN, args.a_mn, args.b_mn);
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int u = unit0; u < num_units; u += unit_stride, ++it) {
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+    // the whole warp walks the schedule (descriptors stay warp-uniform, in uniform
+    // registers); one elected lane issues each k-block's MMAs
+    const uint32_t idesc = idesc_bf16_f32(BM, BN, args.a_mn, args.b_mn);
+    const uint64_t a0 = args.a_mn ? sw128_desc(smem_u32(sA), 8192, 1024) : sw128_desc(smem_u32(sA), 16, 1024);
+    const uint64_t b0 = args.b_mn ? sw128_desc(smem_u32(sB), 8192, 1024) : sw128_desc(smem_u32(sB), 16, 1024);
+    // per-K=16-step descriptor advance (16-byte units): MN-major +2048 B, K-major +32 B
+    const uint64_t a_step = args.a_mn ? 128 : 2, b_step = args.b_mn ? 128 : 2;
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int u = unit0; u < num_units; u += unit_stride, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * C::kABytes);
-          const uint32_t b_addr = smem_u32(sB + stage * C::kBBytes);
+        const uint64_t ad = a0 + (uint64_t)(stage * (C::kABytes >> 4));
+        const uint64_t bd = b0 + (uint64_t)(stage * (C::kBBytes >> 4));
+        if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ad = args.a_mn ? sw128_desc(a_addr + kk * 2048, 8192, 1024) : sw128_desc(a_addr + kk * 32, 16, 1024);
-            const uint64_t bd = args.b_mn ? sw128_desc(b_addr + kk * 2048, 8192, 1024) : sw128_desc(b_addr + kk * 32, 16, 1024);
-            umma_f16_ss(d_tmem, ad, bd, idesc, (kb | kk) != 0);
-          }
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_f16_ss(d_tmem, ad + kk * a_step, bd + kk * b_step, idesc, (kb | kk) != 0);
           if (MC == 2)
             umma_commit_mc(&empty[stage], 0x3);  // release the stage in both CTAs (B is shared)
           else
             umma_commit(&empty[stage]);
-          if (++stage == C::kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
         }
-        umma_commit(&tfull[acc]);
+        __syncwarp();
+        if (++stage == C::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
     }
-    __syncwarp();
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> registers -> global ----------------
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
@@ -248,103 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_wait();
         const int col0 = tn * BN + c * 32;
         if (!row_ok || col0 >= e.N) continue;
-        if (e.rope_cos && col0 < e.rope_cols) {
-          // 32 columns = 16 pairs of one head (rope_hd % 32 == 0 is required on this path)
-          const int half = e.rope_hd >> 1;
-          const int p0 = (col0 % e.rope_hd) >> 1;
-          const int64_t tb = (int64_t)(row % e.rope_T) * half + p0;
-          const float4* cs4 = reinterpret_cast<const float4*>(e.rope_cos + tb);
-          const float4* sn4 = reinterpret_cast<const float4*>(e.rope_sin + tb);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float4 cq = cs4[j], sq = sn4[j];
-            const float cc[4] = {cq.x, cq.y, cq.z, cq.w}, ss[4] = {sq.x, sq.y, sq.z, sq.w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int k = (j * 4 + i) * 2;
-              const float ev = __uint_as_float(v[k]), od = __uint_as_float(v[k + 1]);
-              v[k] = __float_as_uint(ev * cc[i] - od * ss[i]);
-              v[k + 1] = __float_as_uint(ev * ss[i] + od * cc[i]);
-            }
-          }
-        }
-        const bool full_chunk = col0 + 32 <= e.N;
-        const bool fast = full_chunk && !e.accumulate && !e.R && e.alpha == 1.f && !e.d_f32 && ((e.ldd & 7) == 0) &&
-                          ((reinterpret_cast<uintptr_t>(e.D) & 15) == 0);
-        const bool vec = full_chunk && ((e.ldd & 7) == 0) && ((reinterpret_cast<uintptr_t>(e.D) & 31) == 0) &&
-                         (!e.R || (((e.ldr & 7) == 0) && ((reinterpret_cast<uintptr_t>(e.R) & 31) == 0)));
-        if (!fast && vec) {
-          // general epilogue, 8 columns (one 16/32-byte vector) at a time
-#pragma unroll
-          for (int g8 = 0; g8 < 4; ++g8) {
-            float o[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) o[i] = __uint_as_float(v[g8 * 8 + i]) * e.alpha;
-            const int64_t di = (int64_t)row * e.ldd + col0 + g8 * 8;
-            if (e.accumulate) {
-              if (e.d_f32) {
-                const float4* s = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.D) + di);
-                const float4 a = s[0], b = s[1];
-                o[0] += a.x; o[1] += a.y; o[2] += a.z; o[3] += a.w; o[4] += b.x; o[5] += b.y; o[6] += b.z; o[7] += b.w;
-              } else {
-                const uint4 t = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(e.D) + di);
-                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&t);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  const float2 f = __bfloat1622float2(h2[i]);
-                  o[2 * i] += f.x;
-                  o[2 * i + 1] += f.y;
-                }
-              }
-            }
-            if (e.R) {
-              const int64_t ri = (int64_t)row * e.ldr + col0 + g8 * 8;
-              if (e.r_f32) {
-                const float4* s = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.R) + ri);
-                const float4 a = s[0], b = s[1];
-                o[0] += a.x; o[1] += a.y; o[2] += a.z; o[3] += a.w; o[4] += b.x; o[5] += b.y; o[6] += b.z; o[7] += b.w;
-              } else {
-                const uint4 t = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(e.R) + ri);
-                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&t);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  const float2 f = __bfloat1622float2(h2[i]);
-                  o[2 * i] += f.x;
-                  o[2 * i + 1] += f.y;
-                }
-              }
-            }
-            if (e.d_f32) {
-              float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.D) + di);
-              d[0] = make_float4(o[0], o[1], o[2], o[3]);
-              d[1] = make_float4(o[4], o[5], o[6], o[7]);
-            } else {
-              uint4 t;
-              __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&t);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) h2[i] = __floats2bfloat162_rn(o[2 * i], o[2 * i + 1]);
-              *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(e.D) + di) = t;
-            }
-          }
-        } else if (fast) {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(e.D) + (int64_t)row * e.ldd + col0);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            uint4 pk;
-            uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-              __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(v[j * 8 + 2 * h]), __uint_as_float(v[j * 8 + 2 * h + 1]));
-              w[h] = *reinterpret_cast<uint32_t*>(&b2);
-            }
-            dst[j] = pk;
-          }
-        } else {
-          const int lim = min(32, e.N - col0);
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < lim) epi_store1(e, row, col0 + j, __uint_as_float(v[j]));
-        }
+        epi_chunk(e, v, row, col0);
       }
       tc_fence_before();
       __syncwarp();
@@ -362,12 +372,219 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-static int g_gemm_mc = 2;  // B-multicast cluster pairs (1 disables; tests compare both)
+// CTA-pair engine (cta_group::2): a cluster of two CTAs computes one 256 x 256 tile with a
+// single tcgen05.mma stream issued by the leader.  Each CTA stages its own 128 rows of A and
+// its own 128 columns of B (the hardware feeds each SM's tensor core the other half of B from
+// the peer), so per SM the shared-memory operand traffic per FLOP is a third lower than the
+// 1-CTA 128 x 256 tile and the two SMs share one MMA issue stream.  Each CTA's TMEM holds the
+// 128 x 256 accumulator of its rows (double-buffered: 512 columns).
+struct Cfg2 {
+  static constexpr int kStages = 6;
+  static constexpr int kABytes = BM * BK * 2;  // 16 KB: this CTA's 128 rows of A
+  static constexpr int kBBytes = 128 * BK * 2; // 16 KB: this CTA's 128 columns of B
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Args args) {
+  using C = Cfg2;
+  constexpr int BN = 256;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::kStages * C::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)cluster_ctarank();
+  const bool leader = rank == 0;
+  const int tiles_mg = (args.tiles_m + 1) / 2;  // 256-row tile pairs
+  const int num_units = tiles_mg * args.tiles_n;
+  const int unit0 = (int)(blockIdx.x >> 1), unit_stride = (int)(gridDim.x >> 1);
+  const int nk = (args.K + BK - 1) / BK;
+  auto coords = [&](int u, int& tm, int& tn) {
+    int tg;
+    tile_coords(u, tiles_mg, args.tiles_n, tg, tn);
+    tm = tg * 2 + rank;
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);   // leader: its expect_tx arrive; both CTAs' loads complete_tx here
+      mbar_init(&empty[s], 1);  // the leader's MMA commit (multicast to both CTAs)
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 8);  // leader's copy: 4 epilogue warps of each CTA
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs; completions land on the leader's barrier) ----
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = unit0; u < num_units; u += unit_stride) {
+      int tm, tn;
+      coords(u, tm, tn);
+      const int m0 = tm * BM, nb = tn * BN + rank * 128;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* a_dst = sA + stage * C::kABytes;
+        uint8_t* b_dst = sB + stage * C::kBBytes;
+        const int k0 = kb * BK;
+        if (elect_one()) {
+          const uint32_t fb = leader_addr(&full[stage]);
+          if (leader) mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
+          if (!args.a_mn) {
+            tma_load_2d_pair(a_dst, &tmA, fb, k0, m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(a_dst + j * 8192, &tmA, fb, m0 + 64 * j, k0);
+          }
+          if (!args.b_mn) {
+            tma_load_2d_pair(b_dst, &tmB, fb, k0, nb);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) tma_load_2d_pair(b_dst + j * 8192, &tmB, fb, nb + 64 * j, k0);
+          }
+        }
+        __syncwarp();
+        if (++stage == C::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader CTA only) ----------------
+    if (leader) {
+      const uint32_t idesc = idesc_bf16_f32(2 * BM, BN, args.a_mn, args.b_mn);
+      const uint64_t a0 = args.a_mn ? sw128_desc(smem_u32(sA), 8192, 1024) : sw128_desc(smem_u32(sA), 16, 1024);
+      const uint64_t b0 = args.b_mn ? sw128_desc(smem_u32(sB), 8192, 1024) : sw128_desc(smem_u32(sB), 16, 1024);
+      const uint64_t a_step = args.a_mn ? 128 : 2, b_step = args.b_mn ? 128 : 2;
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int u = unit0; u < num_units; u += unit_stride, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = a0 + (uint64_t)(stage * (C::kABytes >> 4));
+          const uint64_t bd = b0 + (uint64_t)(stage * (C::kBBytes >> 4));
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk)
+              umma_f16_ss_pair(d_tmem, ad + kk * a_step, bd + kk * b_step, idesc, (kb | kk) != 0);
+            umma_commit_pair_mc(&empty[stage], 0x3);
+          }
+          __syncwarp();
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (elect_one()) umma_commit_pair_mc(&tfull[acc], 0x3);
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue (both CTAs: each drains its own 128 rows) ----------------
+    const int q = warp & 3;
+    const Epi& e = args.e;
+    const uint32_t tempty_leader0 = leader_addr(&tempty[0]);
+    int it = 0;
+    for (int u = unit0; u < num_units; u += unit_stride, ++it) {
+      int tm, tn;
+      coords(u, tm, tn);
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int row = tm * BM + q * 32 + lane;
+      const bool row_ok = row < e.M;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
+        tmem_ld_wait();
+        const int col0 = tn * BN + c * 32;
+        if (!row_ok || col0 >= e.N) continue;
+        epi_chunk(e, v, row, col0);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();  // neither CTA leaves while the pair's MMAs / multicasts may still target it
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, 512);
+  }
+}
+
+static int g_gemm_mc = 3;  // 3: CTA-pair MMA, 2: B-multicast cluster pairs, 1: single CTA
+
+int launch_pair(const Args& a, const void* A, int64_t lda, const void* B, int64_t ldb, cudaStream_t st) {
+  using C = Cfg2;
+  CUtensorMap ta, tb;
+  int s;
+  if (!a.a_mn)
+    s = make_tmap_2d_bf16(&ta, A, a.M, a.K, lda, BM, BK);
+  else
+    s = make_tmap_2d_bf16(&ta, A, a.K, a.M, lda, BK, 64);
+  if (s) return s;
+  if (!a.b_mn)
+    s = make_tmap_2d_bf16(&tb, B, a.N, a.K, ldb, 128, BK);
+  else
+    s = make_tmap_2d_bf16(&tb, B, a.K, a.N, ldb, BK, 64);
+  if (s) return s;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    attr_set = true;
+  }
+  const int pairs = ((a.tiles_m + 1) / 2) * a.tiles_n;
+  const int grid = 2 * std::min(pairs, kNumSMs / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc2, ta, tb, a);
+  if (e != cudaSuccess) return fail(CB_ERR_CUDA, "gemm_tc2 cluster launch: %s", cudaGetErrorString(e));
+  return check_launch("gemm_tc_pair");
+}
 
 template <int BN>
 int launch(const Args& a, const void* A, int64_t lda, const void* B, int64_t ldb, cudaStream_t st) {
   using C = Cfg<BN>;
-  const int mc = (g_gemm_mc == 2 && a.tiles_m >= 2) ? 2 : 1;
+  if (BN == 256 && g_gemm_mc == 3 && a.tiles_m >= 2) return launch_pair(a, A, lda, B, ldb, st);
+  const int mc = (g_gemm_mc >= 2 && a.tiles_m >= 2) ? 2 : 1;
   CUtensorMap ta, tb;
   int s;
   // A: op(A) is MxK.  K-major -> stored [M][K]; MN-major -> stored [K][M].
@@ -490,8 +707,10 @@ static thread_local int g_last_gemm_tc = 0;  // did the last gemm_impl call run 
 
 using namespace cb;
 
-extern "C" int cb_gemm_set_multicast(int enable) {
-  tc::g_gemm_mc = enable ? 2 : 1;
+extern "C" int cb_gemm_set_multicast(int mode) {
+  // 0: single-CTA tiles, 1: default (CTA pair), 2: B-multicast cluster pairs, 3: CTA pair
+  if (mode < 0 || mode > 3) return fail(CB_ERR_ARG, "gemm cluster mode must be 0..3");
+  tc::g_gemm_mc = mode == 0 ? 1 : mode == 1 ? 3 : mode;
   return CB_OK;
 }
 

@@ -30,7 +30,7 @@ def _operands(M, N, K, ta, tb, dtype, dev):
 
 @pytest.mark.parametrize("M,N,K", SHAPES + [(384, 768, 512), (640, 256, 128)])  # odd tile-pair counts
 @pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
-@pytest.mark.parametrize("mc", [1, 0])
+@pytest.mark.parametrize("mc", [1, 2, 0])  # CTA pair, B-multicast pair, single CTA
 def test_gemm_tcgen05_bf16(cuda, M, N, K, ta, tb, mc):
     from paper_2507_05411_b200 import _lib, ops
 
