@@ -287,7 +287,7 @@ def main():
         "mfu": value * fpt / (world * NOMINAL_BF16_PFLOPS),
         "model_flops_per_token": fpt,
         "loss": final_loss,
-        "roofline": {"bound": "tensor", "kernel": "gemm_tc (tcgen05 persistent GEMM)", "achieved": achieved,
+        "roofline": {"bound": "tensor", "kernel": "gemm_tc2 (tcgen05 CTA-pair persistent GEMM)", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "peak_source": f"{pk_src} bf16_tflops_sustained (kernel timed inside the step)",
                      "traffic": traffic,
