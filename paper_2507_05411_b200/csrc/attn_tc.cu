@@ -16,6 +16,8 @@
 //   warps 4-7    softmax of tile A, warps 8-11 softmax of tile B: one thread owns one
 //                query row (no shuffles), exp2 domain, lazy O rescale (only when the row
 //                max grows by more than 2^8), then the epilogue (O / l, natural-log LSE).
+#include <type_traits>
+
 #include "attn.cuh"
 #include "composer_b200.h"
 
@@ -45,7 +47,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef CB_ATTN_EMU
-#define CB_ATTN_EMU 3
+#define CB_ATTN_EMU 2
 #endif
 constexpr int kEmuPairs = CB_ATTN_EMU;  // of every 8 exp2 pairs, this many on the FMA pipe
 
@@ -216,7 +218,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t ocol = tmem + lane_off + 256u + x * 128u;
     const float c = p.scale * kLog2e;
     float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < nblk; ++j) {
+    // one K/V block of the online softmax; kRagged (the last block when T % 128 != 0) masks
+    // the columns past T — a separate instantiation keeps the masking out of the hot loop
+    auto block = [&](int j, auto ragged) {
+      constexpr bool kRagged = decltype(ragged)::value;
       mbar_wait(&s_full[x], j & 1);
       tc_fence_after();
       if (q == 0 && lane == 0) ATTN_TRACE(4 + 3 * x, j);
@@ -229,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       reg_fence(sv[1]);
       reg_fence(sv[2]);
       reg_fence(sv[3]);
-      if (valid < BN) {  // ragged last block: columns past T take no part
+      if (kRagged) {  // columns past T take no part
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc)
 #pragma unroll
@@ -301,7 +306,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (q == 0 && lane == 0) ATTN_TRACE(6 + 3 * x, j);
       if (lane == 0) mbar_arrive(&p_ready[x]);
-    }
+    };
+    const int nfull = p.T / BN;
+    for (int j = 0; j < nfull; ++j) block(j, std::false_type{});
+    if (nfull < nblk) block(nfull, std::true_type{});
     // epilogue
     mbar_wait(&o_done[x], (nblk - 1) & 1);
     tc_fence_after();

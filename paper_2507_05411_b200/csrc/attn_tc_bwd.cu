@@ -496,6 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int ks = j % kKSlots;
       mbar_wait(&k_full[ks], (j / kKSlots) & 1);
       tc_fence_after();
+      BWD_TRACE(10, j);
       const uint64_t dKj = sw128_desc(smem_u32(sK + ks * kTile), 16, 1024);
       if (elect_one()) {
 #pragma unroll
@@ -508,6 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto issue_dp = [&](int j) {
       mbar_wait(&v_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
+      BWD_TRACE(12, j);
       const uint64_t dVj = sw128_desc(smem_u32(sV + (j & 1) * kTile), 16, 1024);
       if (elect_one()) {
 #pragma unroll
@@ -525,6 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (j + 1 < nk) issue_s(j + 1);
       mbar_wait(ds_ready, j & 1);
       tc_fence_after();
+      BWD_TRACE(11, j);
       const uint64_t mK = sw128_desc(smem_u32(sK + (j % kKSlots) * kTile), kBox, 1024);
       if (elect_one()) {
 #pragma unroll
@@ -554,6 +557,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int valid = min(BT, p.T - j * BT) - ch * 64;
       mbar_wait(&s_full[st], (j >> 1) & 1);
       tc_fence_after();
+      if (warp == 4) BWD_TRACE(13, j);
       float2 pr[32];
       {
         uint32_t sv[2][32];
@@ -570,6 +574,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mbar_wait(dp_full, j & 1);
       tc_fence_after();
+      if (warp == 4) BWD_TRACE(14, j);
       {
         uint32_t dv[2][32];
         ld64(tmem + lo + cP + ch * 64, dv);
@@ -580,6 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
+      if (warp == 4) BWD_TRACE(15, j);
       if (lane == 0) mbar_arrive(ds_ready);
     }
     mbar_wait(mma_done, 0);

@@ -62,5 +62,15 @@ int main() {
     for (int e = 0; e < 10; ++e) printf(" %7lld", (long long)(tr[e][j] - t0));
     printf("\n");
   }
+  const unsigned long long t1 = tr[10][0];
+  const char* qn[6] = {"S", "dQ", "dP", "c.S", "c.dP", "c.dS"};
+  printf("dq kernel\n  j");
+  for (int e = 0; e < 6; ++e) printf(" %7s", qn[e]);
+  printf("\n");
+  for (int j = 0; j < 12; ++j) {
+    printf("%3d", j);
+    for (int e = 0; e < 6; ++e) printf(" %7lld", (long long)(tr[10 + e][j] - t1));
+    printf("\n");
+  }
   return 0;
 }

@@ -87,6 +87,17 @@ __global__ void __launch_bounds__(NW * 32, 1) alu_bench(unsigned long long* cyc,
         float y;
         asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x[i]));
         x[i] = y - 1.0f;
+      } else if (MODE == 2) {
+        uint32_t r;
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(x[i]), "f"(x[(i + 1) & 7]));
+        x[i] = __uint_as_float(r);
+      } else if (MODE == 3) {
+        float y, z;
+        asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x[i]));
+        uint32_t r;
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(x[(i + 3) & 7]), "f"(x[(i + 1) & 7]));
+        z = __uint_as_float(r);
+        x[i] = y - z;
       } else {
         x[i] = fmaf(x[i], 0.999f, -0.0001f);
       }
@@ -152,9 +163,9 @@ int main() {
 #define ALU(NW, M)                                                                                        \
   {                                                                                                       \
     double c = runf(alu_bench<NW, M>, NW * 32);                                                            \
-    printf("%s warps=%2d: %8.0f cyc  %6.1f ops/clk/SM\n", M == 0 ? "ex2 " : "fma ", NW, c,                 \
+    printf("%s warps=%2d: %8.0f cyc  %6.1f ops/clk/SM\n", M == 0 ? "ex2 " : M == 2 ? "f2fp" : M == 3 ? "ex2+f2fp" : "fma ", NW, c, \
            (double)NW * 32 * 8 * kIters / c);                                                             \
   }
-  ALU(4, 0) ALU(8, 0) ALU(16, 0) ALU(4, 1) ALU(8, 1) ALU(16, 1)
+  ALU(4, 0) ALU(8, 0) ALU(4, 1) ALU(8, 1) ALU(4, 2) ALU(8, 2) ALU(16, 2) ALU(4, 3) ALU(8, 3)
   return 0;
 }
