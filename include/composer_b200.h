@@ -61,6 +61,21 @@ CB_API int cb_gemm_set_multicast(int mode);
 CB_API int cb_gemm_rope(int M, int N, int K, int in_dtype, const void* A, int64_t lda, int trans_a, const void* B,
                         int64_t ldb, int trans_b, void* D, int64_t ldd, int d_dtype, int seq_len, int head_dim,
                         int rope_cols, const float* cos_t, const float* sin_t, void* stream);
+/* Gated-activation FFN GEMMs with the activation in the epilogue (replace reference
+ * layers.py:405-416, act0(x @ w1) * act1(x @ w1_gate), and its backward); bf16, CTA-pair
+ * tcgen05 engine.  act ids as cb_act_fwd.
+ *   fwd: pre[M, 2H] = A @ B with B = [w1 | w1_gate] ([K, 2H] or its transpose),
+ *        hidden[M, H] = act0(pre[:, :H]) * act1(pre[:, H:]) (from the bf16-rounded pre). H % 128 == 0.
+ *   bwd: dhidden = A @ B (A = d(ffn output), B = w2^T); dpre[:, :H] = dhidden act0'(a) act1(g),
+ *        dpre[:, H:] = dhidden act0(a) act1'(g) with [a | g] = pre; dhidden is never stored.
+ * Both return CB_ERR_UNSUPPORTED without launching anything when the fused form does not
+ * apply (M < 256, H % 32, alignment, engine disabled): the caller runs cb_gemm + cb_act_*. */
+CB_API int cb_gemm_gated_fwd(int M, int H, int K, const void* A, int64_t lda, int trans_a, const void* B,
+                             int64_t ldb, int trans_b, void* pre, int64_t ldpre, void* hidden, int64_t ldh, int act0,
+                             int act1, void* stream);
+CB_API int cb_gemm_gated_bwd(int M, int H, int K, const void* A, int64_t lda, int trans_a, const void* B,
+                             int64_t ldb, int trans_b, const void* pre, int64_t ldpre, void* dpre, int64_t lddpre,
+                             int act0, int act1, void* stream);
 
 /* ---------------------------------------------------------------------------------
  * RMSNorm (layers.py:176-193): y = x / sqrt(mean(x^2) + eps) * scale, rstd[row] saved.

@@ -51,6 +51,8 @@ SIGNATURES: dict[str, list] = {
                          _P, _L, _F, _P],
     "cb_attention_set_path": [_I],
     "cb_gemm_rope": [_I, _I, _I, _I, _P, _L, _I, _P, _L, _I, _P, _L, _I, _I, _I, _I, _P, _P, _P],
+    "cb_gemm_gated_fwd": [_I, _I, _I, _P, _L, _I, _P, _L, _I, _P, _L, _P, _L, _I, _I, _P],
+    "cb_gemm_gated_bwd": [_I, _I, _I, _P, _L, _I, _P, _L, _I, _P, _L, _P, _L, _I, _I, _P],
     "cb_attention_bwd_rope": [_I, _I, _I, _I, _I, _I, _P, _L, _P, _L, _P, _L, _P, _L, _P, _P, _L, _P, _P, _L, _P,
                               _L, _P, _L, _F, _P, _P, _P],
     "cb_attention_set_tc": [_I],
@@ -124,3 +126,14 @@ def check(status: int, what: str = "") -> None:
 def call(name: str, *args) -> None:
     lib = load()
     check(getattr(lib, name)(*args), name)
+
+
+def try_call(name: str, *args) -> bool:
+    """Like call(), but CB_ERR_UNSUPPORTED (the entry point declined; nothing launched)
+    returns False so the caller can take its unfused GPU route."""
+    lib = load()
+    status = getattr(lib, name)(*args)
+    if status == CB_ERR_UNSUPPORTED:
+        return False
+    check(status, name)
+    return True

@@ -72,6 +72,37 @@ __device__ __forceinline__ float stable_sigmoid(float x) {
   return x >= 0.f ? r : e * r;
 }
 
+// activations of reference layers.py:55-77 (ids shared with the C ABI's act arguments)
+enum Act { ACT_LINEAR = 0, ACT_RELU = 1, ACT_SILU = 2, ACT_SIGMOID = 3, ACT_TANH = 4 };
+
+__device__ __forceinline__ float act_f(int a, float x) {
+  switch (a) {
+    case ACT_RELU: return fmaxf(x, 0.f);
+    case ACT_SILU: return x * stable_sigmoid(x);
+    case ACT_SIGMOID: return stable_sigmoid(x);
+    case ACT_TANH: return tanhf(x);
+    default: return x;
+  }
+}
+__device__ __forceinline__ float act_df(int a, float x) {
+  switch (a) {
+    case ACT_RELU: return x > 0.f ? 1.f : 0.f;
+    case ACT_SILU: {
+      const float s = stable_sigmoid(x);
+      return s * (1.f + x * (1.f - s));
+    }
+    case ACT_SIGMOID: {
+      const float s = stable_sigmoid(x);
+      return s * (1.f - s);
+    }
+    case ACT_TANH: {
+      const float t = tanhf(x);
+      return 1.f - t * t;
+    }
+    default: return 1.f;
+  }
+}
+
 // ------------------------------------------------------------------------------------
 // PTX wrappers: mbarrier, TMA, tcgen05 (TMEM + UMMA)
 // ------------------------------------------------------------------------------------

@@ -36,6 +36,16 @@ struct Epi {
   const float* rope_cos = nullptr;
   const float* rope_sin = nullptr;
   int rope_T = 0, rope_hd = 0, rope_cols = 0;
+  // gated-activation epilogues (CTA-pair engine, bf16): glu = 1 forward — the tile's 256
+  // columns are 128 columns of the a half and the same 128 of the g half of pre = x @ [W1|Wg]
+  // (D = pre [M, 2H]); also writes hidden = act0(a) * act1(g) to glu_out [M, H].
+  // glu = 2 backward — the accumulator is dhidden [M, H] (never stored); reads pre from
+  // glu_pre and writes dpre = [da | dg] to glu_out [M, 2H].
+  int glu = 0, glu_h = 0, glu_a0 = 0, glu_a1 = 0;
+  void* glu_out = nullptr;
+  int64_t ld_glu_out = 0;
+  const void* glu_pre = nullptr;
+  int64_t ld_glu_pre = 0;
 };
 
 __device__ __forceinline__ float epi_load(const void* p, int64_t idx, int f32) {
@@ -372,6 +382,150 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// bf16 pack / unpack of 8 values (one 16-byte vector)
+__device__ __forceinline__ uint4 pack8(const float* v) {
+  uint4 t;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&t);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+  return t;
+}
+__device__ __forceinline__ void unpack8(uint4 t, float* v) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&t);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+}
+// Gated activation act0(a) * act1(g) and its partials with the activation ids as template
+// parameters (a runtime switch per element compiles to jump tables in the epilogue loop).
+// (A0 / A1 = -1: the runtime ids r0 / r1 of the other pairs.)
+template <int A0, int A1>
+__device__ __forceinline__ float glu_f(float a, float g, int r0, int r1) {
+  return act_f(A0 < 0 ? r0 : A0, a) * act_f(A1 < 0 ? r1 : A1, g);
+}
+template <int A0, int A1>
+__device__ __forceinline__ void glu_df(float d, float a, float g, float& da, float& dg, int r0, int r1) {
+  if (A0 == ACT_LINEAR && A1 == ACT_SILU) {  // SwiGLU: one sigmoid serves silu and silu'
+    const float sg = stable_sigmoid(g);
+    const float sl = g * sg;
+    da = d * sl;
+    dg = d * a * (sg + sl * (1.f - sg));
+  } else {
+    const int x0 = A0 < 0 ? r0 : A0, x1 = A1 < 0 ? r1 : A1;
+    da = d * act_df(x0, a) * act_f(x1, g);
+    dg = d * act_f(x0, a) * act_df(x1, g);
+  }
+}
+
+// The gated epilogues' operands, passed by value (in registers) to the out-of-line tile
+// functions.
+struct Glu {
+  __nv_bfloat16* pre;  // fwd: pre output (D); bwd: unused
+  int64_t ldpre;
+  __nv_bfloat16* out;  // fwd: hidden; bwd: dpre
+  int64_t ldout;
+  const __nv_bfloat16* pin;  // bwd: pre input
+  int64_t ldpin;
+  int h, n, a0, a1;
+};
+
+// forward gated epilogue for 32 columns: va / vg are the a / g accumulators of columns
+// [col, col + 32) of each half; values are rounded to bf16 first, exactly as the unfused
+// path reads them back from pre.
+template <int A0, int A1>
+__device__ __forceinline__ void glu_fwd_chunk(const Glu& q, const uint32_t (&va)[32], const uint32_t (&vg)[32],
+                                              int row, int col) {
+  __nv_bfloat16* pre = q.pre + (int64_t)row * q.ldpre;
+  __nv_bfloat16* hid = q.out + (int64_t)row * q.ldout;
+#pragma unroll
+  for (int g8 = 0; g8 < 4; ++g8) {
+    float a[8], g[8], h[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      a[i] = __uint_as_float(va[g8 * 8 + i]);
+      g[i] = __uint_as_float(vg[g8 * 8 + i]);
+    }
+    const uint4 pa = pack8(a), pg = pack8(g);
+    *reinterpret_cast<uint4*>(pre + col + g8 * 8) = pa;
+    *reinterpret_cast<uint4*>(pre + q.h + col + g8 * 8) = pg;
+    unpack8(pa, a);
+    unpack8(pg, g);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) h[i] = glu_f<A0, A1>(a[i], g[i], q.a0, q.a1);
+    *reinterpret_cast<uint4*>(hid + col + g8 * 8) = pack8(h);
+  }
+}
+// backward gated epilogue for 32 columns of dhidden (rounded to bf16 like the stored dhidden
+// of the unfused path); pa / pg hold the chunk's pre values (loaded ahead)
+template <int A0, int A1>
+__device__ __forceinline__ void glu_bwd_chunk(const Glu& q, const uint32_t (&vd)[32], const uint4 (&pa)[4],
+                                              const uint4 (&pg)[4], int row, int col) {
+  __nv_bfloat16* dpre = q.out + (int64_t)row * q.ldout;
+#pragma unroll
+  for (int g8 = 0; g8 < 4; ++g8) {
+    float d[8], a[8], g[8], da[8], dg[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d[i] = __uint_as_float(vd[g8 * 8 + i]);
+    unpack8(pack8(d), d);
+    unpack8(pa[g8], a);
+    unpack8(pg[g8], g);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) glu_df<A0, A1>(d[i], a[i], g[i], da[i], dg[i], q.a0, q.a1);
+    *reinterpret_cast<uint4*>(dpre + col + g8 * 8) = pack8(da);
+    *reinterpret_cast<uint4*>(dpre + q.h + col + g8 * 8) = pack8(dg);
+  }
+}
+__device__ __forceinline__ void glu_load(const Glu& q, int row, int col, bool ok, uint4 (&pa)[4], uint4 (&pg)[4]) {
+  if (!ok) return;
+  const uint4* a = reinterpret_cast<const uint4*>(q.pin + (int64_t)row * q.ldpin + col);
+  const uint4* g = reinterpret_cast<const uint4*>(q.pin + (int64_t)row * q.ldpin + q.h + col);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    pa[i] = __ldg(a + i);
+    pg[i] = __ldg(g + i);
+  }
+}
+
+// One tile of the gated epilogues for a fixed activation pair (out of line: keeps the
+// register allocation of the main epilogue loop unaffected).
+template <int A0, int A1>
+__device__ __noinline__ void glu_tile(const Glu q, int glu, uint32_t tbase, int row, bool row_ok, int tn) {
+  if (glu == 1) {
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t va[32], vg[32];
+      tmem_ld32(tbase + c * 32, va);
+      tmem_ld32(tbase + 128 + c * 32, vg);
+      tmem_ld_wait_regs(va);
+      reg_fence(vg);
+      const int col = tn * 128 + c * 32;
+      if (row_ok && col < q.h) glu_fwd_chunk<A0, A1>(q, va, vg, row, col);
+    }
+  } else {
+    // pre for chunk c + 1 is in flight while chunk c is computed
+    uint4 ca[4], cg[4], na[4], ng[4];
+    const int n0 = tn * 256;
+    glu_load(q, row, n0, row_ok && n0 < q.n, ca, cg);
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+      const int col = n0 + c * 32;
+      glu_load(q, row, col + 32, c + 1 < 8 && row_ok && col + 32 < q.n, na, ng);
+      uint32_t v[32];
+      tmem_ld32(tbase + c * 32, v);
+      tmem_ld_wait_regs(v);
+      if (row_ok && col < q.n) glu_bwd_chunk<A0, A1>(q, v, ca, cg, row, col);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        ca[i] = na[i];
+        cg[i] = ng[i];
+      }
+    }
+  }
+}
+
 // CTA-pair engine (cta_group::2): a cluster of two CTAs computes one 256 x 256 tile with a
 // single tcgen05.mma stream issued by the leader.  Each CTA stages its own 128 rows of A and
 // its own 128 columns of B (the hardware feeds each SM's tensor core the other half of B from
@@ -439,7 +593,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int u = unit0; u < num_units; u += unit_stride) {
       int tm, tn;
       coords(u, tm, tn);
-      const int m0 = tm * BM, nb = tn * BN + rank * 128;
+      const int m0 = tm * BM;
+      // B columns this CTA stages: its half of the 256-column tile, or (gated forward) the
+      // tile's 128 columns of the a half (rank 0) / of the g half (rank 1)
+      const int nb = args.e.glu == 1 ? rank * args.e.glu_h + tn * 128 : tn * BN + rank * 128;
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* a_dst = sA + stage * C::kABytes;
@@ -518,14 +675,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int row = tm * BM + q * 32 + lane;
       const bool row_ok = row < e.M;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if (e.glu) {
+        const Glu gq{reinterpret_cast<__nv_bfloat16*>(e.D), e.ldd, reinterpret_cast<__nv_bfloat16*>(e.glu_out),
+                     e.ld_glu_out, reinterpret_cast<const __nv_bfloat16*>(e.glu_pre), e.ld_glu_pre, e.glu_h, e.N,
+                     e.glu_a0, e.glu_a1};
+        if (e.glu_a0 == ACT_LINEAR && e.glu_a1 == ACT_SILU)  // SwiGLU
+          glu_tile<ACT_LINEAR, ACT_SILU>(gq, e.glu, tbase, row, row_ok, tn);
+        else
+          glu_tile<-1, -1>(gq, e.glu, tbase, row, row_ok, tn);
+      } else {
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
-        tmem_ld_wait();
-        const int col0 = tn * BN + c * 32;
-        if (!row_ok || col0 >= e.N) continue;
-        epi_chunk(e, v, row, col0);
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tbase + c * 32, v);
+          tmem_ld_wait();
+          const int col0 = tn * BN + c * 32;
+          if (!row_ok || col0 >= e.N) continue;
+          epi_chunk(e, v, row, col0);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -706,6 +874,66 @@ static thread_local int g_last_gemm_tc = 0;  // did the last gemm_impl call run 
 }  // namespace cb
 
 using namespace cb;
+
+// Gated-activation FFN GEMMs on the CTA-pair engine (bf16).  Both return
+// CB_ERR_UNSUPPORTED — without launching anything — when the fused form does not apply
+// (shape / alignment / engine disabled); the caller then runs cb_gemm + cb_act_fwd/bwd.
+static bool glu_ok(int M, int H, int K, const void* A, int64_t lda, const void* B, int64_t ldb, const void* p0,
+                   int64_t ld0, const void* p1, int64_t ld1) {
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  return tc::g_gemm_mc == 3 && g_gemm_path != 1 && M >= 2 * tc::BM && K > 0 && H % 32 == 0 && al(A) && al(B) &&
+         al(p0) && al(p1) && ((lda | ldb | ld0 | ld1) & 7) == 0;
+}
+
+extern "C" int cb_gemm_gated_fwd(int M, int H, int K, const void* A, int64_t lda, int trans_a, const void* B,
+                                 int64_t ldb, int trans_b, void* pre, int64_t ldpre, void* hidden, int64_t ldh,
+                                 int act0, int act1, void* stream) {
+  if (M < 0 || H < 0 || K < 0) return fail(CB_ERR_SHAPE, "gemm_gated_fwd: negative extent");
+  if (H % 128 != 0 || !glu_ok(M, H, K, A, lda, B, ldb, pre, ldpre, hidden, ldh))
+    return fail(CB_ERR_UNSUPPORTED, "gemm_gated_fwd: fused epilogue not applicable (M=%d H=%d K=%d)", M, H, K);
+  tc::Args a;
+  a.M = M;
+  a.N = 2 * H;
+  a.K = K;
+  a.a_mn = trans_a ? 1 : 0;
+  a.b_mn = trans_b ? 0 : 1;
+  a.tiles_m = (M + tc::BM - 1) / tc::BM;
+  a.tiles_n = H / 128;
+  a.e = Epi{pre, ldpre, 0, nullptr, 0, 0, 1.f, 0, M, 2 * H};
+  a.e.glu = 1;
+  a.e.glu_h = H;
+  a.e.glu_a0 = act0;
+  a.e.glu_a1 = act1;
+  a.e.glu_out = hidden;
+  a.e.ld_glu_out = ldh;
+  return tc::launch_pair(a, A, lda, B, ldb, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int cb_gemm_gated_bwd(int M, int H, int K, const void* A, int64_t lda, int trans_a, const void* B,
+                                 int64_t ldb, int trans_b, const void* pre, int64_t ldpre, void* dpre, int64_t lddpre,
+                                 int act0, int act1, void* stream) {
+  if (M < 0 || H < 0 || K < 0) return fail(CB_ERR_SHAPE, "gemm_gated_bwd: negative extent");
+  if (!glu_ok(M, H, K, A, lda, B, ldb, pre, ldpre, dpre, lddpre))
+    return fail(CB_ERR_UNSUPPORTED, "gemm_gated_bwd: fused epilogue not applicable (M=%d H=%d K=%d)", M, H, K);
+  tc::Args a;
+  a.M = M;
+  a.N = H;
+  a.K = K;
+  a.a_mn = trans_a ? 1 : 0;
+  a.b_mn = trans_b ? 0 : 1;
+  a.tiles_m = (M + tc::BM - 1) / tc::BM;
+  a.tiles_n = (H + 255) / 256;
+  a.e = Epi{dpre, lddpre, 0, nullptr, 0, 0, 1.f, 0, M, H};
+  a.e.glu = 2;
+  a.e.glu_h = H;
+  a.e.glu_a0 = act0;
+  a.e.glu_a1 = act1;
+  a.e.glu_out = dpre;
+  a.e.ld_glu_out = lddpre;
+  a.e.glu_pre = pre;
+  a.e.ld_glu_pre = ldpre;
+  return tc::launch_pair(a, A, lda, B, ldb, reinterpret_cast<cudaStream_t>(stream));
+}
 
 extern "C" int cb_gemm_set_multicast(int mode) {
   // 0: single-CTA tiles, 1: default (CTA pair), 2: B-multicast cluster pairs, 3: CTA pair

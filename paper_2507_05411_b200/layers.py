@@ -559,17 +559,22 @@ class FeedForwardBehavior(Behavior):
         x2 = ops.cast(ops.rows2d(x), adt)
         h = cfg.get("hidden_dim")
         pair = activation_pair(cfg.get("activation"))
+        fused = None
         if pair:
             w1, wg = param("w1"), param("w1_gate")
             wcat = fused_columns(w1, wg)
-            if wcat is not None:
+            if wcat is not None and option("fuse_glu", True):
+                fused = ops.gemm_gated_fwd(x2, wcat, pair[0], pair[1])
+            if fused is not None:
+                pre, hidden = fused
+            elif wcat is not None:
                 pre = _linear_fwd(x2, wcat, adt)
             else:
                 pre = torch.empty((x2.shape[0], 2 * h), device=x.device, dtype=adt)
                 ops.gemm(x2, w1, pre[:, :h])
                 ops.gemm(x2, wg, pre[:, h:])
-            a, g = pre[:, :h], pre[:, h:]
-            hidden = ops.act_fwd(a, g, pair[0], pair[1])
+            if fused is None:
+                hidden = ops.act_fwd(pre[:, :h], pre[:, h:], pair[0], pair[1])
         else:
             pre = _linear_fwd(x2, param("w1"), adt)
             hidden = ops.act_fwd(pre, None, cfg.get("activation"))
@@ -584,13 +589,26 @@ class FeedForwardBehavior(Behavior):
         adt = act_dtype()
         h = cfg.get("hidden_dim")
         g = ops.rows2d(ops.cast(dout, adt))
-        dhidden = _linear_bwd(s["hidden"], param("w2"), g, param_grad("w2"), adt)
         pre = s["pre"]
-        dpre = torch.empty_like(pre)
         pair = activation_pair(cfg.get("activation"))
         x2 = s["x2"]
+        dw2 = param_grad("w2")
+        dpre = None
+        if pair and option("fuse_glu", True):
+            # dhidden = g @ w2^T formed and consumed by the gated-activation backward in one
+            # GEMM epilogue (dhidden never reaches HBM)
+            dpre = ops.gemm_gated_bwd(g, param("w2"), pre, pair[0], pair[1])
+        if dpre is not None:
+            if dw2 is not None:
+                ops.gemm(s["hidden"], g, dw2, trans_a=True, accumulate=True)
+        else:
+            dhidden = _linear_bwd(s["hidden"], param("w2"), g, dw2, adt)
+            dpre = torch.empty_like(pre)
+            if pair:
+                ops.act_bwd(pre[:, :h], pre[:, h:], dhidden, dpre[:, :h], dpre[:, h:], pair[0], pair[1])
+            else:
+                ops.act_bwd(pre, None, dhidden, dpre, None, cfg.get("activation"))
         if pair:
-            ops.act_bwd(pre[:, :h], pre[:, h:], dhidden, dpre[:, :h], dpre[:, h:], pair[0], pair[1])
             w1, wg = param("w1"), param("w1_gate")
             wcat = fused_columns(w1, wg)
             gcat = fused_columns(param_grad("w1"), param_grad("w1_gate"))
@@ -603,7 +621,6 @@ class FeedForwardBehavior(Behavior):
                 ops.gemm(dpre[:, :h], w1, dx, trans_b=True)
                 ops.gemm(dpre[:, h:], wg, dx, trans_b=True, accumulate=True)
         else:
-            ops.act_bwd(pre, None, dhidden, dpre, None, cfg.get("activation"))
             dx = _linear_bwd(x2, param("w1"), dpre, param_grad("w1"), torch.float32)
         return dx.view(*dout.shape[:-1], x2.shape[1])
 

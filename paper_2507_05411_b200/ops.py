@@ -127,6 +127,37 @@ def gemm_rope(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, seq_len: int,
     return out
 
 
+def gemm_gated_fwd(x2: torch.Tensor, wcat: torch.Tensor, act0: str, act1: str):
+    """pre = x2 @ wcat and hidden = act0(pre[:, :H]) * act1(pre[:, H:]) from one CTA-pair GEMM
+    (activation in the epilogue).  Returns (pre, hidden), or None when the fused form does
+    not apply (the caller then runs gemm + act_fwd)."""
+    M, K = x2.shape
+    if x2.dtype != torch.bfloat16 or wcat.dtype != torch.bfloat16 or wcat.shape[0] != K or wcat.shape[1] % 2:
+        return None
+    H = wcat.shape[1] // 2
+    pre = torch.empty((M, 2 * H), device=x2.device, dtype=torch.bfloat16)
+    hidden = torch.empty((M, H), device=x2.device, dtype=torch.bfloat16)
+    ok = _profiled("gemm_bf16", 2 * M * 2 * H * K, _lib.try_call, "cb_gemm_gated_fwd", M, H, K, x2.data_ptr(),
+                   ld(x2, "A"), 0, wcat.data_ptr(), ld(wcat, "B"), 0, pre.data_ptr(), ld(pre), hidden.data_ptr(),
+                   ld(hidden), ACT_IDS[act0], ACT_IDS[act1], stream_ptr())
+    return (pre, hidden) if ok else None
+
+
+def gemm_gated_bwd(dy: torch.Tensor, w2: torch.Tensor, pre: torch.Tensor, act0: str, act1: str):
+    """dpre = d/d(pre) of act0(a) * act1(g) given d(out) = dy and out = hidden @ w2, with
+    dhidden = dy @ w2^T formed and consumed inside one CTA-pair GEMM.  None when the fused
+    form does not apply."""
+    M, K = dy.shape
+    H = w2.shape[0]
+    if dy.dtype != torch.bfloat16 or w2.dtype != torch.bfloat16 or w2.shape[1] != K or pre.shape != (M, 2 * H):
+        return None
+    dpre = torch.empty_like(pre)
+    ok = _profiled("gemm_bf16", 2 * M * H * K, _lib.try_call, "cb_gemm_gated_bwd", M, H, K, dy.data_ptr(),
+                   ld(dy, "A"), 0, w2.data_ptr(), ld(w2, "B"), 1, pre.data_ptr(), ld(pre), dpre.data_ptr(),
+                   ld(dpre), ACT_IDS[act0], ACT_IDS[act1], stream_ptr())
+    return dpre if ok else None
+
+
 def set_gemm_path(path: int) -> None:
     _lib.call("cb_gemm_set_path", int(path))
 

@@ -82,3 +82,49 @@ def test_gemm_epilogues(cuda):
             assert ((acc - exp2).norm() / exp2.norm()) < 1e-5
         finally:
             ops.set_gemm_path(0)
+
+
+@pytest.mark.parametrize("M,K,H", [(512, 256, 384), (300, 128, 640), (1024, 512, 1152)])
+@pytest.mark.parametrize("acts", [("linear", "silu"), ("relu", "linear"), ("silu", "tanh")])
+def test_gemm_gated_epilogues_match_unfused(cuda, M, K, H, acts):
+    """The CTA-pair GEMM with the gated activation in its epilogue (forward) and the
+    activation backward fused into the w2 dgrad GEMM equal the unfused gemm + act kernels."""
+    from paper_2507_05411_b200 import ops
+
+    g = torch.Generator(device="cpu").manual_seed(M + K + H)
+    x = (torch.randn(M, K, generator=g) * 0.5).to(cuda, torch.bfloat16)
+    wcat = (torch.randn(K, 2 * H, generator=g) / K ** 0.5).to(cuda, torch.bfloat16)
+    w2 = (torch.randn(H, K, generator=g) / H ** 0.5).to(cuda, torch.bfloat16)
+    dy = torch.randn(M, K, generator=g).to(cuda, torch.bfloat16)
+
+    fused = ops.gemm_gated_fwd(x, wcat, *acts)
+    assert fused is not None, "fused forward declined an eligible shape"
+    pre_f, hid_f = fused
+    pre_u = torch.empty(M, 2 * H, device=cuda, dtype=torch.bfloat16)
+    ops.gemm(x, wcat, pre_u)
+    hid_u = ops.act_fwd(pre_u[:, :H], pre_u[:, H:], *acts)
+    torch.cuda.synchronize()
+    assert torch.equal(pre_f, pre_u)
+    assert ((hid_f.float() - hid_u.float()).norm() / hid_u.float().norm()) < 1e-6
+
+    dpre_f = ops.gemm_gated_bwd(dy, w2, pre_u, *acts)
+    assert dpre_f is not None, "fused backward declined an eligible shape"
+    dh = torch.empty(M, H, device=cuda, dtype=torch.bfloat16)
+    ops.gemm(dy, w2, dh, trans_b=True)
+    dpre_u = torch.empty_like(pre_u)
+    ops.act_bwd(pre_u[:, :H], pre_u[:, H:], dh, dpre_u[:, :H], dpre_u[:, H:], *acts)
+    torch.cuda.synchronize()
+    err = (dpre_f.float() - dpre_u.float()).norm() / dpre_u.float().norm()
+    assert err < 1e-4, f"rel err {err}"  # a few bf16 ulps from operation order
+
+
+def test_gemm_gated_declines_ineligible(cuda):
+    """Shapes the fused epilogue cannot take return None (nothing launched) instead of failing."""
+    from paper_2507_05411_b200 import ops
+
+    x = torch.randn(128, 64, device=cuda).bfloat16()  # M < 256: no CTA pair
+    wcat = torch.randn(64, 256, device=cuda).bfloat16()
+    assert ops.gemm_gated_fwd(x, wcat, "linear", "silu") is None
+    x = torch.randn(512, 64, device=cuda).bfloat16()
+    wcat = torch.randn(64, 2 * 96, device=cuda).bfloat16()  # H % 128 != 0
+    assert ops.gemm_gated_fwd(x, wcat, "linear", "silu") is None
