@@ -59,3 +59,4 @@ from .experiments import (
     synthetic_batch,
 )
 from .engine import TrainEngine, model_precision, set_dtype_policy
+from .step import forward_loss, train_step

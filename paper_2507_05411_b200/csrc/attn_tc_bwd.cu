@@ -144,10 +144,11 @@ __device__ __forceinline__ void pack_store(uint32_t dst, const float2 (&v)[32]) 
 
 // ====================================================================== dK / dV
 // 128-query tiles.  TMEM: S^T | dP^T | dV | dK (128 columns each).  Compute warps w and w+4
-// share TMEM lane quadrant w%4: half ch takes query columns [64 ch, 64 ch + 64) and writes
-// its bf16 pairs to columns [64 ch, 64 ch + 32) of the same region, so the halves never
-// touch each other's inputs; the dV / dK MMAs read the packed A operand from both halves.
-// MMA order per tile u:  [p_ready(u)] dV(u) S(u+1) | [ds_ready(u)] dK(u) dP(u+1).
+// share TMEM lane quadrant w%4: half ch takes query columns [64 ch, 64 ch + 64).  A tile's
+// S^T is read into registers at once (s_free), so S(u+1) is issued while tile u is still
+// being computed; P^T and dS^T (bf16 pairs) are then written over the dP^T region the half
+// has already read: P^T at columns [64 ch, 64 ch + 32), dS^T at [64 ch + 32, 64 ch + 64).
+// MMA order per tile u:  [s_free(u)] S(u+1) | [pd_ready(u)] dV(u) dK(u) dP(u+1).
 // smem: K, V, Q ring [3], dO ring [2], lse/delta ring [2] = 226 KB: this needs the dynamic
 // shared-memory base to be 1024-aligned already (checked).
 constexpr int kQSlots = 3, kGSlots = 2;
@@ -177,8 +178,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* ld_empty = bars + 13;  // [2]
   uint64_t* s_full = bars + 15;
   uint64_t* dp_full = bars + 16;
-  uint64_t* p_ready = bars + 17;
-  uint64_t* ds_ready = bars + 18;
+  uint64_t* s_free = bars + 17;    // the compute warps hold S^T(u) in registers
+  uint64_t* pd_ready = bars + 18;  // P^T(u) and dS^T(u) are in the dP^T region
   uint64_t* mma_done = bars + 19;
   uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 20);
 
@@ -207,8 +208,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
-    mbar_init(p_ready, 8);
-    mbar_init(ds_ready, 8);
+    mbar_init(s_free, 8);
+    mbar_init(pd_ready, 8);
     mbar_init(mma_done, 1);
     fence_mbar_init();
   }
@@ -305,28 +306,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     issue_dp(0);
     for (int u = 0; u < total; ++u) {
       const uint64_t mQ = sw128_desc(tileQ(u), kBox, 1024), mG = sw128_desc(tileG(u), kBox, 1024);
-      mbar_wait(p_ready, u & 1);
+      if (u + 1 < total) {  // S^T region: tile u is in registers
+        mbar_wait(s_free, u & 1);
+        tc_fence_after();
+        issue_s(u + 1);
+      }
+      mbar_wait(pd_ready, u & 1);
       tc_fence_after();
       BWD_TRACE(0, u);
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < BT / 16; ++k)
-          umma_f16_ts(tmem + cV, tmem + cS + packed_col(k), mG + (uint64_t)(k * 128), id_acc, (u | k) != 0);
+          umma_f16_ts(tmem + cV, tmem + cP + packed_col(k), mG + (uint64_t)(k * 128), id_acc, (u | k) != 0);
         umma_commit(&g_empty[u & 1]);  // dO(u) is done (dP(u) and dV(u))
-      }
-      __syncwarp();
-      if (u + 1 < total) issue_s(u + 1);  // S^T region: P^T(u) already consumed (in-order)
-      mbar_wait(ds_ready, u & 1);
-      tc_fence_after();
-      BWD_TRACE(2, u);
-      if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < BT / 16; ++k)
-          umma_f16_ts(tmem + cK, tmem + cP + packed_col(k), mQ + (uint64_t)(k * 128), id_acc, (u | k) != 0);
+          umma_f16_ts(tmem + cK, tmem + cP + 32 + packed_col(k), mQ + (uint64_t)(k * 128), id_acc, (u | k) != 0);
         umma_commit(&q_empty[u % kQSlots]);
       }
       __syncwarp();
-      if (u + 1 < total) issue_dp(u + 1);  // dP^T region: dS^T(u) already consumed
+      BWD_TRACE(2, u);
+      if (u + 1 < total) issue_dp(u + 1);  // dP^T region: P^T(u), dS^T(u) consumed (in order)
     }
     if (elect_one()) umma_commit(mma_done);
     __syncwarp();
@@ -348,18 +348,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       {
         uint32_t sv[2][32];
         ld64(tmem + lo + cS + half, sv);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_free);
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
           const float4 l4 = lds4(sL + 8 * i);
           pr[i] = exp2_pair(ffma2(col2(sv, i), c2, fmul2(make_float2(l4.x, l4.y), nlog2e)), i);
           pr[i + 1] = exp2_pair(ffma2(col2(sv, i + 1), c2, fmul2(make_float2(l4.z, l4.w), nlog2e)), i + 1);
         }
-        pack_store(tmem + lo + cS + half, pr);  // over this half's own S^T columns
       }
-      tc_fence_before();
-      __syncwarp();
       if (warp == 4) BWD_TRACE(5, u);
-      if (lane == 0) mbar_arrive(p_ready);
       mbar_wait(dp_full, u & 1);
       tc_fence_after();
       if (warp == 4) BWD_TRACE(6, u);
@@ -373,13 +372,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           ds[i] = fmul2(pr[i], ffma2(make_float2(d4.x, d4.y), make_float2(-1.f, -1.f), col2(dv, i)));
           ds[i + 1] = fmul2(pr[i + 1], ffma2(make_float2(d4.z, d4.w), make_float2(-1.f, -1.f), col2(dv, i + 1)));
         }
-        pack_store(tmem + lo + cP + half, ds);
+        pack_store(tmem + lo + cP + half, pr);       // P^T over this half's dP^T columns
+        pack_store(tmem + lo + cP + half + 32, ds);  // dS^T next to it
       }
       tc_fence_before();
       __syncwarp();
       if (warp == 4) BWD_TRACE(7, u);
       if (lane == 0) {
-        mbar_arrive(ds_ready);
+        mbar_arrive(pd_ready);
         mbar_arrive(&ld_empty[u & 1]);
       }
     }

@@ -217,6 +217,8 @@ class TrainEngine:
         self.buckets = build_layout(self.module)
         self._alloc()
         self.options = {"precision": self.precision, "validate_ids": False}
+        if self.d.world > 1:  # summaries that are global-batch statistics reduce over this group
+            self.options["dp_group"] = self.d.group if self.d.group is not None else self.d.dist.group.WORLD
         if init:
             self.init_params(root_key(seed))
 
@@ -346,6 +348,34 @@ class TrainEngine:
             self._host_bucket(b, rec, lambda e: _tree_get(state, e.path, e.name))
         torch.cuda.synchronize(self.device)
 
+    def load_opt_state(self, opt_state: dict | None) -> None:
+        """AdamW state in the reference's tree layout: {"m": tree, "v": tree, "step": int}
+        (None resets to the zero state of step 0)."""
+        if opt_state is None:
+            for rec in self.bufs:
+                rec["m"].zero_()
+                rec["v"].zero_()
+            self.step_count = 0
+            return
+        for which in ("m", "v"):
+            tree = opt_state[which]
+            for b, rec in zip(self.buckets, self.bufs):
+                host = np.zeros(rec["total"], dtype=np.float32)
+                for e in b.entries:
+                    arr = np.asarray(_tree_get(tree, e.path, e.name), dtype=np.float64)
+                    if e.ld:
+                        rows, cols = e.shape
+                        host[e.offset:e.offset + rows * e.ld].reshape(rows, e.ld)[:, e.col0:e.col0 + cols] = arr
+                    else:
+                        host[e.offset:e.offset + arr.size] = arr.reshape(-1)
+                r0 = 0 if b.replicated else self.d.rank * rec["shard"]
+                rec[which].copy_(torch.from_numpy(host[r0:r0 + rec["shard"]]).to(self.device))
+        self.step_count = int(opt_state.get("step", 0))
+        torch.cuda.synchronize(self.device)
+
+    def opt_state_numpy(self) -> dict:
+        return {"m": self._export("m"), "v": self._export("v"), "step": self.step_count}
+
     def _gather_full(self, buf: torch.Tensor, rec) -> torch.Tensor:
         if self.d.world == 1 or buf.numel() == rec["total"]:
             return buf
@@ -396,21 +426,30 @@ class TrainEngine:
     def step_key(self, step: int):
         return child_key(root_key(self.seed), "step", step)
 
-    def loss(self, tokens, step: int | None = None) -> float:
-        """Forward-only loss (the reference's invoke(module, state, key, batch) result)."""
+    def loss(self, tokens, step: int | None = None, key=None, collection: bool = False):
+        """Forward-only loss (the reference's invoke(module, state, key, batch) result); with
+        collection=True also the OutputCollection (summaries)."""
         toks = self.upload_tokens(tokens)
         provider = FSDPProvider(self) if self.d.world > 1 else None
         if provider:
             provider.start_step()
-        out, col = invoke(self.module, self.state, self.step_key(self.step_count if step is None else step),
-                          {"tokens": toks}, keep_outputs=False, provider=provider, options=self.options)
+        if key is None:
+            key = self.step_key(self.step_count if step is None else step)
+        out, col = invoke(self.module, self.state, key, {"tokens": toks}, keep_outputs=False, provider=provider,
+                          options=self.options)
+        if collection:
+            if self.d.world > 1:
+                t = torch.tensor([out], device=self.device, dtype=torch.float64)
+                self.d.dist.all_reduce(t, op=self.d.dist.ReduceOp.AVG, group=self.d.group)
+                out = float(t.item())
+            return out, col
         if self.d.world > 1:
             t = torch.tensor([out], device=self.device, dtype=torch.float64)
             self.d.dist.all_reduce(t, op=self.d.dist.ReduceOp.AVG, group=self.d.group)
             return float(t.item())
         return out
 
-    def compute_grads(self, tokens, update: bool = False):
+    def compute_grads(self, tokens, update: bool = False, key=None):
         """Forward + backward; gradients land in the (sharded) grad buffers.  Returns (loss, collection).
 
         update=True also applies AdamW (step counter advanced first): each layer bucket is
@@ -419,7 +458,8 @@ class TrainEngine:
         the backward GEMMs of earlier layers.
         """
         toks = self.upload_tokens(tokens)
-        key = self.step_key(self.step_count)
+        if key is None:
+            key = self.step_key(self.step_count)
         if update:
             self.step_count += 1
         for rec in self.bufs:

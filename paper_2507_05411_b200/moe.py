@@ -104,6 +104,20 @@ class MoEBehavior(Behavior):
                   idx.data_ptr(), w.data_ptr(), probs.data_ptr(), ops.stream_ptr())
         stats = torch.empty((1 + 2 * E,), device=dev, dtype=torch.float64)
         _lib.call("cb_moe_stats", n, E, k, idx.data_ptr(), probs.data_ptr(), stats.data_ptr(), ops.stream_ptr())
+        grp = L.option("dp_group")
+        if grp is not None:
+            # data parallel: f_e and p_e are global-batch statistics, so the per-expert counts
+            # and probability sums are all-reduced before forming E * sum_e f_e p_e (SURVEY
+            # §8(e) C3); a (1 + 2E)-double collective on the compute stream
+            import torch.distributed as dist
+
+            raw = stats[1:].clone()
+            raw[E:] *= n
+            dist.all_reduce(raw, group=grp)
+            n_glob = n * dist.get_world_size(grp)
+            f = raw[:E] / (n_glob * k)
+            p = raw[E:] / n_glob
+            stats = torch.cat([(E * (f * p).sum()).view(1), raw[:E], p])
         add_summary("load_balance_loss", stats[0:1] if L.is_recording() else float(stats[0].item()))
         if L.option("record_routing", False):  # debug summary: the chosen experts per token
             add_summary("route_indices", idx.view(B, T, k))

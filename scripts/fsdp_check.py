@@ -64,13 +64,22 @@ def main():
     for step in range(args.steps):
         toks = synthetic_batch(0, step, B, T, V)["tokens"]
         mine = toks[rank * per:(rank + 1) * per]
-        loss, _ = eng.compute_grads(mine)
+        loss, col = eng.compute_grads(mine)
         loss = float(loss.item())
+        summ = col.flat_summaries()
         grads = eng.grads_numpy() if step == 0 else None
         eng.apply_update()
-        lo, go, st, mm, vv, _ = O.train_step(st, toks, spec, O.AdamW(lr=eng.lr), mm, vv, step + 1)
+        lo, go, st, mm, vv, osum = O.train_step(st, toks, spec, O.AdamW(lr=eng.lr), mm, vv, step + 1)
         rec = {"loss": loss, "oracle": lo, "loss_rel": abs(loss - lo) / lo}
         ok &= rec["loss_rel"] < tol
+        # MoE load-balance summaries are global-batch statistics (reduced across ranks)
+        for key, ref in sorted(osum.items()):
+            if key.endswith("load_balance_loss") and key in summ:
+                got = float(summ[key][0])
+                rel = abs(got - ref) / abs(ref)
+                rec.setdefault("lb_rel_max", 0.0)
+                rec["lb_rel_max"] = max(rec["lb_rel_max"], rel)
+                ok &= rel < tol
         if grads is not None:
             worst = 0.0
             for (k, a), (_, b) in zip(O.leaves(grads), O.leaves(go)):

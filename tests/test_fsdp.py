@@ -101,3 +101,17 @@ def test_fsdp_two_gpus_matches_oracle(precision):
            "8" if precision == "f32" else "128"]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+
+
+@pytest.mark.gpu
+def test_fsdp_two_gpus_moe_global_summaries():
+    """MoE under FSDP: loss, gradients, updated parameters and the load_balance_loss summaries
+    (global-batch statistics, reduced across ranks) match the oracle on the global batch."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs (run with gpurun --gpus 2)")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(REPO, "scripts", "fsdp_check.py"),
+           "--precision", "f32", "--config", "txf_moe", "--seq", "8"]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    assert '"lb_rel_max"' in res.stdout, res.stdout[-2000:]

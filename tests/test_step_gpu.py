@@ -209,3 +209,41 @@ def test_two_steps_train(cuda):
     mine = dict(_leaves(eng.state_numpy()))
     for k, v in _leaves(st):
         assert _rel(mine[k], v) < 1e-5, k
+
+
+def test_functional_train_step_api(cuda):
+    """train_step / forward_loss on the reference's state trees (SURVEY §8(b) step entry):
+    fresh state in, (loss, summaries, new_state, new_opt_state, grads) out, inputs untouched,
+    two chained steps against the oracle; forward_loss equals the reference invoke loss."""
+    from paper_2507_05411_b200 import (build_experiment, child_key, forward_loss, init_state, instantiate, root_key,
+                                       synthetic_batch, train_step)
+
+    m = instantiate(build_experiment("txf_moe"))
+    st = st0 = init_state(m, root_key(0))
+    before = {k: v.copy() for k, v in _leaves(st0)}
+    spec = O.spec_from_config(m.config)
+    opt = None
+    ost, mm, vv = st, None, None
+    for step in range(2):
+        toks = synthetic_batch(0, step, 4, 8)["tokens"]
+        key = child_key(root_key(0), "step", step)
+        loss, summ, new_st, opt, grads = train_step(m, st, opt, key, {"tokens": toks}, return_grads=True)
+        lo, go, ost, mm, vv, osum = O.train_step(ost, toks, spec, O.AdamW(lr=1e-3), mm, vv, step + 1)
+        assert abs(loss - lo) / lo < 1e-5
+        for k, v in _leaves(go):
+            assert _rel(dict(_leaves(grads))[k], v) < 1e-5, k
+        for k, ref in osum.items():
+            assert abs(summ[k][0] - ref) / abs(ref) < 1e-5, k
+        assert opt["step"] == step + 1
+        mine = dict(_leaves(new_st))
+        for k, v in _leaves(ost):
+            assert _rel(mine[k], v) < 1e-5, k
+        for k, v in _leaves(mm):
+            assert _rel(dict(_leaves(opt["m"]))[k], v) < 1e-5, k
+        st = new_st
+    for k, v in _leaves(st0):
+        assert np.array_equal(before[k], v)  # the caller's arrays were not mutated
+    rec = GOLD["experiments"]["txf_moe"]
+    loss, col = forward_loss(m, init_state(m, root_key(0)), child_key(root_key(0), "step", 0),
+                             {"tokens": np.array(rec["tokens"], dtype=np.int64)})
+    assert abs(loss - rec["loss"]) / rec["loss"] < 1e-5
