@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--batch", type=int, default=8, help="global batch")
     ap.add_argument("--seq", type=int, default=8)
+    ap.add_argument("--ckpt", default=None, help="save a sharded checkpoint here after training")
     args = ap.parse_args()
 
     import torch
@@ -93,6 +94,17 @@ def main():
         worst = max(worst, float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)))
     out["param_rel_max"] = worst
     ok &= worst < tol
+    if args.ckpt:
+        from paper_2507_05411_b200.checkpoint import save_checkpoint
+
+        rep = save_checkpoint(eng, args.ckpt)
+        out["ckpt"] = rep
+        opt = eng.opt_state_numpy()
+        if rank == 0:  # reference copy of the full state for the restore test
+            flat = {f"p:{k}": v for k, v in O.leaves(params)}
+            flat.update({f"m:{k}": v for k, v in O.leaves(opt["m"])})
+            flat.update({f"v:{k}": v for k, v in O.leaves(opt["v"])})
+            np.savez(os.path.join(args.ckpt, "ref_state.npz"), **flat)
     out["ok"] = bool(ok)
     if rank == 0:
         print(json.dumps(out), flush=True)

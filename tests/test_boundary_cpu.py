@@ -155,3 +155,26 @@ def test_engine_layout_fuses_and_aligns():
             assert e.offset % ALIGN == 0
     rep = buckets[-1]
     assert all(e.name == "scale" for e in rep.entries)
+
+
+def test_checkpoint_plan_and_retention():
+    """Checkpoint planning / retention restated from reference runtime_sim.py:22-157:
+    exact partition, replicated shards round-robin, owned shards stay with their owner."""
+    import pytest
+
+    from paper_2507_05411_b200.checkpoint import GcPolicy, Shard, ShardManifest, gc_retained, plan_checkpoint
+
+    shards = (Shard("a", 10), Shard("b", 20), Shard("c", 30, replicated=False, owner=1), Shard("d", 5),
+              Shard("e", 7, replicated=False, owner=0), Shard("f", 1))
+    plan = plan_checkpoint(ShardManifest(shards, replicas=2))
+    assert [s.name for s in plan[0]] == ["a", "d", "e"] and [s.name for s in plan[1]] == ["b", "c", "f"]
+    assert sorted(s.name for r in plan.values() for s in r) == sorted(s.name for s in shards)
+    single = plan_checkpoint(ShardManifest(shards[:2], replicas=1))
+    assert [s.name for s in single[0]] == ["a", "b"]
+    with pytest.raises(ValueError):
+        ShardManifest((Shard("x", 1), Shard("x", 2)))
+    with pytest.raises(ValueError):
+        ShardManifest((Shard("x", 1, replicated=False, owner=3),), replicas=2)
+    assert gc_retained([1, 2, 3, 4, 5, 6], GcPolicy(keep_last_n=2, keep_every_k=3)) == {3, 5, 6}
+    with pytest.raises(ValueError):
+        GcPolicy()

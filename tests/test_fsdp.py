@@ -115,3 +115,38 @@ def test_fsdp_two_gpus_moe_global_summaries():
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     assert '"lb_rel_max"' in res.stdout, res.stdout[-2000:]
+
+
+@pytest.mark.gpu
+def test_sharded_checkpoint_two_gpus_restores_on_one(tmp_path):
+    """A checkpoint written by 2 FSDP ranks (each rank its own shards, replicated buckets
+    round-robin) restores bit-exactly into a 1-GPU engine (re-sliced buckets)."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs (run with gpurun --gpus 2)")
+    import numpy as np
+
+    from oracle import decoder_oracle as O
+    from paper_2507_05411_b200 import TrainEngine, set_dtype_policy
+    from paper_2507_05411_b200.checkpoint import list_steps, load_checkpoint
+    from paper_2507_05411_b200.experiments import transformer_trainer
+
+    ck = str(tmp_path / "ckpt")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(REPO, "scripts", "fsdp_check.py"),
+           "--precision", "bf16", "--config", "mid", "--seq", "128", "--ckpt", ck]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    assert list_steps(ck) == [2]
+    cfg = transformer_trainer(256, 2, ("linear", "silu"), pos_kind="RoPE", heads=2, vocab=512)
+    for i in range(2):
+        cfg = cfg.set(f"model.decoder.transformer.layer[{i}].feed_forward.hidden_dim", 768)
+    eng = TrainEngine(set_dtype_policy(cfg, "bf16"), device="cuda:0")
+    assert load_checkpoint(eng, ck) == 2
+    ref = np.load(os.path.join(ck, "ref_state.npz"))
+    got = {f"p:{k}": v for k, v in O.leaves(eng.state_numpy())}
+    opt = eng.opt_state_numpy()
+    got.update({f"m:{k}": v for k, v in O.leaves(opt["m"])})
+    got.update({f"v:{k}": v for k, v in O.leaves(opt["v"])})
+    assert sorted(got) == sorted(ref.files)
+    for k in ref.files:
+        assert np.array_equal(got[k], ref[k]), k

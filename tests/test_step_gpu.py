@@ -247,3 +247,27 @@ def test_functional_train_step_api(cuda):
     loss, col = forward_loss(m, init_state(m, root_key(0)), child_key(root_key(0), "step", 0),
                              {"tokens": np.array(rec["tokens"], dtype=np.int64)})
     assert abs(loss - rec["loss"]) / rec["loss"] < 1e-5
+
+
+def test_checkpoint_resume_is_bit_exact(cuda, tmp_path):
+    """save -> fresh engine -> load -> the next step equals the uninterrupted run exactly;
+    retention keeps the newest checkpoints only."""
+    from paper_2507_05411_b200 import TrainEngine, set_dtype_policy, synthetic_batch
+    from paper_2507_05411_b200.checkpoint import GcPolicy, list_steps, load_checkpoint, save_checkpoint
+
+    cfg = set_dtype_policy(_mid(128), "bf16")
+    toks = [synthetic_batch(0, s, 2, 256, 512)["tokens"] for s in range(4)]
+    a = TrainEngine(cfg, device="cuda:0")
+    root = str(tmp_path / "ck")
+    for s in range(3):
+        a.step(toks[s])
+        save_checkpoint(a, root, gc=GcPolicy(keep_last_n=2))
+    assert list_steps(root) == [2, 3]
+    la, _ = a.step(toks[3])
+    b = TrainEngine(cfg, device="cuda:0", init=False)
+    assert load_checkpoint(b, root) == 3
+    lb, _ = b.step(toks[3])
+    assert float(la.item()) == float(lb.item())
+    sa, sb = dict(_leaves(a.state_numpy())), dict(_leaves(b.state_numpy()))
+    for k in sa:
+        assert np.array_equal(sa[k], sb[k]), k
