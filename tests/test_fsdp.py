@@ -72,8 +72,8 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_data_parallel_invariants_gloo():
-    world = 2
+@pytest.mark.parametrize("world", [2, 8])  # 8 = the box the scaling run uses
+def test_data_parallel_invariants_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
