@@ -55,6 +55,11 @@ CB_API int cb_gemm_set_path(int path);
    tiles); 2 = cluster pairs sharing the B tile via TMA multicast; 3 = CTA pair; 0 = one CTA
    per 128-row tile. */
 CB_API int cb_gemm_set_multicast(int mode);
+/* Registers a caller-owned device buffer (16-byte aligned) the CTA-pair engine may use for
+   split-K partials (f32 [S][M][N]) on GEMMs whose tile count leaves the last wave mostly
+   idle; slices are summed in a fixed order by a second kernel (deterministic).  bytes = 0
+   disables split-K.  The library never allocates. */
+CB_API int cb_gemm_set_workspace(void* ptr, int64_t bytes);
 /* D = op(A) @ op(B) with RoPE (layers.py:235-257; positions = row % seq_len) applied to
  * output columns [0, rope_cols) — the q|k part of the fused QKV projection (layers.py:340-343).
  * Rotated in the tcgen05 epilogue (no extra HBM pass); other engines rotate afterwards. */

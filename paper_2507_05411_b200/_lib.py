@@ -51,6 +51,7 @@ SIGNATURES: dict[str, list] = {
                          _P, _L, _F, _P],
     "cb_attention_set_path": [_I],
     "cb_gemm_rope": [_I, _I, _I, _I, _P, _L, _I, _P, _L, _I, _P, _L, _I, _I, _I, _I, _P, _P, _P],
+    "cb_gemm_set_workspace": [_P, _L],
     "cb_gemm_gated_fwd": [_I, _I, _I, _P, _L, _I, _P, _L, _I, _P, _L, _P, _L, _I, _I, _P],
     "cb_gemm_gated_bwd": [_I, _I, _I, _P, _L, _I, _P, _L, _I, _P, _L, _P, _L, _I, _I, _P],
     "cb_attention_bwd_rope": [_I, _I, _I, _I, _I, _I, _P, _L, _P, _L, _P, _L, _P, _L, _P, _P, _L, _P, _P, _L, _P,

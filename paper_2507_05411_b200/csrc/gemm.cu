@@ -15,6 +15,7 @@
 //   * gemm_simt — f32 FMA tiles; the fp32 parity mode (1e-5 contract) and shapes TMA
 //                 cannot describe (row strides not 16-byte aligned, e.g. hidden 341).
 #include <algorithm>
+#include <cmath>
 
 #include "common.cuh"
 #include "composer_b200.h"
@@ -87,6 +88,11 @@ struct Args {
   int a_mn, b_mn;
   int tiles_m, tiles_n;
   Epi e;
+  // split-K (CTA-pair engine): slice s of every tile covers k-blocks [s*nk/S, (s+1)*nk/S)
+  // and stores its raw f32 partial to ws[s] ([M][N]); splitk_reduce_k sums the slices in
+  // order and applies the epilogue (deterministic: no atomics)
+  int splits = 1;
+  float* ws = nullptr;
 };
 
 __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
@@ -558,13 +564,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int rank = (int)cluster_ctarank();
   const bool leader = rank == 0;
   const int tiles_mg = (args.tiles_m + 1) / 2;  // 256-row tile pairs
-  const int num_units = tiles_mg * args.tiles_n;
+  const int S = args.splits;
+  const int num_units = tiles_mg * args.tiles_n * S;
   const int unit0 = (int)(blockIdx.x >> 1), unit_stride = (int)(gridDim.x >> 1);
-  const int nk = (args.K + BK - 1) / BK;
+  const int nk_all = (args.K + BK - 1) / BK;
   auto coords = [&](int u, int& tm, int& tn) {
     int tg;
-    tile_coords(u, tiles_mg, args.tiles_n, tg, tn);
+    tile_coords(u / S, tiles_mg, args.tiles_n, tg, tn);
     tm = tg * 2 + rank;
+  };
+  // k-block range of unit u (its split-K slice)
+  auto krange = [&](int u, int& kb0, int& kb1) {
+    const int sl = u % S;
+    kb0 = (int)((int64_t)sl * nk_all / S);
+    kb1 = (int)((int64_t)(sl + 1) * nk_all / S);
   };
 
   if (warp == 0 && lane == 0) {
@@ -597,7 +610,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // B columns this CTA stages: its half of the 256-column tile, or (gated forward) the
       // tile's 128 columns of the a half (rank 0) / of the g half (rank 1)
       const int nb = args.e.glu == 1 ? rank * args.e.glu_h + tn * 128 : tn * BN + rank * 128;
-      for (int kb = 0; kb < nk; ++kb) {
+      int kb0, kb1;
+      krange(u, kb0, kb1);
+      for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* a_dst = sA + stage * C::kABytes;
         uint8_t* b_dst = sB + stage * C::kBBytes;
@@ -640,7 +655,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < nk; ++kb) {
+        int kb0, kb1;
+        krange(u, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t ad = a0 + (uint64_t)(stage * (C::kABytes >> 4));
@@ -648,7 +665,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk)
-              umma_f16_ss_pair(d_tmem, ad + kk * a_step, bd + kk * b_step, idesc, (kb | kk) != 0);
+              umma_f16_ss_pair(d_tmem, ad + kk * a_step, bd + kk * b_step, idesc, (kb > kb0 || kk) ? 1u : 0u);
             umma_commit_pair_mc(&empty[stage], 0x3);
           }
           __syncwarp();
@@ -684,6 +701,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           glu_tile<ACT_LINEAR, ACT_SILU>(gq, e.glu, tbase, row, row_ok, tn);
         else
           glu_tile<-1, -1>(gq, e.glu, tbase, row, row_ok, tn);
+      } else if (S > 1) {
+        // split-K slice: raw f32 partial to ws[slice] (the reduce kernel applies the epilogue)
+        float* part = args.ws + (int64_t)(u % S) * e.M * e.N + (int64_t)row * e.N;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tbase + c * 32, v);
+          tmem_ld_wait();
+          const int col0 = tn * BN + c * 32;
+          if (!row_ok || col0 >= e.N) continue;
+          if (col0 + 32 <= e.N) {
+            float4* dst = reinterpret_cast<float4*>(part + col0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              dst[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                   __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+          } else {
+            for (int j = 0; j < e.N - col0; ++j) part[col0 + j] = __uint_as_float(v[j]);
+          }
+        }
       } else {
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
@@ -708,6 +745,66 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Split-K reduction: D = alpha * sum_s ws[s] (+ D) (+ R), slices summed in order s = 0..S-1
+// (deterministic), 4 columns per thread.
+__global__ void __launch_bounds__(256) splitk_reduce_k(const float* __restrict__ ws, int S, const Epi e) {
+  const int64_t q = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int nq = (e.N + 3) >> 2;
+  const int64_t row = q / nq;
+  const int col = (int)(q - row * nq) * 4;
+  if (row >= e.M) return;
+  const int64_t mn = (int64_t)e.M * e.N, base = row * e.N + col;
+  if (col + 4 <= e.N && (e.N & 3) == 0) {
+    float4 acc = *reinterpret_cast<const float4*>(ws + base);
+    for (int sl = 1; sl < S; ++sl) {
+      const float4 t = *reinterpret_cast<const float4*>(ws + sl * mn + base);
+      acc.x += t.x;
+      acc.y += t.y;
+      acc.z += t.z;
+      acc.w += t.w;
+    }
+    const float v[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) epi_store1(e, (int)row, col + j, v[j]);
+  } else {
+    for (int j = 0; j < 4 && col + j < e.N; ++j) {
+      float v = 0.f;
+      for (int sl = 0; sl < S; ++sl) v += ws[sl * mn + base + j];
+      epi_store1(e, (int)row, col + j, v);
+    }
+  }
+}
+
+// Caller-provided split-K workspace (cb_gemm_set_workspace; PyTorch owns the buffer).
+static float* g_ws = nullptr;
+static int64_t g_ws_bytes = 0;
+
+// Number of split-K slices for a CTA-pair GEMM: more slices only when the tile count leaves
+// the last wave of the 74 pairs mostly empty and K is long enough to split, trading the
+// saved MMA wave time against the f32 partial round trip through HBM.
+static int choose_splits(const Args& a) {
+  if (!g_ws || a.e.glu || a.e.rope_cos) return 1;
+  const int P = kNumSMs / 2;
+  const int units = ((a.tiles_m + 1) / 2) * a.tiles_n;
+  const int nk = (a.K + BK - 1) / BK;
+  if (units >= 4 * P || nk < 32) return 1;
+  const double kblock_s = 0.4e-6;  // one 256x256x64 k-block on a pair, ~1.5 GHz
+  const double hbm = 5.5e12;       // B/s for the partial write + reduce read
+  double best_t = std::ceil((double)units / P) * nk * kblock_s;
+  int best = 1;
+  for (int S = 2; S <= 8; ++S) {
+    if (nk / S < 16) break;
+    const double bytes = 4.0 * S * (double)a.M * a.N;
+    if (bytes > (double)g_ws_bytes) break;
+    const double t = std::ceil((double)units * S / P) * ((double)nk / S) * kblock_s + 2.0 * bytes / hbm;
+    if (t < 0.97 * best_t) {
+      best_t = t;
+      best = S;
+    }
+  }
+  return best;
+}
+
 static int g_gemm_mc = 3;  // 3: CTA-pair MMA, 2: B-multicast cluster pairs, 1: single CTA
 
 int launch_pair(const Args& a, const void* A, int64_t lda, const void* B, int64_t ldb, cudaStream_t st) {
@@ -729,7 +826,10 @@ int launch_pair(const Args& a, const void* A, int64_t lda, const void* B, int64_
     cudaFuncSetAttribute(gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     attr_set = true;
   }
-  const int pairs = ((a.tiles_m + 1) / 2) * a.tiles_n;
+  Args args = a;
+  args.splits = choose_splits(a);
+  args.ws = args.splits > 1 ? g_ws : nullptr;
+  const int pairs = ((a.tiles_m + 1) / 2) * a.tiles_n * args.splits;
   const int grid = 2 * std::min(pairs, kNumSMs / 2);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -743,9 +843,13 @@ int launch_pair(const Args& a, const void* A, int64_t lda, const void* B, int64_
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc2, ta, tb, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc2, ta, tb, args);
   if (e != cudaSuccess) return fail(CB_ERR_CUDA, "gemm_tc2 cluster launch: %s", cudaGetErrorString(e));
-  return check_launch("gemm_tc_pair");
+  if (int r = check_launch("gemm_tc_pair")) return r;
+  if (args.splits == 1) return CB_OK;
+  const int64_t quads = (int64_t)a.M * ((a.N + 3) / 4);
+  splitk_reduce_k<<<(unsigned)((quads + 255) / 256), 256, 0, st>>>(g_ws, args.splits, a.e);
+  return check_launch("gemm_splitk_reduce");
 }
 
 template <int BN>
@@ -779,7 +883,10 @@ int launch(const Args& a, const void* A, int64_t lda, const void* B, int64_t ldb
     gemm_tc<BN, 1><<<grid, kThreads, C::kSmem, st>>>(ta, tb, a);
     return check_launch("gemm_tc");
   }
-  const int pairs = ((a.tiles_m + 1) / 2) * a.tiles_n;
+  Args args = a;
+  args.splits = choose_splits(a);
+  args.ws = args.splits > 1 ? g_ws : nullptr;
+  const int pairs = ((a.tiles_m + 1) / 2) * a.tiles_n * args.splits;
   const int grid = 2 * std::min(pairs, kNumSMs / 2);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -933,6 +1040,14 @@ extern "C" int cb_gemm_gated_bwd(int M, int H, int K, const void* A, int64_t lda
   a.e.glu_pre = pre;
   a.e.ld_glu_pre = ldpre;
   return tc::launch_pair(a, A, lda, B, ldb, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int cb_gemm_set_workspace(void* ptr, int64_t bytes) {
+  if (bytes < 0 || (bytes > 0 && !ptr) || (reinterpret_cast<uintptr_t>(ptr) & 15))
+    return fail(CB_ERR_ARG, "gemm workspace: need a 16-byte aligned buffer");
+  tc::g_ws = bytes > 0 ? reinterpret_cast<float*>(ptr) : nullptr;
+  tc::g_ws_bytes = bytes;
+  return CB_OK;
 }
 
 extern "C" int cb_gemm_set_multicast(int mode) {

@@ -216,6 +216,7 @@ class TrainEngine:
         self.d = _Dist(group)
         self.buckets = build_layout(self.module)
         self._alloc()
+        ops.ensure_gemm_workspace(self.device)
         self.options = {"precision": self.precision, "validate_ids": False}
         if self.d.world > 1:  # summaries that are global-batch statistics reduce over this group
             self.options["dp_group"] = self.d.group if self.d.group is not None else self.d.dist.group.WORLD

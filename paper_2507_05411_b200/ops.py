@@ -158,6 +158,19 @@ def gemm_gated_bwd(dy: torch.Tensor, w2: torch.Tensor, pre: torch.Tensor, act0: 
     return dpre if ok else None
 
 
+_GEMM_WS: dict = {}
+
+
+def ensure_gemm_workspace(device, nbytes: int = 256 << 20) -> None:
+    """Registers a split-K workspace for the tcgen05 GEMM on this device (PyTorch-owned)."""
+    key = str(device)
+    if key in _GEMM_WS and _GEMM_WS[key].numel() * 4 >= nbytes:
+        return
+    buf = torch.empty(nbytes // 4, device=device, dtype=torch.float32)
+    _GEMM_WS[key] = buf
+    _lib.call("cb_gemm_set_workspace", buf.data_ptr(), buf.numel() * 4)
+
+
 def set_gemm_path(path: int) -> None:
     _lib.call("cb_gemm_set_path", int(path))
 

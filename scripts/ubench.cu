@@ -91,6 +91,15 @@ __global__ void __launch_bounds__(NW * 32, 1) alu_bench(unsigned long long* cyc,
         uint32_t r;
         asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(x[i]), "f"(x[(i + 1) & 7]));
         x[i] = __uint_as_float(r);
+      } else if (MODE == 4) {
+        uint32_t h2, r;
+        asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h2) : "f"(x[i]), "f"(x[(i + 1) & 7]));
+        asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(h2));
+        x[i] = __uint_as_float(r) - 1.0f;
+      } else if (MODE == 5) {
+        uint32_t r;
+        asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(__float_as_uint(x[i])));
+        x[i] = __uint_as_float(r & 0xbfffbfffu);
       } else if (MODE == 3) {
         float y, z;
         asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x[i]));
@@ -163,9 +172,9 @@ int main() {
 #define ALU(NW, M)                                                                                        \
   {                                                                                                       \
     double c = runf(alu_bench<NW, M>, NW * 32);                                                            \
-    printf("%s warps=%2d: %8.0f cyc  %6.1f ops/clk/SM\n", M == 0 ? "ex2 " : M == 2 ? "f2fp" : M == 3 ? "ex2+f2fp" : "fma ", NW, c, \
+    printf("%s warps=%2d: %8.0f cyc  %6.1f ops/clk/SM\n", M == 0 ? "ex2 " : M == 2 ? "f2fp" : M == 3 ? "ex2+f2fp" : M == 4 ? "cvt+ex2.f16x2" : M == 5 ? "ex2.f16x2" : "fma ", NW, c, \
            (double)NW * 32 * 8 * kIters / c);                                                             \
   }
-  ALU(4, 0) ALU(8, 0) ALU(4, 1) ALU(8, 1) ALU(4, 2) ALU(8, 2) ALU(16, 2) ALU(4, 3) ALU(8, 3)
+  ALU(4, 0) ALU(8, 0) ALU(8, 4) ALU(16, 4) ALU(8, 5) ALU(16, 5)
   return 0;
 }

@@ -128,3 +128,36 @@ def test_gemm_gated_declines_ineligible(cuda):
     x = torch.randn(512, 64, device=cuda).bfloat16()
     wcat = torch.randn(64, 2 * 96, device=cuda).bfloat16()  # H % 128 != 0
     assert ops.gemm_gated_fwd(x, wcat, "linear", "silu") is None
+
+
+@pytest.mark.parametrize("M,N,K,ta,tb", [(512, 512, 16384, 1, 0), (640, 768, 8192, 0, 1), (2048, 1024, 32768, 1, 0)])
+def test_gemm_split_k_matches(cuda, M, N, K, ta, tb):
+    """Few tiles + long K take the split-K route (f32 partials in the registered workspace,
+    summed in a fixed order by a second kernel): same result as the single pass within f32
+    rounding, bit-reproducible across calls, and the epilogue (alpha / accumulate / residual /
+    bf16 out) applied exactly once."""
+    from paper_2507_05411_b200 import _lib, ops
+
+    a, b = _operands(M, N, K, ta, tb, torch.bfloat16, cuda)
+    ref = _ref(a, b, ta, tb)
+    ws = torch.empty((64 << 20) // 4, device=cuda)
+    r = torch.randn(M, N, device=cuda)
+    outs = {}
+    try:
+        for mode in ("plain", "split", "split2"):
+            _lib.call("cb_gemm_set_workspace", ws.data_ptr() if mode != "plain" else None,
+                      ws.numel() * 4 if mode != "plain" else 0)
+            acc = torch.ones(M, N, device=cuda)
+            ops.gemm(a, b, acc, trans_a=bool(ta), trans_b=bool(tb), accumulate=True)
+            bo = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+            ops.gemm(a, b, bo, trans_a=bool(ta), trans_b=bool(tb), alpha=0.5, residual=r)
+            outs[mode] = (acc, bo)
+    finally:
+        _lib.call("cb_gemm_set_workspace", None, 0)
+    torch.cuda.synchronize()
+    for mode in ("plain", "split"):
+        acc, bo = outs[mode]
+        assert ((acc - 1.0 - ref).norm() / ref.norm()) < 1e-4, mode  # f32 accumulation over K up to 32768
+        exp = 0.5 * ref + r
+        assert ((bo.float() - exp).norm() / exp.norm()) < 1e-2, mode
+    assert torch.equal(outs["split"][0], outs["split2"][0])  # deterministic
