@@ -129,6 +129,31 @@ __device__ __forceinline__ float2 exp2_pair(float2 a, int i) {
   if ((i & 7) < kEmuPairs) return exp2_poly2(a);
   return make_float2(fast_exp2(a.x), fast_exp2(a.y));
 }
+// W f32 TMEM columns of this thread's row (W = 32 or 64), all loads in flight, one wait
+template <int W>
+__device__ __forceinline__ void ldW(uint32_t src, uint32_t (&v)[W / 32][32]) {
+#pragma unroll
+  for (int i = 0; i < W / 32; ++i) tmem_ld32(src + 32 * i, v[i]);
+  tmem_ld_wait_regs(v[0]);
+#pragma unroll
+  for (int i = 1; i < W / 32; ++i) reg_fence(v[i]);
+}
+template <int NB>
+__device__ __forceinline__ float2 colp(const uint32_t (&v)[NB][32], int i) {  // columns 2i, 2i+1
+  return make_float2(__uint_as_float(v[i >> 4][2 * (i & 15)]), __uint_as_float(v[i >> 4][2 * (i & 15) + 1]));
+}
+// pack NP pairs to bf16 and store them as NP TMEM columns at dst (NP = 16 or 32)
+template <int NP>
+__device__ __forceinline__ void pack_storeN(uint32_t dst, const float2 (&v)[NP]) {
+#pragma unroll
+  for (int h = 0; h < NP / 16; ++h) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) pk[i] = pack2(v[16 * h + i].x, v[16 * h + i].y);
+    tmem_st16(dst + 16 * h, pk);
+  }
+  tmem_st_wait();
+}
 // pack 32 pairs to bf16 and store them as 32 TMEM columns at dst
 __device__ __forceinline__ void pack_store(uint32_t dst, const float2 (&v)[32]) {
   uint32_t pk[2][16];
@@ -152,12 +177,25 @@ __device__ __forceinline__ void pack_store(uint32_t dst, const float2 (&v)[32]) 
 // smem: K, V, Q ring [3], dO ring [2], lse/delta ring [2] = 226 KB: this needs the dynamic
 // shared-memory base to be 1024-aligned already (checked).
 constexpr int kQSlots = 3, kGSlots = 2;
+#ifndef CB_DKDV_GROUPS
+#define CB_DKDV_GROUPS 2
+#endif
+constexpr int kDkdvGroups = CB_DKDV_GROUPS;  // 2: 8 compute warps, 4: 16 compute warps
 constexpr int kSmemDkdv = (2 + kQSlots + kGSlots) * kTile + 2 * 1024 + 8 * 24;
 
 // TMEM column of the k-th K=16 step of a packed bf16 A operand written by the two halves
 __device__ __forceinline__ uint32_t packed_col(int k) { return (uint32_t)((k >> 2) * 64 + (k & 3) * 8); }
+// Same with NQ column groups of W = 128 / NQ query columns: group g packs P^T into
+// [g W, g W + W/2) and dS^T into [g W + W/2, (g + 1) W) of the dP^T region.
+template <int NQ>
+__device__ __forceinline__ uint32_t packed_colq(int k) {
+  constexpr int W = 128 / NQ;
+  return (uint32_t)((k * 16 / W) * W + ((k * 16) % W) / 2);
+}
 
-__global__ void __launch_bounds__(kThreads, 1)
+// NQ column groups -> 4 NQ compute warps (warps 4 .. 4 + 4 NQ), 128 + 128 NQ threads
+template <int NQ>
+__global__ void __launch_bounds__(128 + 128 * NQ, 1)
     dkdv_k(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmG, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -204,12 +242,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&g_full[s], 1);
       mbar_init(&g_empty[s], 1);
       mbar_init(&ld_full[s], 1);
-      mbar_init(&ld_empty[s], 8);
+      mbar_init(&ld_empty[s], 4 * NQ);
     }
     mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
-    mbar_init(s_free, 8);
-    mbar_init(pd_ready, 8);
+    mbar_init(s_free, 4 * NQ);
+    mbar_init(pd_ready, 4 * NQ);
     mbar_init(mma_done, 1);
     fence_mbar_init();
   }
@@ -317,11 +355,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < BT / 16; ++k)
-          umma_f16_ts(tmem + cV, tmem + cP + packed_col(k), mG + (uint64_t)(k * 128), id_acc, (u | k) != 0);
+          umma_f16_ts(tmem + cV, tmem + cP + packed_colq<NQ>(k), mG + (uint64_t)(k * 128), id_acc, (u | k) != 0);
         umma_commit(&g_empty[u & 1]);  // dO(u) is done (dP(u) and dV(u))
 #pragma unroll
         for (int k = 0; k < BT / 16; ++k)
-          umma_f16_ts(tmem + cK, tmem + cP + 32 + packed_col(k), mQ + (uint64_t)(k * 128), id_acc, (u | k) != 0);
+          umma_f16_ts(tmem + cK, tmem + cP + 64 / NQ + packed_colq<NQ>(k), mQ + (uint64_t)(k * 128), id_acc,
+                      (u | k) != 0);
         umma_commit(&q_empty[u % kQSlots]);
       }
       __syncwarp();
@@ -331,31 +370,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (elect_one()) umma_commit(mma_done);
     __syncwarp();
   } else if (warp >= 4) {
+    constexpr int W = 128 / NQ;  // query columns per compute warp
+    constexpr int NP = W / 2;    // column pairs
     const int q = warp & 3;
-    const int ch = (warp - 4) >> 2;  // query-column half of each tile
-    const int t = q * 32 + lane;     // key row inside the tile
+    const int grp = (warp - 4) >> 2;  // query-column group of each tile
+    const int t = q * 32 + lane;      // key row inside the tile
     const uint32_t lo = (uint32_t)(q * 32) << 16;
-    const uint32_t half = (uint32_t)ch * 64u;
+    const uint32_t col = (uint32_t)grp * W;
     const float c = p.scale * kLog2e;
     const float2 c2 = make_float2(c, c), nlog2e = make_float2(-kLog2e, -kLog2e);
     for (int u = 0; u < total; ++u) {
       mbar_wait(&ld_full[u & 1], (u >> 1) & 1);
-      const uint32_t sL = smem_u32(sLD + (u & 1) * 256 + ch * 64);  // lse; delta at +128 floats
+      const uint32_t sL = smem_u32(sLD + (u & 1) * 256 + grp * W);  // lse; delta at +128 floats
       mbar_wait(s_full, u & 1);
       tc_fence_after();
       if (warp == 4) BWD_TRACE(4, u);
-      float2 pr[32];
+      float2 pr[NP];
       {
-        uint32_t sv[2][32];
-        ld64(tmem + lo + cS + half, sv);
+        uint32_t sv[W / 32][32];
+        ldW<W>(tmem + lo + cS + col, sv);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(s_free);
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
+        for (int i = 0; i < NP; i += 2) {
           const float4 l4 = lds4(sL + 8 * i);
-          pr[i] = exp2_pair(ffma2(col2(sv, i), c2, fmul2(make_float2(l4.x, l4.y), nlog2e)), i);
-          pr[i + 1] = exp2_pair(ffma2(col2(sv, i + 1), c2, fmul2(make_float2(l4.z, l4.w), nlog2e)), i + 1);
+          pr[i] = exp2_pair(ffma2(colp(sv, i), c2, fmul2(make_float2(l4.x, l4.y), nlog2e)), i);
+          pr[i + 1] = exp2_pair(ffma2(colp(sv, i + 1), c2, fmul2(make_float2(l4.z, l4.w), nlog2e)), i + 1);
         }
       }
       if (warp == 4) BWD_TRACE(5, u);
@@ -363,17 +404,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       if (warp == 4) BWD_TRACE(6, u);
       {
-        uint32_t dv[2][32];
-        ld64(tmem + lo + cP + half, dv);
-        float2 ds[32];
+        uint32_t dv[W / 32][32];
+        ldW<W>(tmem + lo + cP + col, dv);
+        float2 ds[NP];
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
+        for (int i = 0; i < NP; i += 2) {
           const float4 d4 = lds4(sL + 512 + 8 * i);
-          ds[i] = fmul2(pr[i], ffma2(make_float2(d4.x, d4.y), make_float2(-1.f, -1.f), col2(dv, i)));
-          ds[i + 1] = fmul2(pr[i + 1], ffma2(make_float2(d4.z, d4.w), make_float2(-1.f, -1.f), col2(dv, i + 1)));
+          ds[i] = fmul2(pr[i], ffma2(make_float2(d4.x, d4.y), make_float2(-1.f, -1.f), colp(dv, i)));
+          ds[i + 1] = fmul2(pr[i + 1], ffma2(make_float2(d4.z, d4.w), make_float2(-1.f, -1.f), colp(dv, i + 1)));
         }
-        pack_store(tmem + lo + cP + half, pr);       // P^T over this half's dP^T columns
-        pack_store(tmem + lo + cP + half + 32, ds);  // dS^T next to it
+        pack_storeN<NP>(tmem + lo + cP + col, pr);       // P^T over this group's dP^T columns
+        pack_storeN<NP>(tmem + lo + cP + col + NP, ds);  // dS^T next to it
       }
       tc_fence_before();
       __syncwarp();
@@ -387,13 +428,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const int krow = k0 + t;
     const bool ok = krow < p.T;
-    if (ch == 0) {
-      const float* rc = p.rope_cos ? p.rope_cos + (int64_t)(ok ? krow : 0) * (HD / 2) : nullptr;
-      const float* rs = p.rope_sin ? p.rope_sin + (int64_t)(ok ? krow : 0) * (HD / 2) : nullptr;
-      store_row(tmem + lo + cK, p.o0 + ((int64_t)row0 + krow) * p.ld0 + (int64_t)kvh * HD, p.scale, ok, rc, rs, 4);
+    // the 256 output columns (dK | dV) split evenly over the NQ groups
+    constexpr int kCh = 8 / NQ;  // 32-column chunks per group
+    const int c0 = grp * kCh * 32;
+    if (c0 < 128) {
+      const float* rc = p.rope_cos ? p.rope_cos + (int64_t)(ok ? krow : 0) * (HD / 2) + c0 / 2 : nullptr;
+      const float* rs = p.rope_sin ? p.rope_sin + (int64_t)(ok ? krow : 0) * (HD / 2) + c0 / 2 : nullptr;
+      store_row(tmem + lo + cK + c0, p.o0 + ((int64_t)row0 + krow) * p.ld0 + (int64_t)kvh * HD + c0, p.scale, ok, rc,
+                rs, kCh);
     } else {
-      store_row(tmem + lo + cV, p.o1 + ((int64_t)row0 + krow) * p.ld1 + (int64_t)kvh * HD, 1.f, ok, nullptr,
-                nullptr, 4);
+      store_row(tmem + lo + cV + (c0 - 128), p.o1 + ((int64_t)row0 + krow) * p.ld1 + (int64_t)kvh * HD + (c0 - 128),
+                1.f, ok, nullptr, nullptr, kCh);
     }
   }
   tc_fence_before();
@@ -619,13 +664,14 @@ int attn_bwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, 
   if ((s = make_tmap_2d_bf16(&mg, dout, rows, (uint64_t)g.H * HD, lddo, 128, 64))) return s;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(dkdv_k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDkdv);
+    cudaFuncSetAttribute(dkdv_k<kDkdvGroups>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDkdv);
     cudaFuncSetAttribute(dq_k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDq);
     attr = true;
   }
   Params pk{g.T, g.H, g.KVH, g.B, g.scale, lse, delta, (__nv_bfloat16*)dk, lddk, (__nv_bfloat16*)dv, lddv,
             rope_cos, rope_sin};
-  dkdv_k<<<dim3((g.T + BT - 1) / BT, g.KVH, g.B), kThreads, kSmemDkdv, st>>>(mq, mk, mv, mg, pk);
+  dkdv_k<kDkdvGroups><<<dim3((g.T + BT - 1) / BT, g.KVH, g.B), 128 + 128 * kDkdvGroups, kSmemDkdv, st>>>(mq, mk, mv,
+                                                                                                      mg, pk);
   if (int e = check_launch("flash_bwd_dkdv_tc")) return e;
   Params pq{g.T, g.H, g.KVH, g.B, g.scale, lse, delta, (__nv_bfloat16*)dq, lddq, nullptr, 0, rope_cos, rope_sin};
   dq_k<<<dim3((g.T + BT - 1) / BT, g.H, g.B), kThreads, kSmemDq, st>>>(mq, mk, mv, mg, pq);
