@@ -41,7 +41,13 @@ constexpr int kTileBytes = 128 * 64 * 2;       // one [128 rows][64 cols] bf16 T
 constexpr int kQBytes = 2 * kTileBytes;        // one Q tile: two 64-column K-atoms
 constexpr int kKVBytes = 2 * kTileBytes;       // one K or V tile (two 64-column boxes)
 constexpr int kKSlots = 3, kVSlots = 2;        // K frees after S_B(j), V after PV_B(j)
-constexpr int kSmem = 2 * kQBytes + (kKSlots + kVSlots) * kKVBytes + 1024 + 256;
+// + barriers (256 B) + the row-max exchange buffer of the 2-warps-per-row softmax (2 KB).
+// This needs the dynamic shared-memory base to be 1024-aligned already (checked).
+constexpr int kSmem = 2 * kQBytes + (kKSlots + kVSlots) * kKVBytes + 256 + 2048;
+#ifndef CB_ATTN_FWD_NH
+#define CB_ATTN_FWD_NH 1
+#endif
+constexpr int kFwdNH = CB_ATTN_FWD_NH;  // softmax warps per query row (1 or 2)
 constexpr uint32_t kTmemCols = 512;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -63,17 +69,23 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+// NH softmax warps per query row: warps 4 .. 4 + 8 NH, 128 + 256 NH threads.  With NH = 2
+// the two warps of a TMEM lane quadrant split each S row into column halves and exchange
+// their row maxima through shared memory (named barrier per warp pair).
+template <int NH>
+__global__ void __launch_bounds__(128 + 256 * NH, 1)
     fwd_tc_k(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
              const __grid_constant__ CUtensorMap tmV, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw;
+  if (smem_u32(smem) & 1023) __trap();  // see kSmem
   uint8_t* sQ = smem;  // [2 tiles][kQBytes]
   uint8_t* sK = smem + 2 * kQBytes;    // [kKSlots]
   uint8_t* sV = sK + kKSlots * kKVBytes;  // [kVSlots]
@@ -87,6 +99,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* p_ready = bars + 13;  // [2] tiles
   uint64_t* o_done = bars + 15;   // [2] tiles
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  float* red = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [2 tiles][2 halves][128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -108,7 +121,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_ready[s], 4);
+      mbar_init(&p_ready[s], 4 * NH);
       mbar_init(&o_done[s], 1);
     }
     fence_mbar_init();
@@ -210,13 +223,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    const int x = (warp - 4) >> 2;  // query tile
-    const int q = warp & 3;         // TMEM lane quadrant
+    constexpr int W = BN / NH;  // S columns per warp
+    const int x = (warp - 4) / (4 * NH);   // query tile
+    const int wi = (warp - 4) % (4 * NH);
+    const int q = wi & 3;                  // TMEM lane quadrant
+    const int hf = wi >> 2;                // column half (NH = 2)
     const int row = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const uint32_t scol = tmem + lane_off + x * 128u;
-    const uint32_t ocol = tmem + lane_off + 256u + x * 128u;
+    const uint32_t ocol = tmem + lane_off + 256u + x * 128u + hf * (HD / NH);
     const float c = p.scale * kLog2e;
+    float* myred = red + (x * 2 + hf) * 128 + row;
+    const float* partred = red + (x * 2 + (hf ^ 1)) * 128 + row;
+    const int bar_id = 1 + x * 4 + q;
     float m_used = -INFINITY, l = 0.f;
     // one K/V block of the online softmax; kRagged (the last block when T % 128 != 0) masks
     // the columns past T — a separate instantiation keeps the masking out of the hot loop
@@ -224,43 +243,51 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr bool kRagged = decltype(ragged)::value;
       mbar_wait(&s_full[x], j & 1);
       tc_fence_after();
-      if (q == 0 && lane == 0) ATTN_TRACE(4 + 3 * x, j);
-      // the whole S row (128 f32) in registers: four loads in flight, one wait
-      const int valid = min(BN, p.T - j * BN);
-      uint32_t sv[4][32];
+      if (wi == 0 && lane == 0) ATTN_TRACE(4 + 3 * x, j);
+      // this warp's W columns of the S row in registers: loads in flight, one wait
+      const int valid = min(BN, p.T - j * BN) - hf * W;
+      uint32_t sv[W / 32][32];
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) tmem_ld32(scol + cc * 32, sv[cc]);
+      for (int cc = 0; cc < W / 32; ++cc) tmem_ld32(scol + hf * W + cc * 32, sv[cc]);
       tmem_ld_wait_regs(sv[0]);
-      reg_fence(sv[1]);
-      reg_fence(sv[2]);
-      reg_fence(sv[3]);
+#pragma unroll
+      for (int cc = 1; cc < W / 32; ++cc) reg_fence(sv[cc]);
       if (kRagged) {  // columns past T take no part
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc)
+        for (int cc = 0; cc < W / 32; ++cc)
 #pragma unroll
           for (int i = 0; i < 32; ++i)
             if (cc * 32 + i >= valid) sv[cc][i] = __float_as_uint(-INFINITY);
       }
       float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc)
+      for (int cc = 0; cc < W / 32; ++cc)
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
           mx0 = fmaxf(mx0, fmaxf(__uint_as_float(sv[cc][i]), __uint_as_float(sv[cc][i + 1])));
           mx1 = fmaxf(mx1, fmaxf(__uint_as_float(sv[cc][i + 2]), __uint_as_float(sv[cc][i + 3])));
         }
-      const float mx = fmaxf(mx0, mx1) * c;
-      if (q == 0 && lane == 0) ATTN_TRACE(5 + 3 * x, j);
-      const bool need = mx > m_used + kRescaleThreshold;
+      float mx = fmaxf(mx0, mx1) * c;
+      if (NH == 2) {
+        // row max across the two halves; the first barrier keeps this write after the
+        // partner's read of the previous block, the second publishes it (and orders both
+        // warps' S loads before either overwrites columns with packed P)
+        named_bar(bar_id, 64);
+        *myred = mx;
+        named_bar(bar_id, 64);
+        mx = fmaxf(mx, *partred);
+      }
+      if (wi == 0 && lane == 0) ATTN_TRACE(5 + 3 * x, j);
+      const bool need = mx > m_used + kRescaleThreshold;  // same decision in both halves
       const float m_prev = m_used;
       if (need) m_used = mx;
-      // P = exp2(S c - m) packed to bf16 pairs into the first 64 columns of S.  Pair
-      // arithmetic (FFMA2/FADD2); kEmuPairs of every 8 pairs take the polynomial exp2 on the
-      // FMA pipe so the MUFU (16 ex2/clk/SM) stops being the bound.
+      // P = exp2(S c - m) packed to bf16 pairs: this warp's W columns -> packed columns
+      // [hf W/2, (hf+1) W/2) of the S region.  Pair arithmetic (FFMA2/FADD2); kEmuPairs of
+      // every 8 pairs take the polynomial exp2 on the FMA pipe.
       const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_used, -m_used);
       float2 rsa = make_float2(0.f, 0.f), rsb = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
+      for (int cc = 0; cc < W / 32; ++cc) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -278,18 +305,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             rsa = fadd2(rsa, e);
           pk[i] = pack2(e.x, e.y);
         }
-        tmem_st16(scol + cc * 16, pk);
+        tmem_st16(scol + hf * (W / 2) + cc * 16, pk);
       }
       const float rs = (rsa.x + rsa.y) + (rsb.x + rsb.y);
       // lazy rescale of O (after the exponentials, when the S row is no longer live): only
-      // when some row's max grew past the threshold; PV_j has not been issued yet
+      // when some row's max grew past the threshold; PV_j has not been issued yet.  Each
+      // warp rescales its HD / NH output columns.
       if (__any_sync(0xffffffffu, need)) {
         const float corr = need ? fast_exp2(m_prev - m_used) : 1.f;
         if (j > 0) {
           mbar_wait(&o_done[x], (j - 1) & 1);  // PV_{j-1} has finished writing O
           tc_fence_after();
 #pragma unroll 1
-          for (int cc = 0; cc < HD / 32; ++cc) {
+          for (int cc = 0; cc < HD / NH / 32; ++cc) {
             uint32_t o[32];
             tmem_ld32(ocol + cc * 32, o);
             tmem_ld_wait_regs(o);
@@ -304,20 +332,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (q == 0 && lane == 0) ATTN_TRACE(6 + 3 * x, j);
+      if (wi == 0 && lane == 0) ATTN_TRACE(6 + 3 * x, j);
       if (lane == 0) mbar_arrive(&p_ready[x]);
     };
     const int nfull = p.T / BN;
     for (int j = 0; j < nfull; ++j) block(j, std::false_type{});
     if (nfull < nblk) block(nfull, std::true_type{});
-    // epilogue
+    // epilogue: the row sum is the sum of the halves' partial sums
+    if (NH == 2) {
+      named_bar(bar_id, 64);
+      *myred = l;
+      named_bar(bar_id, 64);
+      l += *partred;
+    }
     mbar_wait(&o_done[x], (nblk - 1) & 1);
     tc_fence_after();
     const int qrow = q0 + x * BM + row;
     const float inv = 1.f / l;
-    __nv_bfloat16* orow = p.o + ((int64_t)row0 + qrow) * p.ldo + (int64_t)h * HD;
+    __nv_bfloat16* orow = p.o + ((int64_t)row0 + qrow) * p.ldo + (int64_t)h * HD + hf * (HD / NH);
 #pragma unroll 1
-    for (int cc = 0; cc < HD / 32; ++cc) {
+    for (int cc = 0; cc < HD / NH / 32; ++cc) {
       uint32_t o[32];
       tmem_ld32(ocol + cc * 32, o);
       tmem_ld_wait();
@@ -334,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if (qrow < p.T) p.lse[((int64_t)b * p.H + h) * p.T + qrow] = (m_used + log2f(l)) * kLn2;
+    if (qrow < p.T && hf == 0) p.lse[((int64_t)b * p.H + h) * p.T + qrow] = (m_used + log2f(l)) * kLn2;
   }
   tc_fence_before();
   __syncthreads();
@@ -365,12 +399,12 @@ int attn_fwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, 
   if ((s = make_tmap_2d_bf16(&mv, v, rows, (uint64_t)g.KVH * HD, g.ldv, 128, 64))) return s;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(fwd_tc_k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(fwd_tc_k<kFwdNH>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     attr = true;
   }
   Params p{g.T, g.H, g.KVH, g.B, g.scale, (__nv_bfloat16*)o, g.ldo, lse};
   dim3 grid((g.T + 2 * BM - 1) / (2 * BM), g.H, g.B);
-  fwd_tc_k<<<grid, kThreads, kSmem, st>>>(mq, mk, mv, p);
+  fwd_tc_k<kFwdNH><<<grid, 128 + 256 * kFwdNH, kSmem, st>>>(mq, mk, mv, p);
   return check_launch("flash_fwd_tc");
 }
 
