@@ -24,6 +24,8 @@ PyTorch arithmetic, only C-ABI kernel launches.  PyTorch provides memory, stream
 
 from __future__ import annotations
 
+import os
+
 import math
 import re
 from dataclasses import dataclass, field
@@ -216,7 +218,10 @@ class TrainEngine:
         self.d = _Dist(group)
         self.buckets = build_layout(self.module)
         self._alloc()
-        ops.ensure_gemm_workspace(self.device)
+        # split-K is opt-in: measured on the 1B and MoE steps its partial round trip cost
+        # more than the wave-quantization time it recovers (CB_GEMM_SPLITK=1 enables it)
+        if os.environ.get("CB_GEMM_SPLITK", "0") == "1":
+            ops.ensure_gemm_workspace(self.device)
         self.options = {"precision": self.precision, "validate_ids": False}
         if self.d.world > 1:  # summaries that are global-batch statistics reduce over this group
             self.options["dp_group"] = self.d.group if self.d.group is not None else self.d.dist.group.WORLD
