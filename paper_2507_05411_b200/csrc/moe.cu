@@ -1,7 +1,8 @@
 // Mixture-of-experts routing, dispatch and combine (reference layers.py:422-533).
 //
 //  cb_moe_route     probs = softmax(x @ router) computed in f64 per token (one warp per
-//                   token, lane e owns expert e), stable top-k by (prob desc, id asc) —
+//                   token: for E <= 8 every lane accumulates all experts over a column
+//                   slice, lanes summed in a fixed order), stable top-k by (prob desc, id asc) —
 //                   exactly argsort(-probs, kind="stable")[:k] (layers.py:437) — and the
 //                   renormalized gate weights picked/sum(picked) (layers.py:440).  Router
 //                   inputs that are bit-identical to the reference's give bit-identical
@@ -11,6 +12,8 @@
 //  cb_gather_rows   dispatch: rows of x into expert-sorted order (perm from cb_sort_ids).
 //  cb_moe_combine   out[t] = sum_slot w[t,slot] * y[pos(t,slot)] in slot order (layers.py:529-531).
 //  cb_moe_combine_bwd / cb_moe_router_bwd: the reverse of combine, renormalization and softmax.
+#include <algorithm>
+
 #include "common.cuh"
 #include "composer_b200.h"
 
@@ -67,6 +70,97 @@ __global__ void __launch_bounds__(128) moe_route_k(int64_t n, int d, int E, int 
     for (int j = 0; j < k; ++j) {
       idx[t * k + j] = pid[j];
       w[t * k + j] = (float)(picked[j] / psum);
+    }
+  }
+}
+
+// E <= 8 experts, bf16 x: the router matrix staged once per CTA in shared memory (f32,
+// zero-padded to 8 experts, split into two [d] float4 planes), one warp per token with every lane accumulating all experts over
+// its columns (stride 32), lanes summed by a fixed-order f64 butterfly; softmax / stable
+// top-k / renormalisation as moe_route_k.  Grid-stride over tokens.
+constexpr int kRouteWarps = 8;
+__global__ void __launch_bounds__(kRouteWarps * 32) moe_route8_k(int64_t n, int d, int E, int k,
+                                                                  const __nv_bfloat16* __restrict__ x, int64_t ldx,
+                                                                  const float* __restrict__ router,
+                                                                  int32_t* __restrict__ idx, float* __restrict__ w,
+                                                                  float* __restrict__ probs) {
+  extern __shared__ float4 rsm4[];  // [2][d] float4: experts 0-3 of column c, then experts 4-7
+  float* rsm = reinterpret_cast<float*>(rsm4);
+  for (int i = threadIdx.x; i < d * 8; i += blockDim.x) {
+    const int c = i >> 3, e = i & 7;
+    rsm[(e >> 2) * d * 4 + c * 4 + (e & 3)] = e < E ? router[(int64_t)c * E + e] : 0.f;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t t = (int64_t)blockIdx.x * kRouteWarps + warp; t < n; t += (int64_t)gridDim.x * kRouteWarps) {
+    const __nv_bfloat16* xr = x + t * ldx;
+    double acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+    // lane l takes columns l, l + 32, ... so a warp reads 32 consecutive router rows (1 KB,
+    // bank-conflict free) per step
+#pragma unroll 4
+    for (int c = lane; c < d; c += 32) {
+      {
+        const float4 r0 = rsm4[c], r1 = rsm4[d + c];
+        const double xd = (double)__bfloat162float(xr[c]);
+        acc[0] = fma(xd, (double)r0.x, acc[0]);
+        acc[1] = fma(xd, (double)r0.y, acc[1]);
+        acc[2] = fma(xd, (double)r0.z, acc[2]);
+        acc[3] = fma(xd, (double)r0.w, acc[3]);
+        acc[4] = fma(xd, (double)r1.x, acc[4]);
+        acc[5] = fma(xd, (double)r1.y, acc[5]);
+        acc[6] = fma(xd, (double)r1.z, acc[6]);
+        acc[7] = fma(xd, (double)r1.w, acc[7]);
+      }
+    }
+    double logit = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+      if (lane == e && e < E) logit = acc[e];
+    }
+    double mx = logit;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const double ex = lane < E ? exp(logit - mx) : 0.0;
+    double sum = ex;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const double pr = ex / sum;
+    if (lane < E) probs[t * E + lane] = (float)pr;
+    // stable top-k: repeatedly take (max prob, lowest id); k <= 8
+    bool taken = lane >= E;
+    double picked[8];
+    int pid[8];
+    double psum = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j >= k) break;
+      double bv = taken ? -1.0 : pr;
+      int bi = taken ? 1 << 30 : lane;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (lane == bi) taken = true;
+      picked[j] = bv;
+      pid[j] = bi;
+      psum += bv;
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j >= k) break;
+        idx[t * k + j] = pid[j];
+        w[t * k + j] = (float)(picked[j] / psum);
+      }
     }
   }
 }
@@ -195,6 +289,20 @@ extern "C" int cb_moe_route(int64_t n, int dim, int experts, int top_k, const vo
   if (top_k < 1 || top_k > experts) return fail(CB_ERR_SHAPE, "top_k=%d must lie in [1, %d]", top_k, experts);
   if (n <= 0) return CB_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  const size_t rsm_bytes = (size_t)dim * 8 * sizeof(float);
+  if (x_dtype == CB_DT_BF16 && experts <= 8 && dim % 8 == 0 && ldx % 8 == 0 &&
+      (reinterpret_cast<uintptr_t>(x) & 15) == 0 && rsm_bytes <= 200 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(moe_route8_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    const int64_t need = (n + kRouteWarps - 1) / kRouteWarps;
+    const int blocks8 = (int)std::min<int64_t>(need, 2 * kNumSMs);
+    moe_route8_k<<<blocks8, kRouteWarps * 32, rsm_bytes, st>>>(n, dim, experts, top_k, (const __nv_bfloat16*)x, ldx,
+                                                               router, idx, weights, probs);
+    return check_launch("moe_route8");
+  }
   const int blocks = (int)((n + 3) / 4);
   if (x_dtype == CB_DT_F32)
     moe_route_k<float><<<blocks, 128, 0, st>>>(n, dim, experts, top_k, (const float*)x, ldx, router, idx, weights, probs);
@@ -260,46 +368,75 @@ extern "C" int cb_moe_router_bwd(int64_t n, int experts, int top_k, const float*
 // Router backward products, E <= 32 experts (tiny N/K that GEMM tiles waste):
 //   partial[blk][c*E + e] = sum_{t in blk's tokens} x[t][c] * dlog[t][e]   (then col-reduce)
 //   dx[t][c] += sum_e dlog[t][e] * router[c][e]
-template <typename TX>
+// NE: compile-time expert bound (8 or kMaxExperts) so the per-expert loops unroll to E.
+template <typename TX, int NE>
 __global__ void __launch_bounds__(256) router_wgrad_k(int64_t n, int d, int E, int tok_per_blk,
                                                       const TX* __restrict__ x, int64_t ldx,
                                                       const float* __restrict__ dlog, float* __restrict__ partial) {
-  __shared__ float sg[64][kMaxExperts];
+  __shared__ __align__(16) float sg[64][NE];
   const int64_t t0 = (int64_t)blockIdx.x * tok_per_blk;
   const int64_t t1 = min(n, t0 + tok_per_blk);
   const int c0 = blockIdx.y * 256 + threadIdx.x;  // this thread's column
-  float acc[kMaxExperts];
+  float acc[NE];
 #pragma unroll
-  for (int e = 0; e < kMaxExperts; ++e) acc[e] = 0.f;
+  for (int e = 0; e < NE; ++e) acc[e] = 0.f;
   for (int64_t tb = t0; tb < t1; tb += 64) {
     const int cnt = (int)(t1 - tb < 64 ? t1 - tb : 64);
     __syncthreads();
-    for (int i = threadIdx.x; i < cnt * E; i += blockDim.x) sg[i / E][i % E] = dlog[(tb + i / E) * E + i % E];
+    for (int i = threadIdx.x; i < 64 * NE; i += blockDim.x) {
+      const int j = i / NE, e = i % NE;
+      sg[j][e] = (j < cnt && e < E) ? dlog[(tb + j) * E + e] : 0.f;
+    }
     __syncthreads();
     if (c0 < d) {
+#pragma unroll 4
       for (int j = 0; j < cnt; ++j) {
         const float xv = to_f32(x[(tb + j) * ldx + c0]);
 #pragma unroll
-        for (int e = 0; e < kMaxExperts; ++e)
-          if (e < E) acc[e] = fmaf(xv, sg[j][e], acc[e]);
+        for (int e = 0; e < NE; e += 4) {
+          const float4 g = *reinterpret_cast<const float4*>(&sg[j][e]);
+          acc[e] = fmaf(xv, g.x, acc[e]);
+          acc[e + 1] = fmaf(xv, g.y, acc[e + 1]);
+          acc[e + 2] = fmaf(xv, g.z, acc[e + 2]);
+          acc[e + 3] = fmaf(xv, g.w, acc[e + 3]);
+        }
       }
     }
   }
   if (c0 < d) {
     float* pr = partial + (int64_t)blockIdx.x * d * E + (int64_t)c0 * E;
-    for (int e = 0; e < E; ++e) pr[e] = acc[e];
+#pragma unroll
+    for (int e = 0; e < NE; ++e)
+      if (e < E) pr[e] = acc[e];
   }
 }
 
+template <int NE>
 __global__ void __launch_bounds__(256) router_dx_k(int64_t n, int d, int E, const float* __restrict__ dlog,
                                                    const float* __restrict__ router, float* __restrict__ dx,
                                                    int64_t lddx) {
   const int64_t t = blockIdx.x;
-  float g[kMaxExperts];
-  for (int e = 0; e < E; ++e) g[e] = dlog[t * E + e];
+  float g[NE];
+#pragma unroll
+  for (int e = 0; e < NE; ++e) g[e] = e < E ? dlog[t * E + e] : 0.f;
   for (int c = threadIdx.x; c < d; c += blockDim.x) {
     float s = 0.f;
-    for (int e = 0; e < E; ++e) s = fmaf(g[e], router[(int64_t)c * E + e], s);
+    if (NE == 8 && E == 8) {  // one 32-byte router row
+      const float4 r0 = *reinterpret_cast<const float4*>(router + (int64_t)c * 8);
+      const float4 r1 = *reinterpret_cast<const float4*>(router + (int64_t)c * 8 + 4);
+      s = fmaf(g[0], r0.x, s);
+      s = fmaf(g[1], r0.y, s);
+      s = fmaf(g[2], r0.z, s);
+      s = fmaf(g[3], r0.w, s);
+      s = fmaf(g[4], r1.x, s);
+      s = fmaf(g[5], r1.y, s);
+      s = fmaf(g[6], r1.z, s);
+      s = fmaf(g[7], r1.w, s);
+    } else {
+#pragma unroll
+      for (int e = 0; e < NE; ++e)
+        if (e < E) s = fmaf(g[e], router[(int64_t)c * E + e], s);
+    }
     dx[t * lddx + c] += s;
   }
 }
@@ -339,13 +476,28 @@ extern "C" int cb_moe_router_bwd_gemms(int64_t n, int dim, int experts, const vo
   const int tpb = 512;
   const int nblk = (int)((n + tpb - 1) / tpb);
   dim3 grid(nblk, (dim + 255) / 256);
-  if (x_dtype == CB_DT_F32)
-    router_wgrad_k<float><<<grid, 256, 0, st>>>(n, dim, experts, tpb, (const float*)x, ldx, dlogits, workspace);
-  else
-    router_wgrad_k<__nv_bfloat16><<<grid, 256, 0, st>>>(n, dim, experts, tpb, (const __nv_bfloat16*)x, ldx, dlogits,
-                                                        workspace);
+  const bool small = experts <= 8;
+  if (x_dtype == CB_DT_F32) {
+    if (small)
+      router_wgrad_k<float, 8><<<grid, 256, 0, st>>>(n, dim, experts, tpb, (const float*)x, ldx, dlogits, workspace);
+    else
+      router_wgrad_k<float, kMaxExperts><<<grid, 256, 0, st>>>(n, dim, experts, tpb, (const float*)x, ldx, dlogits,
+                                                               workspace);
+  } else {
+    if (small)
+      router_wgrad_k<__nv_bfloat16, 8><<<grid, 256, 0, st>>>(n, dim, experts, tpb, (const __nv_bfloat16*)x, ldx,
+                                                             dlogits, workspace);
+    else
+      router_wgrad_k<__nv_bfloat16, kMaxExperts><<<grid, 256, 0, st>>>(n, dim, experts, tpb,
+                                                                       (const __nv_bfloat16*)x, ldx, dlogits,
+                                                                       workspace);
+  }
   if (int s = check_launch("moe_router_wgrad")) return s;
   if (int s = cb_col_reduce(nblk, dim * experts, workspace, drouter, 1, stream)) return s;
-  router_dx_k<<<(int)n, 256, 0, st>>>(n, dim, experts, dlogits, router, dx, lddx);
+  const bool vec = experts == 8 && (reinterpret_cast<uintptr_t>(router) & 15) == 0;
+  if (vec)
+    router_dx_k<8><<<(int)n, 256, 0, st>>>(n, dim, experts, dlogits, router, dx, lddx);
+  else
+    router_dx_k<kMaxExperts><<<(int)n, 256, 0, st>>>(n, dim, experts, dlogits, router, dx, lddx);
   return check_launch("moe_router_dx");
 }

@@ -125,17 +125,19 @@ def build_layout(module: Module) -> list[Bucket]:
         fuse = None
         if mod.kind in ("Attention", "GroupedQueryAttention") and {"wq", "wk", "wv"} <= set(names):
             fuse = ["wq", "wk", "wv"]
-        elif mod.kind == "FeedForward" and {"w1", "w1_gate"} <= set(names):
+        elif mod.kind in ("FeedForward", "MoE") and {"w1", "w1_gate"} <= set(names):
+            # gate and up projections side by side ([.., d, 2h]; per expert for MoE): one wide
+            # GEMM with the gated activation in its epilogue
             fuse = ["w1", "w1_gate"]
         done = set()
         if fuse:
-            rows = names[fuse[0]][0]
-            width = sum(names[n][1] for n in fuse)
+            rows = int(np.prod(names[fuse[0]][:-1]))
+            width = sum(names[n][-1] for n in fuse)
             off = b.numel
             col = 0
             for n in fuse:
                 b.entries.append(Entry(path, n, tuple(names[n]), off, col, width, mod.kind))
-                col += names[n][1]
+                col += names[n][-1]
                 done.add(n)
             b.numel = _align(off + rows * width)
         for pname, shape in plist:
@@ -149,10 +151,19 @@ def build_layout(module: Module) -> list[Bucket]:
     return [b for b in out if b.entries]
 
 
+def _rc(e: Entry) -> tuple[int, int]:
+    """(rows, cols) of an entry seen as a row-major matrix (leading dims folded into rows)."""
+    return int(np.prod(e.shape[:-1])), int(e.shape[-1])
+
+
 def _view(buf: torch.Tensor, e: Entry) -> torch.Tensor:
     if e.ld:
-        rows, cols = e.shape
-        return buf.as_strided((rows, cols), (e.ld, 1), buf.storage_offset() + e.offset + e.col0)
+        # column block of a fused group: row stride ld; a leading expert dim folds into rows
+        strides, acc = [1], e.ld
+        for dim in reversed(e.shape[:-1]):
+            strides.insert(0, acc)
+            acc *= dim
+        return buf.as_strided(tuple(e.shape), tuple(strides), buf.storage_offset() + e.offset + e.col0)
     n = int(np.prod(e.shape))
     return buf[e.offset:e.offset + n].view(e.shape)
 
@@ -222,7 +233,8 @@ class TrainEngine:
         # more than the wave-quantization time it recovers (CB_GEMM_SPLITK=1 enables it)
         if os.environ.get("CB_GEMM_SPLITK", "0") == "1":
             ops.ensure_gemm_workspace(self.device)
-        self.options = {"precision": self.precision, "validate_ids": False}
+        self.options = {"precision": self.precision, "validate_ids": False,
+                        "fuse_glu": os.environ.get("CB_FUSE_GLU", "1") != "0"}
         if self.d.world > 1:  # summaries that are global-batch statistics reduce over this group
             self.options["dp_group"] = self.d.group if self.d.group is not None else self.d.dist.group.WORLD
         if init:
@@ -272,9 +284,9 @@ class TrainEngine:
             if tuple(arr.shape) != tuple(e.shape):
                 raise ShapeError(f"{e.path}.{e.name}: shape {arr.shape} != {e.shape}")
             if e.ld:
-                rows, cols = e.shape
+                rows, cols = _rc(e)
                 blk = host[e.offset:e.offset + rows * e.ld].reshape(rows, e.ld)
-                blk[:, e.col0:e.col0 + cols] = arr
+                blk[:, e.col0:e.col0 + cols] = arr.reshape(rows, cols)
             else:
                 host[e.offset:e.offset + arr.size] = arr.reshape(-1)
         r0 = 0 if b.replicated else self.d.rank * rec["shard"]
@@ -370,8 +382,9 @@ class TrainEngine:
                 for e in b.entries:
                     arr = np.asarray(_tree_get(tree, e.path, e.name), dtype=np.float64)
                     if e.ld:
-                        rows, cols = e.shape
-                        host[e.offset:e.offset + rows * e.ld].reshape(rows, e.ld)[:, e.col0:e.col0 + cols] = arr
+                        rows, cols = _rc(e)
+                        host[e.offset:e.offset + rows * e.ld].reshape(rows, e.ld)[:, e.col0:e.col0 + cols] = \
+                            arr.reshape(rows, cols)
                     else:
                         host[e.offset:e.offset + arr.size] = arr.reshape(-1)
                 r0 = 0 if b.replicated else self.d.rank * rec["shard"]
@@ -398,8 +411,9 @@ class TrainEngine:
             host = src.float().cpu().numpy().astype(np.float64)
             for e in b.entries:
                 if e.ld:
-                    rows, cols = e.shape
-                    arr = host[e.offset:e.offset + rows * e.ld].reshape(rows, e.ld)[:, e.col0:e.col0 + cols].copy()
+                    rows, cols = _rc(e)
+                    arr = host[e.offset:e.offset + rows * e.ld].reshape(rows, e.ld)[:, e.col0:e.col0 + cols]
+                    arr = arr.copy().reshape(e.shape)
                 else:
                     arr = host[e.offset:e.offset + int(np.prod(e.shape))].reshape(e.shape).copy()
                 _tree_set(out, e.path, e.name, arr)

@@ -138,18 +138,28 @@ class MoEBehavior(Behavior):
         pre = torch.empty((n * k, width), device=dev, dtype=adt)
         hid = torch.empty((n * k, h), device=dev, dtype=adt)
         ye = torch.empty((n * k, d), device=dev, dtype=torch.float32)
+        hid = torch.empty((n * k, h), device=dev, dtype=adt)
+        fused_all = pair is not None and L.option("fuse_glu", True)
+        unfused = []
         for e in range(E):
             r0, r1 = int(off[e]), int(off[e + 1])
             if r1 == r0:
                 continue
             xs = xe[r0:r1]
+            wcat = L.fused_columns(w1[e], wg[e]) if fused_all else None
+            # gate / up GEMM with the gated activation in its epilogue (rows of expert e)
+            if wcat is not None and ops.gemm_gated_fwd(xs, wcat, pair[0], pair[1], pre=pre[r0:r1],
+                                                       hidden=hid[r0:r1]) is not None:
+                continue
             ops.gemm(xs, w1[e], pre[r0:r1, :h])
             if pair:
                 ops.gemm(xs, wg[e], pre[r0:r1, h:])
-        if pair:
-            hid = ops.act_fwd(pre[:, :h], pre[:, h:], pair[0], pair[1])
-        else:
-            hid = ops.act_fwd(pre, None, cfg.get("activation"))
+            unfused.append((r0, r1))
+        for r0, r1 in unfused:
+            if pair:
+                ops.act_fwd(pre[r0:r1, :h], pre[r0:r1, h:], pair[0], pair[1], out=hid[r0:r1])
+            else:
+                ops.act_fwd(pre[r0:r1], None, cfg.get("activation"), out=hid[r0:r1])
         for e in range(E):
             r0, r1 = int(off[e]), int(off[e + 1])
             if r1 > r0:
@@ -181,18 +191,26 @@ class MoEBehavior(Behavior):
         wg = param("w1_gate") if pair else None
         gwg = param_grad("w1_gate") if pair else None
         off, pre, hid, xe = s["off"], s["pre"], s["hid"], s["xe"]
-        dhid = torch.empty_like(hid)
+        dpre = torch.empty_like(pre)
+        dhid = None
+        fuse = pair is not None and L.option("fuse_glu", True)
         for e in range(E):
             r0, r1 = int(off[e]), int(off[e + 1])
             if r1 == r0:
                 continue
             ops.gemm(hid[r0:r1], dye[r0:r1], gw2[e], trans_a=True, accumulate=True)
+            # dhidden = dye @ w2^T consumed by the gated-activation backward in the epilogue
+            if fuse and ops.gemm_gated_bwd(dye[r0:r1], w2[e], pre[r0:r1], pair[0], pair[1],
+                                           dpre=dpre[r0:r1]) is not None:
+                continue
+            if dhid is None:
+                dhid = torch.empty_like(hid)
             ops.gemm(dye[r0:r1], w2[e], dhid[r0:r1], trans_b=True)
-        dpre = torch.empty_like(pre)
-        if pair:
-            ops.act_bwd(pre[:, :h], pre[:, h:], dhid, dpre[:, :h], dpre[:, h:], pair[0], pair[1])
-        else:
-            ops.act_bwd(pre, None, dhid, dpre, None, cfg.get("activation"))
+            if pair:
+                ops.act_bwd(pre[r0:r1, :h], pre[r0:r1, h:], dhid[r0:r1], dpre[r0:r1, :h], dpre[r0:r1, h:], pair[0],
+                            pair[1])
+            else:
+                ops.act_bwd(pre[r0:r1], None, dhid[r0:r1], dpre[r0:r1], None, cfg.get("activation"))
         dxe = torch.empty((n * k, d), device=dev, dtype=torch.float32)
         for e in range(E):
             r0, r1 = int(off[e]), int(off[e + 1])

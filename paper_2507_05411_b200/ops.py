@@ -127,31 +127,36 @@ def gemm_rope(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, seq_len: int,
     return out
 
 
-def gemm_gated_fwd(x2: torch.Tensor, wcat: torch.Tensor, act0: str, act1: str):
+def gemm_gated_fwd(x2: torch.Tensor, wcat: torch.Tensor, act0: str, act1: str, pre=None, hidden=None):
     """pre = x2 @ wcat and hidden = act0(pre[:, :H]) * act1(pre[:, H:]) from one CTA-pair GEMM
-    (activation in the epilogue).  Returns (pre, hidden), or None when the fused form does
-    not apply (the caller then runs gemm + act_fwd)."""
+    (activation in the epilogue), into `pre` / `hidden` when given.  Returns (pre, hidden),
+    or None when the fused form does not apply (the caller then runs gemm + act_fwd)."""
     M, K = x2.shape
     if x2.dtype != torch.bfloat16 or wcat.dtype != torch.bfloat16 or wcat.shape[0] != K or wcat.shape[1] % 2:
         return None
     H = wcat.shape[1] // 2
-    pre = torch.empty((M, 2 * H), device=x2.device, dtype=torch.bfloat16)
-    hidden = torch.empty((M, H), device=x2.device, dtype=torch.bfloat16)
+    if pre is None:
+        pre = torch.empty((M, 2 * H), device=x2.device, dtype=torch.bfloat16)
+    if hidden is None:
+        hidden = torch.empty((M, H), device=x2.device, dtype=torch.bfloat16)
+    if tuple(pre.shape) != (M, 2 * H) or tuple(hidden.shape) != (M, H):
+        raise ShapeError("gemm_gated_fwd: output shape mismatch")
     ok = _profiled("gemm_bf16", 2 * M * 2 * H * K, _lib.try_call, "cb_gemm_gated_fwd", M, H, K, x2.data_ptr(),
                    ld(x2, "A"), 0, wcat.data_ptr(), ld(wcat, "B"), 0, pre.data_ptr(), ld(pre), hidden.data_ptr(),
                    ld(hidden), ACT_IDS[act0], ACT_IDS[act1], stream_ptr())
     return (pre, hidden) if ok else None
 
 
-def gemm_gated_bwd(dy: torch.Tensor, w2: torch.Tensor, pre: torch.Tensor, act0: str, act1: str):
+def gemm_gated_bwd(dy: torch.Tensor, w2: torch.Tensor, pre: torch.Tensor, act0: str, act1: str, dpre=None):
     """dpre = d/d(pre) of act0(a) * act1(g) given d(out) = dy and out = hidden @ w2, with
-    dhidden = dy @ w2^T formed and consumed inside one CTA-pair GEMM.  None when the fused
-    form does not apply."""
+    dhidden = dy @ w2^T formed and consumed inside one CTA-pair GEMM (into `dpre` when
+    given).  None when the fused form does not apply."""
     M, K = dy.shape
     H = w2.shape[0]
     if dy.dtype != torch.bfloat16 or w2.dtype != torch.bfloat16 or w2.shape[1] != K or pre.shape != (M, 2 * H):
         return None
-    dpre = torch.empty_like(pre)
+    if dpre is None:
+        dpre = torch.empty_like(pre)
     ok = _profiled("gemm_bf16", 2 * M * H * K, _lib.try_call, "cb_gemm_gated_bwd", M, H, K, dy.data_ptr(),
                    ld(dy, "A"), 0, w2.data_ptr(), ld(w2, "B"), 1, pre.data_ptr(), ld(pre), dpre.data_ptr(),
                    ld(dpre), ACT_IDS[act0], ACT_IDS[act1], stream_ptr())
@@ -248,9 +253,10 @@ def rope_(x2d: torch.Tensor, seq_len: int, heads: int, head_dim: int, cos_t, sin
 
 
 # ---------------------------------------------------------------------- activations
-def act_fwd(a: torch.Tensor, g: torch.Tensor | None, act0: str, act1: str = "linear"):
+def act_fwd(a: torch.Tensor, g: torch.Tensor | None, act0: str, act1: str = "linear", out=None):
     rows, cols = a.shape
-    out = torch.empty((rows, cols), device=a.device, dtype=a.dtype)
+    if out is None:
+        out = torch.empty((rows, cols), device=a.device, dtype=a.dtype)
     _lib.call("cb_act_fwd", rows, cols, ACT_IDS[act0], ACT_IDS[act1], a.data_ptr(), ld(a), _ptr(g),
               ld(g) if g is not None else 0, out.data_ptr(), ld(out), dt(a), stream_ptr())
     return out
