@@ -156,8 +156,15 @@ __global__ void __launch_bounds__(1024) xent_reg_k(int T, int V, const float* __
                     __expf(r[i].w - m) * inv};
       const int base = j * 4;
       if (target >= base && target < base + 4) p[target - base] -= grad_scale;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) gr[base + e] = from_f32<TG>(p[e]);
+      if constexpr (sizeof(TG) == 2) {  // one 8-byte store of 4 bf16
+        __nv_bfloat162 lo = __floats2bfloat162_rn(p[0], p[1]), hi = __floats2bfloat162_rn(p[2], p[3]);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(gr + base) = pk;
+      } else {
+        *reinterpret_cast<float4*>(gr + base) = make_float4(p[0], p[1], p[2], p[3]);
+      }
     }
   }
 }
@@ -195,8 +202,10 @@ extern "C" int cb_xent_fwd_bwd(int batch, int seq_len, int vocab, const void* lo
   if (vocab <= 0) return fail(CB_ERR_SHAPE, "xent: vocab must be positive");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t rows = (int64_t)batch * seq_len;
+  const int64_t gal = g_dtype == CB_DT_F32 ? 16 : 8;  // vector store of 4 gradients
   const bool reg_ok = l_dtype == CB_DT_F32 && vocab % 4 == 0 && vocab <= 8 * 4 * 1024 && (ld % 4) == 0 &&
-                      !(reinterpret_cast<uintptr_t>(logits) & 15) && (!dlogits || dlogits != logits);
+                      !(reinterpret_cast<uintptr_t>(logits) & 15) && (!dlogits || dlogits != logits) &&
+                      (!dlogits || ((ldg % 4) == 0 && (reinterpret_cast<uintptr_t>(dlogits) % gal) == 0));
   if (reg_ok) {
     if (g_dtype == CB_DT_F32)
       xent_reg_k<8, float><<<rows, 1024, 0, st>>>(seq_len, vocab, (const float*)logits, ld, tokens, row_loss,
