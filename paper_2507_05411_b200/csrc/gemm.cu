@@ -133,7 +133,25 @@ __device__ __forceinline__ void epi_chunk(const Epi& e, uint32_t (&v)[32], int r
                     ((reinterpret_cast<uintptr_t>(e.D) & 15) == 0);
   const bool vec = full_chunk && ((e.ldd & 7) == 0) && ((reinterpret_cast<uintptr_t>(e.D) & 31) == 0) &&
                    (!e.R || (((e.ldr & 7) == 0) && ((reinterpret_cast<uintptr_t>(e.R) & 31) == 0)));
-  if (!fast && vec) {
+  if (!fast && vec && e.d_f32 && ((e.R && e.r_f32) != (bool)e.accumulate)) {
+    // f32 output plus exactly one f32 addend (the residual R, or D itself when accumulating):
+    // all of the chunk's addend loads are issued before any store (one memory latency per
+    // chunk instead of one per 8 columns)
+    const int64_t di = (int64_t)row * e.ldd + col0;
+    const float4* src = e.accumulate
+                            ? reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.D) + di)
+                            : reinterpret_cast<const float4*>(reinterpret_cast<const float*>(e.R) + (int64_t)row * e.ldr + col0);
+    float4 add[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) add[i] = src[i];
+    float4* d = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.D) + di);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      d[i] = make_float4(fmaf(__uint_as_float(v[4 * i]), e.alpha, add[i].x),
+                         fmaf(__uint_as_float(v[4 * i + 1]), e.alpha, add[i].y),
+                         fmaf(__uint_as_float(v[4 * i + 2]), e.alpha, add[i].z),
+                         fmaf(__uint_as_float(v[4 * i + 3]), e.alpha, add[i].w));
+  } else if (!fast && vec) {
     // general epilogue, 8 columns (one 16/32-byte vector) at a time
 #pragma unroll
     for (int g8 = 0; g8 < 4; ++g8) {
@@ -546,6 +564,9 @@ struct Cfg2 {
   static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
 };
 
+// GLU: instantiation with the gated-activation epilogues (kept out of the plain kernel so its
+// register allocation is not inflated by them)
+template <bool GLU>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Args args) {
   using C = Cfg2;
@@ -693,7 +714,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = tm * BM + q * 32 + lane;
       const bool row_ok = row < e.M;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      if (e.glu) {
+      if (GLU) {
         const Glu gq{reinterpret_cast<__nv_bfloat16*>(e.D), e.ldd, reinterpret_cast<__nv_bfloat16*>(e.glu_out),
                      e.ld_glu_out, reinterpret_cast<const __nv_bfloat16*>(e.glu_pre), e.ld_glu_pre, e.glu_h, e.N,
                      e.glu_a0, e.glu_a1};
@@ -718,7 +739,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               dst[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
                                    __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
           } else {
-            for (int j = 0; j < e.N - col0; ++j) part[col0 + j] = __uint_as_float(v[j]);
+            const int lim = e.N - col0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < lim) part[col0 + j] = __uint_as_float(v[j]);
           }
         }
       } else {
@@ -823,7 +847,8 @@ int launch_pair(const Args& a, const void* A, int64_t lda, const void* B, int64_
   if (s) return s;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    cudaFuncSetAttribute(gemm_tc2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    cudaFuncSetAttribute(gemm_tc2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     attr_set = true;
   }
   Args args = a;
@@ -843,7 +868,8 @@ int launch_pair(const Args& a, const void* A, int64_t lda, const void* B, int64_
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc2, ta, tb, args);
+  cudaError_t e = a.e.glu ? cudaLaunchKernelEx(&cfg, gemm_tc2<true>, ta, tb, args)
+                          : cudaLaunchKernelEx(&cfg, gemm_tc2<false>, ta, tb, args);
   if (e != cudaSuccess) return fail(CB_ERR_CUDA, "gemm_tc2 cluster launch: %s", cudaGetErrorString(e));
   if (int r = check_launch("gemm_tc_pair")) return r;
   if (args.splits == 1) return CB_OK;
