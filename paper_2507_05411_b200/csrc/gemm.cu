@@ -758,7 +758,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty_leader0 + acc * 8);
+      // the accumulator buffer is free once this warp's tcgen05.ld completed (fence above);
+      // its global stores need no ordering with the next tile's MMAs
+      if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader0 + acc * 8);
     }
   }
   tc_fence_before();
