@@ -63,10 +63,30 @@ __device__ __forceinline__ float fast_exp2(float x) {
 __device__ __forceinline__ uint64_t koff(int kk) { return (uint64_t)(((kk >> 2) * kBox + (kk & 3) * 32) >> 4); }
 
 #ifdef CB_ATTN_TRACE
-__device__ unsigned long long g_btrace[16][64];
+__device__ unsigned long long g_btrace[24][64];
 #define BWD_TRACE(ev, j) \
   if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 64 && (threadIdx.x & 31) == 0) g_btrace[ev][j] = clock64()
+// per-CTA timeline: [kernel][cta] = {start ns, end ns, smid}
+__device__ unsigned long long g_cta[2][8192][3];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define CTA_TRACE(kern, which)                                                                    \
+  if (threadIdx.x == 0) {                                                                         \
+    const int id_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);               \
+    if (id_ < 8192) {                                                                             \
+      g_cta[kern][id_][which] = gtimer();                                                         \
+      if (which == 0) {                                                                           \
+        unsigned s_;                                                                              \
+        asm volatile("mov.u32 %0, %smid;" : "=r"(s_));                                            \
+        g_cta[kern][id_][2] = s_;                                                                 \
+      }                                                                                           \
+    }                                                                                             \
+  }
 #else
+#define CTA_TRACE(kern, which)
 #define BWD_TRACE(ev, j)
 #endif
 
@@ -201,6 +221,7 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if (smem_u32(smem) & 1023) __trap();  // see kSmemDkdv
+  CTA_TRACE(0, 0);
   uint8_t* sK = smem;
   uint8_t* sV = smem + kTile;
   uint8_t* sQ = smem + 2 * kTile;                               // [kQSlots]
@@ -443,6 +464,7 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
   }
   tc_fence_before();
   __syncthreads();
+  CTA_TRACE(0, 1);
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, kCols);
@@ -455,6 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
          const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmG, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  CTA_TRACE(1, 0);
   uint8_t* sQ = smem;
   uint8_t* sG = smem + kTile;
   uint8_t* sK = smem + 2 * kTile;      // [kKSlots]
@@ -515,6 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < nk; ++j) {
         const int st = j % kKSlots;
         mbar_wait(&k_empty[st], ((j / kKSlots) & 1) ^ 1);
+        BWD_TRACE(16, j);
         mbar_expect_tx(&k_full[st], kTile);
         tma_load_2d(sK + st * kTile, &tmK, &k_full[st], kvh * HD, row0 + j * BT);
         tma_load_2d(sK + st * kTile + kBox, &tmK, &k_full[st], kvh * HD + 64, row0 + j * BT);
@@ -527,6 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < nk; ++j) {
         const int st = j & 1;
         mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        BWD_TRACE(17, j);
         mbar_expect_tx(&v_full[st], kTile);
         tma_load_2d(sV + st * kTile, &tmV, &v_full[st], kvh * HD, row0 + j * BT);
         tma_load_2d(sV + st * kTile + kBox, &tmV, &v_full[st], kvh * HD + 64, row0 + j * BT);
@@ -642,6 +667,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  CTA_TRACE(1, 1);
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, kCols);

@@ -5,6 +5,7 @@
 //     paper_2507_05411_b200/csrc/runtime.cu -o scripts/bin/attn_bwd_trace -lcuda
 #include <cstdio>
 #include <vector>
+#include <algorithm>
 
 #include "../paper_2507_05411_b200/csrc/attn_tc.cu"
 #include "../paper_2507_05411_b200/csrc/attn_tc_bwd.cu"
@@ -50,7 +51,7 @@ int main() {
   cudaEventElapsedTime(&ms, e0, e1);
   ms /= 10;
   printf("bwd %.3f ms  %.1f TFLOP/s (5 GEMMs algorithmic)\n", ms, 10.0 * B * T * (double)T * H * hd / ms / 1e9);
-  unsigned long long tr[16][64];
+  unsigned long long tr[24][64];
   cudaMemcpyFromSymbol(tr, cb::tcb::g_btrace, sizeof(tr));
   const unsigned long long t0 = tr[1][0];
   const char* names[10] = {"dV", "S+1", "dK", "dP+1", "c.S", "c.P", "c.dP", "c.dS", "ld.Q", "ld.dO"};
@@ -63,14 +64,49 @@ int main() {
     printf("\n");
   }
   const unsigned long long t1 = tr[10][0];
-  const char* qn[6] = {"S", "dQ", "dP", "c.S", "c.dP", "c.dS"};
+  const char* qn[8] = {"S", "dQ", "dP", "c.S", "c.dP", "c.dS", "ld.K", "ld.V"};
   printf("dq kernel\n  j");
-  for (int e = 0; e < 6; ++e) printf(" %7s", qn[e]);
+  for (int e = 0; e < 8; ++e) printf(" %7s", qn[e]);
   printf("\n");
   for (int j = 0; j < 12; ++j) {
     printf("%3d", j);
-    for (int e = 0; e < 6; ++e) printf(" %7lld", (long long)(tr[10 + e][j] - t1));
+    for (int e = 0; e < 8; ++e) printf(" %7lld", (long long)(tr[10 + e][j] - t1));
     printf("\n");
+  }
+  printf("steady-state period (tiles 4..15): dkdv %.0f cycles, dq %.0f cycles\n", (tr[0][15] - tr[0][4]) / 11.0,
+         (tr[11][15] - tr[11][4]) / 11.0);
+  // per-CTA timeline of the last launch: CTA duration, gap to the next CTA on the same SM
+  static unsigned long long ct[2][8192][3];
+  cudaMemcpyFromSymbol(ct, cb::tcb::g_cta, sizeof(ct));
+  const int ncta = (T / 128) * H * B;
+  for (int kk = 0; kk < 2; ++kk) {
+    unsigned long long lo = ~0ull, hi = 0;
+    double dur = 0, gap = 0;
+    int ngap = 0;
+    std::vector<std::vector<std::pair<unsigned long long, unsigned long long>>> per(160);
+    for (int i = 0; i < ncta; ++i) {
+      lo = std::min(lo, ct[kk][i][0]);
+      hi = std::max(hi, ct[kk][i][1]);
+      dur += (double)(ct[kk][i][1] - ct[kk][i][0]);
+      per[ct[kk][i][2] % 160].push_back({ct[kk][i][0], ct[kk][i][1]});
+    }
+    int nsm = 0;
+    double first_start = 0, last_end = 0;
+    for (auto& v : per) {
+      if (v.empty()) continue;
+      ++nsm;
+      std::sort(v.begin(), v.end());
+      first_start += (double)(v.front().first - lo);
+      last_end += (double)(hi - v.back().second);
+      for (size_t j = 1; j < v.size(); ++j) {
+        gap += (double)v[j].first - (double)v[j - 1].second;
+        ++ngap;
+      }
+    }
+    printf("%s: span %.1f us, %d SMs, %d CTAs, mean CTA %.2f us, mean gap between CTAs on an SM %.2f us, "
+           "mean first start %.2f us, mean idle tail %.2f us\n",
+           kk ? "dq" : "dkdv", (hi - lo) / 1e3, nsm, ncta, dur / ncta / 1e3, ngap ? gap / ngap / 1e3 : 0.0,
+           first_start / nsm / 1e3, last_end / nsm / 1e3);
   }
   return 0;
 }

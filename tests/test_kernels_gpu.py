@@ -63,6 +63,7 @@ def test_xent_matches_torch(cuda):
     (4, 128, 2, 2, 128, torch.bfloat16, 0),  # single key tile; second query tile of the CTA is padding
     (4, 128, 2, 2, 128, torch.bfloat16, 2),
     (3, 64, 2, 1, 128, torch.bfloat16, 0),   # T < tile
+    (1, 1152, 4, 4, 128, torch.bfloat16, 0),  # 9 key / query tiles: every smem ring and TMEM phase wraps
 ])
 def test_attention_fwd_bwd(cuda, B, T, H, KVH, hd, dt, path):
     from paper_2507_05411_b200 import _lib, ops
@@ -82,6 +83,11 @@ def test_attention_fwd_bwd(cuda, B, T, H, KVH, hd, dt, path):
         dqkv = torch.empty_like(qkv)
         ops.attention_bwd(q, k, v, o, lse, do, dqkv[:, :d], dqkv[:, d:d + kvd], dqkv[:, d + kvd:], B, T, H, KVH, hd,
                           scale)
+        # the backward is deterministic (no atomics): a second run is bit-identical
+        again = torch.empty_like(qkv)
+        ops.attention_bwd(q, k, v, o, lse, do, again[:, :d], again[:, d:d + kvd], again[:, d + kvd:], B, T, H, KVH,
+                          hd, scale)
+        assert torch.equal(again, dqkv)
     finally:
         ops.set_attention_path(0)
         _lib.call("cb_attention_set_tc", 1)
