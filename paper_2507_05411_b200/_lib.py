@@ -33,6 +33,7 @@ SIGNATURES: dict[str, list] = {
     "cb_abi_version": [],
     "cb_gemm_set_path": [_I],
     "cb_gemm_set_multicast": [_I],
+    "cb_gemm_set_staged_epilogue": [_I],
     "cb_gemm": [_I, _I, _I, _I, _P, _L, _I, _P, _L, _I, _P, _L, _I, _P, _L, _I, _F, _I, _P],
     "cb_rmsnorm_fwd": [_I, _I, _P, _L, _I, _P, _F, _P, _L, _I, _P, _P],
     "cb_rmsnorm_bwd_workspace": [_I, _I, ctypes.POINTER(ctypes.c_int64)],

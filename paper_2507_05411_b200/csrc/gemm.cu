@@ -68,6 +68,11 @@ __device__ __forceinline__ void epi_store1(const Epi& e, int r, int c, float v) 
 // tcgen05 engine
 // ======================================================================================
 namespace tc {
+// 1 (default): the CTA-pair engine's epilogues go through the per-warp shared-memory stage
+// (coalesced global I/O); 0: per-lane stores (A/B and tests, cb_gemm_set_staged_epilogue)
+// bits: kStagedBf16 | kStagedF32 | kStagedAddLoads | kStagedGlu (default: bf16 + gated)
+__constant__ int g_epi_staged = 9;
+constexpr int kStagedBf16 = 1, kStagedF32 = 2, kStagedAddLoads = 4, kStagedGlu = 8;
 constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle atom of bf16 along K
 constexpr int kThreads = 256;
@@ -550,6 +555,235 @@ __device__ __noinline__ void glu_tile(const Glu q, int glu, uint32_t tbase, int 
   }
 }
 
+// ---- coalesced epilogue I/O through a per-warp shared-memory stage -------------------------
+// The accumulator layout puts one output row in each lane, so direct stores touch 32 rows per
+// instruction (32 L2 requests of 16 bytes: the epilogue of the wide GEMMs was L2-request bound,
+// tensor pipe ~55% busy).  Instead each lane writes its row piece to the stage and the warp
+// moves the 32 rows with lanes along rows: 4 (128-byte rows) or 8 (64-byte rows) requests per
+// instruction.  A staged row is RB = 64 or 128 bytes; with RB = 128, bytes [0, 64) of row r
+// live at g0 + r * ld and bytes [64, 128) at g1 + r * ld (g1 = g0 + 64: one contiguous piece).
+constexpr int kStagePitch = 144;  // 16-byte pad: the lanes' own-row accesses are conflict-free
+
+template <int RB>
+__device__ __forceinline__ const uint8_t* stage_src(const uint8_t* g0, const uint8_t* g1, int c) {
+  return RB == 128 && c >= 4 ? g1 + (c - 4) * 16 : g0 + c * 16;
+}
+// global -> registers (lanes along rows); rows >= nrows are skipped
+template <int RB>
+__device__ __forceinline__ void stage_gload(uint4 (&v)[RB / 16], int lane, const void* g0, const void* g1, int64_t ld,
+                                            int nrows) {
+  constexpr int LPR = RB / 16;  // lanes per row
+#pragma unroll
+  for (int i = 0; i < RB / 16; ++i) {
+    const int r = i * (32 / LPR) + lane / LPR, c = lane % LPR;
+    if (r < nrows)
+      v[i] = __ldg(reinterpret_cast<const uint4*>(
+          stage_src<RB>(reinterpret_cast<const uint8_t*>(g0), reinterpret_cast<const uint8_t*>(g1), c) + r * ld));
+  }
+}
+// registers (from stage_gload) -> stage
+template <int RB>
+__device__ __forceinline__ void stage_put(uint8_t* st, const uint4 (&v)[RB / 16], int lane) {
+  constexpr int LPR = RB / 16;
+#pragma unroll
+  for (int i = 0; i < RB / 16; ++i) {
+    const int r = i * (32 / LPR) + lane / LPR, c = lane % LPR;
+    *reinterpret_cast<uint4*>(st + r * kStagePitch + c * 16) = v[i];
+  }
+}
+// stage -> global (lanes along rows); rows >= nrows are skipped
+template <int RB>
+__device__ __forceinline__ void stage_gstore(const uint8_t* st, int lane, void* g0, void* g1, int64_t ld, int nrows) {
+  constexpr int LPR = RB / 16;
+#pragma unroll
+  for (int i = 0; i < RB / 16; ++i) {
+    const int r = i * (32 / LPR) + lane / LPR, c = lane % LPR;
+    const uint4 v = *reinterpret_cast<const uint4*>(st + r * kStagePitch + c * 16);
+    if (r < nrows)
+      *reinterpret_cast<uint4*>(
+          const_cast<uint8_t*>(stage_src<RB>(reinterpret_cast<const uint8_t*>(g0), reinterpret_cast<const uint8_t*>(g1), c)) +
+          r * ld) = v;
+  }
+}
+__device__ __forceinline__ uint4 stage_own(const uint8_t* st, int lane, int j) {
+  return *reinterpret_cast<const uint4*>(st + lane * kStagePitch + j * 16);
+}
+__device__ __forceinline__ void stage_set_own(uint8_t* st, int lane, int j, uint4 v) {
+  *reinterpret_cast<uint4*>(st + lane * kStagePitch + j * 16) = v;
+}
+
+// Backward gated epilogue of one tile through the stage: per 32-column chunk of dhidden the
+// warp loads the chunk's pre rows (a | g, 64 + 64 bytes) coalesced (the next chunk's loads in
+// flight during this one), and stores dpre (da | dg) coalesced.  row0 = the warp's first row.
+template <int A0, int A1>
+__device__ __noinline__ void glu_bwd_tile_staged(const Glu q, uint32_t tbase, int row0, int nrows, int tn,
+                                                 uint8_t* st, int lane) {
+  const int n0 = tn * 256;
+  const int64_t ldi = q.ldpin * 2, ldo = q.ldout * 2;
+  const __nv_bfloat16* pin = q.pin + (int64_t)row0 * q.ldpin;
+  __nv_bfloat16* pout = q.out + (int64_t)row0 * q.ldout;
+  uint4 nxt[8];
+  stage_gload<128>(nxt, lane, pin + n0, pin + q.h + n0, ldi, nrows);
+#pragma unroll 1
+  for (int c = 0; c < 8; ++c) {
+    const int col = n0 + c * 32;
+    if (col >= q.n) break;  // warp-uniform (q.n % 32 == 0 on this path)
+    stage_put<128>(st, nxt, lane);
+    if (c + 1 < 8 && col + 32 < q.n) stage_gload<128>(nxt, lane, pin + col + 32, pin + q.h + col + 32, ldi, nrows);
+    uint32_t v[32];
+    tmem_ld32(tbase + c * 32, v);
+    __syncwarp();
+    uint4 pa[4], pg[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      pa[j] = stage_own(st, lane, j);
+      pg[j] = stage_own(st, lane, 4 + j);
+    }
+    tmem_ld_wait_regs(v);
+#pragma unroll
+    for (int g8 = 0; g8 < 4; ++g8) {
+      float d[8], a[8], g[8], da[8], dg[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) d[i] = __uint_as_float(v[g8 * 8 + i]);
+      unpack8(pack8(d), d);
+      unpack8(pa[g8], a);
+      unpack8(pg[g8], g);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) glu_df<A0, A1>(d[i], a[i], g[i], da[i], dg[i], q.a0, q.a1);
+      stage_set_own(st, lane, g8, pack8(da));
+      stage_set_own(st, lane, 4 + g8, pack8(dg));
+    }
+    __syncwarp();
+    stage_gstore<128>(st, lane, pout + col, pout + q.h + col, ldo, nrows);
+    __syncwarp();
+  }
+}
+
+// RoPE rotation of one 32-column chunk held in registers (columns [0, rope_cols) only)
+__device__ __forceinline__ void epi_rope(const Epi& e, uint32_t (&v)[32], int row, int col0) {
+  if (!(e.rope_cos && col0 < e.rope_cols)) return;
+  const int half = e.rope_hd >> 1;
+  const int p0 = (col0 % e.rope_hd) >> 1;
+  const int64_t tb = (int64_t)(row % e.rope_T) * half + p0;
+  const float4* cs4 = reinterpret_cast<const float4*>(e.rope_cos + tb);
+  const float4* sn4 = reinterpret_cast<const float4*>(e.rope_sin + tb);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float4 cq = cs4[j], sq = sn4[j];
+    const float cc[4] = {cq.x, cq.y, cq.z, cq.w}, ss[4] = {sq.x, sq.y, sq.z, sq.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = (j * 4 + i) * 2;
+      const float ev = __uint_as_float(v[k]), od = __uint_as_float(v[k + 1]);
+      v[k] = __float_as_uint(ev * cc[i] - od * ss[i]);
+      v[k + 1] = __float_as_uint(ev * ss[i] + od * cc[i]);
+    }
+  }
+}
+
+// Which staged epilogue a GEMM's output takes (0 = none: the per-lane epi_chunk path).
+// 1: bf16 out, no addend; 2: f32 out, no addend; 3: f32 out plus one f32 addend (the residual
+// R, or D itself when accumulating).  Requires every 32-column chunk to be full and 16-byte
+// aligned rows.
+__host__ __device__ __forceinline__ int staged_mode(const Epi& e) {
+  if (e.N % 32 != 0 || (e.ldd & 7) != 0 || (reinterpret_cast<uintptr_t>(e.D) & 15) != 0) return 0;
+  if (!e.d_f32) return !e.accumulate && !e.R ? 1 : 0;
+  if (!e.accumulate && !e.R) return 2;
+  if (e.accumulate && e.R) return 0;
+  if (e.R && (!e.r_f32 || (e.ldr & 3) != 0 || (reinterpret_cast<uintptr_t>(e.R) & 15) != 0)) return 0;
+  return 3;
+}
+
+// One 128-row x BN tile of this warp's 32 rows through the staged epilogue (mode from
+// staged_mode, warp-uniform).
+template <int BN>
+__device__ __noinline__ void epi_tile_staged(const Epi e, int mode, uint32_t tbase, int row0, int nrows, int tn,
+                                             uint8_t* st, int lane) {
+  const int row = row0 + lane;
+  const int c0 = tn * BN;
+  if (mode == 1) {
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      const int col0 = c0 + c * 32;
+      if (col0 >= e.N) break;
+      uint32_t v[32];
+      tmem_ld32(tbase + c * 32, v);
+      tmem_ld_wait_regs(v);
+      epi_rope(e, v, row, col0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float o[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = __uint_as_float(v[j * 8 + i]) * e.alpha;
+        stage_set_own(st, lane, j, pack8(o));
+      }
+      __syncwarp();
+      __nv_bfloat16* g = reinterpret_cast<__nv_bfloat16*>(e.D) + (int64_t)row0 * e.ldd + col0;
+      stage_gstore<64>(st, lane, g, g, e.ldd * 2, nrows);
+      __syncwarp();
+    }
+    return;
+  }
+  const float* add = mode == 3 ? (e.accumulate ? reinterpret_cast<const float*>(e.D) : reinterpret_cast<const float*>(e.R))
+                               : nullptr;
+  const int64_t lda = e.accumulate ? e.ldd : e.ldr;
+  const float* arow = add ? add + (int64_t)row0 * lda : nullptr;
+  float* drow = reinterpret_cast<float*>(e.D) + (int64_t)row0 * e.ldd;
+  // the addend rows: through the stage (coalesced, kStagedAddLoads) or loaded by each lane
+  // (the 8 loads of a lane hit one 128-byte line, which L1 serves after the first)
+  const bool sload = add && (g_epi_staged & kStagedAddLoads);
+  const bool ok = row0 + lane < e.M;
+  uint4 nxt[8];
+  auto lane_load = [&](int col) {
+    if (ok) {
+      const uint4* src = reinterpret_cast<const uint4*>(arow + (int64_t)lane * lda + col);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) nxt[j] = __ldg(src + j);
+    }
+  };
+  if (sload)
+    stage_gload<128>(nxt, lane, arow + c0, arow + c0 + 16, lda * 4, nrows);
+  else if (add)
+    lane_load(c0);
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    const int col0 = c0 + c * 32;
+    if (col0 >= e.N) break;
+    uint4 cur[8];
+    if (sload) {
+      stage_put<128>(st, nxt, lane);
+      if (c + 1 < BN / 32 && col0 + 32 < e.N)
+        stage_gload<128>(nxt, lane, arow + col0 + 32, arow + col0 + 48, lda * 4, nrows);
+    } else if (add) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) cur[j] = nxt[j];
+      if (c + 1 < BN / 32 && col0 + 32 < e.N) lane_load(col0 + 32);
+    }
+    uint32_t v[32];
+    tmem_ld32(tbase + c * 32, v);
+    tmem_ld_wait_regs(v);
+    epi_rope(e, v, row, col0);
+    if (sload) __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float4 o = make_float4(__uint_as_float(v[4 * j]) * e.alpha, __uint_as_float(v[4 * j + 1]) * e.alpha,
+                             __uint_as_float(v[4 * j + 2]) * e.alpha, __uint_as_float(v[4 * j + 3]) * e.alpha);
+      if (add) {
+        const uint4 a = sload ? stage_own(st, lane, j) : cur[j];
+        o.x += __uint_as_float(a.x);
+        o.y += __uint_as_float(a.y);
+        o.z += __uint_as_float(a.z);
+        o.w += __uint_as_float(a.w);
+      }
+      stage_set_own(st, lane, j, make_uint4(__float_as_uint(o.x), __float_as_uint(o.y), __float_as_uint(o.z),
+                                            __float_as_uint(o.w)));
+    }
+    __syncwarp();
+    stage_gstore<128>(st, lane, drow + col0, drow + col0 + 16, e.ldd * 4, nrows);
+    __syncwarp();
+  }
+}
+
 // CTA-pair engine (cta_group::2): a cluster of two CTAs computes one 256 x 256 tile with a
 // single tcgen05.mma stream issued by the leader.  Each CTA stages its own 128 rows of A and
 // its own 128 columns of B (the hardware feeds each SM's tensor core the other half of B from
@@ -561,7 +795,8 @@ struct Cfg2 {
   static constexpr int kABytes = BM * BK * 2;  // 16 KB: this CTA's 128 rows of A
   static constexpr int kBBytes = 128 * BK * 2; // 16 KB: this CTA's 128 columns of B
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+  static constexpr int kEpiBytes = 4 * 32 * 144;  // per epilogue warp: 32 staged rows (see stage_*)
+  static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024 + 256;
 };
 
 // GLU: instantiation with the gated-activation epilogues (kept out of the plain kernel so its
@@ -704,6 +939,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     const Epi& e = args.e;
     const uint32_t tempty_leader0 = leader_addr(&tempty[0]);
+    uint8_t* stg = smem + C::kStages * C::kStageBytes + 256 + q * 32 * kStagePitch;  // this warp's stage
+    const int smode = S > 1 ? 0 : staged_mode(e);
+    // gated backward through the stage: pre / dpre rows 16-byte aligned, whole 32-column chunks
+    const bool glu_staged = GLU && e.glu == 2 && e.N % 32 == 0 && e.glu_h % 8 == 0 && (e.ld_glu_pre & 7) == 0 &&
+                            (e.ld_glu_out & 7) == 0 && (reinterpret_cast<uintptr_t>(e.glu_pre) & 15) == 0 &&
+                            (reinterpret_cast<uintptr_t>(e.glu_out) & 15) == 0;
     int it = 0;
     for (int u = unit0; u < num_units; u += unit_stride, ++it) {
       int tm, tn;
@@ -711,17 +952,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
-      const int row = tm * BM + q * 32 + lane;
+      const int row0 = tm * BM + q * 32;
+      const int row = row0 + lane;
       const bool row_ok = row < e.M;
+      const int nrows = max(0, min(32, e.M - row0));
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       if (GLU) {
         const Glu gq{reinterpret_cast<__nv_bfloat16*>(e.D), e.ldd, reinterpret_cast<__nv_bfloat16*>(e.glu_out),
                      e.ld_glu_out, reinterpret_cast<const __nv_bfloat16*>(e.glu_pre), e.ld_glu_pre, e.glu_h, e.N,
                      e.glu_a0, e.glu_a1};
-        if (e.glu_a0 == ACT_LINEAR && e.glu_a1 == ACT_SILU)  // SwiGLU
+        if (glu_staged && (g_epi_staged & kStagedGlu)) {
+          if (e.glu_a0 == ACT_LINEAR && e.glu_a1 == ACT_SILU)  // SwiGLU
+            glu_bwd_tile_staged<ACT_LINEAR, ACT_SILU>(gq, tbase, row0, nrows, tn, stg, lane);
+          else
+            glu_bwd_tile_staged<-1, -1>(gq, tbase, row0, nrows, tn, stg, lane);
+        } else if (e.glu_a0 == ACT_LINEAR && e.glu_a1 == ACT_SILU) {  // SwiGLU
           glu_tile<ACT_LINEAR, ACT_SILU>(gq, e.glu, tbase, row, row_ok, tn);
-        else
+        } else {
           glu_tile<-1, -1>(gq, e.glu, tbase, row, row_ok, tn);
+        }
+      } else if (smode && (g_epi_staged & (smode == 1 ? kStagedBf16 : kStagedF32))) {
+        epi_tile_staged<BN>(e, smode, tbase, row0, nrows, tn, stg, lane);
       } else if (S > 1) {
         // split-K slice: raw f32 partial to ws[slice] (the reduce kernel applies the epilogue)
         float* part = args.ws + (int64_t)(u % S) * e.M * e.N + (int64_t)row * e.N;
@@ -1075,6 +1326,13 @@ extern "C" int cb_gemm_set_workspace(void* ptr, int64_t bytes) {
     return fail(CB_ERR_ARG, "gemm workspace: need a 16-byte aligned buffer");
   tc::g_ws = bytes > 0 ? reinterpret_cast<float*>(ptr) : nullptr;
   tc::g_ws_bytes = bytes;
+  return CB_OK;
+}
+
+extern "C" int cb_gemm_set_staged_epilogue(int enable) {
+  const int v = enable < 0 ? 0 : enable == 1 ? 15 : enable;
+  if (cudaMemcpyToSymbol(tc::g_epi_staged, &v, sizeof(v)) != cudaSuccess)
+    return fail(CB_ERR_CUDA, "cb_gemm_set_staged_epilogue: cudaMemcpyToSymbol failed");
   return CB_OK;
 }
 

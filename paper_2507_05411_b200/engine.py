@@ -33,7 +33,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import ops
+from . import _lib, ops
 from .config import ConfigNode, visit
 from .errors import ShapeError, TypeMismatchError
 from .module import Module, ParamProvider, instantiate, invoke, iter_param_specs, value_and_grad
@@ -233,6 +233,9 @@ class TrainEngine:
         # more than the wave-quantization time it recovers (CB_GEMM_SPLITK=1 enables it)
         if os.environ.get("CB_GEMM_SPLITK", "0") == "1":
             ops.ensure_gemm_workspace(self.device)
+        # epilogue staging mask of the CTA-pair GEMM (cb_gemm_set_staged_epilogue; A/B runs)
+        if "CB_GEMM_STAGED_EPILOGUE" in os.environ and self.device.type == "cuda":
+            _lib.call("cb_gemm_set_staged_epilogue", int(os.environ["CB_GEMM_STAGED_EPILOGUE"]))
         self.options = {"precision": self.precision, "validate_ids": False,
                         "fuse_glu": os.environ.get("CB_FUSE_GLU", "1") != "0"}
         if self.d.world > 1:  # summaries that are global-batch statistics reduce over this group

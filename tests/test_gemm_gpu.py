@@ -161,3 +161,53 @@ def test_gemm_split_k_matches(cuda, M, N, K, ta, tb):
         exp = 0.5 * ref + r
         assert ((bo.float() - exp).norm() / exp.norm()) < 1e-2, mode
     assert torch.equal(outs["split"][0], outs["split2"][0])  # deterministic
+
+
+@pytest.mark.parametrize("M,N,K", [(512, 768, 320), (300, 640, 256), (1000, 2048, 512)])
+def test_staged_epilogue_bit_identical(cuda, M, N, K):
+    """The CTA-pair GEMM's shared-memory-staged epilogue (coalesced output / addend / gated-pre
+    I/O) writes exactly what the per-lane epilogue writes, for every output mode, including
+    ragged row blocks (M % 32 != 0)."""
+    from paper_2507_05411_b200 import _lib, ops
+    from paper_2507_05411_b200.layers import rope_tables
+
+    g = torch.Generator(device="cpu").manual_seed(M + N + K)
+    a = torch.randn(M, K, generator=g).to(cuda, torch.bfloat16)
+    b = (torch.randn(K, N, generator=g) / K ** 0.5).to(cuda, torch.bfloat16)
+    r32 = torch.randn(M, N, generator=g).to(cuda)
+    acc0 = torch.randn(M, N, generator=g).to(cuda)
+    cs, sn = rope_tables(128, 128, 10000.0, cuda)
+    H = N // 2
+    w2 = (torch.randn(H, K, generator=g) / H ** 0.5).to(cuda, torch.bfloat16)
+    pre = torch.randn(M, 2 * H, generator=g).to(cuda, torch.bfloat16)
+
+    def run():
+        outs = {}
+        o = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+        outs["bf16"] = ops.gemm(a, b, o).clone()
+        o = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+        outs["bf16_rope"] = ops.gemm_rope(a, b, o, 128, 128, max(128, N // 256 * 128), cs, sn).clone()
+        o = torch.empty(M, N, device=cuda)
+        outs["f32"] = ops.gemm(a, b, o, alpha=0.75).clone()
+        o = torch.empty(M, N, device=cuda)
+        outs["f32_res"] = ops.gemm(a, b, o, residual=r32).clone()
+        o = acc0.clone()
+        outs["f32_acc"] = ops.gemm(a, b, o, accumulate=True).clone()
+        o = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+        outs["bf16_res"] = ops.gemm(a, b, o, residual=r32).clone()  # not staged: per-lane path both times
+        d = ops.gemm_gated_bwd(a, w2, pre, "linear", "silu")
+        if d is not None:
+            outs["glu_bwd"] = d.clone()
+        torch.cuda.synchronize()
+        return outs
+
+    try:
+        _lib.call("cb_gemm_set_staged_epilogue", 1)
+        staged = run()
+        _lib.call("cb_gemm_set_staged_epilogue", 0)
+        plain = run()
+    finally:
+        _lib.call("cb_gemm_set_staged_epilogue", 1)
+    assert staged.keys() == plain.keys()
+    for k in staged:
+        assert torch.equal(staged[k], plain[k]), k
