@@ -94,8 +94,8 @@ __device__ __forceinline__ void combine_ms(float& m, float& s, float m2, float s
   m = mm;
 }
 
-template <int NV4, typename TG>
-__global__ void __launch_bounds__(1024) xent_reg_k(int T, int V, const float* __restrict__ logits, int64_t ld,
+template <int NV4, int NT, typename TG>
+__global__ void __launch_bounds__(NT) xent_reg_k(int T, int V, const float* __restrict__ logits, int64_t ld,
                                                    const int64_t* __restrict__ tokens, float* __restrict__ row_loss,
                                                    TG* __restrict__ dlogits, int64_t ldg, float grad_scale) {
   __shared__ float sm[32], ss[32];
@@ -115,16 +115,25 @@ __global__ void __launch_bounds__(1024) xent_reg_k(int T, int V, const float* __
   const float target_logit = tid == 0 ? lr[target] : 0.f;
   float4 r[NV4];
   float m = -INFINITY, s = 0.f;
+  // every load of the row in flight before any arithmetic
 #pragma unroll
   for (int i = 0; i < NV4; ++i) {
-    const int j = i * 1024 + tid;
-    if (j < V4) {
-      r[i] = reinterpret_cast<const float4*>(lr)[j];
-      const float mx = fmaxf(fmaxf(r[i].x, r[i].y), fmaxf(r[i].z, r[i].w));
-      const float sub = __expf(r[i].x - mx) + __expf(r[i].y - mx) + __expf(r[i].z - mx) + __expf(r[i].w - mx);
-      combine_ms(m, s, mx, sub);
+    const int j = i * NT + tid;
+    r[i] = j < V4 ? __ldcs(reinterpret_cast<const float4*>(lr) + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  // the thread's max, then exp(x - max) kept in place of the logits: the gradient pass needs
+  // a single exp per thread (the rescale to the row max)
+#pragma unroll
+  for (int i = 0; i < NV4; ++i)
+    if (i * NT + tid < V4) m = fmaxf(m, fmaxf(fmaxf(r[i].x, r[i].y), fmaxf(r[i].z, r[i].w)));
+#pragma unroll
+  for (int i = 0; i < NV4; ++i) {
+    if (i * NT + tid < V4) {
+      r[i] = make_float4(__expf(r[i].x - m), __expf(r[i].y - m), __expf(r[i].z - m), __expf(r[i].w - m));
+      s += (r[i].x + r[i].y) + (r[i].z + r[i].w);
     }
   }
+  const float tmax = m;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) combine_ms(m, s, __shfl_xor_sync(0xffffffffu, m, o), __shfl_xor_sync(0xffffffffu, s, o));
   if (lane == 0) {
@@ -148,14 +157,17 @@ __global__ void __launch_bounds__(1024) xent_reg_k(int T, int V, const float* __
   if (tid == 0) row_loss[row] = m + logf(s) - target_logit;
   if (!gr) return;
   const float inv = grad_scale / s;
+  const float sc = tmax == -INFINITY ? 0.f : __expf(tmax - m) * inv;
 #pragma unroll
   for (int i = 0; i < NV4; ++i) {
-    const int j = i * 1024 + tid;
+    const int j = i * NT + tid;
     if (j < V4) {
-      float p[4] = {__expf(r[i].x - m) * inv, __expf(r[i].y - m) * inv, __expf(r[i].z - m) * inv,
-                    __expf(r[i].w - m) * inv};
       const int base = j * 4;
-      if (target >= base && target < base + 4) p[target - base] -= grad_scale;
+      // the one-hot term by comparison (a dynamic index would put p[] in local memory)
+      float p[4] = {r[i].x * sc - (target == base ? grad_scale : 0.f),
+                    r[i].y * sc - (target == base + 1 ? grad_scale : 0.f),
+                    r[i].z * sc - (target == base + 2 ? grad_scale : 0.f),
+                    r[i].w * sc - (target == base + 3 ? grad_scale : 0.f)};
       if constexpr (sizeof(TG) == 2) {  // one 8-byte store of 4 bf16
         __nv_bfloat162 lo = __floats2bfloat162_rn(p[0], p[1]), hi = __floats2bfloat162_rn(p[2], p[3]);
         uint2 pk;
@@ -208,11 +220,11 @@ extern "C" int cb_xent_fwd_bwd(int batch, int seq_len, int vocab, const void* lo
                       (!dlogits || ((ldg % 4) == 0 && (reinterpret_cast<uintptr_t>(dlogits) % gal) == 0));
   if (reg_ok) {
     if (g_dtype == CB_DT_F32)
-      xent_reg_k<8, float><<<rows, 1024, 0, st>>>(seq_len, vocab, (const float*)logits, ld, tokens, row_loss,
-                                                  (float*)dlogits, ldg, grad_scale);
+      xent_reg_k<8, 1024, float><<<rows, 1024, 0, st>>>(seq_len, vocab, (const float*)logits, ld, tokens, row_loss,
+                                                        (float*)dlogits, ldg, grad_scale);
     else
-      xent_reg_k<8, __nv_bfloat16><<<rows, 1024, 0, st>>>(seq_len, vocab, (const float*)logits, ld, tokens, row_loss,
-                                                          (__nv_bfloat16*)dlogits, ldg, grad_scale);
+      xent_reg_k<8, 1024, __nv_bfloat16><<<rows, 1024, 0, st>>>(seq_len, vocab, (const float*)logits, ld, tokens,
+                                                                row_loss, (__nv_bfloat16*)dlogits, ldg, grad_scale);
   } else if (l_dtype == CB_DT_F32 && g_dtype == CB_DT_F32)
     xent_k<float, float><<<rows, 512, 0, st>>>(seq_len, vocab, (const float*)logits, ld, tokens, row_loss,
                                                (float*)dlogits, ldg, grad_scale);
