@@ -289,14 +289,43 @@ class EmbeddingBehavior(Behavior):
             if lo < 0 or hi >= vocab:
                 raise ShapeError(f"token ids out of range [0, {vocab})")
         out = ops.embedding_fwd(ids, param("weight"), torch.float32)
-        save(ids=ids)
+        sort = None
+        if ids.is_cuda and is_recording():
+            # the backward's deterministic id sort depends only on the ids: run it now on a side
+            # stream, hidden behind the forward
+            side = _sort_stream(ids.device)
+            ready = torch.cuda.Event()
+            ready.record()
+            side.wait_event(ready)
+            with torch.cuda.stream(side):
+                offsets, perm = ops.sort_ids(ids, vocab)
+                done = torch.cuda.Event()
+                done.record(side)
+            sort = (offsets, perm, done)
+        save(ids=ids, sort=sort)
         return out
 
     def backward(self, module, dout):
         s = saved()
-        offsets, perm = ops.sort_ids(s["ids"], module.config.get("num_embeddings"))
+        if s.get("sort") is not None:
+            offsets, perm, done = s["sort"]
+            cur = torch.cuda.current_stream(dout.device)
+            cur.wait_event(done)
+            offsets.record_stream(cur)  # allocated on the side stream, consumed on this one
+            perm.record_stream(cur)
+        else:
+            offsets, perm = ops.sort_ids(s["ids"], module.config.get("num_embeddings"))
         ops.embedding_bwd(offsets, perm, dout, param_grad("weight"))
         return None
+
+
+_SORT_STREAMS: dict = {}
+
+
+def _sort_stream(device) -> torch.cuda.Stream:
+    if device not in _SORT_STREAMS:
+        _SORT_STREAMS[device] = torch.cuda.Stream(device)
+    return _SORT_STREAMS[device]
 
 
 # -------------------------------------------------------------- positional kinds
