@@ -485,12 +485,28 @@ class TrainEngine:
             key = self.step_key(self.step_count)
         if update:
             self.step_count += 1
-        for rec in self.bufs:
-            ops.zero_(rec["grad"])
         if self.d.world > 1:
             provider = FSDPProvider(self, update=update)
         else:
             provider = LocalUpdateProvider(self) if update else None
+        if provider is not None and self.device.type == "cuda":
+            # the gradient buffers are cleared on a side stream while the forward runs (nothing
+            # touches them before the backward, whose first hook waits for this)
+            cur = torch.cuda.current_stream(self.device)
+            if not hasattr(self, "_zero_stream"):
+                self._zero_stream = torch.cuda.Stream(self.device)
+            ready = torch.cuda.Event()
+            ready.record(cur)
+            with torch.cuda.stream(self._zero_stream):
+                self._zero_stream.wait_event(ready)
+                for rec in self.bufs:
+                    ops.zero_(rec["grad"])
+                zeroed = torch.cuda.Event()
+                zeroed.record(self._zero_stream)
+            provider.grads_zeroed = zeroed
+        else:
+            for rec in self.bufs:
+                ops.zero_(rec["grad"])
         if provider:
             provider.start_step()
         loss, col, _ = value_and_grad(self.module, self.state, self.grads, key, {"tokens": toks}, provider=provider,
@@ -585,12 +601,16 @@ class FSDPProvider(ParamProvider):
         if pos + 1 < len(self.layer_order):
             self._ag(self.layer_order[pos + 1])
 
+    def before_backward(self, path: str) -> None:
+        _wait_grads_zeroed(self)
+
     def after_backward(self, path: str) -> None:
         i = self.index.get(path)
         if i is not None:
             self._rs(i)
 
     def finish_backward(self) -> None:
+        _wait_grads_zeroed(self)
         for i, b in enumerate(self.e.buckets):
             if b.name == "root" or b.replicated:
                 self._rs(i)
@@ -620,15 +640,28 @@ class LocalUpdateProvider(ParamProvider):
             self.e._adamw_bucket(i)
         self.done.add(i)
 
+    def before_backward(self, path: str) -> None:
+        _wait_grads_zeroed(self)
+
     def after_backward(self, path: str) -> None:
         i = self.index.get(path)
         if i is not None:
             self._update(i)
 
     def finish_backward(self) -> None:
+        _wait_grads_zeroed(self)
         for i in range(len(self.e.buckets)):
             if i not in self.done:
                 self._update(i)
         fin = torch.cuda.Event()
         fin.record(self.side)
         self.compute.wait_event(fin)
+
+
+def _wait_grads_zeroed(provider) -> None:
+    """The compute stream waits (once per step) for the side-stream clearing of the gradient
+    buffers before the first backward kernel can write them."""
+    ev = getattr(provider, "grads_zeroed", None)
+    if ev is not None:
+        provider.compute.wait_event(ev)
+        provider.grads_zeroed = None

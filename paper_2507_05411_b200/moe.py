@@ -125,12 +125,19 @@ class MoEBehavior(Behavior):
         ids64 = torch.empty((n * k,), device=dev, dtype=torch.int64)
         _lib.call("cb_widen_i32", n * k, idx.data_ptr(), ids64.data_ptr(), ops.stream_ptr())
         offsets, perm = ops.sort_ids(ids64, E)
+        # the E+1 expert offsets size the per-expert GEMMs on the host: copied out right after
+        # the sort, so the host waits only for the sort while the gather below still runs
+        off_host = _pinned_offsets(E + 1)
+        off_host.copy_(offsets, non_blocking=True)
+        off_ready = torch.cuda.Event()
+        off_ready.record()
         inv = torch.empty((n * k,), device=dev, dtype=torch.int32)
         _lib.call("cb_invert_perm", n * k, perm.data_ptr(), inv.data_ptr(), ops.stream_ptr())
         xe = torch.empty((n * k, d), device=dev, dtype=adt)
         _lib.call("cb_gather_rows", n * k, d, perm.data_ptr(), k, x2.data_ptr(), ops.ld(x2), xe.data_ptr(),
                   ops.ld(xe), ops.dt(xe), ops.stream_ptr())
-        off = offsets.cpu().numpy().astype(np.int64)  # E+1 ints: sizes the per-expert GEMMs
+        off_ready.synchronize()
+        off = off_host.numpy().astype(np.int64)
         pair = L.activation_pair(cfg.get("activation"))
         w1, w2 = param("w1"), param("w2")
         wg = param("w1_gate") if pair else None
@@ -236,3 +243,14 @@ class MoEBehavior(Behavior):
                   router.data_ptr(), param_grad("router").data_ptr(), dx.data_ptr(), ops.ld(dx), ws.data_ptr(),
                   ops.stream_ptr())
         return dx.view(B, T, d)
+
+
+_PINNED: dict = {}
+
+
+def _pinned_offsets(n: int) -> torch.Tensor:
+    """A reusable pinned int32 host buffer for the expert offsets (read before the next use)."""
+    t = _PINNED.get(n)
+    if t is None:
+        t = _PINNED[n] = torch.empty((n,), dtype=torch.int32, pin_memory=True)
+    return t
