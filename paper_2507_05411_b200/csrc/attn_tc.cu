@@ -56,6 +56,10 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #define CB_ATTN_EMU 2
 #endif
 constexpr int kEmuPairs = CB_ATTN_EMU;  // of every 8 exp2 pairs, this many on the FMA pipe
+#ifndef CB_ATTN_SPLIT_P
+#define CB_ATTN_SPLIT_P 96
+#endif
+constexpr int kSplitP = CB_ATTN_SPLIT_P;  // keys of P V issued before the softmax finishes (x 32)
 
 struct Params {
   int T, H, KVH, B;
@@ -98,7 +102,8 @@ __global__ void __launch_bounds__(128 + 256 * NH, 1)
   uint64_t* s_full = bars + 11;   // [2] tiles
   uint64_t* p_ready = bars + 13;  // [2] tiles
   uint64_t* o_done = bars + 15;   // [2] tiles
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* p_part = bars + 17;   // [2] tiles: the first kSplitP S columns' P is in TMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
   float* red = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [2 tiles][2 halves][128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -122,6 +127,7 @@ __global__ void __launch_bounds__(128 + 256 * NH, 1)
       mbar_init(&v_empty[s], 1);
       mbar_init(&s_full[s], 1);
       mbar_init(&p_ready[s], 4 * NH);
+      mbar_init(&p_part[s], 4 * NH);
       mbar_init(&o_done[s], 1);
     }
     fence_mbar_init();
@@ -182,17 +188,29 @@ __global__ void __launch_bounds__(128 + 256 * NH, 1)
       }
       __syncwarp();
     };
+    // O += P V in two parts: the K-steps over the first kSplitP keys as soon as the softmax
+    // warps have stored that much of P (p_part), the rest after p_ready, so the PV MMAs start
+    // while the softmax finishes its last columns
     auto issue_pv = [&](int x, int j) {
       if (x == 0) ATTN_TRACE(14, j);
-      mbar_wait(&p_ready[x], j & 1);
       if (x == 0) mbar_wait(&v_full[j & 1], (j >> 1) & 1);
-      tc_fence_after();
-      ATTN_TRACE(2 + x, j);
       const uint64_t vd = sw128_desc(smem_u32(sV + (j & 1) * kKVBytes), 16384, 1024);
       const uint32_t o = tmem + 256u + x * 128u, pa = tmem + x * 128u;
+      mbar_wait(&p_part[x], j & 1);
+      tc_fence_after();
+      ATTN_TRACE(2 + x, j);
       if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < BN / 16; ++k) umma_f16_ts(o, pa + k * 8, vd + (uint64_t)(k * 128), idesc_o, (j | k) != 0);
+        for (int k = 0; k < kSplitP / 16; ++k)
+          umma_f16_ts(o, pa + k * 8, vd + (uint64_t)(k * 128), idesc_o, (j | k) != 0);
+      }
+      __syncwarp();
+      mbar_wait(&p_ready[x], j & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int k = kSplitP / 16; k < BN / 16; ++k)
+          umma_f16_ts(o, pa + k * 8, vd + (uint64_t)(k * 128), idesc_o, (j | k) != 0);
         umma_commit(&o_done[x]);
       }
       __syncwarp();
@@ -286,8 +304,17 @@ __global__ void __launch_bounds__(128 + 256 * NH, 1)
       // every 8 pairs take the polynomial exp2 on the FMA pipe.
       const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_used, -m_used);
       float2 rsa = make_float2(0.f, 0.f), rsb = make_float2(0.f, 0.f);
+      // a pending O rescale must precede every PV MMA of this block: then p_part is signalled
+      // only after the rescale below (with p_ready)
+      const bool early = NH == 1 && kSplitP < BN && !__any_sync(0xffffffffu, need);
 #pragma unroll
       for (int cc = 0; cc < W / 32; ++cc) {
+        if (early && cc == kSplitP / 32) {
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_part[x]);
+        }
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -333,7 +360,10 @@ __global__ void __launch_bounds__(128 + 256 * NH, 1)
       tc_fence_before();
       __syncwarp();
       if (wi == 0 && lane == 0) ATTN_TRACE(6 + 3 * x, j);
-      if (lane == 0) mbar_arrive(&p_ready[x]);
+      if (lane == 0) {
+        if (!early) mbar_arrive(&p_part[x]);
+        mbar_arrive(&p_ready[x]);
+      }
     };
     const int nfull = p.T / BN;
     for (int j = 0; j < nfull; ++j) block(j, std::false_type{});
