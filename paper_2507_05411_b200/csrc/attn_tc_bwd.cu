@@ -193,7 +193,8 @@ __device__ __forceinline__ void pack_store(uint32_t dst, const float2 (&v)[32]) 
 // S^T is read into registers at once (s_free), so S(u+1) is issued while tile u is still
 // being computed; P^T and dS^T (bf16 pairs) are then written over the dP^T region the half
 // has already read: P^T at columns [64 ch, 64 ch + 32), dS^T at [64 ch + 32, 64 ch + 64).
-// MMA order per tile u:  [s_free(u)] S(u+1) | [pd_ready(u)] dV(u) dK(u) dP(u+1).
+// MMA order per tile u:  [s_free(u)] S(u+1) | [p_ready(u)] dV(u) | [pd_ready(u)] dK(u) dP(u+1):
+// P^T is stored (and signalled) before dS^T is computed, so dV(u) overlaps the dS math.
 // smem: K, V, Q ring [3], dO ring [2], lse/delta ring [2] = 226 KB: this needs the dynamic
 // shared-memory base to be 1024-aligned already (checked).
 constexpr int kQSlots = 3, kGSlots = 2;
@@ -238,9 +239,10 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
   uint64_t* s_full = bars + 15;
   uint64_t* dp_full = bars + 16;
   uint64_t* s_free = bars + 17;    // the compute warps hold S^T(u) in registers
-  uint64_t* pd_ready = bars + 18;  // P^T(u) and dS^T(u) are in the dP^T region
+  uint64_t* pd_ready = bars + 18;  // dS^T(u) is in the dP^T region (after P^T)
   uint64_t* mma_done = bars + 19;
-  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 20);
+  uint64_t* p_ready = bars + 20;   // P^T(u) is in the dP^T region: dV(u) may start
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 21);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kt = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
@@ -269,6 +271,7 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
     mbar_init(dp_full, 1);
     mbar_init(s_free, 4 * NQ);
     mbar_init(pd_ready, 4 * NQ);
+    mbar_init(p_ready, 4 * NQ);
     mbar_init(mma_done, 1);
     fence_mbar_init();
   }
@@ -370,7 +373,7 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
         tc_fence_after();
         issue_s(u + 1);
       }
-      mbar_wait(pd_ready, u & 1);
+      mbar_wait(p_ready, u & 1);  // dV(u) runs while the compute warps form dS^T(u)
       tc_fence_after();
       BWD_TRACE(0, u);
       if (elect_one()) {
@@ -378,6 +381,11 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
         for (int k = 0; k < BT / 16; ++k)
           umma_f16_ts(tmem + cV, tmem + cP + packed_colq<NQ>(k), mG + (uint64_t)(k * 128), id_acc, (u | k) != 0);
         umma_commit(&g_empty[u & 1]);  // dO(u) is done (dP(u) and dV(u))
+      }
+      __syncwarp();
+      mbar_wait(pd_ready, u & 1);
+      tc_fence_after();
+      if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < BT / 16; ++k)
           umma_f16_ts(tmem + cK, tmem + cP + 64 / NQ + packed_colq<NQ>(k), mQ + (uint64_t)(k * 128), id_acc,
@@ -427,6 +435,12 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
       {
         uint32_t dv[W / 32][32];
         ldW<W>(tmem + lo + cP + col, dv);
+        // P^T first (over this group's dP^T columns, now in registers), so dV(u) starts while
+        // dS^T is formed
+        pack_storeN<NP>(tmem + lo + cP + col, pr);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_ready);
         float2 ds[NP];
 #pragma unroll
         for (int i = 0; i < NP; i += 2) {
@@ -434,7 +448,6 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
           ds[i] = fmul2(pr[i], ffma2(make_float2(d4.x, d4.y), make_float2(-1.f, -1.f), colp(dv, i)));
           ds[i + 1] = fmul2(pr[i + 1], ffma2(make_float2(d4.z, d4.w), make_float2(-1.f, -1.f), colp(dv, i + 1)));
         }
-        pack_storeN<NP>(tmem + lo + cP + col, pr);       // P^T over this group's dP^T columns
         pack_storeN<NP>(tmem + lo + cP + col + NP, ds);  // dS^T next to it
       }
       tc_fence_before();
