@@ -172,8 +172,14 @@ def main():
     ap.add_argument("--seq", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--remat", default=None,
+                    help="remat policy alias for every layer (reference mesh.py:204-252 names); default: "
+                         "save_qkvo_flash for 70b_layer (BASELINE configs[4]: FSDP + rematerialisation; the "
+                         "policy of the reference's gpu-H100 mesh rule, experiments.py:49), none otherwise")
     args = ap.parse_args()
-    defaults = {"tiny": (8, 256), "1b": (8, 4096), "7b": (2, 4096), "moe": (4, 4096), "70b_layer": (1, 4096)}
+    defaults = {"tiny": (8, 256), "1b": (8, 4096), "7b": (2, 4096), "moe": (4, 4096), "70b_layer": (2, 4096)}
+    if args.remat is None:
+        args.remat = "save_qkvo_flash" if args.config == "70b_layer" else "save_all"
     args.batch = args.batch or defaults[args.config][0]
     args.seq = args.seq or defaults[args.config][1]
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
@@ -194,6 +200,11 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     dtype = "f32" if args.config == "tiny" else "bf16"
     cfg = BENCH_CONFIGS[args.config](batch=args.batch, seq=args.seq, dtype=dtype)
+    if args.remat != "save_all":
+        from paper_2507_05411_b200.remat import POLICY_ALIASES
+
+        for i in range(len(cfg.get("model.decoder.transformer.layer"))):
+            cfg = cfg.set(f"model.decoder.transformer.layer[{i}].remat_policy", POLICY_ALIASES[args.remat])
     eng = TrainEngine(cfg, device=dev)
     V = eng.cfg.get("model.vocab_size")
     B, T = args.batch, args.seq
@@ -282,7 +293,7 @@ def main():
         "data": "synthetic (reference synthetic_batch token stream; reference init_state weights)",
         "config": {"workload": args.config, "global_batch": world * B, "per_gpu_batch": B, "seq_len": T,
                    "d_model": eng.cfg.get("model.dim"), "layers": len(eng.cfg.get("model.decoder.transformer.layer")),
-                   "vocab": V, "params": eng.param_count(), "parallelism": f"fsdp{world}",
+                   "vocab": V, "params": eng.param_count(), "parallelism": f"fsdp{world}", "remat": args.remat,
                    "l2": "inputs larger than L2 (bf16 params + activations >> 126 MB)"},
         "mfu": value * fpt / (world * NOMINAL_BF16_PFLOPS),
         "model_flops_per_token": fpt,
