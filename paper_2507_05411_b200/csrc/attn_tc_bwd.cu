@@ -505,7 +505,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* dp_full = bars + 13;
   uint64_t* ds_ready = bars + 14;
   uint64_t* mma_done = bars + 15;
-  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* ds_part = bars + 16;  // the first 32 key columns of each half's dS are in TMEM
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 17);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -530,6 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(dp_full, 1);
     mbar_init(ds_ready, 8);
+    mbar_init(ds_part, 8);
     mbar_init(mma_done, 1);
     fence_mbar_init();
   }
@@ -608,14 +610,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < nk; ++j) {
       const int st = j & 1;
       if (j + 1 < nk) issue_s(j + 1);
-      mbar_wait(ds_ready, j & 1);
-      tc_fence_after();
-      BWD_TRACE(11, j);
+      // dQ += dS K in two parts: the K-steps over the first 32 keys of each half (k = 0, 1,
+      // 4, 5) once those dS columns are stored, the rest after the whole dS pass
       const uint64_t mK = sw128_desc(smem_u32(sK + (j % kKSlots) * kTile), kBox, 1024);
+      mbar_wait(ds_part, j & 1);
+      tc_fence_after();
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < BT / 16; ++k)
-          umma_f16_ts(tmem + cQ, tmem + st * 128u + packed_col(k), mK + (uint64_t)(k * 128), id_acc, (j | k) != 0);
+          if ((k & 3) < 2)
+            umma_f16_ts(tmem + cQ, tmem + st * 128u + packed_col(k), mK + (uint64_t)(k * 128), id_acc,
+                        (j | k) != 0);
+      }
+      __syncwarp();
+      mbar_wait(ds_ready, j & 1);
+      tc_fence_after();
+      BWD_TRACE(11, j);
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < BT / 16; ++k)
+          if ((k & 3) >= 2)
+            umma_f16_ts(tmem + cQ, tmem + st * 128u + packed_col(k), mK + (uint64_t)(k * 128), id_acc, 1);
         umma_commit(&k_empty[j % kKSlots]);
       }
       __syncwarp();
@@ -661,13 +676,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       {
         uint32_t dv[2][32];
         ld64(tmem + lo + cP + ch * 64, dv);
-        float2 ds[32];
+        // dS over this half's own S columns, in two 32-column parts (ds_part after the first)
 #pragma unroll
-        for (int i = 0; i < 32; ++i) ds[i] = fmul2(pr[i], fadd2(col2(dv, i), nd2));
-        pack_store(tmem + lo + st * 128u + ch * 64, ds);  // over this half's own S columns
+        for (int part = 0; part < 2; ++part) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float2 d = fmul2(pr[16 * part + i], fadd2(col2(dv, 16 * part + i), nd2));
+            pk[i] = pack2(d.x, d.y);
+          }
+          tmem_st16(tmem + lo + st * 128u + ch * 64 + 16 * part, pk);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (part == 0 && lane == 0) mbar_arrive(ds_part);
+        }
       }
-      tc_fence_before();
-      __syncwarp();
       if (warp == 4) BWD_TRACE(15, j);
       if (lane == 0) mbar_arrive(ds_ready);
     }
