@@ -242,7 +242,8 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
   uint64_t* pd_ready = bars + 18;  // dS^T(u) is in the dP^T region (after P^T)
   uint64_t* mma_done = bars + 19;
   uint64_t* p_ready = bars + 20;   // P^T(u) is in the dP^T region: dV(u) may start
-  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 21);
+  uint64_t* ds_part = bars + 21;   // the first half of each group's dS^T(u) is stored
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 22);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kt = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
     mbar_init(s_free, 4 * NQ);
     mbar_init(pd_ready, 4 * NQ);
     mbar_init(p_ready, 4 * NQ);
+    mbar_init(ds_part, 4 * NQ);
     mbar_init(mma_done, 1);
     fence_mbar_init();
   }
@@ -383,13 +385,26 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
         umma_commit(&g_empty[u & 1]);  // dO(u) is done (dP(u) and dV(u))
       }
       __syncwarp();
+      // dK += dS^T Q in two parts: the K-steps over the first half of each group's query
+      // columns once stored (ds_part), the rest after the whole dS pass
+      constexpr int KPG = BT / 16 / NQ;  // K-steps per query-column group
+      mbar_wait(ds_part, u & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < BT / 16; ++k)
+          if (k % KPG < KPG / 2)
+            umma_f16_ts(tmem + cK, tmem + cP + 64 / NQ + packed_colq<NQ>(k), mQ + (uint64_t)(k * 128), id_acc,
+                        (u | k) != 0);
+      }
+      __syncwarp();
       mbar_wait(pd_ready, u & 1);
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < BT / 16; ++k)
-          umma_f16_ts(tmem + cK, tmem + cP + 64 / NQ + packed_colq<NQ>(k), mQ + (uint64_t)(k * 128), id_acc,
-                      (u | k) != 0);
+          if (k % KPG >= KPG / 2)
+            umma_f16_ts(tmem + cK, tmem + cP + 64 / NQ + packed_colq<NQ>(k), mQ + (uint64_t)(k * 128), id_acc, 1);
         umma_commit(&q_empty[u % kQSlots]);
       }
       __syncwarp();
@@ -441,14 +456,27 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_ready);
-        float2 ds[NP];
+        // dS^T next to it, in two halves (ds_part after the first) when a half fills whole
+        // 16-column TMEM stores
+        constexpr int kParts = NP >= 32 ? 2 : 1;
 #pragma unroll
-        for (int i = 0; i < NP; i += 2) {
-          const float4 d4 = lds4(sL + 512 + 8 * i);
-          ds[i] = fmul2(pr[i], ffma2(make_float2(d4.x, d4.y), make_float2(-1.f, -1.f), colp(dv, i)));
-          ds[i + 1] = fmul2(pr[i + 1], ffma2(make_float2(d4.z, d4.w), make_float2(-1.f, -1.f), colp(dv, i + 1)));
+        for (int part = 0; part < kParts; ++part) {
+          float2 ds[NP / kParts];
+#pragma unroll
+          for (int i = 0; i < NP / kParts; i += 2) {
+            const int c2i = part * (NP / kParts) + i;
+            const float4 d4 = lds4(sL + 512 + 8 * c2i);
+            ds[i] = fmul2(pr[c2i], ffma2(make_float2(d4.x, d4.y), make_float2(-1.f, -1.f), colp(dv, c2i)));
+            ds[i + 1] =
+                fmul2(pr[c2i + 1], ffma2(make_float2(d4.z, d4.w), make_float2(-1.f, -1.f), colp(dv, c2i + 1)));
+          }
+          pack_storeN<NP / kParts>(tmem + lo + cP + col + NP + part * (NP / kParts), ds);
+          if (part == 0) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(ds_part);
+          }
         }
-        pack_storeN<NP>(tmem + lo + cP + col + NP, ds);  // dS^T next to it
       }
       tc_fence_before();
       __syncwarp();
