@@ -8,13 +8,14 @@
 //           P^T = exp2(S^T c - lse2), dS^T = P^T (dP^T - delta)   [CUDA cores, per key row]
 //           dV += P^T dO_u        (A = P^T from TMEM, B = dO_u smem MN-major)
 //           dK += dS^T Q_u        (A = dS^T from TMEM, B = Q_u  smem MN-major)
-//         MMA issue order  dV(u) S(u+1) | dK(u) dP(u+1)  lets the exp pass of tile u+1
-//         overlap dK(u)/dP(u+1) and the dS pass overlap dV(u+1)/S(u+2) with single-buffered
-//         TMEM (S^T | dP^T | dV | dK = 512 columns).
+//         MMA issue order  S(u+1) | dV(u) | dK(u) dP(u+1): S(u+1) as soon as S^T(u) is in
+//         registers, dV(u) as soon as P^T(u) is stored, half of dK(u) after the first half of
+//         dS^T(u), so the exp and dS passes overlap the MMAs with single-buffered TMEM
+//         (S^T | dP^T | dV | dK = 512 columns).
 //   dq:   one CTA per (128-query tile, head, batch); sweeps every 128-key tile j:
 //           S_j = Q K_j^T (double-buffered), dP_j = dO V_j^T, dS = P (dP - delta),
-//           dQ += dS K_j (B = K_j MN-major); S_{j+1} is issued before dQ_j.
-//           TMEM: S[2] | dP | dQ.
+//           dQ += dS K_j (B = K_j MN-major); S_{j+1} is issued before dQ_j, half of dQ_j
+//           after the first half of dS_j.  TMEM: S[2] | dP | dQ.
 // Roles: warp 0 TMA, warp 1 MMA (single thread), warp 2 TMEM alloc, warps 4-11 compute
 // (warps w and w+4 share TMEM lane quadrant w%4 and split each tile's columns in halves).
 #include "attn.cuh"
@@ -193,8 +194,9 @@ __device__ __forceinline__ void pack_store(uint32_t dst, const float2 (&v)[32]) 
 // S^T is read into registers at once (s_free), so S(u+1) is issued while tile u is still
 // being computed; P^T and dS^T (bf16 pairs) are then written over the dP^T region the half
 // has already read: P^T at columns [64 ch, 64 ch + 32), dS^T at [64 ch + 32, 64 ch + 64).
-// MMA order per tile u:  [s_free(u)] S(u+1) | [p_ready(u)] dV(u) | [pd_ready(u)] dK(u) dP(u+1):
-// P^T is stored (and signalled) before dS^T is computed, so dV(u) overlaps the dS math.
+// MMA order per tile u:  [s_free(u)] S(u+1) | [p_ready(u)] dV(u) | [ds_part(u)] dK_a(u) |
+// [pd_ready(u)] dK_b(u) dP(u+1): P^T is stored (and signalled) before dS^T is computed, so
+// dV(u) overlaps the dS math, and dK(u) starts on the first half of each group's dS^T.
 // smem: K, V, Q ring [3], dO ring [2], lse/delta ring [2] = 226 KB: this needs the dynamic
 // shared-memory base to be 1024-aligned already (checked).
 constexpr int kQSlots = 3, kGSlots = 2;
