@@ -609,6 +609,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t dQ = sw128_desc(smem_u32(sQ), 16, 1024), dG = sw128_desc(smem_u32(sG), 16, 1024);
     auto issue_s = [&](int j) {
       const int ks = j % kKSlots;
+      BWD_TRACE(18, j);
       mbar_wait(&k_full[ks], (j / kKSlots) & 1);
       tc_fence_after();
       BWD_TRACE(10, j);

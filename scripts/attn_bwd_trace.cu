@@ -73,6 +73,9 @@ int main() {
     for (int e = 0; e < 8; ++e) printf(" %7lld", (long long)(tr[10 + e][j] - t1));
     printf("\n");
   }
+  printf("dq: k_full wait per tile (S issue ready -> K tile present), cycles:");
+  for (int j = 4; j < 12; ++j) printf(" %lld", (long long)(tr[10][j] - tr[18][j]));
+  printf("\n");
   printf("steady-state period (tiles 4..15): dkdv %.0f cycles, dq %.0f cycles\n", (tr[0][15] - tr[0][4]) / 11.0,
          (tr[11][15] - tr[11][4]) / 11.0);
   // per-CTA timeline of the last launch: CTA duration, gap to the next CTA on the same SM
