@@ -3,6 +3,7 @@
 consecutive kernels on the compute stream (with the kernel before each gap).
 
     python scripts/gap_profile.py --config moe --steps 2
+    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 scripts/gap_profile.py --config 1b
 """
 import argparse
 import os
@@ -17,7 +18,15 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="1b")
 ap.add_argument("--steps", type=int, default=2)
 args = ap.parse_args()
-dev = torch.device("cuda", 0)
+world = int(os.environ.get("WORLD_SIZE", "1"))
+rank = int(os.environ.get("RANK", "0"))
+local = int(os.environ.get("LOCAL_RANK", "0"))
+torch.cuda.set_device(local)
+dev = torch.device("cuda", local)
+if world > 1:  # under torchrun: FSDP over the ranks, rank 0 reports
+    import torch.distributed as dist
+
+    dist.init_process_group("nccl", device_id=dev)
 cfg = BENCH_CONFIGS[args.config](dtype="bf16")
 eng = TrainEngine(cfg, device=dev)
 V = eng.cfg.get("model.vocab_size")
@@ -30,6 +39,8 @@ with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) a
     for s in range(args.steps):
         eng.step(toks[3 + s])
     torch.cuda.synchronize()
+if rank != 0:
+    sys.exit(0)
 evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA and e.time_range.elapsed_us() > 0
        and "memcpy" not in e.name.lower() and "memset" not in e.name.lower()]
 by_stream = {}
