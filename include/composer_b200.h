@@ -55,10 +55,9 @@ CB_API int cb_gemm_set_path(int path);
    tiles); 2 = cluster pairs sharing the B tile via TMA multicast; 3 = CTA pair; 0 = one CTA
    per 128-row tile. */
 CB_API int cb_gemm_set_multicast(int mode);
-/* The CTA-pair GEMM's epilogues can move their rows through a per-warp shared-memory stage
- * so global accesses are coalesced.  Bit mask: 1 bf16 outputs, 2 f32 outputs, 4 f32 addend
- * (residual / accumulate) loads, 8 gated-activation backward; 1 = all; 0 = per-lane row
- * stores everywhere (A/B and tests). */
+/* The CTA-pair GEMM's epilogues move their rows through a per-warp shared-memory stage so
+ * global accesses are coalesced.  Bit mask: 1 bf16 outputs, 2 gated-activation backward;
+ * 1 = both (default); 0 = per-lane row stores everywhere (A/B and tests). */
 CB_API int cb_gemm_set_staged_epilogue(int enable);
 /* Registers a caller-owned device buffer (16-byte aligned) the CTA-pair engine may use for
    split-K partials (f32 [S][M][N]) on GEMMs whose tile count leaves the last wave mostly

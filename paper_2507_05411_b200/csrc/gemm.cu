@@ -70,9 +70,9 @@ __device__ __forceinline__ void epi_store1(const Epi& e, int r, int c, float v) 
 namespace tc {
 // 1 (default): the CTA-pair engine's epilogues go through the per-warp shared-memory stage
 // (coalesced global I/O); 0: per-lane stores (A/B and tests, cb_gemm_set_staged_epilogue)
-// bits: kStagedBf16 | kStagedF32 | kStagedAddLoads | kStagedGlu (default: bf16 + gated)
-__constant__ int g_epi_staged = 9;
-constexpr int kStagedBf16 = 1, kStagedF32 = 2, kStagedAddLoads = 4, kStagedGlu = 8;
+// bits: kStagedBf16 | kStagedGlu (default: both)
+__constant__ int g_epi_staged = 3;
+constexpr int kStagedBf16 = 1, kStagedGlu = 2;
 constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle atom of bf16 along K
 constexpr int kThreads = 256;
@@ -681,105 +681,39 @@ __device__ __forceinline__ void epi_rope(const Epi& e, uint32_t (&v)[32], int ro
   }
 }
 
-// Which staged epilogue a GEMM's output takes (0 = none: the per-lane epi_chunk path).
-// 1: bf16 out, no addend; 2: f32 out, no addend; 3: f32 out plus one f32 addend (the residual
-// R, or D itself when accumulating).  Requires every 32-column chunk to be full and 16-byte
-// aligned rows.
-__host__ __device__ __forceinline__ int staged_mode(const Epi& e) {
-  if (e.N % 32 != 0 || (e.ldd & 7) != 0 || (reinterpret_cast<uintptr_t>(e.D) & 15) != 0) return 0;
-  if (!e.d_f32) return !e.accumulate && !e.R ? 1 : 0;
-  if (!e.accumulate && !e.R) return 2;
-  if (e.accumulate && e.R) return 0;
-  if (e.R && (!e.r_f32 || (e.ldr & 3) != 0 || (reinterpret_cast<uintptr_t>(e.R) & 15) != 0)) return 0;
-  return 3;
+// Whether a GEMM's output takes the staged epilogue: bf16 output without addend (alpha and
+// RoPE allowed), whole 32-column chunks, 16-byte aligned rows.  f32 outputs keep the per-lane
+// epilogue: staging them measured ~10% slower on the O projection (each lane's eight 16-byte
+// residual loads already hit one L1 line; the stage round trips lengthen the chunk chain).
+__host__ __device__ __forceinline__ bool staged_ok(const Epi& e) {
+  return e.N % 32 == 0 && (e.ldd & 7) == 0 && (reinterpret_cast<uintptr_t>(e.D) & 15) == 0 && !e.d_f32 &&
+         !e.accumulate && !e.R;
 }
 
-// One 128-row x BN tile of this warp's 32 rows through the staged epilogue (mode from
-// staged_mode, warp-uniform).
+// One 128-row x BN tile (bf16 output) of this warp's 32 rows through the stage.
 template <int BN>
-__device__ __noinline__ void epi_tile_staged(const Epi e, int mode, uint32_t tbase, int row0, int nrows, int tn,
-                                             uint8_t* st, int lane) {
+__device__ __noinline__ void epi_tile_staged(const Epi e, uint32_t tbase, int row0, int nrows, int tn, uint8_t* st,
+                                             int lane) {
   const int row = row0 + lane;
   const int c0 = tn * BN;
-  if (mode == 1) {
-#pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
-      const int col0 = c0 + c * 32;
-      if (col0 >= e.N) break;
-      uint32_t v[32];
-      tmem_ld32(tbase + c * 32, v);
-      tmem_ld_wait_regs(v);
-      epi_rope(e, v, row, col0);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float o[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = __uint_as_float(v[j * 8 + i]) * e.alpha;
-        stage_set_own(st, lane, j, pack8(o));
-      }
-      __syncwarp();
-      __nv_bfloat16* g = reinterpret_cast<__nv_bfloat16*>(e.D) + (int64_t)row0 * e.ldd + col0;
-      stage_gstore<64>(st, lane, g, g, e.ldd * 2, nrows);
-      __syncwarp();
-    }
-    return;
-  }
-  const float* add = mode == 3 ? (e.accumulate ? reinterpret_cast<const float*>(e.D) : reinterpret_cast<const float*>(e.R))
-                               : nullptr;
-  const int64_t lda = e.accumulate ? e.ldd : e.ldr;
-  const float* arow = add ? add + (int64_t)row0 * lda : nullptr;
-  float* drow = reinterpret_cast<float*>(e.D) + (int64_t)row0 * e.ldd;
-  // the addend rows: through the stage (coalesced, kStagedAddLoads) or loaded by each lane
-  // (the 8 loads of a lane hit one 128-byte line, which L1 serves after the first)
-  const bool sload = add && (g_epi_staged & kStagedAddLoads);
-  const bool ok = row0 + lane < e.M;
-  uint4 nxt[8];
-  auto lane_load = [&](int col) {
-    if (ok) {
-      const uint4* src = reinterpret_cast<const uint4*>(arow + (int64_t)lane * lda + col);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) nxt[j] = __ldg(src + j);
-    }
-  };
-  if (sload)
-    stage_gload<128>(nxt, lane, arow + c0, arow + c0 + 16, lda * 4, nrows);
-  else if (add)
-    lane_load(c0);
 #pragma unroll 1
   for (int c = 0; c < BN / 32; ++c) {
     const int col0 = c0 + c * 32;
     if (col0 >= e.N) break;
-    uint4 cur[8];
-    if (sload) {
-      stage_put<128>(st, nxt, lane);
-      if (c + 1 < BN / 32 && col0 + 32 < e.N)
-        stage_gload<128>(nxt, lane, arow + col0 + 32, arow + col0 + 48, lda * 4, nrows);
-    } else if (add) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) cur[j] = nxt[j];
-      if (c + 1 < BN / 32 && col0 + 32 < e.N) lane_load(col0 + 32);
-    }
     uint32_t v[32];
     tmem_ld32(tbase + c * 32, v);
     tmem_ld_wait_regs(v);
     epi_rope(e, v, row, col0);
-    if (sload) __syncwarp();
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float4 o = make_float4(__uint_as_float(v[4 * j]) * e.alpha, __uint_as_float(v[4 * j + 1]) * e.alpha,
-                             __uint_as_float(v[4 * j + 2]) * e.alpha, __uint_as_float(v[4 * j + 3]) * e.alpha);
-      if (add) {
-        const uint4 a = sload ? stage_own(st, lane, j) : cur[j];
-        o.x += __uint_as_float(a.x);
-        o.y += __uint_as_float(a.y);
-        o.z += __uint_as_float(a.z);
-        o.w += __uint_as_float(a.w);
-      }
-      stage_set_own(st, lane, j, make_uint4(__float_as_uint(o.x), __float_as_uint(o.y), __float_as_uint(o.z),
-                                            __float_as_uint(o.w)));
+    for (int j = 0; j < 4; ++j) {
+      float o[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = __uint_as_float(v[j * 8 + i]) * e.alpha;
+      stage_set_own(st, lane, j, pack8(o));
     }
     __syncwarp();
-    stage_gstore<128>(st, lane, drow + col0, drow + col0 + 16, e.ldd * 4, nrows);
+    __nv_bfloat16* g = reinterpret_cast<__nv_bfloat16*>(e.D) + (int64_t)row0 * e.ldd + col0;
+    stage_gstore<64>(st, lane, g, g, e.ldd * 2, nrows);
     __syncwarp();
   }
 }
@@ -940,7 +874,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const Epi& e = args.e;
     const uint32_t tempty_leader0 = leader_addr(&tempty[0]);
     uint8_t* stg = smem + C::kStages * C::kStageBytes + 256 + q * 32 * kStagePitch;  // this warp's stage
-    const int smode = S > 1 ? 0 : staged_mode(e);
+    const bool staged = S == 1 && staged_ok(e) && (g_epi_staged & kStagedBf16);
     // gated backward through the stage: pre / dpre rows 16-byte aligned, whole 32-column chunks
     const bool glu_staged = GLU && e.glu == 2 && e.N % 32 == 0 && e.glu_h % 8 == 0 && (e.ld_glu_pre & 7) == 0 &&
                             (e.ld_glu_out & 7) == 0 && (reinterpret_cast<uintptr_t>(e.glu_pre) & 15) == 0 &&
@@ -971,8 +905,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           glu_tile<-1, -1>(gq, e.glu, tbase, row, row_ok, tn);
         }
-      } else if (smode && (g_epi_staged & (smode == 1 ? kStagedBf16 : kStagedF32))) {
-        epi_tile_staged<BN>(e, smode, tbase, row0, nrows, tn, stg, lane);
+      } else if (staged) {
+        epi_tile_staged<BN>(e, tbase, row0, nrows, tn, stg, lane);
       } else if (S > 1) {
         // split-K slice: raw f32 partial to ws[slice] (the reduce kernel applies the epilogue)
         float* part = args.ws + (int64_t)(u % S) * e.M * e.N + (int64_t)row * e.N;
@@ -1330,7 +1264,7 @@ extern "C" int cb_gemm_set_workspace(void* ptr, int64_t bytes) {
 }
 
 extern "C" int cb_gemm_set_staged_epilogue(int enable) {
-  const int v = enable < 0 ? 0 : enable == 1 ? 15 : enable;
+  const int v = enable == 1 ? 3 : enable < 0 ? 0 : enable & 3;
   if (cudaMemcpyToSymbol(tc::g_epi_staged, &v, sizeof(v)) != cudaSuccess)
     return fail(CB_ERR_CUDA, "cb_gemm_set_staged_epilogue: cudaMemcpyToSymbol failed");
   return CB_OK;
