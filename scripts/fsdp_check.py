@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--batch", type=int, default=8, help="global batch")
     ap.add_argument("--seq", type=int, default=8)
     ap.add_argument("--ckpt", default=None, help="save a sharded checkpoint here after training")
+    ap.add_argument("--decomposed", action="store_true",
+                    help="hold the update to AdamW on the GPU's own gradients instead of the oracle's parameters")
     args = ap.parse_args()
 
     import torch
@@ -62,14 +64,25 @@ def main():
     out = {"world": world, "precision": args.precision, "config": args.config, "steps": []}
     tol = 1e-5 if args.precision == "f32" else 2e-2
     ok = True
+    own_worst = 0.0  # AdamW applied in f64 to the GPU's own gradients vs the GPU's update
     for step in range(args.steps):
         toks = synthetic_batch(0, step, B, T, V)["tokens"]
         mine = toks[rank * per:(rank + 1) * per]
         loss, col = eng.compute_grads(mine)
         loss = float(loss.item())
         summ = col.flat_summaries()
-        grads = eng.grads_numpy() if step == 0 else None
+        g_all = eng.grads_numpy()
+        grads = g_all if step == 0 else None
+        p_before, o_before = eng.state_numpy(), eng.opt_state_numpy()
         eng.apply_update()
+        p_after = eng.state_numpy()
+        opt = O.AdamW(lr=eng.lr, beta1=eng.beta1, beta2=eng.beta2)
+        for (k, p0), (_, g0), (_, m0), (_, v0), (_, p1) in zip(O.leaves(p_before), O.leaves(g_all),
+                                                                O.leaves(o_before["m"]), O.leaves(o_before["v"]),
+                                                                O.leaves(p_after)):
+            exp_p, _, _ = O.adamw_update(p0.astype(np.float64), g0.astype(np.float64), m0.astype(np.float64),
+                                         v0.astype(np.float64), step + 1, opt)
+            own_worst = max(own_worst, float(np.linalg.norm(p1 - exp_p) / max(np.linalg.norm(exp_p), 1e-30)))
         lo, go, st, mm, vv, osum = O.train_step(st, toks, spec, O.AdamW(lr=eng.lr), mm, vv, step + 1)
         rec = {"loss": loss, "oracle": lo, "loss_rel": abs(loss - lo) / lo}
         ok &= rec["loss_rel"] < tol
@@ -93,7 +106,11 @@ def main():
     for (k, a), (_, b) in zip(O.leaves(params), O.leaves(st)):
         worst = max(worst, float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)))
     out["param_rel_max"] = worst
-    ok &= worst < tol
+    out["adamw_own_grads_rel_max"] = own_worst
+    # --decomposed: the update is checked against AdamW on the GPU's own gradients (the
+    # gradients themselves are held to tol above); step-1 AdamW ~ lr * sign(g) amplifies
+    # ulp-level gradient differences of near-zero entries by 1/eps (DESIGN (c)(i))
+    ok &= (own_worst < tol) if args.decomposed else (worst < tol)
     if args.ckpt:
         from paper_2507_05411_b200.checkpoint import save_checkpoint
 
