@@ -165,7 +165,7 @@ def run_reference(args) -> None:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)  # time >= 20 steps
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="1b", choices=["tiny", "1b", "7b", "moe", "70b_layer"])
     ap.add_argument("--batch", type=int, default=None, help="per-GPU batch (sequences)")

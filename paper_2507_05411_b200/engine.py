@@ -238,6 +238,16 @@ class TrainEngine:
             _lib.call("cb_gemm_set_staged_epilogue", int(os.environ["CB_GEMM_STAGED_EPILOGUE"]))
         self.options = {"precision": self.precision, "validate_ids": False,
                         "fuse_glu": os.environ.get("CB_FUSE_GLU", "1") != "0"}
+        # weight-gradient GEMMs on their own stream (layers._wgrad), at most CB_WGRAD_STREAM of
+        # them in flight; 0 keeps them on the compute stream
+        self._wgrad_stream = None
+        depth = int(os.environ.get("CB_WGRAD_STREAM", "4"))
+        if self.device.type == "cuda" and depth > 0:
+            self._wgrad_stream = torch.cuda.Stream(self.device)
+            self.options["wgrad_stream"] = self._wgrad_stream
+            self.options["wgrad_depth"] = depth
+            self.options["wgrad_wave_eff"] = float(os.environ.get("CB_WGRAD_WAVE_EFF", "0.9"))
+            self.options["wgrad_pending"] = self._wgrad_pending = []
         if self.d.world > 1:  # summaries that are global-batch statistics reduce over this group
             self.options["dp_group"] = self.d.group if self.d.group is not None else self.d.dist.group.WORLD
         if init:
@@ -513,9 +523,19 @@ class TrainEngine:
                                       options=self.options)
         if provider:
             provider.finish_backward()
+        if self._wgrad_stream is not None:
+            self._join_wgrad(torch.cuda.current_stream(self.device))
+            self._wgrad_pending.clear()  # operands released after the compute stream's wait
         if self.d.world > 1:
             self.d.dist.all_reduce(loss, op=self.d.dist.ReduceOp.AVG, group=self.d.group)
         return loss, col
+
+    def _join_wgrad(self, stream) -> None:
+        """`stream` waits for every weight-gradient GEMM issued so far (layers._wgrad)."""
+        if self._wgrad_stream is not None and stream is not None:
+            ev = torch.cuda.Event()
+            ev.record(self._wgrad_stream)
+            stream.wait_event(ev)
 
     def _adamw_bucket(self, i: int) -> None:
         b, rec = self.buckets[i], self.bufs[i]
@@ -577,6 +597,7 @@ class FSDPProvider(ParamProvider):
         ready.record(self.compute)
         with torch.cuda.stream(self.comm):
             self.comm.wait_event(ready)
+            self.e._join_wgrad(self.comm)
             if b.replicated:
                 self.dist.all_reduce(rec["grad"], op=self.dist.ReduceOp.AVG, group=self.group)
             else:
@@ -637,6 +658,7 @@ class LocalUpdateProvider(ParamProvider):
         ready.record(self.compute)
         with torch.cuda.stream(self.side):
             self.side.wait_event(ready)
+            self.e._join_wgrad(self.side)
             self.e._adamw_bucket(i)
         self.done.add(i)
 

@@ -145,10 +145,50 @@ def _linear_fwd(x2: torch.Tensor, w: torch.Tensor, out_dtype: torch.dtype) -> to
     return ops.gemm(x2, w, out)
 
 
+def _wave_efficiency(m: int, n: int, tile: int = 256, units: int = 74) -> float:
+    """Busy fraction of the CTA-pair GEMM's waves for an m x n output (256 x 256 tiles over
+    74 SM pairs): 1B step QKV / wo wgrad 0.86, w2 0.79, w1|w1_gate 0.95; 7B wo 0.86, others >= 0.93."""
+    tiles = -(-m // tile) * -(-n // tile)
+    waves = -(-tiles // units)
+    return tiles / (waves * units)
+
+
+def _wgrad(x2: torch.Tensor, dy: torch.Tensor, dw: torch.Tensor) -> None:
+    """dw += x2^T dy.  With the engine's weight-gradient stream (option "wgrad_stream") the
+    product runs there, beside the data-gradient chain: weight gradients have few output tiles
+    (1B step: QKV 192, w2 176, wo 64 CTA-pair tiles over 74 pairs, K = all tokens), so their
+    last wave leaves SMs idle that the next data-gradient / attention kernel fills.  Only those
+    whose waves are less than option "wgrad_wave_eff" busy go there: on the power-capped B200
+    the extra concurrency lowers the SM clock (7B step with every wgrad on the side stream:
+    -1%, 1376 -> 1316 MHz), so it pays only where there is a real tail to fill.  At most
+    option "wgrad_depth" weight gradients are in flight: beyond that the compute stream waits
+    for the oldest, whose operands are then released in compute-stream order (no record_stream:
+    its deferred frees made the caching allocator thrash on the memory-tight 7B step).  The
+    engine's update / reduce-scatter of a bucket waits for this stream (engine._join_wgrad)."""
+    ws = option("wgrad_stream")
+    if ws is not None and _wave_efficiency(dw.shape[0], dw.shape[1]) >= option("wgrad_wave_eff", 0.9):
+        ws = None  # a full last wave: nothing to fill, and concurrent kernels only raise power
+    if ws is None:
+        ops.gemm(x2, dy, dw, trans_a=True, accumulate=True)
+        return
+    cur = torch.cuda.current_stream(x2.device)
+    pending = option("wgrad_pending")  # [(done event, operands)] of the GEMMs in flight
+    while len(pending) >= option("wgrad_depth", 1):
+        cur.wait_event(pending.pop(0)[0])
+    ready = torch.cuda.Event()
+    ready.record(cur)
+    ws.wait_event(ready)
+    with torch.cuda.stream(ws):
+        ops.gemm(x2, dy, dw, trans_a=True, accumulate=True)
+    done = torch.cuda.Event()
+    done.record(ws)
+    pending.append((done, (x2, dy)))
+
+
 def _linear_bwd(x2: torch.Tensor, w: torch.Tensor, dy: torch.Tensor, dw: torch.Tensor | None, dx_dtype):
     """dw += x^T dy ; returns dx = dy w^T (dy already in the operand dtype)."""
     if dw is not None:
-        ops.gemm(x2, dy, dw, trans_a=True, accumulate=True)
+        _wgrad(x2, dy, dw)
     dx = torch.empty((dy.shape[0], w.shape[0]), device=dy.device, dtype=dx_dtype)
     return ops.gemm(dy, w, dx, trans_b=True)
 
@@ -629,7 +669,7 @@ class FeedForwardBehavior(Behavior):
             dpre = ops.gemm_gated_bwd(g, param("w2"), pre, pair[0], pair[1])
         if dpre is not None:
             if dw2 is not None:
-                ops.gemm(s["hidden"], g, dw2, trans_a=True, accumulate=True)
+                _wgrad(s["hidden"], g, dw2)
         else:
             dhidden = _linear_bwd(s["hidden"], param("w2"), g, dw2, adt)
             dpre = torch.empty_like(pre)

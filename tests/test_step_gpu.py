@@ -191,6 +191,24 @@ def test_remat_policies_are_exact(cuda, policy):
         assert np.array_equal(outs[0][1][k], outs[1][1][k]), k
 
 
+def test_wgrad_stream_is_exact(cuda, monkeypatch):
+    """Weight gradients on the side stream (CB_WGRAD_STREAM, layers._wgrad) run the same
+    deterministic GEMMs: two AdamW steps give bit-identical losses and parameters."""
+    from paper_2507_05411_b200 import TrainEngine, set_dtype_policy, synthetic_batch
+
+    cfg = set_dtype_policy(_mid(128), "bf16")
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("CB_WGRAD_STREAM", flag)
+        eng = TrainEngine(cfg, device="cuda:0")
+        assert (eng._wgrad_stream is not None) == (flag == "1")
+        losses = [float(eng.step(synthetic_batch(0, s, 4, 256, 512)["tokens"])[0].item()) for s in range(2)]
+        outs.append((losses, dict(_leaves(eng.state_numpy()))))
+    assert outs[0][0] == outs[1][0]
+    for k in outs[0][1]:
+        assert np.array_equal(outs[0][1][k], outs[1][1][k]), k
+
+
 def test_two_steps_train(cuda):
     """Multi-step: oracle and engine stay within tolerance after 3 AdamW steps (f32)."""
     from paper_2507_05411_b200 import TrainEngine, build_experiment, init_state, instantiate, root_key, synthetic_batch
