@@ -135,6 +135,11 @@ CB_API int cb_act_bwd(int64_t rows, int cols, int act0, int act1, const void* a,
 CB_API int cb_copy2d(int64_t rows, int cols, const void* in, int64_t ldi, int in_dtype, void* out, int64_t ldo,
                      int out_dtype, float alpha, int accumulate, void* stream);
 CB_API int cb_memset_zero(void* ptr, int64_t bytes, void* stream);
+/* out[i] = scale * sum_q parts[q][i] for q = 0..nparts-1 in order (1 <= nparts <= 8; f32;
+ * n % 4 == 0; 16-byte aligned).  `parts` is a HOST array of nparts device pointers.  The
+ * local half of the FSDP gradient reduce-scatter (replaces the reduce in NCCL's
+ * reduce_scatter_tensor(AVG); the reference has no distributed step). */
+CB_API int cb_sum_parts(int nparts, int64_t n, const void* parts, void* out, float scale, void* stream);
 
 /* ---------------------------------------------------------------------------------
  * Attention (layers.py:282-348), unmasked, flash-style (P never stored).  q/k/v/o

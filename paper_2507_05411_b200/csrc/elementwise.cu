@@ -309,3 +309,49 @@ extern "C" int cb_memset_zero(void* ptr, int64_t bytes, void* stream) {
   if (e != cudaSuccess) return fail(CB_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
   return CB_OK;
 }
+
+// ---- FSDP gradient reduce-scatter, local half -------------------------------------------
+// out[i] = scale * sum_q parts[q][i], q = 0..nparts-1 in order (every rank sums its slice in
+// rank order: deterministic).  The peers' slices arrive by copy-engine reads of their
+// symmetric-memory gradient buffers (engine.FSDPProvider._rs); this is the only SM work of
+// the reduce-scatter.  HBM-bound: (nparts + 1) * 4 bytes per element.
+struct SumParts {
+  const float* p[8];
+};
+
+__global__ void __launch_bounds__(256) sum_parts_k(SumParts s, int nparts, int64_t n4, float* __restrict__ out,
+                                                   float scale) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 a = __ldcs(reinterpret_cast<const float4*>(s.p[0]) + i);
+    for (int q = 1; q < nparts; ++q) {
+      const float4 b = __ldcs(reinterpret_cast<const float4*>(s.p[q]) + i);
+      a.x += b.x;
+      a.y += b.y;
+      a.z += b.z;
+      a.w += b.w;
+    }
+    a.x *= scale;
+    a.y *= scale;
+    a.z *= scale;
+    a.w *= scale;
+    reinterpret_cast<float4*>(out)[i] = a;
+  }
+}
+
+extern "C" int cb_sum_parts(int nparts, int64_t n, const void* parts, void* out, float scale, void* stream) {
+  if (n <= 0) return CB_OK;
+  if (nparts < 1 || nparts > 8) return fail(CB_ERR_SHAPE, "sum_parts: nparts %d not in [1, 8]", nparts);
+  if (n % 4) return fail(CB_ERR_SHAPE, "sum_parts: n %lld not a multiple of 4", (long long)n);
+  SumParts s{};
+  const float* const* hp = reinterpret_cast<const float* const*>(parts);
+  for (int q = 0; q < nparts; ++q) {
+    s.p[q] = hp[q];
+    if (reinterpret_cast<uintptr_t>(hp[q]) & 15) return fail(CB_ERR_SHAPE, "sum_parts: part %d not 16-byte aligned", q);
+  }
+  if (reinterpret_cast<uintptr_t>(out) & 15) return fail(CB_ERR_SHAPE, "sum_parts: out not 16-byte aligned");
+  const int64_t n4 = n / 4;
+  const int blocks = (int)std::min<int64_t>((n4 + 255) / 256, 148 * 8);
+  sum_parts_k<<<blocks, 256, 0, (cudaStream_t)stream>>>(s, nparts, n4, (float*)out, scale);
+  return check_launch("sum_parts");
+}

@@ -261,6 +261,9 @@ class TrainEngine:
         # profiles/r01s3_ce_gather_ab/); CB_FSDP_CE_GATHER=0 gathers with NCCL
         self._ce_gather = (N > 1 and dev.type == "cuda" and self.d.world > 1
                            and os.environ.get("CB_FSDP_CE_GATHER", "1") == "1")
+        # gradient reduce-scatter as copy-engine reads of the peers' slices + a local in-order
+        # sum (cb_sum_parts); CB_FSDP_CE_REDUCE=0 reduce-scatters with NCCL
+        self._ce_reduce = self._ce_gather and N <= 8 and os.environ.get("CB_FSDP_CE_REDUCE", "1") == "1"
         self.bufs = []
         for b in self.buckets:
             if b.replicated:
@@ -279,7 +282,10 @@ class TrainEngine:
                     work = _symm_mem().empty(total, dtype=self.work_dtype, device=dev).zero_()
                 else:
                     work = torch.zeros(total, device=dev, dtype=self.work_dtype)
-                grad = torch.zeros(total, device=dev, dtype=torch.float32)
+                if self._ce_reduce:
+                    grad = _symm_mem().empty(total, dtype=torch.float32, device=dev).zero_()
+                else:
+                    grad = torch.zeros(total, device=dev, dtype=torch.float32)
                 grad_shard = grad if N == 1 else torch.zeros(shard, device=dev, dtype=torch.float32)
                 rec = dict(total=total, shard=shard, master=master, work=work, grad=grad, grad_shard=grad_shard)
             rec["m"] = torch.zeros(rec["shard"], device=dev, dtype=torch.float32)
@@ -290,6 +296,11 @@ class TrainEngine:
             for b, rec in zip(self.buckets, self.bufs):
                 if not b.replicated:
                     rec["symm"] = _symm_mem().rendezvous(rec["work"], group)
+                    if self._ce_reduce:
+                        rec["gsymm"] = _symm_mem().rendezvous(rec["grad"], group)
+            if self._ce_reduce:  # the peers' slices of one bucket's gradient, read before the sum
+                big = max(r["shard"] for b, r in zip(self.buckets, self.bufs) if not b.replicated)
+                self._rs_stage = torch.empty((N - 1) * big, device=dev, dtype=torch.float32)
         self.state = _skeleton(self.module)
         self.grads = _skeleton(self.module)
         for b, rec in zip(self.buckets, self.bufs):
@@ -626,6 +637,24 @@ class FSDPProvider(ParamProvider):
             self.e._join_wgrad(self.comm)
             if b.replicated:
                 self.dist.all_reduce(rec["grad"], op=self.dist.ReduceOp.AVG, group=self.group)
+            elif rec.get("gsymm") is not None:
+                # barrier 1: every peer's backward of this bucket is complete (its comm stream
+                # joined its compute and weight-gradient streams first); barrier 2: every peer
+                # has read this rank's slices before they are cleared for the next step
+                h, N, r, s = rec["gsymm"], self.e.d.world, self.e.d.rank, rec["shard"]
+                grad, stage = rec["grad"], self.e._rs_stage
+                h.barrier(channel=0)
+                parts, j = [], 0
+                for q in range(N):
+                    if q == r:
+                        parts.append(grad[r * s:(r + 1) * s])
+                    else:
+                        slot = stage[j * s:(j + 1) * s]
+                        slot.copy_(h.get_buffer(q, (rec["total"],), torch.float32)[r * s:(r + 1) * s])
+                        parts.append(slot)
+                        j += 1
+                h.barrier(channel=0)
+                ops.sum_parts(parts, rec["grad_shard"], 1.0 / N)
             else:
                 self.dist.reduce_scatter_tensor(rec["grad_shard"], rec["grad"], op=self.dist.ReduceOp.AVG,
                                                 group=self.group)

@@ -269,6 +269,19 @@ def act_bwd(a, g, dout, da, dg, act0: str, act1: str = "linear"):
               ld(dg) if dg is not None else 0, dt(a), stream_ptr())
 
 
+def sum_parts(parts: list, out: torch.Tensor, scale: float = 1.0) -> torch.Tensor:
+    """out = scale * sum(parts) in list order (f32, deterministic; cb_sum_parts)."""
+    import ctypes
+
+    for t in parts:
+        if t.dtype != torch.float32 or out.dtype != torch.float32 or t.numel() != out.numel():
+            raise ShapeError("sum_parts: f32 parts of out's size expected")
+    ptrs = (ctypes.c_void_p * len(parts))(*[t.data_ptr() for t in parts])
+    _lib.call("cb_sum_parts", len(parts), out.numel(), ctypes.addressof(ptrs), out.data_ptr(), float(scale),
+              stream_ptr())
+    return out
+
+
 def copy2d(src: torch.Tensor, dst: torch.Tensor, alpha: float = 1.0, accumulate: bool = False):
     s2, d2 = rows2d(src), rows2d(dst)
     if s2.shape != d2.shape:

@@ -224,3 +224,25 @@ def test_adamw_kernel(cuda):
         pn, mn, vn = O.adamw_update(pn, gr.double().numpy(), mn, vn, step, O.AdamW(1e-3, weight_decay=0.01))
     assert np.abs(P.cpu().double().numpy() - pn).max() < 1e-6
     assert torch.equal(bf, P.to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("nparts", [1, 2, 4, 8])
+def test_sum_parts_in_order(cuda, nparts):
+    """cb_sum_parts (local half of the FSDP reduce-scatter): scale * sum of the parts in list
+    order, bit-identical to the same-order f32 sum."""
+    import torch
+
+    from paper_2507_05411_b200 import ops
+
+    g = torch.Generator(device="cuda").manual_seed(nparts)
+    n = 1 << 20
+    parts = [torch.randn(n, device="cuda", generator=g) for _ in range(nparts)]
+    out = torch.empty(n, device="cuda")
+    ops.sum_parts(parts, out, 1.0 / nparts)
+    ref = parts[0].clone()
+    for t in parts[1:]:
+        ref += t
+    ref *= 1.0 / nparts
+    assert torch.equal(out, ref)
+    with pytest.raises(Exception):
+        ops.sum_parts(parts, torch.empty(n - 1, device="cuda"))
