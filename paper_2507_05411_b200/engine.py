@@ -264,6 +264,18 @@ class TrainEngine:
         # gradient reduce-scatter as copy-engine reads of the peers' slices + a local in-order
         # sum (cb_sum_parts); CB_FSDP_CE_REDUCE=0 reduce-scatters with NCCL
         self._ce_reduce = self._ce_gather and N <= 8 and os.environ.get("CB_FSDP_CE_REDUCE", "1") == "1"
+        if self._ce_gather:
+            # probe once: a box whose driver cannot map peer memory raises here on every rank
+            # alike, and the step keeps NCCL collectives (same results, SM-holding kernels)
+            try:
+                group = self.d.group if self.d.group is not None else self.d.dist.group.WORLD
+                probe = _symm_mem().empty(16, dtype=torch.float32, device=dev)
+                _symm_mem().rendezvous(probe, group)
+            except Exception as exc:  # noqa: BLE001
+                import warnings
+
+                warnings.warn(f"symmetric memory unavailable ({exc}); FSDP collectives use NCCL")
+                self._ce_gather = self._ce_reduce = False
         self.bufs = []
         for b in self.buckets:
             if b.replicated:
