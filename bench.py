@@ -142,9 +142,11 @@ def run_reference(args) -> None:
         return
     from paper_2507_05411_b200 import BENCH_CONFIGS
 
-    for _ in range(args.warmup):
+    # each sample is ~8 s of CPU work: at most 1 warm-up and 5 timed samples, so any
+    # --steps / --warmup the driver passes ends within a few minutes
+    for _ in range(min(args.warmup, 1)):
         cpu_sample(args.config)
-    vals = [cpu_sample(args.config) for _ in range(args.steps)]
+    vals = [cpu_sample(args.config) for _ in range(max(1, min(args.steps, 5)))]
     v = statistics.median(x["value"] for x in vals)
     cfg = BENCH_CONFIGS[args.config](batch=args.batch, seq=args.seq)
     line = {
@@ -155,7 +157,7 @@ def run_reference(args) -> None:
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "global_batch": args.batch * args.gpus, "seq_len": args.seq,
                    "d_model": cfg.get("model.dim"), "layers": len(cfg.get("model.decoder.transformer.layer"))},
-        "cpu_baseline": {**vals[-1], "value": v},
+        "cpu_baseline": {**vals[-1], "value": v, "samples_timed": len(vals)},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -294,6 +296,10 @@ def main():
         "config": {"workload": args.config, "global_batch": world * B, "per_gpu_batch": B, "seq_len": T,
                    "d_model": eng.cfg.get("model.dim"), "layers": len(eng.cfg.get("model.decoder.transformer.layer")),
                    "vocab": V, "params": eng.param_count(), "parallelism": f"fsdp{world}", "remat": args.remat,
+                   "collectives": ("none" if world == 1 else
+                                   ("all-gather " + ("copy-engine/symm-mem" if eng._ce_gather else "nccl")
+                                    + ", reduce-scatter " + ("copy-engine/symm-mem + cb_sum_parts"
+                                                             if eng._ce_reduce else "nccl"))),
                    "l2": "inputs larger than L2 (bf16 params + activations >> 126 MB)"},
         "mfu": value * fpt / (world * NOMINAL_BF16_PFLOPS),
         "model_flops_per_token": fpt,
