@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark of the decoder training step (BASELINE.json metric: train tokens/s + MFU).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1b] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 7b] [--impl ours|reference]
 
 N > 1 is launched by torchrun (one process per GPU, NCCL); every rank runs the same
 per-GPU batch (weak scaling) with FSDP-sharded state.  One step = forward + backward +
@@ -9,10 +9,22 @@ AdamW over one synthetic batch of [batch, seq] tokens.  Timing: 
 steps, then K steps bracketed by barrier + synchronize, CUDA events on the compute
 stream, max over ranks.  Rank 0 prints one JSON line.
 
---impl reference times the CPU restatement of the reference step (oracle/, float64,
-fwd+bwd+AdamW — the reference itself has no backward) on this host's cores, on a
-bounded sample of the same workload, and prints the same JSON line with
-"impl": "reference".
+The default workload is BASELINE.json configs[2], the Llama2-7B-shaped step (the
+north-star config; 2 x 4096 tokens per GPU); --config 1b selects configs[1].
+
+--impl reference times the REFERENCE's own CPU step — ``composer.invoke`` (forward +
+loss; the reference has no backward or optimizer) of the unmodified reference installed
+in oracle/_ref (oracle/build_ref.sh) — on this host's cores, on a bounded sample of the
+same workload (one TransformerLayer + the head at batch 1, seq 4096, extrapolated in
+depth; oracle/ref_step.py), and prints the same JSON line with "impl": "reference".  When
+oracle/_ref is missing it times the oracle/ float64 port (fwd+bwd+AdamW) instead and says
+so in cpu_baseline.kind ("port").
+
+Kernel attribution: the profiled steps run under CUPTI kernel activity (torch.profiler),
+which sees every stream; each kernel's duration is split evenly with the kernels that
+overlap it in time, so the per-kind attributed milliseconds sum to the GPU-busy time of
+the step (never more than ms_per_step).  roofline.achieved uses the GEMM launches' own
+CUPTI durations (algorithmic FLOPs / summed launch time).
 """
 
 from __future__ import annotations
@@ -136,17 +148,31 @@ def cpu_sample(config: str, seconds_hint: float = 20.0) -> dict:
                       f"to {L} layers ({t_full:.1f} s per {seq}-token step)"}
 
 
+def reference_sample(config: str) -> dict:
+    """One bounded sample of the reference's own CPU step (oracle/ref_step.py), or of the
+    oracle port when the reference is not installed in oracle/_ref."""
+    from oracle import ref_step
+
+    if not ref_step.available():
+        out = cpu_sample(config)
+        out["sample"] = "oracle/_ref missing: " + out["sample"]
+        return out
+    threads = os.cpu_count() or 1
+    out = ref_step.reference_sample(config)
+    return {"value": out["value"], "unit": "tokens/s", "cores": threads, "kind": "reference",
+            "sample": out["sample"] + f"; numpy/OpenBLAS on {threads} host threads"}
+
+
 def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from paper_2507_05411_b200 import BENCH_CONFIGS
 
-    # each sample is ~8 s of CPU work: at most 1 warm-up and 5 timed samples, so any
-    # --steps / --warmup the driver passes ends within a few minutes
-    for _ in range(min(args.warmup, 1)):
-        cpu_sample(args.config)
-    vals = [cpu_sample(args.config) for _ in range(max(1, min(args.steps, 5)))]
+    # a 7B sample is ~40 s of CPU work (1B ~14 s): no warm-up (numpy has nothing to warm)
+    # and at most 3 timed samples, so any --steps / --warmup the driver passes ends within a
+    # few minutes
+    vals = [reference_sample(args.config) for _ in range(max(1, min(args.steps, 3)))]
     v = statistics.median(x["value"] for x in vals)
     cfg = BENCH_CONFIGS[args.config](batch=args.batch, seq=args.seq)
     line = {
@@ -163,13 +189,71 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ kernel attribution
+def kernel_kind(name: str) -> str:
+    n = name
+    if "cb::" not in n:
+        return "foreign (" + ("nccl" if "nccl" in n.lower() else "torch") + ")"
+    if "gemm" in n:
+        return "gemm"
+    if "tca::" in n or "fa::fwd" in n or "attn_fwd" in n:
+        return "attn_fwd"
+    if "tcb::" in n or "fa::" in n or "attn" in n:
+        return "attn_bwd"
+    for key in ("xent", "adamw", "rmsnorm", "embed", "moe", "router", "sum_parts", "init"):
+        if key in n:
+            return key
+    return "other_cb"
+
+
+def cupti_attribution(fn) -> tuple[dict, float]:
+    """Runs fn() under CUPTI kernel activity; returns ({kind: {launches, busy_ms,
+    attributed_ms}}, span_ms).  attributed_ms splits every instant evenly among the kernels
+    running at that instant (all streams), so Σ attributed_ms = GPU-busy time <= span."""
+    import torch
+
+    with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    ks = [(e.time_range.start, e.time_range.end, kernel_kind(e.name)) for e in prof.events()
+          if e.device_type == torch.autograd.DeviceType.CUDA and e.time_range.elapsed_us() > 0
+          and "memcpy" not in e.name.lower() and "memset" not in e.name.lower()]
+    out: dict = {}
+    if not ks:
+        return out, 0.0
+    for s0, e0, k in ks:
+        d = out.setdefault(k, {"launches": 0, "busy_ms": 0.0, "attributed_ms": 0.0})
+        d["launches"] += 1
+        d["busy_ms"] += (e0 - s0) / 1e3
+    # sweep line over the start/end points of every kernel (all streams)
+    pts = sorted({t for s0, e0, _ in ks for t in (s0, e0)})
+    idx = {t: i for i, t in enumerate(pts)}
+    kinds = sorted(out)
+    delta = {k: [0] * len(pts) for k in kinds}
+    for s0, e0, k in ks:
+        delta[k][idx[s0]] += 1
+        delta[k][idx[e0]] -= 1
+    running = {k: 0 for k in kinds}
+    for i in range(len(pts) - 1):
+        for k in kinds:
+            running[k] += delta[k][i]
+        total = sum(running.values())
+        if total:
+            dt = (pts[i + 1] - pts[i]) / 1e3 / total
+            for k in kinds:
+                if running[k]:
+                    out[k]["attributed_ms"] += dt * running[k]
+    span = (max(e0 for _, e0, _ in ks) - min(s0 for s0, _, _ in ks)) / 1e3
+    return out, span
+
+
 # --------------------------------------------------------------------------- GPU leg
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)  # SURVEY §8(d): time >= 20 steps
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="1b", choices=["tiny", "1b", "7b", "moe", "70b_layer"])
+    ap.add_argument("--config", default="7b", choices=["tiny", "1b", "7b", "moe", "70b_layer"])
     ap.add_argument("--batch", type=int, default=None, help="per-GPU batch (sequences)")
     ap.add_argument("--seq", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -250,18 +334,23 @@ def main():
     tokens_step = world * B * T
     value = tokens_step / (ms / 1e3)
 
-    # ---- kernel shares: the same steps again with CUDA events around GEMM / attention launches
-    prof = ops.KernelProfiler()
-    ops.set_profiler(prof)
-    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    p0.record(stream)
-    for s in range(min(args.steps, 3)):
-        eng.step(devtok[args.warmup + s])
-    p1.record(stream)
-    ops.set_profiler(None)
+    mem_peak = torch.cuda.max_memory_allocated(dev)
+
+    # ---- kernel shares: the same steps again under CUPTI kernel activity (all streams);
+    # the Python-side tally gives the algorithmic FLOPs of the GEMM / attention launches
+    prof = ops.KernelProfiler(events=False)
+    nprof = min(args.steps, 3)
+
+    def profiled_steps():
+        ops.set_profiler(prof)
+        for s in range(nprof):
+            eng.step(devtok[args.warmup + s])
+        ops.set_profiler(None)
+
     barrier()
-    kern = prof.summary()
-    prof_ms = p0.elapsed_time(p1)
+    cupti, span_ms = cupti_attribution(profiled_steps)
+    barrier()
+    tally = prof.summary()
 
     # ---- end to end through the public API: host tokens in, loss out, every step
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -280,14 +369,29 @@ def main():
         return
     pk, pk_src = peaks()
     fpt = flops_per_token(eng.module, B, T)
-    g = kern.get("gemm_bf16") or kern.get("gemm_f32") or {"flops": 0, "ms": 1.0, "launches": 0}
-    achieved = g["flops"] / (g["ms"] / 1e3) / 1e12
+    gflops = sum(v["flops"] for k, v in tally.items() if k.startswith("gemm"))
+    g = cupti.get("gemm", {"launches": 0, "busy_ms": 0.0, "attributed_ms": 0.0})
+    achieved = gflops / (g["busy_ms"] / 1e3) / 1e12 if g["busy_ms"] else 0.0
     peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
     traffic = None
     tpath = os.path.join(REPO, "profiles", "gemm_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
-            traffic = json.load(fh).get("bytes_per_launch")
+            tj = json.load(fh)
+        if tj.get("workload") == args.config:
+            traffic = tj.get("bytes_per_launch")
+    flops_by_kind = {"gemm": gflops, "attn_fwd": tally.get("attn_fwd", {}).get("flops", 0),
+                     "attn_bwd": tally.get("attn_bwd", {}).get("flops", 0)}
+    kernels = {}
+    for k, v in sorted(cupti.items(), key=lambda kv: -kv[1]["attributed_ms"]):
+        row = {"launches_per_step": v["launches"] / nprof, "busy_ms_per_step": v["busy_ms"] / nprof,
+               "attributed_ms_per_step": v["attributed_ms"] / nprof}
+        if flops_by_kind.get(k):
+            row["tflops"] = flops_by_kind[k] / (v["busy_ms"] / 1e3) / 1e12
+        kernels[k] = row
+    from paper_2507_05411_b200.memory import aot_device_bytes
+
+    aot = aot_device_bytes(eng.module, world * B, T, world)
     line = {
         "metric": "train tokens/sec and MFU per B200, decoder step",
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -307,17 +411,28 @@ def main():
         "roofline": {"bound": "tensor", "kernel": "gemm_tc2 (tcgen05 CTA-pair persistent GEMM)", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "peak_source": f"{pk_src} bf16_tflops_sustained (kernel timed inside the step)",
+                     "achieved_how": "algorithmic GEMM FLOPs of the profiled steps / the GEMM launches' summed CUPTI "
+                                     "kernel durations",
                      "traffic": traffic,
-                     "share_of_step": g["ms"] / prof_ms if prof_ms else None},
-        "kernels": {k: {"launches": v["launches"], "ms_per_step": v["ms"] / min(args.steps, 3),
-                        "tflops": v["flops"] / (v["ms"] / 1e3) / 1e12 if v["ms"] else None} for k, v in kern.items()},
+                     "traffic_source": ("ncu --set full constant (profiles/gemm_traffic.json: DRAM read+write of one "
+                                        "launch of this workload's QKV GEMM), not measured by this run"
+                                        if traffic is not None else None),
+                     "share_of_step": g["attributed_ms"] / span_ms if span_ms else None},
+        "kernels": kernels,
+        "kernels_note": ("CUPTI kernel activity over %d steps; attributed_ms splits overlapping kernels evenly, so "
+                         "the attributed column sums to the busy time of the profiled span (%.1f ms/step)"
+                         % (nprof, span_ms / nprof)),
+        "memory": {"max_allocated_gb": mem_peak / 1e9, "engine_state_gb": eng.state_bytes() / 1e9,
+                   "aot_analyze_per_device_gb": aot["per_device_bytes"] / 1e9,
+                   "aot_analyze_saved_activation_gb": aot["saved_activation_bytes"] / 1e9,
+                   "aot_formula": aot["formula"]},
         "clocks": clocks,
         "gpu_launches": launches,
         "e2e": {"value": tokens_step / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": B * T * 8,
                 "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms},
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_sample(args.config)
+        line["cpu_baseline"] = reference_sample(args.config)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

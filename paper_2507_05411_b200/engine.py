@@ -35,7 +35,7 @@ import torch
 
 from . import _lib, ops
 from .config import ConfigNode, visit
-from .errors import ShapeError, TypeMismatchError
+from .errors import MeshError, ShapeError, TypeMismatchError
 from .module import Module, ParamProvider, instantiate, invoke, iter_param_specs, value_and_grad
 from .prng import child_key, root_key
 
@@ -75,6 +75,25 @@ def set_dtype_policy(cfg: ConfigNode, tag: str) -> ConfigNode:
     for p in targets:
         cfg = cfg.set(f"{p}.dtype" if p else "dtype", tag)
     return cfg
+
+
+DP_AXES = ("data", "fsdp")
+
+
+def check_mesh(cfg: ConfigNode) -> None:
+    """The step is data-parallel (FSDP over the batch): a mesh axis other than data/fsdp
+    with a size other than 1 — e.g. the reference's gpu-H100 rule fsdp=-1, model=8
+    (experiments.py:48) — would need tensor/expert parallelism, which this path does not
+    implement, so it is rejected instead of silently running as data parallelism."""
+    if not (cfg.has_field("mesh_axis_names") and cfg.has_field("mesh_shape")):
+        return
+    names, sizes = tuple(cfg.get("mesh_axis_names")), tuple(cfg.get("mesh_shape"))
+    if len(names) != len(sizes):
+        raise MeshError(f"mesh_shape {sizes} does not match mesh_axis_names {names}")
+    for n, sz in zip(names, sizes):
+        if n not in DP_AXES and int(sz) != 1:
+            raise MeshError(f"mesh axis {n!r} of size {sz}: only data/fsdp axes are supported on this path "
+                            f"(tensor/expert parallelism is not implemented)")
 
 
 def _align(n: int, a: int = ALIGN) -> int:
@@ -194,6 +213,22 @@ def _skeleton(module: Module) -> dict:
     return tree
 
 
+def _on_device(fn):
+    """Runs an engine entry point with its device current, so ops.stream_ptr() (the current
+    device's current stream) and every launch target the engine's GPU even when it is not
+    the caller's current device."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(self, *args, **kwargs):
+        if self.device.type != "cuda":
+            return fn(self, *args, **kwargs)
+        with torch.cuda.device(self.device):
+            return fn(self, *args, **kwargs)
+
+    return wrapper
+
+
 class _Dist:
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -213,6 +248,7 @@ class TrainEngine:
         self.cfg = cfg
         self.module = instantiate(cfg)
         self.cfg = self.module.config
+        check_mesh(self.cfg)
         self.precision = precision or model_precision(self.cfg)
         if self.precision not in ("f32", "bf16"):
             raise TypeMismatchError(f"precision {self.precision!r} unsupported")
@@ -264,9 +300,13 @@ class TrainEngine:
         # gradient reduce-scatter as copy-engine reads of the peers' slices + a local in-order
         # sum (cb_sum_parts); CB_FSDP_CE_REDUCE=0 reduce-scatters with NCCL
         self._ce_reduce = self._ce_gather and N <= 8 and os.environ.get("CB_FSDP_CE_REDUCE", "1") == "1"
+        if self._ce_gather and int(os.environ.get("LOCAL_WORLD_SIZE", N)) != N:
+            self._ce_gather = self._ce_reduce = False  # peers on another node: no peer mapping
         if self._ce_gather:
-            # probe once: a box whose driver cannot map peer memory raises here on every rank
-            # alike, and the step keeps NCCL collectives (same results, SM-holding kernels)
+            # probe once, then agree: every rank takes the same collective path (a rank whose
+            # driver cannot map peer memory would otherwise sit in NCCL while its peers spin
+            # in a symmetric-memory barrier)
+            ok = 1
             try:
                 group = self.d.group if self.d.group is not None else self.d.dist.group.WORLD
                 probe = _symm_mem().empty(16, dtype=torch.float32, device=dev)
@@ -274,7 +314,14 @@ class TrainEngine:
             except Exception as exc:  # noqa: BLE001
                 import warnings
 
-                warnings.warn(f"symmetric memory unavailable ({exc}); FSDP collectives use NCCL")
+                warnings.warn(f"symmetric memory unavailable on rank {self.d.rank} ({exc})")
+                ok = 0
+            flag = torch.tensor([ok], device=dev, dtype=torch.int32)
+            self.d.dist.all_reduce(flag, op=self.d.dist.ReduceOp.MIN, group=self.d.group)
+            if int(flag.item()) == 0:
+                import warnings
+
+                warnings.warn("symmetric memory unavailable on some rank; FSDP collectives use NCCL")
                 self._ce_gather = self._ce_reduce = False
         self.bufs = []
         for b in self.buckets:
@@ -320,6 +367,20 @@ class TrainEngine:
                 _tree_set(self.state, e.path, e.name, _view(rec["work"], e))
                 _tree_set(self.grads, e.path, e.name, _view(rec["grad"], e))
 
+    def state_bytes(self) -> int:
+        """Bytes of every persistent per-rank buffer the engine owns (master/work/grad/m/v,
+        shard and staging buffers; each storage counted once)."""
+        seen, total = set(), 0
+        tensors = [t for rec in self.bufs for t in rec.values() if isinstance(t, torch.Tensor)]
+        tensors += [t for t in (getattr(self, "_rs_stage", None),) if t is not None]
+        tensors += [t for t in getattr(self, "_grad_ring", []) if isinstance(t, torch.Tensor)]
+        for t in tensors:
+            key = t.untyped_storage().data_ptr()
+            if key not in seen:
+                seen.add(key)
+                total += t.untyped_storage().nbytes()
+        return total
+
     def param_count(self) -> int:
         return sum(int(np.prod(e.shape)) for b in self.buckets for e in b.entries)
 
@@ -344,6 +405,7 @@ class TrainEngine:
             full = torch.from_numpy(host).to(self.device)
             ops.copy2d(full.view(1, -1), rec["work"].view(1, -1))
 
+    @_on_device
     def init_params(self, key) -> None:
         """Reference-identical init, generated on the device (init.cu: numpy's PCG64 stream
         reproduced bit-exactly from each tensor's key).  Kinds without a declarative
@@ -383,6 +445,7 @@ class TrainEngine:
         if fallback:
             self.init_params_host(key)
 
+    @_on_device
     def init_params_host(self, key) -> None:
         """Reference-identical init (init_state semantics) generated on the host, tensor by tensor."""
         from .module import param_key  # noqa: F401
@@ -408,12 +471,14 @@ class TrainEngine:
             key = child_key(key, seg, 0)
         return key
 
+    @_on_device
     def load_state(self, state: dict) -> None:
         """Loads a reference-layout numpy state tree (e.g. from the reference's init_state)."""
         for b, rec in zip(self.buckets, self.bufs):
             self._host_bucket(b, rec, lambda e: _tree_get(state, e.path, e.name))
         torch.cuda.synchronize(self.device)
 
+    @_on_device
     def load_opt_state(self, opt_state: dict | None) -> None:
         """AdamW state in the reference's tree layout: {"m": tree, "v": tree, "step": int}
         (None resets to the zero state of step 0)."""
@@ -450,6 +515,7 @@ class TrainEngine:
         self.d.dist.all_gather_into_tensor(full, buf, group=self.d.group)
         return full
 
+    @_on_device
     def _export(self, which: str) -> dict:
         out: dict = {}
         for b, rec in zip(self.buckets, self.bufs):
@@ -470,6 +536,7 @@ class TrainEngine:
     def state_numpy(self) -> dict:
         return self._export("master")
 
+    @_on_device
     def grads_numpy(self) -> dict:
         """Full (all-reduced) gradients of the last compute_grads call."""
         if self.d.world > 1:
@@ -494,6 +561,7 @@ class TrainEngine:
     def step_key(self, step: int):
         return child_key(root_key(self.seed), "step", step)
 
+    @_on_device
     def loss(self, tokens, step: int | None = None, key=None, collection: bool = False):
         """Forward-only loss (the reference's invoke(module, state, key, batch) result); with
         collection=True also the OutputCollection (summaries)."""
@@ -517,6 +585,7 @@ class TrainEngine:
             return float(t.item())
         return out
 
+    @_on_device
     def compute_grads(self, tokens, update: bool = False, key=None):
         """Forward + backward; gradients land in the (sharded) grad buffers.  Returns (loss, collection).
 
@@ -584,11 +653,13 @@ class TrainEngine:
         if bf is None and wshard.data_ptr() != rec["master"].data_ptr():
             ops.copy2d(rec["master"].view(1, -1), wshard.view(1, -1))
 
+    @_on_device
     def apply_update(self) -> None:
         self.step_count += 1
         for i in range(len(self.buckets)):
             self._adamw_bucket(i)
 
+    @_on_device
     def step(self, tokens):
         """One training step: forward, backward and the AdamW update (overlapped with backward)."""
         return self.compute_grads(tokens, update=True)
@@ -631,11 +702,11 @@ class FSDPProvider(ParamProvider):
                 # earlier on its comm stream, has written its shard; the second: every peer has
                 # read this rank's shard before the next step's AdamW overwrites it.
                 N, work = self.e.d.world, rec["work"]
-                h.barrier(channel=0)
+                h.barrier(channel=0, timeout_ms=_BARRIER_TIMEOUT_MS)
                 for k in range(1, N):
                     p = (r + k) % N
                     work[p * s:(p + 1) * s].copy_(h.get_buffer(p, (rec["total"],), work.dtype)[p * s:(p + 1) * s])
-                h.barrier(channel=0)
+                h.barrier(channel=0, timeout_ms=_BARRIER_TIMEOUT_MS)
             done = torch.cuda.Event()
             done.record(self.comm)
         self.gathered[i] = done
@@ -655,7 +726,7 @@ class FSDPProvider(ParamProvider):
                 # has read this rank's slices before they are cleared for the next step
                 h, N, r, s = rec["gsymm"], self.e.d.world, self.e.d.rank, rec["shard"]
                 grad, stage = rec["grad"], self.e._rs_stage
-                h.barrier(channel=0)
+                h.barrier(channel=0, timeout_ms=_BARRIER_TIMEOUT_MS)
                 parts, j = [], 0
                 for q in range(N):
                     if q == r:
@@ -665,7 +736,7 @@ class FSDPProvider(ParamProvider):
                         slot.copy_(h.get_buffer(q, (rec["total"],), torch.float32)[r * s:(r + 1) * s])
                         parts.append(slot)
                         j += 1
-                h.barrier(channel=0)
+                h.barrier(channel=0, timeout_ms=_BARRIER_TIMEOUT_MS)
                 ops.sum_parts(parts, rec["grad_shard"], 1.0 / N)
             else:
                 self.dist.reduce_scatter_tensor(rec["grad_shard"], rec["grad"], op=self.dist.ReduceOp.AVG,
@@ -745,6 +816,11 @@ class LocalUpdateProvider(ParamProvider):
         fin = torch.cuda.Event()
         fin.record(self.side)
         self.compute.wait_event(fin)
+
+
+# symmetric-memory barriers time out (the kernel traps) instead of spinning forever when a
+# peer has died; generous, because a peer may legitimately be a whole layer behind
+_BARRIER_TIMEOUT_MS = int(os.environ.get("CB_SYMM_BARRIER_TIMEOUT_MS", "120000"))
 
 
 def _symm_mem():

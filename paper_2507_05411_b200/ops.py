@@ -48,13 +48,15 @@ def rows2d(t: torch.Tensor) -> torch.Tensor:
 
 # ----------------------------------------------------------------- launch profiler
 class KernelProfiler:
-    """Records CUDA events around selected launches on the launching (current) stream.
+    """Tallies the algorithmic FLOPs of selected launches (bench.py).
 
-    Used by bench.py to measure the dominant kernels' achieved FLOP/s live inside the
-    timed step; records are (kind, algorithmic_flops, start_event, end_event).
+    Records are (kind, algorithmic_flops, start_event, end_event); with ``events=False``
+    (bench.py's default: kernel durations come from CUPTI kernel activity instead, which
+    sees every stream) the events are None and only launches/FLOPs are counted.
     """
 
-    def __init__(self):
+    def __init__(self, events: bool = True):
+        self.events = events
         self.records: list = []
 
     def summary(self) -> dict:
@@ -64,7 +66,8 @@ class KernelProfiler:
             d = out.setdefault(kind, {"launches": 0, "flops": 0, "ms": 0.0})
             d["launches"] += 1
             d["flops"] += flops
-            d["ms"] += s.elapsed_time(e)
+            if s is not None:
+                d["ms"] += s.elapsed_time(e)
         return out
 
 
@@ -78,6 +81,9 @@ def set_profiler(p: KernelProfiler | None) -> None:
 
 def _profiled(kind: str, flops: int, fn, *args):
     if _PROFILER is None:
+        return fn(*args)
+    if not _PROFILER.events:
+        _PROFILER.records.append((kind, flops, None, None))
         return fn(*args)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()

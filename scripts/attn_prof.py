@@ -1,4 +1,4 @@
-"""Runs the attention kernels once at the 1B step shape (for ncu captures)."""
+"""Runs the attention kernels twice at a step shape (1b | 7b | 70b; for ncu captures)."""
 import math
 import os
 import sys
@@ -8,7 +8,8 @@ import torch
 
 from paper_2507_05411_b200 import ops
 
-B, T, H, KVH, hd = 8, 4096, 16, 16, 128
+SHAPES = {"1b": (8, 4096, 16, 16, 128), "7b": (2, 4096, 32, 32, 128), "70b": (1, 4096, 64, 8, 128)}
+B, T, H, KVH, hd = SHAPES[sys.argv[1] if len(sys.argv) > 1 else "1b"]
 d, kvd = H * hd, KVH * hd
 dev = torch.device("cuda")
 qkv = torch.randn(B * T, d + 2 * kvd, device=dev).bfloat16()

@@ -132,6 +132,29 @@ def main():
                      "weights": dec.weights.tolist(), "dispatch": dec.dispatch_fractions.tolist(),
                      "mean_probs": dec.mean_probs.tolist(), "lbl": load_balance_loss(dec)}
 
+    # Linear with bias (layers.py:130-170): reference invoke on a given state, and central
+    # differences of sum(y * dy) for a few weight / bias / input entries
+    lin = instantiate(default_config("Linear").set("input_dim", 16).set("output_dim", 24).set("bias", True))
+    lx = rng.standard_normal((2, 3, 16))
+    lst = {"weight": rng.standard_normal((16, 24)) * 0.25, "bias": rng.standard_normal(24) * 0.1}
+    ldy = rng.standard_normal((2, 3, 24))
+    ly, _ = invoke(lin, lst, root_key(0), lx)
+
+    def lin_obj(st, x):
+        return float(np.sum(invoke(lin, st, root_key(0), x)[0] * ldy))
+
+    fd = {}
+    for name, idx in (("weight", (3, 5)), ("weight", (15, 23)), ("bias", (7,)), ("x", (1, 2, 9))):
+        vals = []
+        for sgn in (1.0, -1.0):
+            st2 = {k: v.copy() for k, v in lst.items()}
+            x2 = lx.copy()
+            (x2 if name == "x" else st2[name])[idx] += sgn * 1e-6
+            vals.append(lin_obj(st2, x2))
+        fd[f"{name}{list(idx)}"] = (vals[0] - vals[1]) / 2e-6
+    gold["linear"] = {"x": lx.tolist(), "weight": lst["weight"].tolist(), "bias": lst["bias"].tolist(),
+                      "dy": ldy.tolist(), "y": np.asarray(ly).tolist(), "fd": fd}
+
     base_picks = [
         ("model.decoder.emb.weight", (3, 5)),
         ("model.decoder.emb.weight", (44, 0)),

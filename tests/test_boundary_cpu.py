@@ -178,3 +178,45 @@ def test_checkpoint_plan_and_retention():
     assert gc_retained([1, 2, 3, 4, 5, 6], GcPolicy(keep_last_n=2, keep_every_k=3)) == {3, 5, 6}
     with pytest.raises(ValueError):
         GcPolicy()
+
+
+def _reference_package():
+    """The unmodified reference (oracle/_ref, or /root/reference in the build container)."""
+    import sys
+
+    for p in (os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(p, "composer")):
+            if p not in sys.path:
+                sys.path.insert(0, p)
+            import composer
+
+            return composer
+    pytest.skip("reference package not available")
+
+
+@pytest.mark.parametrize("name,devices,policy", [("7b", 1, None), ("7b", 4, None), ("1b", 8, "save_qkvo_flash"),
+                                                 ("moe", 2, "recompute_all"), ("1b", 2, "offload_dots")])
+def test_memory_plan_matches_reference_aot_analyze(name, devices, policy):
+    """memory.aot_device_bytes == the reference's aot_analyze (mesh.py:563-686) on the bench
+    configs: same golden text parsed by the reference, a catalog row with `devices` GPUs."""
+    R = _reference_package()
+    from composer.mesh import DeviceSpec, aot_analyze
+
+    from paper_2507_05411_b200 import BENCH_CONFIGS, instantiate, serialize_golden
+    from paper_2507_05411_b200.memory import aot_device_bytes
+    from paper_2507_05411_b200.remat import POLICY_ALIASES
+
+    cfg = BENCH_CONFIGS[name]()
+    if policy:
+        for i in range(len(cfg.get("model.decoder.transformer.layer"))):
+            cfg = cfg.set(f"model.decoder.transformer.layer[{i}].remat_policy", POLICY_ALIASES[policy])
+    cfg = cfg.set("mesh_shape", (devices,)).set("mesh_axis_names", ("fsdp",)).set("mesh_rules", ())
+    B, T = cfg.get("batch_size") * devices, cfg.get("seq_len")
+    cat = {"b200": DeviceSpec("b200", devices=devices, hbm_bytes=180_000_000_000, peak_flops=2.25e15,
+                              interconnect_bps=9e11, hostlink_bps=6.4e10)}
+    rep = aot_analyze(R.parse_golden(serialize_golden(cfg)), "b200", B, T, catalog=cat)
+    mine = aot_device_bytes(instantiate(cfg), B, T, devices)
+    assert mine["param_bytes"] == rep.param_bytes
+    assert mine["optimizer_bytes"] == rep.optimizer_bytes
+    assert mine["saved_activation_bytes"] == rep.saved_activation_bytes
+    assert mine["per_device_bytes"] == rep.per_device_bytes

@@ -107,7 +107,9 @@ def test_attention_fwd_bwd(cuda, B, T, H, KVH, hd, dt, path):
     P = torch.softmax(Q @ K.repeat_interleave(rep, 1).transpose(-1, -2) * scale, -1)
     O = P @ Vv.repeat_interleave(rep, 1)
     O.backward(do.double().view(B, T, H, hd).transpose(1, 2))
-    tol = 1e-5 if dt == torch.float32 else 2e-2
+    # bf16: identical bf16 inputs, so the error is the kernels' own rounding (bf16 O, P and dS
+    # operands of the second GEMMs, f32 accumulation): ~3e-3 expected
+    tol = 1e-5 if dt == torch.float32 else 5e-3
     assert _rel(o.view(B, T, H, hd).transpose(1, 2), O.detach()) < tol
     assert _rel(dqkv[:, :d].view(B, T, H, hd).transpose(1, 2), Q.grad) < tol
     assert _rel(dqkv[:, d:d + kvd].view(B, T, KVH, hd).transpose(1, 2), K.grad) < tol
@@ -246,3 +248,39 @@ def test_sum_parts_in_order(cuda, nparts):
     assert torch.equal(out, ref)
     with pytest.raises(Exception):
         ops.sum_parts(parts, torch.empty(n - 1, device="cuda"))
+
+
+@pytest.mark.parametrize("precision", ["f32", "bf16"])
+def test_linear_with_bias_matches_reference(cuda, precision):
+    """a15: Linear with bias (reference layers.py:130-170) through the module API on the GPU:
+    forward equals the reference's invoke output and the gradients equal the reference's
+    central finite differences (tests/golden: `linear`) and the f64 closed form."""
+    import json
+    import os
+
+    from paper_2507_05411_b200 import default_config, instantiate, root_key
+    from paper_2507_05411_b200.module import value_and_grad
+
+    lg = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_goldens.json")))["linear"]
+    m = instantiate(default_config("Linear").set("input_dim", 16).set("output_dim", 24).set("bias", True))
+    wdt = torch.float32 if precision == "f32" else torch.bfloat16
+    x = np.array(lg["x"])
+    W, b, dy = np.array(lg["weight"]), np.array(lg["bias"]), np.array(lg["dy"])
+    state = {"weight": torch.tensor(W, dtype=wdt, device=cuda), "bias": torch.tensor(b, dtype=torch.float32, device=cuda)}
+    grads = {"weight": torch.zeros(16, 24, device=cuda), "bias": torch.zeros(24, device=cuda)}
+    xt = torch.tensor(x, dtype=torch.float32, device=cuda)
+    y, _, dx = value_and_grad(m, state, grads, root_key(0), xt, seed_grad=torch.tensor(dy, dtype=torch.float32, device=cuda),
+                              options={"precision": precision})
+    torch.cuda.synchronize()
+    tol = 1e-5 if precision == "f32" else 2e-2
+    y = y.double().cpu().numpy()
+    assert _rel(torch.tensor(y), torch.tensor(np.array(lg["y"]))) < tol
+    gw, gb, gx = grads["weight"].double().cpu().numpy(), grads["bias"].double().cpu().numpy(), dx.double().cpu().numpy()
+    x2, dy2 = x.reshape(-1, 16), dy.reshape(-1, 24)
+    assert _rel(torch.tensor(gw), torch.tensor(x2.T @ dy2)) < tol
+    assert _rel(torch.tensor(gb), torch.tensor(dy2.sum(0))) < tol
+    assert _rel(torch.tensor(gx), torch.tensor(dy @ W.T)) < tol
+    fd = lg["fd"]
+    for key, got in (("weight[3, 5]", gw[3, 5]), ("weight[15, 23]", gw[15, 23]), ("bias[7]", gb[7]),
+                     ("x[1, 2, 9]", gx[1, 2, 9])):
+        assert abs(got - fd[key]) <= 1e-6 + (1e-5 if precision == "f32" else 2e-2) * abs(fd[key]), key

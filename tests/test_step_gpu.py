@@ -10,6 +10,7 @@ import os
 
 import numpy as np
 import pytest
+import torch
 
 from oracle import decoder_oracle as O
 
@@ -34,27 +35,46 @@ def _leaves(t, pre=""):
             yield p, v
 
 
-def run_parity(cfg, precision, B, T, tol, seed=0, check_update=True, decomposed=True, loose=None):
-    """decomposed: compare updated params with AdamW applied (in f64) to the GPU's own
-    gradients.  Step-1 AdamW is ~lr*sign(g) and amplifies ulp-level gradient differences
-    of elements with |g| ~ eps=1e-8 by 1/eps, so on some shapes the
-    end-to-end param check measures that conditioning, not the kernels; the gradients
-    themselves are still held to `tol` against the oracle.
+def fp32_oracle_errors(st, toks, spec, opt, forced=None):
+    """Per-tensor error of a plain fp32 restatement (the oracle run in torch float32) against
+    the f64 oracle, for gradients and step-1 updated parameters: what fp32 arithmetic itself
+    permits.  Step-1 AdamW is ~lr*sign(g): gradient entries with |g| ~ eps=1e-8 turn ulp-level
+    differences into lr-sized parameter changes, so on some shapes fp32 itself misses 1e-5 on
+    the updated parameters (profiles/r02_f32_oracle_error.txt)."""
+    _, g64, _ = O.value_and_grad(st, toks, spec, forced)
+    _, g32, _ = O.value_and_grad(st, toks, spec, forced, dtype=torch.float32)
+    g64, g32, st0 = dict(_leaves(g64)), dict(_leaves(g32)), dict(_leaves(st))
+
+    def upd(g, k):
+        return O.adamw_update(st0[k], g, 0 * st0[k], 0 * st0[k], 1, opt)[0]
+
+    return ({k: _rel(g32[k], g64[k]) for k in g64}, {k: _rel(upd(g32[k], k), upd(g64[k], k)) for k in g64})
+
+
+def run_parity(cfg, precision, B, T, tol, seed=0, check_update=True, loose=None, exact_routing=False, report=None):
+    """Loss, every gradient and every updated parameter vs the f64 oracle (relative L2).
+
+    f32 mode: each tensor is held to 1e-5, or — only where a plain fp32 restatement itself
+    misses 1e-5 (fp32_oracle_errors) — to 3x that fp32 error.
+    bf16 mode: 2e-2; MoE layers are compared at the GPU's expert choices (bf16 router inputs
+    flip ~0.5% of top-k choices against the f64 oracle), unless exact_routing.
+    exact_routing: the GPU's top-k indices must equal the oracle's bit for bit.
     loose: {substring: tol} for tensors with a documented, larger bf16 error."""
+    import torch
+
     from paper_2507_05411_b200 import TrainEngine, init_state, instantiate, root_key, set_dtype_policy, synthetic_batch
 
     cfg = set_dtype_policy(cfg, precision)
     eng = TrainEngine(cfg, device="cuda:0", seed=seed)
     V = eng.cfg.get("model.vocab_size")
     toks = synthetic_batch(seed, 0, B, T, V)["tokens"]
-    if precision == "bf16":
-        eng.options["record_routing"] = True
+    eng.options["record_routing"] = True
     loss, col = eng.compute_grads(toks)
     loss = float(loss.item())
-    forced = {}
+    routing = {}
     for key, vals in col.flat_summaries().items():
-        if key.endswith("/route_indices"):  # bf16: compare at the GPU's routing decisions
-            forced[int(key.split("layer[")[1].split("]")[0])] = np.asarray(vals[0]).astype(np.int64)
+        if key.endswith("/route_indices"):
+            routing[int(key.split("layer[")[1].split("]")[0])] = np.asarray(vals[0]).astype(np.int64)
     grads = dict(_leaves(eng.grads_numpy()))
     eng.apply_update()
     params = dict(_leaves(eng.state_numpy()))
@@ -62,30 +82,37 @@ def run_parity(cfg, precision, B, T, tol, seed=0, check_update=True, decomposed=
     m = instantiate(cfg)
     st = init_state(m, root_key(seed))
     spec = O.spec_from_config(m.config)
-    lo, go, po, _, _, summ = O.train_step(st, toks, spec, O.AdamW(lr=eng.lr, beta1=eng.beta1, beta2=eng.beta2),
-                                          forced_routing=forced or None)
+    opt = O.AdamW(lr=eng.lr, beta1=eng.beta1, beta2=eng.beta2)
+    forced = routing if (precision == "bf16" and not exact_routing) else None
+    oracle_routing = {}
+    lo, go, po, _, _, summ = O.train_step(st, toks, spec, opt, forced_routing=forced or None, routing=oracle_routing)
+    if exact_routing:
+        assert set(routing) == set(oracle_routing)
+        for i in routing:
+            assert np.array_equal(routing[i], oracle_routing[i]), f"layer {i}: top-k differs from the oracle"
     go, po = dict(_leaves(go)), dict(_leaves(po))
     assert set(grads) == set(go)
     assert abs(loss - lo) / abs(lo) < tol, (loss, lo)
     loose = loose or {}
-
-    def tol_for(k):
-        return max([tol] + [v for s, v in loose.items() if s in k])
-
-    bad = [(_rel(grads[k], go[k]), k) for k in go if _rel(grads[k], go[k]) >= tol_for(k)]
-    assert not bad, f"grad {sorted(bad)[-3:]}"
+    gbound = {k: tol for k in go}
+    pbound = dict(gbound)
+    if precision == "f32":
+        e_g, e_p = fp32_oracle_errors(st, toks, spec, opt, forced)
+        gbound = {k: max(tol, 3 * e_g[k]) for k in go}
+        pbound = {k: max(tol, 3 * e_p[k]) for k in go}
+    for k in go:
+        for sub, v in loose.items():
+            if sub in k:
+                gbound[k], pbound[k] = max(gbound[k], v), max(pbound[k], v)
+    gerr = {k: _rel(grads[k], go[k]) for k in go}
+    perr = {k: _rel(params[k], po[k]) for k in po}
+    if report is not None:
+        report.update({"loss": abs(loss - lo) / abs(lo), "grad": gerr, "param": perr})
+    bad = sorted((gerr[k], gbound[k], k) for k in go if gerr[k] >= gbound[k])
+    assert not bad, f"grad {bad[-3:]}"
     if check_update:
-        # (1) the update itself: AdamW applied in f64 to the GPU's own gradients — held to tol
-        st0 = dict(_leaves(st))
-        pd = {k: O.adamw_update(st0[k], grads[k], 0 * st0[k], 0 * st0[k], 1,
-                                O.AdamW(lr=eng.lr, beta1=eng.beta1, beta2=eng.beta2))[0] for k in st0}
-        worst_d = max(((_rel(params[k], pd[k]), k) for k in pd))
-        assert worst_d[0] < tol, f"param (update of GPU grads) {worst_d}"
-        # (2) end to end vs the oracle's own update: step-1 AdamW ~ lr*sign(g) turns ulp-level
-        # gradient differences of |g| ~ eps entries into lr-sized flips, so in f32 mode this
-        # is held to 1e-4 (gradients themselves are held to `tol` above)
-        worst_p = max(((_rel(params[k], po[k]), k) for k in po))
-        assert worst_p[0] < (tol if decomposed is None else max(tol, 1e-4)), f"param {worst_p}"
+        bad = sorted((perr[k], pbound[k], k) for k in po if perr[k] >= pbound[k])
+        assert not bad, f"param {bad[-3:]}"
     flat = col.flat_summaries()
     for k, v in summ.items():
         assert abs(flat[k][0] - v) <= max(tol, 1e-6) * abs(v), (k, flat[k], v)
@@ -114,12 +141,28 @@ def test_registry_step_bf16(cuda, name):
 
 
 def test_bf16_relu_d32_characterization(cuda):
-    """Known bf16 limit: on the d=32 ReLU stack with 32 tokens the worst tensor (a norm
-    scale gradient: a 32-term sum with cancellation) sits at ~6% — the 2e-2 contract is
-    held on the SwiGLU/RoPE/MoE configs and the aligned fast-path configs instead."""
-    from paper_2507_05411_b200 import build_experiment
+    """Known bf16 limit, shown to be intrinsic to bf16 operands: on the d=32 ReLU stack with 32
+    tokens a few tensors sit above 2e-2 (pre-activations near ReLU's kink change sign when the
+    GEMM operands are rounded to bf16).  The oracle with ONLY its GEMM operands rounded to bf16
+    (O.bf16_operands: the least rounding any bf16 path does) has the same error (~7% on
+    feed_forward.w1), so every tensor is held to 2e-2 or to 2x that bf16-operand oracle's own
+    error, whichever is larger."""
+    from paper_2507_05411_b200 import build_experiment, init_state, instantiate, root_key, synthetic_batch
 
-    run_parity(build_experiment("txf_d32_l2_relu"), "bf16", 4, 8, 1e-1)
+    cfg = build_experiment("txf_d32_l2_relu")
+    m = instantiate(cfg)
+    st = init_state(m, root_key(0))
+    spec = O.spec_from_config(m.config)
+    toks = synthetic_batch(0, 0, 4, 8, m.config.get("model.vocab_size"))["tokens"]
+    _, g64, _ = O.value_and_grad(st, toks, spec)
+    with O.bf16_operands():
+        _, gb, _ = O.value_and_grad(st, toks, spec)
+    g64, gb = dict(_leaves(g64)), dict(_leaves(gb))
+    emu = {k: _rel(gb[k], g64[k]) for k in g64}
+    assert max(emu.values()) > 2e-2  # the limit is the operand rounding itself
+    loose = {k: 2 * e for k, e in emu.items() if 2 * e > 2e-2}
+    rep = {}
+    run_parity(cfg, "bf16", 4, 8, 2e-2, loose=loose, report=rep)
 
 
 def _mid(hd: int, kind="FeedForward"):
@@ -141,7 +184,7 @@ def test_fast_path_step_bf16(cuda, hd):
 
 @pytest.mark.parametrize("hd", [64, 128])
 def test_fast_path_shape_f32(cuda, hd):
-    run_parity(_mid(hd), "f32", 2, 128, 1e-5, decomposed=True)
+    run_parity(_mid(hd), "f32", 2, 128, 1e-5)
 
 
 def test_fast_path_moe_bf16(cuda):
@@ -152,6 +195,83 @@ def test_fast_path_moe_bf16(cuda):
     tests/test_layers.py:352-359); every tensor is then held to 2e-2.  Bit-exact routing on
     identical inputs is tested in test_kernels_gpu.py::test_moe_router_topk_bit_exact."""
     run_parity(_mid(128, "MoE"), "bf16", 4, 128, 2e-2)
+
+
+def test_moe_f32_unforced_routing_t256(cuda):
+    """f32 MoE at T=256 with the GPU's OWN routing: the top-2 expert choices of every token equal
+    the f64 oracle's bit for bit (reference route_tokens, layers.py:432-443: stable argsort,
+    ties -> lowest id), and every tensor is held to the f32 contract."""
+    run_parity(_mid(128, "MoE"), "f32", 2, 256, 1e-5, exact_routing=True)
+
+
+def _gqa(hd: int, heads: int, kv_heads: int, layers: int = 2):
+    """GroupedQueryAttention (the 70B-layer kind) in a small trainer; d = heads * hd."""
+    from paper_2507_05411_b200 import default_config
+    from paper_2507_05411_b200.experiments import transformer_trainer
+
+    d = heads * hd
+    cfg = transformer_trainer(d, layers, ("linear", "silu"), pos_kind="RoPE", heads=heads, vocab=512)
+    for i in range(layers):
+        p = f"model.decoder.transformer.layer[{i}]"
+        cfg = (cfg.set(f"{p}.self_attention", default_config("GroupedQueryAttention").set("num_kv_heads", kv_heads)
+                       .set("num_heads", heads).set("pos_emb", default_config("RoPE")))
+               .set(f"{p}.feed_forward.hidden_dim", 768))
+    return cfg
+
+
+@pytest.mark.parametrize("hd,heads,kv", [(64, 4, 1), (64, 8, 2), (128, 4, 1), (128, 4, 2), (128, 8, 2)])
+@pytest.mark.parametrize("precision", ["f32", "bf16"])
+def test_gqa_engine_step(cuda, hd, heads, kv, precision):
+    """N1: the GQA kind through TrainEngine against the oracle (which repeats each kv head over
+    its group of query heads, oracle/decoder_oracle.py attention)."""
+    T = 128 if precision == "f32" else 256
+    run_parity(_gqa(hd, heads, kv), precision, 2, T, 1e-5 if precision == "f32" else 2e-2)
+
+
+def test_gqa_with_kv_equal_heads_is_the_reference_attention(cuda):
+    """GroupedQueryAttention with num_kv_heads == num_heads is exactly the reference's Attention
+    (layers.py:282-348): same parameters (same init keys), bit-identical loss and gradients."""
+    from paper_2507_05411_b200 import TrainEngine, synthetic_batch
+    from paper_2507_05411_b200.experiments import transformer_trainer
+
+    toks = synthetic_batch(0, 0, 2, 128, 512)["tokens"]
+    mha = transformer_trainer(256, 2, ("linear", "silu"), pos_kind="RoPE", heads=2, vocab=512)
+    for i in range(2):
+        mha = mha.set(f"model.decoder.transformer.layer[{i}].feed_forward.hidden_dim", 768)
+    outs = []
+    for cfg in (mha, _gqa(128, 2, 2)):
+        eng = TrainEngine(cfg, device="cuda:0")
+        loss, _ = eng.compute_grads(toks)
+        outs.append((float(loss.item()), dict(_leaves(eng.grads_numpy()))))
+    assert outs[0][0] == outs[1][0]
+    assert set(outs[0][1]) == set(outs[1][1])
+    for k in outs[0][1]:
+        assert np.array_equal(outs[0][1][k], outs[1][1][k]), k
+
+
+@pytest.mark.parametrize("act", ["sigmoid", "tanh", "linear", ("tanh", "sigmoid"), ("relu", "linear")])
+@pytest.mark.parametrize("precision", ["f32", "bf16"])
+def test_activation_table_step(cuda, act, precision):
+    """a11: every entry of the activation table (layers.py:55-77), plain and gated, end to end
+    against the oracle."""
+    from paper_2507_05411_b200.experiments import transformer_trainer
+
+    cfg = transformer_trainer(256, 2, act, pos_kind="RoPE", heads=2, vocab=512)
+    for i in range(2):
+        cfg = cfg.set(f"model.decoder.transformer.layer[{i}].feed_forward.hidden_dim", 768)
+    run_parity(cfg, precision, 2, 128, 1e-5 if precision == "f32" else 2e-2)
+
+
+@pytest.mark.parametrize("policy", ["recompute_all", "save_qkvo_flash", "offload_dots"])
+@pytest.mark.parametrize("precision", ["f32", "bf16"])
+def test_remat_policy_against_oracle(cuda, policy, precision):
+    """f2: a rematerialised step against the oracle directly (not only against no-remat)."""
+    from paper_2507_05411_b200.remat import POLICY_ALIASES
+
+    cfg = _mid(128)
+    for i in range(2):
+        cfg = cfg.set(f"model.decoder.transformer.layer[{i}].remat_policy", POLICY_ALIASES[policy])
+    run_parity(cfg, precision, 2, 128 if precision == "f32" else 256, 1e-5 if precision == "f32" else 2e-2)
 
 
 def test_tiny_bench_config_bf16(cuda):
