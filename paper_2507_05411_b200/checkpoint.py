@@ -239,7 +239,6 @@ def load_checkpoint(eng, root: str, step: int | None = None) -> int:
     checkpoint (the newest one when step is None), at this engine's world size."""
     import torch
 
-    from . import ops
     from .errors import ShapeError
 
     steps = list_steps(root)
@@ -269,9 +268,7 @@ def load_checkpoint(eng, root: str, step: int | None = None) -> int:
             r0 = 0 if b.replicated else eng.d.rank * rec["shard"]
             dst = rec["master"] if part == "master" else rec[part]
             dst.copy_(torch.from_numpy(vals[r0:r0 + rec["shard"]]).to(eng.device))
-        if rec["work"] is not rec["master"]:
-            full_master = eng._gather_full(rec["master"], rec)
-            ops.copy2d(full_master.view(1, -1), rec["work"].view(1, -1))
+        eng._refresh_work(i)  # own working-copy slice; peers' slices are gathered by the next step
     eng.step_count = int(meta["step"])
     torch.cuda.synchronize(eng.device)
     _barrier(eng)

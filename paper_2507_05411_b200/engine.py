@@ -323,40 +323,72 @@ class TrainEngine:
 
                 warnings.warn("symmetric memory unavailable on some rank; FSDP collectives use NCCL")
                 self._ce_gather = self._ce_reduce = False
+        # ZeRO-3 (N > 1): a layer's full bf16 working copy exists only in a ring of two gather
+        # buffers (gathered before its forward and again before its backward), and its full f32
+        # gradient only in a ring of two gradient buffers (reduce-scattered into the shard right
+        # after its backward); the root bucket (embedding / final norm, used at both ends of the
+        # step) stays gathered.  CB_FSDP_RESHARD=0 / CB_FSDP_GRAD_RING=0 keep full per-bucket
+        # buffers instead.
+        self.layer_order = [i for i, b in enumerate(self.buckets) if b.name != "root" and not b.replicated]
+        self._pos = {i: p for p, i in enumerate(self.layer_order)}
+        self._reshard = N > 1 and bool(self.layer_order) and os.environ.get("CB_FSDP_RESHARD", "1") == "1"
+        self._grad_ring = N > 1 and bool(self.layer_order) and os.environ.get("CB_FSDP_GRAD_RING", "1") == "1"
+        ring_total = max([_align(self.buckets[i].numel, ALIGN * N) for i in self.layer_order] or [0])
+
+        def symm_or_zeros(n, dtype, symm):
+            if symm:
+                return _symm_mem().empty(n, dtype=dtype, device=dev).zero_()
+            return torch.zeros(n, device=dev, dtype=dtype)
+
+        self._wring = [torch.zeros(ring_total, device=dev, dtype=self.work_dtype) for _ in range(2)] \
+            if self._reshard else []
+        self._gring = [symm_or_zeros(ring_total, torch.float32, self._ce_reduce) for _ in range(2)] \
+            if self._grad_ring else []
         self.bufs = []
-        for b in self.buckets:
+        for i, b in enumerate(self.buckets):
             if b.replicated:
                 total = b.numel
                 master = torch.zeros(total, device=dev, dtype=torch.float32)
-                rec = dict(total=total, shard=total, master=master, work=master,
+                rec = dict(total=total, shard=total, master=master, work=master, wshard=master,
                            grad=torch.zeros(total, device=dev, dtype=torch.float32))
                 rec["grad_shard"] = rec["grad"]
             else:
                 total = _align(b.numel, ALIGN * N)
                 shard = total // N
+                r0 = self.d.rank * shard
+                ringed = i in self._pos
                 master = torch.zeros(shard, device=dev, dtype=torch.float32)
                 if N == 1 and self.work_dtype == torch.float32:
-                    work = master
-                elif self._ce_gather:
-                    work = _symm_mem().empty(total, dtype=self.work_dtype, device=dev).zero_()
+                    work = wshard = master
+                elif self._reshard and ringed:
+                    work = self._wring[self._pos[i] % 2][:total]
+                    wshard = symm_or_zeros(shard, self.work_dtype, self._ce_gather)
                 else:
-                    work = torch.zeros(total, device=dev, dtype=self.work_dtype)
-                if self._ce_reduce:
-                    grad = _symm_mem().empty(total, dtype=torch.float32, device=dev).zero_()
+                    work = symm_or_zeros(total, self.work_dtype, self._ce_gather)
+                    wshard = work[r0:r0 + shard]
+                if N == 1:
+                    grad = grad_shard = torch.zeros(total, device=dev, dtype=torch.float32)
                 else:
-                    grad = torch.zeros(total, device=dev, dtype=torch.float32)
-                grad_shard = grad if N == 1 else torch.zeros(shard, device=dev, dtype=torch.float32)
-                rec = dict(total=total, shard=shard, master=master, work=work, grad=grad, grad_shard=grad_shard)
+                    grad = (self._gring[self._pos[i] % 2][:total] if (self._grad_ring and ringed)
+                            else symm_or_zeros(total, torch.float32, self._ce_reduce))
+                    grad_shard = torch.zeros(shard, device=dev, dtype=torch.float32)
+                rec = dict(total=total, shard=shard, master=master, work=work, wshard=wshard, grad=grad,
+                           grad_shard=grad_shard, ringed=ringed)
             rec["m"] = torch.zeros(rec["shard"], device=dev, dtype=torch.float32)
             rec["v"] = torch.zeros(rec["shard"], device=dev, dtype=torch.float32)
             self.bufs.append(rec)
-        if self._ce_gather:  # collective: every rank maps every peer's working copies
+        if self._ce_gather:  # collective: every rank maps every peer's shards / gradient buffers
             group = self.d.group if self.d.group is not None else self.d.dist.group.WORLD
             for b, rec in zip(self.buckets, self.bufs):
-                if not b.replicated:
-                    rec["symm"] = _symm_mem().rendezvous(rec["work"], group)
-                    if self._ce_reduce:
-                        rec["gsymm"] = _symm_mem().rendezvous(rec["grad"], group)
+                if b.replicated:
+                    continue
+                if self._reshard and rec["ringed"]:
+                    rec["symm"] = _symm_mem().rendezvous(rec["wshard"], group)  # peers read the whole shard
+                else:
+                    rec["symm"] = _symm_mem().rendezvous(rec["work"], group)  # peers read slice p of it
+                if self._ce_reduce and not (self._grad_ring and rec["ringed"]):
+                    rec["gsymm"] = _symm_mem().rendezvous(rec["grad"], group)
+            self._gring_symm = [_symm_mem().rendezvous(g, group) for g in self._gring] if self._ce_reduce else []
             if self._ce_reduce:  # the peers' slices of one bucket's gradient, read before the sum
                 big = max(r["shard"] for b, r in zip(self.buckets, self.bufs) if not b.replicated)
                 self._rs_stage = torch.empty((N - 1) * big, device=dev, dtype=torch.float32)
@@ -366,6 +398,12 @@ class TrainEngine:
             for e in b.entries:
                 _tree_set(self.state, e.path, e.name, _view(rec["work"], e))
                 _tree_set(self.grads, e.path, e.name, _view(rec["grad"], e))
+
+    def _refresh_work(self, i: int) -> None:
+        """This rank's slice of bucket i's working copy <- its f32 master shard."""
+        rec = self.bufs[i]
+        if rec["wshard"].data_ptr() != rec["master"].data_ptr():
+            ops.copy2d(rec["master"].view(1, -1), rec["wshard"].view(1, -1))
 
     def state_bytes(self) -> int:
         """Bytes of every persistent per-rank buffer the engine owns (master/work/grad/m/v,
@@ -401,9 +439,7 @@ class TrainEngine:
         r0 = 0 if b.replicated else self.d.rank * rec["shard"]
         t = torch.from_numpy(host[r0:r0 + rec["shard"]]).to(self.device)
         rec["master"].copy_(t)
-        if rec["work"] is not rec["master"]:
-            full = torch.from_numpy(host).to(self.device)
-            ops.copy2d(full.view(1, -1), rec["work"].view(1, -1))
+        self._refresh_work(self.buckets.index(b))
 
     @_on_device
     def init_params(self, key) -> None:
@@ -415,12 +451,14 @@ class TrainEngine:
         from .prng import pcg64_state
 
         fallback = False
-        for b, rec in zip(self.buckets, self.bufs):
+        for bi, (b, rec) in enumerate(zip(self.buckets, self.bufs)):
             if b.replicated:
                 m0, m1 = 0, rec["total"]
             else:
                 m0, m1 = self.d.rank * rec["shard"], (self.d.rank + 1) * rec["shard"]
-            work = None if rec["work"] is rec["master"] else rec["work"]
+            # one rank holds the whole bucket: master and working copy in one pass; under FSDP
+            # only the own slice is written (from the master below) and peers gather it
+            work = None if (rec["work"] is rec["master"] or self.d.world > 1) else rec["work"]
             wdt = ops.dt(rec["work"])
             for e in b.entries:
                 mod = self.module.child(e.path) if e.path else self.module
@@ -441,6 +479,8 @@ class TrainEngine:
                     _lib.call("cb_init_const", n, float(kind[1]), cols, e.ld, e.col0, e.offset,
                               rec["master"].data_ptr(), m0, m1, work.data_ptr() if work is not None else None, wdt,
                               ops.stream_ptr())
+            if self.d.world > 1:
+                self._refresh_work(bi)
         torch.cuda.synchronize(self.device)
         if fallback:
             self.init_params_host(key)
@@ -519,7 +559,10 @@ class TrainEngine:
     def _export(self, which: str) -> dict:
         out: dict = {}
         for b, rec in zip(self.buckets, self.bufs):
-            src = rec["master"] if which == "master" else rec[which]
+            if which == "grad" and self.d.world > 1 and not b.replicated:
+                src = self._gather_full(rec["grad_shard"], rec)  # the reduce-scattered global mean
+            else:
+                src = rec[which]
             if which in ("master", "m", "v"):
                 src = self._gather_full(src, rec)
             host = src.float().cpu().numpy().astype(np.float64)
@@ -536,13 +579,9 @@ class TrainEngine:
     def state_numpy(self) -> dict:
         return self._export("master")
 
-    @_on_device
     def grads_numpy(self) -> dict:
-        """Full (all-reduced) gradients of the last compute_grads call."""
-        if self.d.world > 1:
-            for b, rec in zip(self.buckets, self.bufs):
-                if not b.replicated:
-                    self.d.dist.all_reduce(rec["grad"], op=self.d.dist.ReduceOp.AVG, group=self.d.group)
+        """Global-batch gradients of the last step (under FSDP: the gathered reduce-scattered
+        shards; replicated buckets were all-reduced in the step)."""
         return self._export("grad")
 
     # -------------------------------------------------------------------- step
@@ -614,13 +653,15 @@ class TrainEngine:
             with torch.cuda.stream(self._zero_stream):
                 self._zero_stream.wait_event(ready)
                 for rec in self.bufs:
-                    ops.zero_(rec["grad"])
+                    if not (self._grad_ring and rec.get("ringed")):
+                        ops.zero_(rec["grad"])
                 zeroed = torch.cuda.Event()
                 zeroed.record(self._zero_stream)
             provider.grads_zeroed = zeroed
         else:
             for rec in self.bufs:
-                ops.zero_(rec["grad"])
+                if not (self._grad_ring and rec.get("ringed")):
+                    ops.zero_(rec["grad"])
         if provider:
             provider.start_step()
         loss, col, _ = value_and_grad(self.module, self.state, self.grads, key, {"tokens": toks}, provider=provider,
@@ -642,11 +683,8 @@ class TrainEngine:
             stream.wait_event(ev)
 
     def _adamw_bucket(self, i: int) -> None:
-        b, rec = self.buckets[i], self.bufs[i]
-        if b.replicated or self.d.world == 1:
-            wshard = rec["work"]
-        else:
-            wshard = rec["work"][self.d.rank * rec["shard"]:(self.d.rank + 1) * rec["shard"]]
+        rec = self.bufs[i]
+        wshard = rec["wshard"]
         bf = wshard if (wshard.dtype == torch.bfloat16) else None
         ops.adamw(rec["master"], rec["grad_shard"], rec["m"], rec["v"], bf, self.lr, self.beta1, self.beta2,
                   self.eps, self.weight_decay, self.step_count)
@@ -666,8 +704,12 @@ class TrainEngine:
 
 
 class FSDPProvider(ParamProvider):
-    """Per-layer all-gather prefetch (copy-engine peer reads of symmetric memory, or NCCL) and
-    reduce-scatter (NCCL) on a side stream."""
+    """Per-layer parameter all-gather (prefetched one layer ahead) and gradient
+    reduce-scatter on a side (comm) stream: copy-engine peer reads of symmetric memory, or
+    NCCL.  Under ZeRO-3 (eng._reshard / eng._grad_ring) layer p's gathered working copy and
+    its full gradient live in ring slot p % 2: a gather waits for the compute stream to be
+    done with the slot's previous layer, and the comm stream clears a gradient slot right
+    after its reduce-scatter has been read by every peer."""
 
     def __init__(self, eng: TrainEngine, update: bool = False):
         self.e = eng
@@ -679,53 +721,80 @@ class FSDPProvider(ParamProvider):
             eng._comm_stream = torch.cuda.Stream(eng.device, priority=_side_priority())
         self.comm = eng._comm_stream
         self.index = {b.name: i for i, b in enumerate(eng.buckets)}
-        self.layer_order = [i for i, b in enumerate(eng.buckets) if b.name != "root" and not b.replicated]
-        self.gathered: dict[int, torch.cuda.Event] = {}
+        self.layer_order = eng.layer_order
+        self.gathered: dict[int, torch.cuda.Event] = {}  # bucket -> gather-done event (this step)
+        self.holder: dict[int, int] = {}  # ring slot -> bucket whose gathered copy it holds
+        self.gslot_free: dict[int, torch.cuda.Event] = {}  # grad ring slot -> cleared event
+
+    def _slot(self, i: int) -> int | None:
+        return self.e._pos[i] % 2 if (self.e._reshard and self.e.bufs[i].get("ringed")) else None
 
     def _ag(self, i: int) -> None:
-        if i in self.gathered:
-            return
         rec, b = self.e.bufs[i], self.e.buckets[i]
         if b.replicated:
             return
+        slot = self._slot(i)
+        if slot is None and i in self.gathered:
+            return
+        if slot is not None and self.holder.get(slot) == i:
+            return
         ready = torch.cuda.Event()
-        ready.record(self.compute)
+        ready.record(self.compute)  # the compute stream is done with the slot's previous layer
         with torch.cuda.stream(self.comm):
             self.comm.wait_event(ready)
-            r, s = self.e.d.rank, rec["shard"]
+            r, s, N = self.e.d.rank, rec["shard"], self.e.d.world
+            work, own = rec["work"], rec["wshard"]
             h = rec.get("symm")
             if h is None:
-                self.dist.all_gather_into_tensor(rec["work"], rec["work"][r * s:(r + 1) * s], group=self.group)
+                self.dist.all_gather_into_tensor(work, own, group=self.group)
             else:
+                if slot is not None:  # the own slice too (in keep mode it is already in place)
+                    work[r * s:(r + 1) * s].copy_(own)
                 # pull every peer's shard over NVLink with the copy engines (no SMs taken from
                 # the compute kernels).  The first barrier: each peer's AdamW of this bucket,
                 # earlier on its comm stream, has written its shard; the second: every peer has
-                # read this rank's shard before the next step's AdamW overwrites it.
-                N, work = self.e.d.world, rec["work"]
+                # read this rank's shard before the next AdamW overwrites it.
                 h.barrier(channel=0, timeout_ms=_BARRIER_TIMEOUT_MS)
                 for k in range(1, N):
                     p = (r + k) % N
-                    work[p * s:(p + 1) * s].copy_(h.get_buffer(p, (rec["total"],), work.dtype)[p * s:(p + 1) * s])
+                    if slot is not None:
+                        src = h.get_buffer(p, (s,), work.dtype)
+                    else:
+                        src = h.get_buffer(p, (rec["total"],), work.dtype)[p * s:(p + 1) * s]
+                    work[p * s:(p + 1) * s].copy_(src)
                 h.barrier(channel=0, timeout_ms=_BARRIER_TIMEOUT_MS)
             done = torch.cuda.Event()
             done.record(self.comm)
         self.gathered[i] = done
+        if slot is not None:
+            self.holder[slot] = i
+
+    def _use(self, i: int) -> None:
+        """Bucket i is about to be read on the compute stream: gathered, and waited for."""
+        self._ag(i)
+        ev = self.gathered.get(i)
+        if ev is not None:
+            self.compute.wait_event(ev)
 
     def _rs(self, i: int) -> None:
         rec, b = self.e.bufs[i], self.e.buckets[i]
         ready = torch.cuda.Event()
         ready.record(self.compute)
+        ring = self.e._grad_ring and rec.get("ringed")
+        gslot = self.e._pos[i] % 2 if ring else None
         with torch.cuda.stream(self.comm):
             self.comm.wait_event(ready)
             self.e._join_wgrad(self.comm)
+            N, r, s = self.e.d.world, self.e.d.rank, rec["shard"]
+            h = self.e._gring_symm[gslot] if (ring and self.e._ce_reduce) else rec.get("gsymm")
             if b.replicated:
                 self.dist.all_reduce(rec["grad"], op=self.dist.ReduceOp.AVG, group=self.group)
-            elif rec.get("gsymm") is not None:
+            elif h is not None:
                 # barrier 1: every peer's backward of this bucket is complete (its comm stream
                 # joined its compute and weight-gradient streams first); barrier 2: every peer
-                # has read this rank's slices before they are cleared for the next step
-                h, N, r, s = rec["gsymm"], self.e.d.world, self.e.d.rank, rec["shard"]
+                # has read this rank's slices before they are cleared for the next use
                 grad, stage = rec["grad"], self.e._rs_stage
+                hn = self.e._gring[0].numel() if ring else rec["total"]  # size of the mapped buffer
                 h.barrier(channel=0, timeout_ms=_BARRIER_TIMEOUT_MS)
                 parts, j = [], 0
                 for q in range(N):
@@ -733,7 +802,7 @@ class FSDPProvider(ParamProvider):
                         parts.append(grad[r * s:(r + 1) * s])
                     else:
                         slot = stage[j * s:(j + 1) * s]
-                        slot.copy_(h.get_buffer(q, (rec["total"],), torch.float32)[r * s:(r + 1) * s])
+                        slot.copy_(h.get_buffer(q, (hn,), torch.float32)[r * s:(r + 1) * s])
                         parts.append(slot)
                         j += 1
                 h.barrier(channel=0, timeout_ms=_BARRIER_TIMEOUT_MS)
@@ -741,12 +810,16 @@ class FSDPProvider(ParamProvider):
             else:
                 self.dist.reduce_scatter_tensor(rec["grad_shard"], rec["grad"], op=self.dist.ReduceOp.AVG,
                                                 group=self.group)
+            if ring:  # the slot is free for the layer two positions further in the backward
+                ops.zero_(rec["grad"])
+                ev = torch.cuda.Event()
+                ev.record(self.comm)
+                self.gslot_free[gslot] = ev
             if self.update:
                 self.e._adamw_bucket(i)
 
     def start_step(self) -> None:
-        self._ag(0)
-        self.compute.wait_event(self.gathered[0])
+        self._use(0)
         if self.layer_order:
             self._ag(self.layer_order[0])
 
@@ -754,14 +827,27 @@ class FSDPProvider(ParamProvider):
         i = self.index.get(path)
         if i is None:
             return
-        self._ag(i)
-        self.compute.wait_event(self.gathered[i])
-        pos = self.layer_order.index(i)
-        if pos + 1 < len(self.layer_order):
+        self._use(i)
+        pos = self.e._pos.get(i)
+        if pos is not None and pos + 1 < len(self.layer_order):
             self._ag(self.layer_order[pos + 1])
 
     def before_backward(self, path: str) -> None:
         _wait_grads_zeroed(self)
+        i = self.index.get(path)
+        if i is None:
+            return
+        pos = self.e._pos.get(i)
+        if pos is None:
+            return
+        if self.e._reshard:
+            self._use(i)
+            if pos > 0:
+                self._ag(self.layer_order[pos - 1])
+        if self.e._grad_ring:
+            ev = self.gslot_free.pop(pos % 2, None)
+            if ev is not None:
+                self.compute.wait_event(ev)
 
     def after_backward(self, path: str) -> None:
         i = self.index.get(path)

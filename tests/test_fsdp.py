@@ -90,31 +90,44 @@ def test_data_parallel_invariants_gloo(world):
     assert ok_views
 
 
-@pytest.mark.gpu
-@pytest.mark.parametrize("precision", ["f32", "bf16"])
-def test_fsdp_two_gpus_matches_oracle(precision):
-    if torch.cuda.device_count() < 2:
-        pytest.skip("needs >= 2 GPUs (run with gpurun --gpus 2)")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+def _fsdp_check(n, *args, timeout=900):
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs >= {n} GPUs (run with gpurun --gpus {n})")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(REPO, "scripts", "fsdp_check.py"),
-           "--precision", precision, "--config", "txf_rope" if precision == "f32" else "mid", "--seq",
-           "8" if precision == "f32" else "128"]
-    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+           *args]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    return res.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision,config,seq", [("f32", "txf_rope", "8"), ("f32", "mid", "128"),
+                                                  ("bf16", "mid", "128")])
+def test_fsdp_two_gpus_step_matches_oracle(precision, config, seq):
+    """The benchmark's path at N=2 — TrainEngine.step(): AdamW on the comm stream after each
+    reduce-scatter, ZeRO-3 gather / gradient rings, copy-engine collectives — for 3 steps
+    against the oracle's chained train_step on the global batch, with the copy-engine
+    collectives and with NCCL, and the two against each other."""
+    _fsdp_check(2, "--precision", precision, "--config", config, "--seq", seq, "--steps", "3", "--mode", "step",
+                "--collectives", "both")
+
+
+@pytest.mark.gpu
+def test_fsdp_two_gpus_decomposed_matches_oracle():
+    """compute_grads() + apply_update() under FSDP (the functional path) against the oracle."""
+    _fsdp_check(2, "--precision", "f32", "--config", "txf_rope", "--seq", "8", "--mode", "decomposed")
 
 
 @pytest.mark.gpu
 def test_fsdp_two_gpus_moe_global_summaries():
     """MoE under FSDP: loss, gradients, updated parameters and the load_balance_loss summaries
     (global-batch statistics, reduced across ranks) match the oracle on the global batch."""
-    if torch.cuda.device_count() < 2:
-        pytest.skip("needs >= 2 GPUs (run with gpurun --gpus 2)")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(REPO, "scripts", "fsdp_check.py"),
-           "--precision", "f32", "--config", "txf_moe", "--seq", "8"]
-    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
-    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
-    assert '"lb_rel_max"' in res.stdout, res.stdout[-2000:]
+    import json
+
+    out = _fsdp_check(2, "--precision", "f32", "--config", "txf_moe", "--seq", "8", "--mode", "step")
+    rec = json.loads(out.strip().splitlines()[-1])
+    assert rec["runs"]["ce"]["lb_rel_max"] is not None and rec["runs"]["ce"]["lb_rel_max"] < 1e-5, rec
 
 
 @pytest.mark.gpu
@@ -131,11 +144,7 @@ def test_sharded_checkpoint_two_gpus_restores_on_one(tmp_path):
     from paper_2507_05411_b200.experiments import transformer_trainer
 
     ck = str(tmp_path / "ckpt")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(REPO, "scripts", "fsdp_check.py"),
-           "--precision", "bf16", "--config", "mid", "--seq", "128", "--ckpt", ck]
-    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
-    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    _fsdp_check(2, "--precision", "bf16", "--config", "mid", "--seq", "128", "--steps", "2", "--ckpt", ck)
     assert list_steps(ck) == [2]
     cfg = transformer_trainer(256, 2, ("linear", "silu"), pos_kind="RoPE", heads=2, vocab=512)
     for i in range(2):
@@ -154,15 +163,9 @@ def test_sharded_checkpoint_two_gpus_restores_on_one(tmp_path):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("precision", ["f32", "bf16"])
-def test_fsdp_four_gpus_matches_oracle(precision):
-    """4-GPU FSDP on the 2-layer d=256 shape: loss and gradients against the oracle on the
-    global batch; the update against f64 AdamW on the GPU's own gradients (--decomposed: the
-    4-way reduce-scatter order moves near-zero gradient entries by ulps, which step-1 AdamW
-    amplifies by 1/eps in the parameters)."""
-    if torch.cuda.device_count() < 4:
-        pytest.skip("needs >= 4 GPUs (run with gpurun --gpus 4)")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
-           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(REPO, "scripts", "fsdp_check.py"),
-           "--precision", precision, "--config", "mid", "--seq", "128", "--decomposed"]
-    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
-    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+def test_fsdp_four_gpus_step_matches_oracle(precision):
+    """TrainEngine.step() at N=4 on the 2-layer d=256 shape, copy-engine and NCCL collectives,
+    3 steps against the oracle (f32: 1e-5 or 3x the fp32-restatement error where fp32 itself
+    cannot meet 1e-5; bf16 2e-2)."""
+    _fsdp_check(4, "--precision", precision, "--config", "mid", "--seq", "128", "--steps", "3", "--mode", "step",
+                "--collectives", "both")
