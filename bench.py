@@ -423,6 +423,7 @@ def main():
                          "the attributed column sums to the busy time of the profiled span (%.1f ms/step)"
                          % (nprof, span_ms / nprof)),
         "memory": {"max_allocated_gb": mem_peak / 1e9, "engine_state_gb": eng.state_bytes() / 1e9,
+                   "forward_leaves_gb": getattr(eng, "last_forward_bytes", 0) / 1e9,
                    "aot_analyze_per_device_gb": aot["per_device_bytes"] / 1e9,
                    "aot_analyze_saved_activation_gb": aot["saved_activation_bytes"] / 1e9,
                    "aot_formula": aot["formula"]},

@@ -664,6 +664,15 @@ class TrainEngine:
                     ops.zero_(rec["grad"])
         if provider:
             provider.start_step()
+        if self.device.type == "cuda":
+            # bytes the forward leaves allocated for the backward (saved activations, logits,
+            # gathered copies) — compared with aot_analyze's saved_activation_bytes in bench.py
+            base = torch.cuda.memory_allocated(self.device)
+
+            def forward_done():
+                self.last_forward_bytes = torch.cuda.memory_allocated(self.device) - base
+
+            self.options["forward_done"] = forward_done
         loss, col, _ = value_and_grad(self.module, self.state, self.grads, key, {"tokens": toks}, provider=provider,
                                       options=self.options)
         if provider:

@@ -42,14 +42,13 @@ from .module import (
     param,
     param_grad,
     param_key,
-    recording,
     register_behavior,
     register_spec_function,
     save,
     saved,
 )
 from .prng import RngKey, uniform
-from .remat import decide_tag, resolve_policy
+from .remat import OFFLOAD, RECOMPUTE, SAVE, decide_tag, resolve_policy
 
 DTYPE_BYTES = {"f32": 4, "bf16": 2, "int8": 1, "fp8": 1}
 ACTIVATION_NAMES = ("linear", "relu", "silu", "sigmoid", "tanh")
@@ -63,6 +62,73 @@ def option(name: str, default=None):
 
 def act_dtype() -> torch.dtype:
     return _TORCH_DT[option("precision", "f32")]
+
+
+# ------------------------------------------------------------- rematerialisation
+def remat_decision(tag: str) -> str:
+    """The governing decision for one of the current module's remat tags: the policy of the
+    nearest enclosing module with a non-empty ``remat_policy`` (inherited down the tree as
+    the reference's aot_analyze does, mesh.py:601-611), applied by ``decide_tag``
+    (mesh.py:240-252: exact key, then the longest matching glob, default save)."""
+    ctx = current_context()
+    while ctx is not None:
+        cfg = ctx.module.config
+        if cfg.has_field("remat_policy"):
+            pol = cfg.get("remat_policy")
+            if pol:
+                return decide_tag(tag, resolve_policy(pol))
+        ctx = ctx.parent
+    return SAVE
+
+
+def remat_plan(*tags: str) -> str:
+    """One decision for a group of tags that share a tensor (e.g. q_proj/k_proj/v_proj: the
+    fused qkv buffer): recompute if any tag recomputes, else offload if any offloads, else
+    save.  Only meaningful while recording (a forward-only call saves nothing)."""
+    ds = {remat_decision(t) for t in tags}
+    return RECOMPUTE if RECOMPUTE in ds else (OFFLOAD if OFFLOAD in ds else SAVE)
+
+
+_D2H: dict = {}
+
+
+class Offloaded:
+    """A saved activation parked in pinned host memory (remat decision "offload"): copied out
+    by the copy engine on a side stream right after it is produced (the device block is
+    released when that copy completes), copied back on the consumer's stream in backward."""
+
+    def __init__(self, t: torch.Tensor):
+        dev = t.device
+        st = _D2H.get(dev)
+        if st is None:
+            st = _D2H[dev] = torch.cuda.Stream(dev)
+        self.device = dev
+        self.host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        ready = torch.cuda.Event()
+        ready.record()
+        with torch.cuda.stream(st):
+            st.wait_event(ready)
+            self.host.copy_(t, non_blocking=True)
+            t.record_stream(st)
+            self.done = torch.cuda.Event()
+            self.done.record(st)
+
+    def load(self) -> torch.Tensor:
+        torch.cuda.current_stream(self.device).wait_event(self.done)
+        return self.host.to(self.device, non_blocking=True)
+
+
+def keep(t, decision: str):
+    """What a forward saves for `t` under a remat decision (None = recompute in backward)."""
+    if t is None or decision == SAVE:
+        return t
+    if decision == OFFLOAD:
+        return Offloaded(t)
+    return None
+
+
+def restore(v):
+    return v.load() if isinstance(v, Offloaded) else v
 
 
 def check_activation(name) -> None:
@@ -471,7 +537,37 @@ class AttentionBehavior(Behavior):
 
     fuses_residual = True  # forward(x, residual=r) returns r + attn(x) from the wo GEMM epilogue
 
+    def _project(self, module, x2, T, rope_ok: bool):
+        """qkv = x2 @ (wq|wk|wv) (+ RoPE in the epilogue); returns (qkv, rope tables or None)."""
+        cfg = module.config
+        d, H = cfg.get("input_dim"), cfg.get("num_heads")
+        hd = d // H
+        kvd = hd * self.kv_heads(cfg)
+        adt = act_dtype()
+        wq, wk, wv = param("wq"), param("wk"), param("wv")
+        wqkv = fused_columns(wq, wk, wv)
+        pos = module.children["pos_emb"]
+        # RoPE folded into the QKV GEMM epilogue (and its inverse into the attention
+        # backward's dQ/dK stores) when the positional child is the stock RoPE kind
+        rope = None
+        if rope_ok and wqkv is not None and pos.kind == "RoPE" and option("fuse_rope", True):
+            rope = rope_tables(T, hd, pos.config.get("base"), x2.device)
+        if wqkv is not None:
+            qkv = torch.empty((x2.shape[0], wqkv.shape[1]), device=x2.device, dtype=adt)
+            if rope is not None:
+                ops.gemm_rope(x2, wqkv, qkv, T, hd, d + kvd, rope[0], rope[1])
+            else:
+                ops.gemm(x2, wqkv, qkv)
+        else:
+            qkv = torch.empty((x2.shape[0], d + 2 * kvd), device=x2.device, dtype=adt)
+            for w, c0, c1 in ((wq, 0, d), (wk, d, d + kvd), (wv, d + kvd, d + 2 * kvd)):
+                ops.gemm(x2, w, qkv[:, c0:c1])
+        return qkv, rope
+
     def forward(self, module, x, residual=None):
+        """Remat tags (reference layers.py:318-329): q_proj/k_proj/v_proj = the fused qkv
+        buffer, context = the attention output o (+ its log-sum-exp), o_proj = this block's
+        output (not needed by the backward, so nothing is kept for it either way)."""
         cfg = module.config
         d, H = cfg.get("input_dim"), cfg.get("num_heads")
         KVH = self.kv_heads(cfg)
@@ -480,49 +576,43 @@ class AttentionBehavior(Behavior):
         kvd = hd * KVH
         adt = act_dtype()
         x2 = ops.cast(ops.rows2d(x), adt)
-        wq, wk, wv, wo = param("wq"), param("wk"), param("wv"), param("wo")
-        wqkv = fused_columns(wq, wk, wv)
-        pos = module.children["pos_emb"]
-        # RoPE folded into the QKV GEMM epilogue (and its inverse into the attention
-        # backward's dQ/dK stores) when the positional child is the stock RoPE kind
-        rope = None
-        if wqkv is not None and pos.kind == "RoPE" and option("fuse_rope", True):
-            rope = rope_tables(T, hd, pos.config.get("base"), x.device)
-        if wqkv is not None:
-            qkv = torch.empty((x2.shape[0], wqkv.shape[1]), device=x.device, dtype=adt)
-            if rope is not None:
-                ops.gemm_rope(x2, wqkv, qkv, T, hd, d + kvd, rope[0], rope[1])
-            else:
-                ops.gemm(x2, wqkv, qkv)
-        else:
-            qkv = torch.empty((x2.shape[0], d + 2 * kvd), device=x.device, dtype=adt)
-            for w, c0, c1 in ((wq, 0, d), (wk, d, d + kvd), (wv, d + kvd, d + 2 * kvd)):
-                ops.gemm(x2, w, qkv[:, c0:c1])
+        qkv, rope = self._project(module, x2, T, True)
         q, k, v = qkv[:, :d], qkv[:, d:d + kvd], qkv[:, d + kvd:]
         if rope is None:
             invoke_child("pos_emb", q, k, T)
         scale = 1.0 / math.sqrt(hd)
         o, lse = ops.attention_fwd(q, k, v, B, T, H, KVH, hd, scale)
         out = torch.empty((o.shape[0], d), device=x.device, dtype=torch.float32)
-        ops.gemm(o, wo, out, residual=ops.rows2d(residual) if residual is not None else None)
-        save(x2=x2, qkv=qkv, o=o, lse=lse, rope=rope, geom=(B, T, H, KVH, hd, d, kvd))
+        ops.gemm(o, param("wo"), out, residual=ops.rows2d(residual) if residual is not None else None)
+        if is_recording():
+            dq = remat_plan("q_proj", "k_proj", "v_proj")
+            dc = remat_plan("context")
+            if dq == RECOMPUTE and rope is None:
+                dq = SAVE  # an unfused positional child would have to be re-run as well
+            save(x2=x2, qkv=keep(qkv, dq), o=keep(o, dc), lse=keep(lse, dc), rope=rope,
+                 geom=(B, T, H, KVH, hd, d, kvd))
         return out.view(B, T, d)
 
     def backward(self, module, dout):
         s = saved()
         B, T, H, KVH, hd, d, kvd = s["geom"]
         adt = act_dtype()
-        g = ops.rows2d(ops.cast(dout, adt))
-        do = _linear_bwd(s["o"], param("wo"), g, param_grad("wo"), adt)
-        qkv = s["qkv"]
-        dqkv = torch.empty_like(qkv)
+        qkv = restore(s["qkv"])
+        if qkv is None:  # q/k/v projections rematerialised from the saved block input
+            qkv, _ = self._project(module, s["x2"], T, True)
         q, k, v = qkv[:, :d], qkv[:, d:d + kvd], qkv[:, d + kvd:]
+        o, lse = restore(s["o"]), restore(s["lse"])
+        if o is None:  # context rematerialised: the attention forward again
+            o, lse = ops.attention_fwd(q, k, v, B, T, H, KVH, hd, 1.0 / math.sqrt(hd))
+        g = ops.rows2d(ops.cast(dout, adt))
+        do = _linear_bwd(o, param("wo"), g, param_grad("wo"), adt)
+        dqkv = torch.empty_like(qkv)
         dq, dk, dv = dqkv[:, :d], dqkv[:, d:d + kvd], dqkv[:, d + kvd:]
         if s["rope"] is not None:
-            ops.attention_bwd_rope(q, k, v, s["o"], s["lse"], do, dq, dk, dv, B, T, H, KVH, hd,
+            ops.attention_bwd_rope(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd,
                                    1.0 / math.sqrt(hd), s["rope"][0], s["rope"][1])
         else:
-            ops.attention_bwd(q, k, v, s["o"], s["lse"], do, dq, dk, dv, B, T, H, KVH, hd, 1.0 / math.sqrt(hd))
+            ops.attention_bwd(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, 1.0 / math.sqrt(hd))
             backward_child("pos_emb", dq, dk)
         wq, wk, wv = param("wq"), param("wk"), param("wv")
         wqkv = fused_columns(wq, wk, wv)
@@ -619,14 +709,12 @@ class FeedForwardBehavior(Behavior):
 
     fuses_residual = True
 
-    def forward(self, module, x, residual=None):
+    def _up(self, module, x2):
+        """pre = x2 @ (w1|w1_gate) and hidden = act(pre) (gated activation in the GEMM epilogue
+        when the layout is fused)."""
         cfg = module.config
-        if x.shape[-1] != cfg.get("input_dim"):
-            raise ShapeError(f"FeedForward expects trailing dim {cfg.get('input_dim')}")
-        lead = x.shape[:-1]
-        adt = act_dtype()
-        x2 = ops.cast(ops.rows2d(x), adt)
         h = cfg.get("hidden_dim")
+        adt = act_dtype()
         pair = activation_pair(cfg.get("activation"))
         fused = None
         if pair:
@@ -639,7 +727,7 @@ class FeedForwardBehavior(Behavior):
             elif wcat is not None:
                 pre = _linear_fwd(x2, wcat, adt)
             else:
-                pre = torch.empty((x2.shape[0], 2 * h), device=x.device, dtype=adt)
+                pre = torch.empty((x2.shape[0], 2 * h), device=x2.device, dtype=adt)
                 ops.gemm(x2, w1, pre[:, :h])
                 ops.gemm(x2, wg, pre[:, h:])
             if fused is None:
@@ -647,9 +735,23 @@ class FeedForwardBehavior(Behavior):
         else:
             pre = _linear_fwd(x2, param("w1"), adt)
             hidden = ops.act_fwd(pre, None, cfg.get("activation"))
+        return pre, hidden
+
+    def forward(self, module, x, residual=None):
+        """Remat tags (reference layers.py:395-403): hidden = the up-projection (pre-activation
+        and activation), output = this block's output (not needed by the backward).
+        Recomputing "hidden" re-runs only the up-projection GEMM in the backward."""
+        cfg = module.config
+        if x.shape[-1] != cfg.get("input_dim"):
+            raise ShapeError(f"FeedForward expects trailing dim {cfg.get('input_dim')}")
+        lead = x.shape[:-1]
+        x2 = ops.cast(ops.rows2d(x), act_dtype())
+        pre, hidden = self._up(module, x2)
         out = torch.empty((x2.shape[0], cfg.get("input_dim")), device=x.device, dtype=torch.float32)
         ops.gemm(hidden, param("w2"), out, residual=ops.rows2d(residual) if residual is not None else None)
-        save(x2=x2, pre=pre, hidden=hidden)
+        if is_recording():
+            dh = remat_plan("hidden")
+            save(x2=x2, pre=keep(pre, dh), hidden=keep(hidden, dh))
         return out.view(*lead, cfg.get("input_dim"))
 
     def backward(self, module, dout):
@@ -658,9 +760,11 @@ class FeedForwardBehavior(Behavior):
         adt = act_dtype()
         h = cfg.get("hidden_dim")
         g = ops.rows2d(ops.cast(dout, adt))
-        pre = s["pre"]
-        pair = activation_pair(cfg.get("activation"))
         x2 = s["x2"]
+        pre, hidden = restore(s["pre"]), restore(s["hidden"])
+        if pre is None:  # "hidden" rematerialised: the up-projection again
+            pre, hidden = self._up(module, x2)
+        pair = activation_pair(cfg.get("activation"))
         dw2 = param_grad("w2")
         dpre = None
         if pair and option("fuse_glu", True):
@@ -669,9 +773,9 @@ class FeedForwardBehavior(Behavior):
             dpre = ops.gemm_gated_bwd(g, param("w2"), pre, pair[0], pair[1])
         if dpre is not None:
             if dw2 is not None:
-                _wgrad(s["hidden"], g, dw2)
+                _wgrad(hidden, g, dw2)
         else:
-            dhidden = _linear_bwd(s["hidden"], param("w2"), g, dw2, adt)
+            dhidden = _linear_bwd(hidden, param("w2"), g, dw2, adt)
             dpre = torch.empty_like(pre)
             if pair:
                 ops.act_bwd(pre[:, :h], pre[:, h:], dhidden, dpre[:, :h], dpre[:, h:], pair[0], pair[1])
@@ -731,52 +835,17 @@ class TransformerLayerBehavior(Behavior):
             return invoke_child(name, normed, residual=residual)
         return ops.add_(invoke_child(name, normed), residual)
 
-    # --- rematerialisation (the layer's remat_policy, reference mesh.py:204-252) -------
-    @staticmethod
-    def _recompute(module, child: str) -> bool:
-        """True if the policy recomputes any remat tag of `child` (tag decisions as the
-        reference's decide_tag: exact key, then the longest matching glob, default save;
-        'offload' is executed as save)."""
-        policy = module.config.get("remat_policy")
-        if not policy:
-            return False
-        policy = resolve_policy(policy)
-        c = module.children[child]
-        tags = [t.name for t in c.behavior.remat_tags(c.config, 1, 1)]
-        return any(decide_tag(t, policy) == "recompute" for t in tags)
-
-    def _attn_block(self, module, x):
-        return self._branch(module, "self_attention", invoke_child("self_attention_norm", x), x)
-
-    def _ffn_block(self, module, h):
-        return self._branch(module, "feed_forward", invoke_child("feed_forward_norm", h), h)
+    # Rematerialisation is per tag: the layer's remat_policy governs its subtree and each
+    # child behavior keeps, offloads or recomputes its own tagged activations
+    # (remat_decision; reference mesh.py:204-252, tags layers.py:318-329, 395-403, 501-511).
 
     def forward(self, module, x):
-        ra = is_recording() and self._recompute(module, "self_attention")
-        rf = is_recording() and self._recompute(module, "feed_forward")
-        if ra:
-            with recording(False):  # activations of this block are recomputed in backward
-                h = self._attn_block(module, x)
-        else:
-            h = self._attn_block(module, x)
-        if rf:
-            with recording(False):
-                out = self._ffn_block(module, h)
-        else:
-            out = self._ffn_block(module, h)
-        save(x=x if ra else None, h=h if rf else None)
-        return out
+        h = self._branch(module, "self_attention", invoke_child("self_attention_norm", x), x)
+        return self._branch(module, "feed_forward", invoke_child("feed_forward_norm", h), h)
 
     def backward(self, module, dout):
-        s = saved()
-        if s.get("h") is not None:
-            with recording(True):
-                self._ffn_block(module, s["h"])
         dn2 = backward_child("feed_forward", dout)
         dh = backward_child("feed_forward_norm", dn2, dres=dout)
-        if s.get("x") is not None:
-            with recording(True):
-                self._attn_block(module, s["x"])
         dn1 = backward_child("self_attention", dh)
         return backward_child("self_attention_norm", dn1, dres=dh)
 

@@ -138,14 +138,36 @@ class MoEBehavior(Behavior):
                   ops.ld(xe), ops.dt(xe), ops.stream_ptr())
         off_ready.synchronize()
         off = off_host.numpy().astype(np.int64)
+        pre, hid = self._experts_up(module, xe, off)
+        ye = self._experts_down(module, hid, off)
+        out = torch.empty((n, d), device=dev, dtype=torch.float32)
+        _lib.call("cb_moe_combine", n, d, k, inv.data_ptr(), w.data_ptr(), ye.data_ptr(), ops.ld(ye), ops.dt(ye),
+                  out.data_ptr(), ops.ld(out), 0, ops.stream_ptr())
+        if L.is_recording():
+            # remat tags (reference layers.py:501-511): router_logits = the router
+            # probabilities, expert_hidden = the experts' up-projections, expert_output = the
+            # experts' outputs (read by the combine backward for the routing-weight gradient)
+            save(x2=x2, idx=idx, w=w, probs=L.keep(probs, L.remat_plan("router_logits")), perm=perm, inv=inv,
+                 off=off, xe=xe, pre=L.keep(pre, L.remat_plan("expert_hidden")),
+                 hid=L.keep(hid, L.remat_plan("expert_hidden")), ye=L.keep(ye, L.remat_plan("expert_output")),
+                 geom=(B, T, d, h, E, k))
+        return out.view(B, T, d)
+
+    def _experts_up(self, module, xe, off):
+        """pre / hid of every expert's rows (gate/up GEMM with the gated activation in its
+        epilogue, per expert on its contiguous rows)."""
+        L = _layers()
+        cfg = module.config
+        h, E = cfg.get("hidden_dim"), cfg.get("num_experts")
+        adt = L.act_dtype()
+        dev = xe.device
+        nk = xe.shape[0]
         pair = L.activation_pair(cfg.get("activation"))
-        w1, w2 = param("w1"), param("w2")
+        w1 = param("w1")
         wg = param("w1_gate") if pair else None
         width = 2 * h if pair else h
-        pre = torch.empty((n * k, width), device=dev, dtype=adt)
-        hid = torch.empty((n * k, h), device=dev, dtype=adt)
-        ye = torch.empty((n * k, d), device=dev, dtype=torch.float32)
-        hid = torch.empty((n * k, h), device=dev, dtype=adt)
+        pre = torch.empty((nk, width), device=dev, dtype=adt)
+        hid = torch.empty((nk, h), device=dev, dtype=adt)
         fused_all = pair is not None and L.option("fuse_glu", True)
         unfused = []
         for e in range(E):
@@ -154,7 +176,6 @@ class MoEBehavior(Behavior):
                 continue
             xs = xe[r0:r1]
             wcat = L.fused_columns(w1[e], wg[e]) if fused_all else None
-            # gate / up GEMM with the gated activation in its epilogue (rows of expert e)
             if wcat is not None and ops.gemm_gated_fwd(xs, wcat, pair[0], pair[1], pre=pre[r0:r1],
                                                        hidden=hid[r0:r1]) is not None:
                 continue
@@ -167,16 +188,18 @@ class MoEBehavior(Behavior):
                 ops.act_fwd(pre[r0:r1, :h], pre[r0:r1, h:], pair[0], pair[1], out=hid[r0:r1])
             else:
                 ops.act_fwd(pre[r0:r1], None, cfg.get("activation"), out=hid[r0:r1])
+        return pre, hid
+
+    def _experts_down(self, module, hid, off):
+        cfg = module.config
+        d, E = cfg.get("input_dim"), cfg.get("num_experts")
+        w2 = param("w2")
+        ye = torch.empty((hid.shape[0], d), device=hid.device, dtype=torch.float32)
         for e in range(E):
             r0, r1 = int(off[e]), int(off[e + 1])
             if r1 > r0:
                 ops.gemm(hid[r0:r1], w2[e], ye[r0:r1])
-        out = torch.empty((n, d), device=dev, dtype=torch.float32)
-        _lib.call("cb_moe_combine", n, d, k, inv.data_ptr(), w.data_ptr(), ye.data_ptr(), ops.ld(ye), ops.dt(ye),
-                  out.data_ptr(), ops.ld(out), 0, ops.stream_ptr())
-        save(x2=x2, idx=idx, w=w, probs=probs, perm=perm, inv=inv, off=off, xe=xe, pre=pre, hid=hid, ye=ye,
-             geom=(B, T, d, h, E, k))
-        return out.view(B, T, d)
+        return ye
 
     def backward(self, module, dout):
         L = _layers()
@@ -186,18 +209,32 @@ class MoEBehavior(Behavior):
         adt = L.act_dtype()
         dev = dout.device
         n = B * T
+        off, xe = s["off"], s["xe"]
+        pre, hid = L.restore(s["pre"]), L.restore(s["hid"])
+        if pre is None:  # expert_hidden rematerialised
+            pre, hid = self._experts_up(module, xe, off)
+        ye = L.restore(s["ye"])
+        if ye is None:  # expert_output rematerialised
+            ye = self._experts_down(module, hid, off)
+        probs = L.restore(s["probs"])
+        if probs is None:  # router_logits rematerialised (same deterministic kernel: same top-k)
+            probs = torch.empty((n, E), device=dev, dtype=torch.float32)
+            i2 = torch.empty((n, k), device=dev, dtype=torch.int32)
+            w2_ = torch.empty((n, k), device=dev, dtype=torch.float32)
+            x2 = s["x2"]
+            _lib.call("cb_moe_route", n, d, E, k, x2.data_ptr(), ops.ld(x2), ops.dt(x2), L._f32(param("router")).data_ptr(),
+                      i2.data_ptr(), w2_.data_ptr(), probs.data_ptr(), ops.stream_ptr())
         g = ops.rows2d(dout).contiguous() if dout.dtype == torch.float32 else ops.cast(ops.rows2d(dout), torch.float32)
         dye = torch.empty((n * k, d), device=dev, dtype=adt)
         dw = torch.empty((n, k), device=dev, dtype=torch.float32)
-        _lib.call("cb_moe_combine_bwd", n, d, k, s["inv"].data_ptr(), s["w"].data_ptr(), s["ye"].data_ptr(),
-                  ops.ld(s["ye"]), g.data_ptr(), ops.ld(g), dye.data_ptr(), ops.ld(dye), ops.dt(dye), dw.data_ptr(),
+        _lib.call("cb_moe_combine_bwd", n, d, k, s["inv"].data_ptr(), s["w"].data_ptr(), ye.data_ptr(),
+                  ops.ld(ye), g.data_ptr(), ops.ld(g), dye.data_ptr(), ops.ld(dye), ops.dt(dye), dw.data_ptr(),
                   ops.stream_ptr())
         pair = L.activation_pair(cfg.get("activation"))
         w1, w2 = param("w1"), param("w2")
         gw1, gw2 = param_grad("w1"), param_grad("w2")
         wg = param("w1_gate") if pair else None
         gwg = param_grad("w1_gate") if pair else None
-        off, pre, hid, xe = s["off"], s["pre"], s["hid"], s["xe"]
         dpre = torch.empty_like(pre)
         dhid = None
         fuse = pair is not None and L.option("fuse_glu", True)
@@ -234,7 +271,7 @@ class MoEBehavior(Behavior):
                   dx.data_ptr(), ops.ld(dx), 0, ops.stream_ptr())
         # router: w = renorm(topk(softmax(x @ router)))
         dlog = torch.empty((n, E), device=dev, dtype=torch.float32)
-        _lib.call("cb_moe_router_bwd", n, E, k, s["probs"].data_ptr(), s["idx"].data_ptr(), s["w"].data_ptr(),
+        _lib.call("cb_moe_router_bwd", n, E, k, probs.data_ptr(), s["idx"].data_ptr(), s["w"].data_ptr(),
                   dw.data_ptr(), dlog.data_ptr(), ops.stream_ptr())
         router = L._f32(param("router"))
         x2 = s["x2"]

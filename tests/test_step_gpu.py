@@ -264,11 +264,12 @@ def test_activation_table_step(cuda, act, precision):
 
 @pytest.mark.parametrize("policy", ["recompute_all", "save_qkvo_flash", "offload_dots"])
 @pytest.mark.parametrize("precision", ["f32", "bf16"])
-def test_remat_policy_against_oracle(cuda, policy, precision):
+@pytest.mark.parametrize("kind", ["FeedForward", "MoE"])
+def test_remat_policy_against_oracle(cuda, policy, precision, kind):
     """f2: a rematerialised step against the oracle directly (not only against no-remat)."""
     from paper_2507_05411_b200.remat import POLICY_ALIASES
 
-    cfg = _mid(128)
+    cfg = _mid(128, kind)
     for i in range(2):
         cfg = cfg.set(f"model.decoder.transformer.layer[{i}].remat_policy", POLICY_ALIASES[policy])
     run_parity(cfg, precision, 2, 128 if precision == "f32" else 256, 1e-5 if precision == "f32" else 2e-2)
@@ -290,25 +291,31 @@ def test_forward_loss_matches_reference_invoke(cuda):
         assert abs(got - rec["loss"]) / rec["loss"] < 1e-5, (name, got, rec["loss"])
 
 
-@pytest.mark.parametrize("policy", ["recompute_all", "save_qkvo_flash"])
+@pytest.mark.parametrize("policy", ["recompute_all", "save_qkvo_flash", "offload_dots",
+                                    {"hidden": "recompute", "context": "offload"}, {"q_proj": "recompute"}])
 def test_remat_policies_are_exact(cuda, policy):
-    """Rematerialised blocks rerun the same deterministic kernels: gradients are bit-identical."""
+    """Rematerialised tags rerun the same deterministic kernels and offloaded ones come back
+    byte for byte: gradients are bit-identical to the save-everything step."""
     from paper_2507_05411_b200 import TrainEngine, set_dtype_policy, synthetic_batch
     from paper_2507_05411_b200.remat import POLICY_ALIASES
 
     base = set_dtype_policy(_mid(128), "bf16")
     remat = base
     for i in range(2):
-        remat = remat.set(f"model.decoder.transformer.layer[{i}].remat_policy", POLICY_ALIASES[policy])
+        remat = remat.set(f"model.decoder.transformer.layer[{i}].remat_policy",
+                          POLICY_ALIASES[policy] if isinstance(policy, str) else policy)
     toks = synthetic_batch(0, 0, 2, 256, 512)["tokens"]
-    outs = []
+    outs, fwd_bytes = [], []
     for cfg in (base, remat):
         eng = TrainEngine(cfg, device="cuda:0")
         loss, _ = eng.compute_grads(toks)
         outs.append((float(loss.item()), dict(_leaves(eng.grads_numpy()))))
+        fwd_bytes.append(eng.last_forward_bytes)
     assert outs[0][0] == outs[1][0]
     for k in outs[0][1]:
         assert np.array_equal(outs[0][1][k], outs[1][1][k]), k
+    # the forward leaves less on the device for the backward
+    assert fwd_bytes[1] < fwd_bytes[0], fwd_bytes
 
 
 def test_wgrad_stream_is_exact(cuda, monkeypatch):
