@@ -146,20 +146,24 @@ CB_API int cb_sum_parts(int nparts, int64_t n, const void* parts, void* out, flo
  * rows are tokens (b*T + t), head h at columns [h*hd, (h+1)*hd).  lse/delta are f32
  * [B][H][T].  kv_heads < heads is grouped-query attention (query head h reads kv head
  * h / (heads/kv_heads)); kv_heads == heads is the reference's attention.
+ * o_lo (bf16 only, nullable, o's layout): the forward writes o - bf16(o), and the backward
+ * forms delta = rowsum(dO * (o + o_lo)) — the flash backward's delta at ~16 significant bits
+ * instead of bf16 o's 8 (it multiplies every dS = P (dP - delta) entry).
  * ------------------------------------------------------------------------------- */
 CB_API int cb_attention_fwd(int batch, int seq_len, int heads, int kv_heads, int head_dim, int dtype, const void* q,
                             int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv, void* o, int64_t ldo,
-                            float* lse, float scale, void* stream);
+                            void* o_lo, float* lse, float scale, void* stream);
 CB_API int cb_attention_bwd(int batch, int seq_len, int heads, int kv_heads, int head_dim, int dtype, const void* q,
                             int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv, const void* o,
-                            int64_t ldo, const float* lse, const void* dout, int64_t lddo, float* delta, void* dq,
-                            int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv, float scale, void* stream);
+                            int64_t ldo, const void* o_lo, const float* lse, const void* dout, int64_t lddo,
+                            float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv,
+                            float scale, void* stream);
 /* Backward for q/k rotated by cb_gemm_rope: dq/dk are returned un-rotated (the RoPE backward). */
 CB_API int cb_attention_bwd_rope(int batch, int seq_len, int heads, int kv_heads, int head_dim, int dtype,
                                  const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
-                                 const void* o, int64_t ldo, const float* lse, const void* dout, int64_t lddo,
-                                 float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv,
-                                 float scale, const float* cos_t, const float* sin_t, void* stream);
+                                 const void* o, int64_t ldo, const void* o_lo, const float* lse, const void* dout,
+                                 int64_t lddo, float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
+                                 int64_t lddv, float scale, const float* cos_t, const float* sin_t, void* stream);
 /* 0 = automatic (tensor-core flash kernels when eligible), 1 = force SIMT (tests). */
 CB_API int cb_attention_set_path(int path);
 /* 1 (default) = use the tcgen05/TMEM forward for head_dim 128; 0 = warp-MMA flash kernel (tests). */

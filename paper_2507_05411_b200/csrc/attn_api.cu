@@ -26,24 +26,30 @@ extern "C" int cb_attention_set_path(int path) {
 
 extern "C" int cb_attention_fwd(int batch, int seq_len, int heads, int kv_heads, int head_dim, int dtype,
                                 const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
-                                void* o, int64_t ldo, float* lse, float scale, void* stream) {
+                                void* o, int64_t ldo, void* o_lo, float* lse, float scale, void* stream) {
   AttnGeom g{batch, seq_len, heads, kv_heads, head_dim, ldq, ldk, ldv, ldo, scale};
   if (int s = check_geom(g)) return s;
   cudaStream_t st = (cudaStream_t)stream;
-  if (g_attn_path == 0 && attn_tc_supported(g, dtype, q, k, v)) return attn_fwd_tc(g, q, k, v, o, lse, st);
+  if (o_lo && dtype != CB_DT_BF16) return fail(CB_ERR_ARG, "attention: o_lo is the bf16 rounding residual of o");
+  if (g_attn_path == 0 && attn_tc_supported(g, dtype, q, k, v)) return attn_fwd_tc(g, q, k, v, o, o_lo, lse, st);
+  if (o_lo) {  // the other engines do not produce the residual: zero (delta then uses bf16 o)
+    cudaError_t e = cudaMemset2DAsync(o_lo, (size_t)ldo * 2, 0, (size_t)heads * head_dim * 2,
+                                      (size_t)batch * seq_len, st);
+    if (e != cudaSuccess) return fail(CB_ERR_CUDA, "attention: o_lo memset: %s", cudaGetErrorString(e));
+  }
   if (g_attn_path == 0 && attn_fa_supported(g, dtype, q, k, v)) return attn_fwd_fa(g, q, k, v, o, lse, st);
   return attn_fwd_simt(g, dtype, q, k, v, o, lse, st);
 }
 
 extern "C" int cb_attention_bwd(int batch, int seq_len, int heads, int kv_heads, int head_dim, int dtype,
                                 const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
-                                const void* o, int64_t ldo, const float* lse, const void* dout, int64_t lddo,
-                                float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv,
-                                float scale, void* stream) {
+                                const void* o, int64_t ldo, const void* o_lo, const float* lse, const void* dout,
+                                int64_t lddo, float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
+                                int64_t lddv, float scale, void* stream) {
   AttnGeom g{batch, seq_len, heads, kv_heads, head_dim, ldq, ldk, ldv, ldo, scale};
   if (int s = check_geom(g)) return s;
   cudaStream_t st = (cudaStream_t)stream;
-  if (int s = attn_delta(g, dtype, o, dout, lddo, delta, st)) return s;
+  if (int s = attn_delta(g, dtype, o, o_lo, dout, lddo, delta, st)) return s;
   if (tc_bwd_ok(g, dtype, q, k, v, lse, delta, lddo, lddq, lddk, lddv))
     return attn_bwd_tc(g, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st);
   if (g_attn_path == 0 && attn_fa_supported(g, dtype, q, k, v))
@@ -57,19 +63,19 @@ extern "C" int cb_attention_bwd(int batch, int seq_len, int heads, int kv_heads,
 // other engines run cb_rope(inverse) afterwards.
 extern "C" int cb_attention_bwd_rope(int batch, int seq_len, int heads, int kv_heads, int head_dim, int dtype,
                                      const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
-                                     int64_t ldv, const void* o, int64_t ldo, const float* lse, const void* dout,
-                                     int64_t lddo, float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk,
-                                     void* dv, int64_t lddv, float scale, const float* cos_t, const float* sin_t,
-                                     void* stream) {
+                                     int64_t ldv, const void* o, int64_t ldo, const void* o_lo, const float* lse,
+                                     const void* dout, int64_t lddo, float* delta, void* dq, int64_t lddq, void* dk,
+                                     int64_t lddk, void* dv, int64_t lddv, float scale, const float* cos_t,
+                                     const float* sin_t, void* stream) {
   AttnGeom g{batch, seq_len, heads, kv_heads, head_dim, ldq, ldk, ldv, ldo, scale};
   if (int s = check_geom(g)) return s;
   cudaStream_t st = (cudaStream_t)stream;
   if (tc_bwd_ok(g, dtype, q, k, v, lse, delta, lddo, lddq, lddk, lddv)) {
-    if (int s = attn_delta(g, dtype, o, dout, lddo, delta, st)) return s;
+    if (int s = attn_delta(g, dtype, o, o_lo, dout, lddo, delta, st)) return s;
     return attn_bwd_tc(g, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st, cos_t, sin_t);
   }
-  if (int s = cb_attention_bwd(batch, seq_len, heads, kv_heads, head_dim, dtype, q, ldq, k, ldk, v, ldv, o, ldo, lse,
-                               dout, lddo, delta, dq, lddq, dk, lddk, dv, lddv, scale, stream))
+  if (int s = cb_attention_bwd(batch, seq_len, heads, kv_heads, head_dim, dtype, q, ldq, k, ldk, v, ldv, o, ldo, o_lo,
+                               lse, dout, lddo, delta, dq, lddq, dk, lddk, dv, lddv, scale, stream))
     return s;
   const int64_t rows = (int64_t)batch * seq_len;
   if (int s = cb_rope(rows, seq_len, heads, head_dim, dq, lddq, dtype, cos_t, sin_t, 1, stream)) return s;

@@ -252,6 +252,7 @@ int attn_fwd_simt(const AttnGeom& g, int dtype, const void* q, const void* k, co
 
 // delta for bf16 with hd % 8 == 0 and 16-byte aligned rows: hd/8 lanes per row, uint4 loads
 __global__ void __launch_bounds__(256) attn_delta_vec_k(AttnGeom g, const __nv_bfloat16* __restrict__ o,
+                                                        const __nv_bfloat16* __restrict__ o_lo,
                                                         const __nv_bfloat16* __restrict__ dout, int64_t lddo,
                                                         float* __restrict__ delta, int lanes_per_row) {
   const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -266,12 +267,15 @@ __global__ void __launch_bounds__(256) attn_delta_vec_k(AttnGeom g, const __nv_b
     tok = row / g.H;
     const uint4 a = *reinterpret_cast<const uint4*>(o + tok * g.ldo + (int64_t)h * g.hd + l * 8);
     const uint4 b = *reinterpret_cast<const uint4*>(dout + tok * lddo + (int64_t)h * g.hd + l * 8);
+    const uint4 c = o_lo ? *reinterpret_cast<const uint4*>(o_lo + tok * g.ldo + (int64_t)h * g.hd + l * 8)
+                         : make_uint4(0, 0, 0, 0);
     const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
     const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&b);
+    const __nv_bfloat162* pc = reinterpret_cast<const __nv_bfloat162*>(&c);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const float2 fa = __bfloat1622float2(pa[i]), fb = __bfloat1622float2(pb[i]);
-      s = fmaf(fa.x, fb.x, fmaf(fa.y, fb.y, s));
+      const float2 fa = __bfloat1622float2(pa[i]), fb = __bfloat1622float2(pb[i]), fc = __bfloat1622float2(pc[i]);
+      s = fmaf(fa.x + fc.x, fb.x, fmaf(fa.y + fc.y, fb.y, s));
     }
   }
   for (int off = lanes_per_row >> 1; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
@@ -281,16 +285,18 @@ __global__ void __launch_bounds__(256) attn_delta_vec_k(AttnGeom g, const __nv_b
   }
 }
 
-int attn_delta(const AttnGeom& g, int dtype, const void* o, const void* dout, int64_t lddo, float* delta,
-               cudaStream_t st) {
+int attn_delta(const AttnGeom& g, int dtype, const void* o, const void* o_lo, const void* dout, int64_t lddo,
+               float* delta, cudaStream_t st) {
   const int lpr = g.hd / 8;
   if (dtype == CB_DT_BF16 && g.hd % 8 == 0 && lpr <= 32 && (lpr & (lpr - 1)) == 0 && !((g.ldo | lddo) & 7) &&
-      !(reinterpret_cast<uintptr_t>(o) & 15) && !(reinterpret_cast<uintptr_t>(dout) & 15)) {
+      !((reinterpret_cast<uintptr_t>(o) | reinterpret_cast<uintptr_t>(o_lo) | reinterpret_cast<uintptr_t>(dout)) &
+        15)) {
     const int64_t threads = (int64_t)g.B * g.T * g.H * lpr;
-    attn_delta_vec_k<<<(int)((threads + 255) / 256), 256, 0, st>>>(g, (const __nv_bfloat16*)o,
-                                                                    (const __nv_bfloat16*)dout, lddo, delta, lpr);
+    attn_delta_vec_k<<<(int)((threads + 255) / 256), 256, 0, st>>>(
+        g, (const __nv_bfloat16*)o, (const __nv_bfloat16*)o_lo, (const __nv_bfloat16*)dout, lddo, delta, lpr);
     return check_launch("attn_delta");
   }
+  if (o_lo) return fail(CB_ERR_ARG, "attention delta: o_lo needs bf16, head_dim %% 8 == 0 and 16-byte rows");
   const int64_t warps = (int64_t)g.B * g.H * g.T;
   const int blocks = (int)((warps + 3) / 4);
   if (dtype == CB_DT_F32)

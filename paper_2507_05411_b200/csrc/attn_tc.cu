@@ -67,6 +67,7 @@ struct Params {
   __nv_bfloat16* o;
   int64_t ldo;
   float* lse;
+  __nv_bfloat16* o_lo;  // optional: o - bf16(o) as bf16 (same layout as o)
 };
 
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
@@ -379,7 +380,8 @@ __global__ void __launch_bounds__(128 + 256 * NH, 1)
     tc_fence_after();
     const int qrow = q0 + x * BM + row;
     const float inv = 1.f / l;
-    __nv_bfloat16* orow = p.o + ((int64_t)row0 + qrow) * p.ldo + (int64_t)h * HD + hf * (HD / NH);
+    const int64_t oofs = ((int64_t)row0 + qrow) * p.ldo + (int64_t)h * HD + hf * (HD / NH);
+    __nv_bfloat16* orow = p.o + oofs;
 #pragma unroll 1
     for (int cc = 0; cc < HD / NH / 32; ++cc) {
       uint32_t o[32];
@@ -389,12 +391,25 @@ __global__ void __launch_bounds__(128 + 256 * NH, 1)
         uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
+          float f[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(o[w * 8 + i]) * inv;
           uint4 pkt;
-          pkt.x = pack2(__uint_as_float(o[w * 8 + 0]) * inv, __uint_as_float(o[w * 8 + 1]) * inv);
-          pkt.y = pack2(__uint_as_float(o[w * 8 + 2]) * inv, __uint_as_float(o[w * 8 + 3]) * inv);
-          pkt.z = pack2(__uint_as_float(o[w * 8 + 4]) * inv, __uint_as_float(o[w * 8 + 5]) * inv);
-          pkt.w = pack2(__uint_as_float(o[w * 8 + 6]) * inv, __uint_as_float(o[w * 8 + 7]) * inv);
+          pkt.x = pack2(f[0], f[1]);
+          pkt.y = pack2(f[2], f[3]);
+          pkt.z = pack2(f[4], f[5]);
+          pkt.w = pack2(f[6], f[7]);
           dst[w] = pkt;
+          if (p.o_lo) {  // the rounding residual, for the backward's delta = rowsum(dO * O)
+            const uint32_t hv[4] = {pkt.x, pkt.y, pkt.z, pkt.w};
+            uint32_t lv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 hf2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hv[i]));
+              lv[i] = pack2(f[2 * i] - hf2.x, f[2 * i + 1] - hf2.y);
+            }
+            reinterpret_cast<uint4*>(p.o_lo + oofs + cc * 32)[w] = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+          }
         }
       }
     }
@@ -418,7 +433,7 @@ bool attn_tc_supported(const AttnGeom& g, int dtype, const void* q, const void* 
   return ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
 }
 
-int attn_fwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, void* o, float* lse,
+int attn_fwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, void* o, void* o_lo, float* lse,
                 cudaStream_t st) {
   using namespace tca;
   CUtensorMap mq, mk, mv;
@@ -432,7 +447,7 @@ int attn_fwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, 
     cudaFuncSetAttribute(fwd_tc_k<kFwdNH>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     attr = true;
   }
-  Params p{g.T, g.H, g.KVH, g.B, g.scale, (__nv_bfloat16*)o, g.ldo, lse};
+  Params p{g.T, g.H, g.KVH, g.B, g.scale, (__nv_bfloat16*)o, g.ldo, lse, (__nv_bfloat16*)o_lo};
   dim3 grid((g.T + 2 * BM - 1) / (2 * BM), g.H, g.B);
   fwd_tc_k<kFwdNH><<<grid, 128 + 256 * kFwdNH, kSmem, st>>>(mq, mk, mv, p);
   return check_launch("flash_fwd_tc");

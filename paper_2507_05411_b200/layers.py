@@ -581,15 +581,17 @@ class AttentionBehavior(Behavior):
         if rope is None:
             invoke_child("pos_emb", q, k, T)
         scale = 1.0 / math.sqrt(hd)
-        o, lse = ops.attention_fwd(q, k, v, B, T, H, KVH, hd, scale)
+        rec = is_recording()
+        # bf16: o's rounding residual too, for the backward's delta (cb_attention_fwd o_lo)
+        o, lse, o_lo = ops.attention_fwd(q, k, v, B, T, H, KVH, hd, scale, want_lo=rec)
         out = torch.empty((o.shape[0], d), device=x.device, dtype=torch.float32)
         ops.gemm(o, param("wo"), out, residual=ops.rows2d(residual) if residual is not None else None)
-        if is_recording():
+        if rec:
             dq = remat_plan("q_proj", "k_proj", "v_proj")
             dc = remat_plan("context")
             if dq == RECOMPUTE and rope is None:
                 dq = SAVE  # an unfused positional child would have to be re-run as well
-            save(x2=x2, qkv=keep(qkv, dq), o=keep(o, dc), lse=keep(lse, dc), rope=rope,
+            save(x2=x2, qkv=keep(qkv, dq), o=keep(o, dc), lse=keep(lse, dc), o_lo=keep(o_lo, dc), rope=rope,
                  geom=(B, T, H, KVH, hd, d, kvd))
         return out.view(B, T, d)
 
@@ -601,18 +603,18 @@ class AttentionBehavior(Behavior):
         if qkv is None:  # q/k/v projections rematerialised from the saved block input
             qkv, _ = self._project(module, s["x2"], T, True)
         q, k, v = qkv[:, :d], qkv[:, d:d + kvd], qkv[:, d + kvd:]
-        o, lse = restore(s["o"]), restore(s["lse"])
+        o, lse, o_lo = restore(s["o"]), restore(s["lse"]), restore(s["o_lo"])
         if o is None:  # context rematerialised: the attention forward again
-            o, lse = ops.attention_fwd(q, k, v, B, T, H, KVH, hd, 1.0 / math.sqrt(hd))
+            o, lse, o_lo = ops.attention_fwd(q, k, v, B, T, H, KVH, hd, 1.0 / math.sqrt(hd), want_lo=True)
         g = ops.rows2d(ops.cast(dout, adt))
         do = _linear_bwd(o, param("wo"), g, param_grad("wo"), adt)
         dqkv = torch.empty_like(qkv)
         dq, dk, dv = dqkv[:, :d], dqkv[:, d:d + kvd], dqkv[:, d + kvd:]
         if s["rope"] is not None:
             ops.attention_bwd_rope(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd,
-                                   1.0 / math.sqrt(hd), s["rope"][0], s["rope"][1])
+                                   1.0 / math.sqrt(hd), s["rope"][0], s["rope"][1], o_lo=o_lo)
         else:
-            ops.attention_bwd(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, 1.0 / math.sqrt(hd))
+            ops.attention_bwd(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, 1.0 / math.sqrt(hd), o_lo=o_lo)
             backward_child("pos_emb", dq, dk)
         wq, wk, wv = param("wq"), param("wk"), param("wv")
         wqkv = fused_columns(wq, wk, wv)

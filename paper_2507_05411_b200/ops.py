@@ -320,34 +320,35 @@ def zero_(t: torch.Tensor):
 
 
 # ------------------------------------------------------------------------ attention
-def attention_fwd(q, k, v, B, T, H, KVH, hd, scale):
+def attention_fwd(q, k, v, B, T, H, KVH, hd, scale, want_lo: bool = False):
+    """Returns (o, lse) or, with want_lo (bf16), (o, lse, o_lo): o_lo = o - bf16(o) for the
+    backward's delta (cb_attention_fwd)."""
     o = torch.empty((B * T, H * hd), device=q.device, dtype=q.dtype)
     lse = torch.empty((B, H, T), device=q.device, dtype=torch.float32)
+    o_lo = torch.empty_like(o) if (want_lo and q.dtype == torch.bfloat16) else None
     _profiled("attn_fwd", 4 * B * T * T * H * hd, _lib.call, "cb_attention_fwd", B, T, H, KVH, hd, dt(q),
-              q.data_ptr(), ld(q), k.data_ptr(), ld(k), v.data_ptr(), ld(v), o.data_ptr(), ld(o), lse.data_ptr(),
-              float(scale), stream_ptr())
-    return o, lse
+              q.data_ptr(), ld(q), k.data_ptr(), ld(k), v.data_ptr(), ld(v), o.data_ptr(), ld(o), _ptr(o_lo),
+              lse.data_ptr(), float(scale), stream_ptr())
+    return (o, lse, o_lo) if want_lo else (o, lse)
 
 
-def attention_bwd_rope(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, scale, cos_t, sin_t):
-    """Backward for q/k rotated in the projection epilogue: dq/dk come back un-rotated."""
-    delta = torch.empty((B, H, T), device=q.device, dtype=torch.float32)
-    _profiled("attn_bwd", 8 * B * T * T * H * hd, _lib.call, "cb_attention_bwd_rope", B, T, H, KVH, hd, dt(q),
-              q.data_ptr(), ld(q), k.data_ptr(), ld(k), v.data_ptr(), ld(v), o.data_ptr(), ld(o), lse.data_ptr(),
-              do.data_ptr(), ld(do), delta.data_ptr(), dq.data_ptr(), ld(dq), dk.data_ptr(), ld(dk), dv.data_ptr(),
-              ld(dv), float(scale), cos_t.data_ptr(), sin_t.data_ptr(), stream_ptr())
-
-
-def attention_bwd(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, scale):
+def attention_bwd_rope(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, scale, cos_t, sin_t, o_lo=None):
     delta = torch.empty((B, H, T), device=q.device, dtype=torch.float32)
     # algorithmic FLOPs: 2x forward (dP, dV, dQ, dK), the reference's backward_multiplier (mesh.py:644)
+    _profiled("attn_bwd", 8 * B * T * T * H * hd, _lib.call, "cb_attention_bwd_rope", B, T, H, KVH, hd, dt(q),
+              q.data_ptr(), ld(q), k.data_ptr(), ld(k), v.data_ptr(), ld(v), o.data_ptr(), ld(o), _ptr(o_lo),
+              lse.data_ptr(), do.data_ptr(), ld(do), delta.data_ptr(), dq.data_ptr(), ld(dq), dk.data_ptr(), ld(dk),
+              dv.data_ptr(), ld(dv), float(scale), cos_t.data_ptr(), sin_t.data_ptr(), stream_ptr())
+
+
+def attention_bwd(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, scale, o_lo=None):
+    delta = torch.empty((B, H, T), device=q.device, dtype=torch.float32)
     _profiled("attn_bwd", 8 * B * T * T * H * hd, _lib.call, "cb_attention_bwd", B, T, H, KVH, hd, dt(q),
-              q.data_ptr(), ld(q), k.data_ptr(), ld(k), v.data_ptr(), ld(v), o.data_ptr(), ld(o), lse.data_ptr(),
-              do.data_ptr(), ld(do), delta.data_ptr(), dq.data_ptr(), ld(dq), dk.data_ptr(), ld(dk), dv.data_ptr(),
-              ld(dv), float(scale), stream_ptr())
+              q.data_ptr(), ld(q), k.data_ptr(), ld(k), v.data_ptr(), ld(v), o.data_ptr(), ld(o), _ptr(o_lo),
+              lse.data_ptr(), do.data_ptr(), ld(do), delta.data_ptr(), dq.data_ptr(), ld(dq), dk.data_ptr(), ld(dk),
+              dv.data_ptr(), ld(dv), float(scale), stream_ptr())
 
 
-# -------------------------------------------------------------------- cross-entropy
 def xent(logits2d: torch.Tensor, tokens: torch.Tensor, dlogits: torch.Tensor | None, grad_scale: float):
     B, T = tokens.shape
     V = logits2d.shape[1]

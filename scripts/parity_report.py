@@ -57,6 +57,15 @@ def yardsticks(cfg, B, T, precision):
     return {k: TS._rel(g32[k], g64[k]) for k in g64}, {k: TS._rel(gb[k], g64[k]) for k in g64}
 
 
+def element_dump(cfg, B, T, precision, key, rep, top=8):
+    """The entries of tensor `key` whose updated values differ most from the oracle's."""
+    g = rep["arrays"]
+    d = np.abs(g["gpu_param"][key] - g["oracle_param"][key]).ravel()
+    idx = np.argsort(-d)[:top]
+    return [{"i": int(i), "dparam": float(d[i]), "g_oracle": float(g["oracle_grad"][key].ravel()[i]),
+             "g_gpu": float(g["gpu_grad"][key].ravel()[i])} for i in idx]
+
+
 def main():
     out = {}
     for name in sys.argv[1:] or list(CASES):
@@ -74,7 +83,13 @@ def main():
         for k in sorted(rep.get("grad", {}), key=lambda k: -rep["grad"][k])[:8]:
             rows.append({"tensor": k, "gpu_grad": rep["grad"][k], "gpu_param": rep["param"][k], "fp32_grad": e32[k],
                          "bf16_operand_grad": ebf[k]})
+        if rep.get("param"):
+            wk = max(rep["param"], key=lambda k: rep["param"][k])
+            out_el = element_dump(mk(), B, T, prec, wk, rep)
+        else:
+            out_el = None
         out[name] = {"precision": prec, "B": B, "T": T, "loss_rel": rep.get("loss"), "assert": err,
+                     "worst_param_elements": out_el,
                      "worst_param": max(rep.get("param", {0: 0}).values()), "rows": rows}
         print(json.dumps({name: out[name]}), flush=True)
 

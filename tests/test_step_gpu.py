@@ -107,7 +107,8 @@ def run_parity(cfg, precision, B, T, tol, seed=0, check_update=True, loose=None,
     gerr = {k: _rel(grads[k], go[k]) for k in go}
     perr = {k: _rel(params[k], po[k]) for k in po}
     if report is not None:
-        report.update({"loss": abs(loss - lo) / abs(lo), "grad": gerr, "param": perr})
+        report.update({"loss": abs(loss - lo) / abs(lo), "grad": gerr, "param": perr,
+                       "arrays": {"gpu_grad": grads, "oracle_grad": go, "gpu_param": params, "oracle_param": po}})
     bad = sorted((gerr[k], gbound[k], k) for k in go if gerr[k] >= gbound[k])
     assert not bad, f"grad {bad[-3:]}"
     if check_update:
