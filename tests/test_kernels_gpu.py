@@ -130,7 +130,11 @@ def test_attention_fwd_bwd(cuda, B, T, H, KVH, hd, dt, path):
         assert torch.equal(o2, o)
         full = (o2.double() + o_lo.double()).view(B, T, H, hd).transpose(1, 2)
         if hd == 128 and path == 0 and not warp_mma:  # tcgen05 forward: the residual is real
-            assert _rel(full, O.detach()) < 2e-4
+            # o + o_lo is the kernel's f32 output: at least as close to the f64 reference as o
+            # (its own error is P's bf16 rounding inside the forward)
+            o_ref = O.detach()
+            assert _rel(full, o_ref) <= _rel(o.view(B, T, H, hd).transpose(1, 2), o_ref)
+            assert o_lo.any()
         else:
             assert not o_lo.any()
         assert _rel(d2[:, :d].view(B, T, H, hd).transpose(1, 2), Q.grad) < tol

@@ -51,11 +51,18 @@ def fp32_oracle_errors(st, toks, spec, opt, forced=None):
     return ({k: _rel(g32[k], g64[k]) for k in g64}, {k: _rel(upd(g32[k], k), upd(g64[k], k)) for k in g64})
 
 
+def _bf16_operand_grads(st, toks, spec, forced=None):
+    with O.bf16_operands():
+        lo, g, summ = O.value_and_grad(st, toks, spec, forced)
+    return lo, dict(_leaves(g)), summ
+
+
 def run_parity(cfg, precision, B, T, tol, seed=0, check_update=True, loose=None, exact_routing=False, report=None):
     """Loss, every gradient and every updated parameter vs the f64 oracle (relative L2).
 
-    f32 mode: each tensor is held to 1e-5, or — only where a plain fp32 restatement itself
-    misses 1e-5 (fp32_oracle_errors) — to 3x that fp32 error.
+    f32 mode: every gradient is held to 1e-5, or — only where a plain fp32 restatement itself
+    misses 1e-5 (fp32_oracle_errors) — to 3x that fp32 error; updated parameters to 1e-5 on
+    the well-conditioned entries (see below).
     bf16 mode: 2e-2; MoE layers are compared at the GPU's expert choices (bf16 router inputs
     flip ~0.5% of top-k choices against the f64 oracle), unless exact_routing.
     exact_routing: the GPU's top-k indices must equal the oracle's bit for bit.
@@ -100,12 +107,39 @@ def run_parity(cfg, precision, B, T, tol, seed=0, check_update=True, loose=None,
         e_g, e_p = fp32_oracle_errors(st, toks, spec, opt, forced)
         gbound = {k: max(tol, 3 * e_g[k]) for k in go}
         pbound = {k: max(tol, 3 * e_p[k]) for k in go}
+    else:
+        # bf16: where the oracle with only its GEMM operands rounded to bf16 (the least
+        # rounding any bf16 path does) already errs by more than tol / 1.5, the tensor is held
+        # to 1.5x that intrinsic error instead (ReLU kinks, sigmoid's common mode)
+        _, gb, _ = _bf16_operand_grads(st, toks, spec, forced)
+        gbound = {k: max(tol, 1.5 * _rel(gb[k], go[k])) for k in go}
     for k in go:
         for sub, v in loose.items():
             if sub in k:
                 gbound[k], pbound[k] = max(gbound[k], v), max(pbound[k], v)
     gerr = {k: _rel(grads[k], go[k]) for k in go}
     perr = {k: _rel(params[k], po[k]) for k in po}
+    if precision == "f32" and check_update:
+        # Step-1 AdamW is p - lr * g / (|g| + eps): for |g| >= 100 eps the update's relative
+        # sensitivity to a relative gradient error is <= eps / |g| <= 1e-2, so those entries are
+        # held end to end to 1e-5 (relative L2 over them).  Entries with |g| < 100 eps are
+        # ill-conditioned — an f32 gradient within the 1e-5 contract can still move such an
+        # update by up to lr (the element dumps of profiles/r02_f32_param_conditioning.txt) — and
+        # are held instead to AdamW applied in f64 to the GPU's own gradients (1e-6 relative).
+        st0 = dict(_leaves(st))
+        cond = {}
+        for k in po:
+            well = np.abs(go[k]) >= 100 * opt.eps
+            own = O.adamw_update(st0[k], grads[k], 0 * st0[k], 0 * st0[k], 1, opt)[0]
+            cond[k] = (_rel(params[k][well], po[k][well]) if well.any() else 0.0,
+                       _rel(params[k][~well], own[~well]) if (~well).any() else 0.0, int((~well).sum()))
+        bad = sorted((c[0], k) for k, c in cond.items() if c[0] >= tol)
+        assert not bad, f"param (well-conditioned entries) {bad[-3:]}"
+        bad = sorted((c[1], k) for k, c in cond.items() if c[1] >= 1e-6)
+        assert not bad, f"param (ill-conditioned entries vs AdamW on the GPU's gradients) {bad[-3:]}"
+        if report is not None:
+            report["param_conditioned"] = cond
+        check_update = False
     if report is not None:
         report.update({"loss": abs(loss - lo) / abs(lo), "grad": gerr, "param": perr,
                        "arrays": {"gpu_grad": grads, "oracle_grad": go, "gpu_param": params, "oracle_param": po}})
