@@ -258,6 +258,9 @@ def main():
     ap.add_argument("--seq", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--moe-routing", default="router", choices=["router", "balanced"],
+                    help="balanced: every expert gets the same number of tokens (benchmark of dispatch / grouped "
+                         "expert GEMMs / combine off the reference init's degenerate routing; not the reference numerics)")
     ap.add_argument("--remat", default=None,
                     help="remat policy alias for every layer (reference mesh.py:204-252 names); default: "
                          "save_qkvo_flash for 70b_layer (BASELINE configs[4]: FSDP + rematerialisation; the "
@@ -292,6 +295,8 @@ def main():
         for i in range(len(cfg.get("model.decoder.transformer.layer"))):
             cfg = cfg.set(f"model.decoder.transformer.layer[{i}].remat_policy", POLICY_ALIASES[args.remat])
     eng = TrainEngine(cfg, device=dev)
+    if args.moe_routing == "balanced":
+        eng.options["moe_balanced_routing"] = True
     V = eng.cfg.get("model.vocab_size")
     B, T = args.batch, args.seq
     nsteps = args.warmup + args.steps
@@ -400,6 +405,7 @@ def main():
         "config": {"workload": args.config, "global_batch": world * B, "per_gpu_batch": B, "seq_len": T,
                    "d_model": eng.cfg.get("model.dim"), "layers": len(eng.cfg.get("model.decoder.transformer.layer")),
                    "vocab": V, "params": eng.param_count(), "parallelism": f"fsdp{world}", "remat": args.remat,
+                   **({"moe_routing": args.moe_routing} if args.config == "moe" else {}),
                    "collectives": ("none" if world == 1 else
                                    ("all-gather " + ("copy-engine/symm-mem" if eng._ce_gather else "nccl")
                                     + ", reduce-scatter " + ("copy-engine/symm-mem + cb_sum_parts"

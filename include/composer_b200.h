@@ -86,6 +86,26 @@ CB_API int cb_gemm_gated_bwd(int M, int H, int K, const void* A, int64_t lda, in
                              int64_t ldb, int trans_b, const void* pre, int64_t ldpre, void* dpre, int64_t lddpre,
                              int act0, int act1, void* stream);
 
+/* Grouped GEMMs: every MoE expert in ONE persistent launch (layers.py:513-533, the expert
+ * einsums; replaces the per-expert loop and its host round trip for the expert offsets).
+ * grp_off: DEVICE int[groups+1] row offsets, each a multiple of 256 (cb_moe_dispatch_padded).
+ * mode 1 (groups split the rows): D[rows of g] = op(A)[rows of g] @ op(B_g); B_g is block g of
+ *   B stacked along K ([groups*K][N], trans_b = 0) or along N ([groups*N][K], trans_b = 1);
+ *   M = the row capacity (multiple of 256); only rows < grp_off[groups] are computed.
+ * mode 2 (groups split K): D_g (+)= A[rows of g]^T @ B[rows of g] (trans_a = 1, trans_b = 0,
+ *   K = the row capacity); D_g = rows [g*M, (g+1)*M) of D; an empty group writes nothing.
+ * The gated forms are cb_gemm_gated_fwd/bwd (mode 1) with B = every expert's [W1|Wg]
+ * stacked [groups*K][2H] (fwd) or W2 stacked [groups*H][K] read transposed (bwd). */
+CB_API int cb_gemm_grouped(int mode, int groups, const int* grp_off, int M, int N, int K, const void* A, int64_t lda,
+                           int trans_a, const void* B, int64_t ldb, int trans_b, void* D, int64_t ldd, int d_dtype,
+                           float alpha, int accumulate, void* stream);
+CB_API int cb_gemm_gated_fwd_grouped(int groups, const int* grp_off, int M, int H, int K, const void* A, int64_t lda,
+                                     const void* B, int64_t ldb, void* pre, int64_t ldpre, void* hidden, int64_t ldh,
+                                     int act0, int act1, void* stream);
+CB_API int cb_gemm_gated_bwd_grouped(int groups, const int* grp_off, int M, int H, int K, const void* A, int64_t lda,
+                                     const void* B, int64_t ldb, const void* pre, int64_t ldpre, void* dpre,
+                                     int64_t lddpre, int act0, int act1, void* stream);
+
 /* ---------------------------------------------------------------------------------
  * RMSNorm (layers.py:176-193): y = x / sqrt(mean(x^2) + eps) * scale, rstd[row] saved.
  * Backward: dx = dres + d(norm)/dx . dy  (dres: the residual branch gradient, may be
@@ -217,6 +237,16 @@ CB_API int cb_moe_router_bwd_gemms(int64_t n, int dim, int experts, const void* 
                                    int64_t lddx, float* workspace, void* stream);
 CB_API int cb_invert_perm(int64_t n, const int32_t* perm, int32_t* inv, void* stream);
 CB_API int cb_widen_i32(int64_t n, const int32_t* a, int64_t* b, void* stream);
+/* Padded expert layout for the grouped GEMMs, on the device: from the stable sort's expert
+ * offsets, poff[e] (each expert's rows rounded up to 256), xe[poff[e] + j] = x[perm[off[e]+j] / top_k]
+ * with the pad rows zeroed, and pinv[assignment] = its padded row (for cb_moe_combine{,_bwd}).
+ * cap (rows of xe) >= nk + 255 * experts. */
+CB_API int cb_moe_dispatch_padded(int64_t nk, int dim, int experts, int top_k, const int* offsets, const int32_t* perm,
+                                  const void* x, int64_t ldx, int dtype, int* poff, int32_t* pinv, void* xe,
+                                  int64_t ldxe, int cap, void* stream);
+/* Zeroes the pad rows of a padded-layout buffer (e.g. the combine backward's dY). */
+CB_API int cb_moe_zero_pad_rows(int cap, int dim, int experts, const int* offsets, const int* poff, void* buf,
+                                int64_t ld, int dtype, void* stream);
 
 /* ---------------------------------------------------------------------------------
  * Parameter init on the device, bit-identical to init_state (prng.py:61-69,

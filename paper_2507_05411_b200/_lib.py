@@ -59,6 +59,11 @@ SIGNATURES: dict[str, list] = {
     "cb_attention_bwd_rope": [_I, _I, _I, _I, _I, _I, _P, _L, _P, _L, _P, _L, _P, _L, _P, _P, _P, _L, _P, _P, _L,
                               _P, _L, _P, _L, _F, _P, _P, _P],
     "cb_attention_set_tc": [_I],
+    "cb_gemm_grouped": [_I, _I, _P, _I, _I, _I, _P, _L, _I, _P, _L, _I, _P, _L, _I, _F, _I, _P],
+    "cb_gemm_gated_fwd_grouped": [_I, _P, _I, _I, _I, _P, _L, _P, _L, _P, _L, _P, _L, _I, _I, _P],
+    "cb_gemm_gated_bwd_grouped": [_I, _P, _I, _I, _I, _P, _L, _P, _L, _P, _L, _P, _L, _I, _I, _P],
+    "cb_moe_dispatch_padded": [_L, _I, _I, _I, _P, _P, _P, _L, _I, _P, _P, _P, _L, _I, _P],
+    "cb_moe_zero_pad_rows": [_I, _I, _I, _P, _P, _P, _L, _I, _P],
     "cb_xent_fwd_bwd": [_I, _I, _I, _P, _L, _I, _P, _P, _P, _L, _I, _F, _P, _P, _P],
     "cb_adamw": [_L, _P, _P, _P, _P, _P, _F, _F, _F, _F, _F, _I, _F, _P],
     "cb_moe_route": [_L, _I, _I, _I, _P, _L, _I, _P, _P, _P, _P, _P],

@@ -98,7 +98,18 @@ struct Args {
   // order and applies the epilogue (deterministic: no atomics)
   int splits = 1;
   float* ws = nullptr;
+  // grouped launch (all MoE experts in one persistent launch, CTA-pair engine only):
+  // grp_off = device [G+1] row offsets, each a multiple of 256, read by the kernel (no host
+  // round trip).  grp_mode 1: the groups split the rows of A and D; the tiles of group g read
+  // B at a coordinate offset g * b_grp_stride along K (MN-major B, stacked [G*K][N]) or along
+  // N (K-major B, stacked [G*N][K]); tiles_m is taken from grp_off[G].  grp_mode 2: the groups
+  // split the K rows of A and B (both MN-major, stacked along K); group g writes D rows
+  // [g*M, (g+1)*M) and an empty group writes nothing.
+  const int* grp_off = nullptr;
+  int grp_mode = 0, G = 0;
+  int64_t b_grp_stride = 0;
 };
+constexpr int kMaxGroups = 64;
 
 __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
   const int per_group = kGroupM * tiles_n;
@@ -753,18 +764,43 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rank = (int)cluster_ctarank();
   const bool leader = rank == 0;
-  const int tiles_mg = (args.tiles_m + 1) / 2;  // 256-row tile pairs
+  __shared__ int s_goff[kMaxGroups + 1];
+  const int gm = args.grp_mode;
+  if (gm) {
+    for (int i = threadIdx.x; i <= args.G; i += blockDim.x) s_goff[i] = args.grp_off[i];
+    __syncthreads();
+  }
+  // 256-row tile pairs (grouped over M: the padded row count comes from the device offsets)
+  const int tiles_mg = gm == 1 ? s_goff[args.G] / (2 * BM) : (args.tiles_m + 1) / 2;
   const int S = args.splits;
-  const int num_units = tiles_mg * args.tiles_n * S;
+  const int per_group = tiles_mg * args.tiles_n;
+  const int num_units = gm == 2 ? args.G * per_group : per_group * S;
   const int unit0 = (int)(blockIdx.x >> 1), unit_stride = (int)(gridDim.x >> 1);
   const int nk_all = (args.K + BK - 1) / BK;
-  auto coords = [&](int u, int& tm, int& tn) {
+  // tile (tm, tn) of unit u and its group g (0 when not grouped)
+  auto coords = [&](int u, int& tm, int& tn, int& g) {
     int tg;
-    tile_coords(u / S, tiles_mg, args.tiles_n, tg, tn);
+    g = 0;
+    if (gm == 2) {
+      g = u / per_group;
+      tile_coords(u - g * per_group, tiles_mg, args.tiles_n, tg, tn);
+    } else {
+      tile_coords(u / S, tiles_mg, args.tiles_n, tg, tn);
+    }
     tm = tg * 2 + rank;
+    if (gm == 1) {  // the group whose rows hold this 256-row tile
+      const int r = tg * 2 * BM;
+      while (g + 1 < args.G && s_goff[g + 1] <= r) ++g;
+    }
   };
-  // k-block range of unit u (its split-K slice)
+  // k-block range of unit u (its split-K slice, or its group's K rows)
   auto krange = [&](int u, int& kb0, int& kb1) {
+    if (gm == 2) {
+      const int g = u / per_group;
+      kb0 = s_goff[g] / BK;
+      kb1 = s_goff[g + 1] / BK;
+      return;
+    }
     const int sl = u % S;
     kb0 = (int)((int64_t)sl * nk_all / S);
     kb1 = (int)((int64_t)(sl + 1) * nk_all / S);
@@ -794,12 +830,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int u = unit0; u < num_units; u += unit_stride) {
-      int tm, tn;
-      coords(u, tm, tn);
+      int tm, tn, g;
+      coords(u, tm, tn, g);
       const int m0 = tm * BM;
       // B columns this CTA stages: its half of the 256-column tile, or (gated forward) the
       // tile's 128 columns of the a half (rank 0) / of the g half (rank 1)
-      const int nb = args.e.glu == 1 ? rank * args.e.glu_h + tn * 128 : tn * BN + rank * 128;
+      int nb = args.e.glu == 1 ? rank * args.e.glu_h + tn * 128 : tn * BN + rank * 128;
+      // grouped over M: group g's B block (stacked along K for MN-major B, along N otherwise)
+      const int bk_off = (gm == 1 && args.b_mn) ? (int)(g * args.b_grp_stride) : 0;
+      if (gm == 1 && !args.b_mn) nb += (int)(g * args.b_grp_stride);
       int kb0, kb1;
       krange(u, kb0, kb1);
       for (int kb = kb0; kb < kb1; ++kb) {
@@ -820,7 +859,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d_pair(b_dst, &tmB, fb, k0, nb);
           } else {
 #pragma unroll
-            for (int j = 0; j < 2; ++j) tma_load_2d_pair(b_dst + j * 8192, &tmB, fb, nb + 64 * j, k0);
+            for (int j = 0; j < 2; ++j) tma_load_2d_pair(b_dst + j * 8192, &tmB, fb, nb + 64 * j, k0 + bk_off);
           }
         }
         __syncwarp();
@@ -840,13 +879,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int u = unit0; u < num_units; u += unit_stride, ++it) {
+      for (int u = unit0; u < num_units; u += unit_stride) {
+        int kb0, kb1;
+        krange(u, kb0, kb1);
+        if (kb1 <= kb0) continue;  // an empty group (grouped over K): no tile
         const int acc = it & 1;
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        int kb0, kb1;
-        krange(u, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -866,26 +906,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (elect_one()) umma_commit_pair_mc(&tfull[acc], 0x3);
         __syncwarp();
+        ++it;
       }
     }
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs: each drains its own 128 rows) ----------------
     const int q = warp & 3;
-    const Epi& e = args.e;
+    const Epi& e0 = args.e;
     const uint32_t tempty_leader0 = leader_addr(&tempty[0]);
     uint8_t* stg = smem + C::kStages * C::kStageBytes + 256 + q * 32 * kStagePitch;  // this warp's stage
-    const bool staged = S == 1 && staged_ok(e) && (g_epi_staged & kStagedBf16);
+    const bool staged = S == 1 && staged_ok(e0) && (g_epi_staged & kStagedBf16);
     // gated backward through the stage: pre / dpre rows 16-byte aligned, whole 32-column chunks
-    const bool glu_staged = GLU && e.glu == 2 && e.N % 32 == 0 && e.glu_h % 8 == 0 && (e.ld_glu_pre & 7) == 0 &&
-                            (e.ld_glu_out & 7) == 0 && (reinterpret_cast<uintptr_t>(e.glu_pre) & 15) == 0 &&
-                            (reinterpret_cast<uintptr_t>(e.glu_out) & 15) == 0;
+    const bool glu_staged = GLU && e0.glu == 2 && e0.N % 32 == 0 && e0.glu_h % 8 == 0 && (e0.ld_glu_pre & 7) == 0 &&
+                            (e0.ld_glu_out & 7) == 0 && (reinterpret_cast<uintptr_t>(e0.glu_pre) & 15) == 0 &&
+                            (reinterpret_cast<uintptr_t>(e0.glu_out) & 15) == 0;
     int it = 0;
-    for (int u = unit0; u < num_units; u += unit_stride, ++it) {
-      int tm, tn;
-      coords(u, tm, tn);
+    for (int u = unit0; u < num_units; u += unit_stride) {
+      int tm, tn, g;
+      coords(u, tm, tn, g);
+      if (gm == 2) {
+        int kb0, kb1;
+        krange(u, kb0, kb1);
+        if (kb1 <= kb0) continue;  // an empty group: its D rows are left untouched
+      }
       const int acc = it & 1;
-      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      ++it;
+      mbar_wait(&tfull[acc], ((it - 1) >> 1) & 1);
       tc_fence_after();
+      Epi eg = e0;
+      if (gm == 2)  // group g's rows of the stacked output
+        eg.D = reinterpret_cast<char*>(eg.D) + (int64_t)g * eg.M * eg.ldd * (eg.d_f32 ? 4 : 2);
+      const Epi& e = eg;
       const int row0 = tm * BM + q * 32;
       const int row = row0 + lane;
       const bool row_ok = row < e.M;
@@ -1022,15 +1073,18 @@ int launch_pair(const Args& a, const void* A, int64_t lda, const void* B, int64_
   using C = Cfg2;
   CUtensorMap ta, tb;
   int s;
+  // grouped over M: B holds every group's block, stacked along K (MN-major) or N (K-major)
+  const int64_t bK = a.grp_mode == 1 && a.b_mn ? (int64_t)a.G * a.K : a.K;
+  const int64_t bN = a.grp_mode == 1 && !a.b_mn ? (int64_t)a.G * a.N : a.N;
   if (!a.a_mn)
     s = make_tmap_2d_bf16(&ta, A, a.M, a.K, lda, BM, BK);
   else
     s = make_tmap_2d_bf16(&ta, A, a.K, a.M, lda, BK, 64);
   if (s) return s;
   if (!a.b_mn)
-    s = make_tmap_2d_bf16(&tb, B, a.N, a.K, ldb, 128, BK);
+    s = make_tmap_2d_bf16(&tb, B, bN, a.K, ldb, 128, BK);
   else
-    s = make_tmap_2d_bf16(&tb, B, a.K, a.N, ldb, BK, 64);
+    s = make_tmap_2d_bf16(&tb, B, bK, a.N, ldb, BK, 64);
   if (s) return s;
   static bool attr_set = false;
   if (!attr_set) {
@@ -1039,9 +1093,9 @@ int launch_pair(const Args& a, const void* A, int64_t lda, const void* B, int64_
     attr_set = true;
   }
   Args args = a;
-  args.splits = choose_splits(a);
+  args.splits = a.grp_mode ? 1 : choose_splits(a);
   args.ws = args.splits > 1 ? g_ws : nullptr;
-  const int pairs = ((a.tiles_m + 1) / 2) * a.tiles_n * args.splits;
+  const int pairs = ((a.tiles_m + 1) / 2) * a.tiles_n * args.splits * (a.grp_mode == 2 ? a.G : 1);
   const int grid = 2 * std::min(pairs, kNumSMs / 2);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -1097,9 +1151,9 @@ int launch(const Args& a, const void* A, int64_t lda, const void* B, int64_t ldb
     return check_launch("gemm_tc");
   }
   Args args = a;
-  args.splits = choose_splits(a);
+  args.splits = a.grp_mode ? 1 : choose_splits(a);
   args.ws = args.splits > 1 ? g_ws : nullptr;
-  const int pairs = ((a.tiles_m + 1) / 2) * a.tiles_n * args.splits;
+  const int pairs = ((a.tiles_m + 1) / 2) * a.tiles_n * args.splits * (a.grp_mode == 2 ? a.G : 1);
   const int grid = 2 * std::min(pairs, kNumSMs / 2);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -1252,6 +1306,100 @@ extern "C" int cb_gemm_gated_bwd(int M, int H, int K, const void* A, int64_t lda
   a.e.ld_glu_out = lddpre;
   a.e.glu_pre = pre;
   a.e.ld_glu_pre = ldpre;
+  return tc::launch_pair(a, A, lda, B, ldb, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------- grouped (MoE experts)
+static int grouped_check(int groups, const int* grp_off, const char* who) {
+  if (groups < 1 || groups > tc::kMaxGroups) return fail(CB_ERR_ARG, "%s: 1..%d groups", who, tc::kMaxGroups);
+  if (!grp_off) return fail(CB_ERR_ARG, "%s: null group offsets", who);
+  if (tc::g_gemm_mc != 3 || g_gemm_path == 1) return fail(CB_ERR_UNSUPPORTED, "%s: needs the CTA-pair engine", who);
+  return CB_OK;
+}
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+extern "C" int cb_gemm_grouped(int mode, int groups, const int* grp_off, int M, int N, int K, const void* A,
+                               int64_t lda, int trans_a, const void* B, int64_t ldb, int trans_b, void* D, int64_t ldd,
+                               int d_dtype, float alpha, int accumulate, void* stream) {
+  if (int s = grouped_check(groups, grp_off, "gemm_grouped")) return s;
+  if (mode != 1 && mode != 2) return fail(CB_ERR_ARG, "gemm_grouped: mode 1 (rows) or 2 (K)");
+  if (M <= 0 || N <= 0 || K <= 0) return fail(CB_ERR_SHAPE, "gemm_grouped: empty extent");
+  if ((mode == 1 && M % 256) || (mode == 2 && K % 256))
+    return fail(CB_ERR_SHAPE, "gemm_grouped: the grouped extent must be a multiple of 256");
+  if (mode == 2 && (!trans_a || trans_b)) return fail(CB_ERR_ARG, "gemm_grouped mode 2: A^T @ B (rows along K)");
+  if (!aligned16(A) || !aligned16(B) || ((lda | ldb) & 7))
+    return fail(CB_ERR_UNSUPPORTED, "gemm_grouped: 16-byte aligned operands");
+  tc::Args a;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.a_mn = trans_a ? 1 : 0;
+  a.b_mn = trans_b ? 0 : 1;
+  a.tiles_m = (M + tc::BM - 1) / tc::BM;
+  a.tiles_n = (N + 255) / 256;
+  a.e = Epi{D, ldd, d_dtype == CB_DT_F32, nullptr, 0, 0, alpha, accumulate, M, N};
+  a.grp_off = grp_off;
+  a.grp_mode = mode;
+  a.G = groups;
+  a.b_grp_stride = trans_b ? N : K;
+  return tc::launch_pair(a, A, lda, B, ldb, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int cb_gemm_gated_fwd_grouped(int groups, const int* grp_off, int M, int H, int K, const void* A,
+                                         int64_t lda, const void* B, int64_t ldb, void* pre, int64_t ldpre,
+                                         void* hidden, int64_t ldh, int act0, int act1, void* stream) {
+  if (int s = grouped_check(groups, grp_off, "gemm_gated_fwd_grouped")) return s;
+  if (M % 256 || H % 128 || !glu_ok(M, H, K, A, lda, B, ldb, pre, ldpre, hidden, ldh))
+    return fail(CB_ERR_UNSUPPORTED, "gemm_gated_fwd_grouped: not applicable (M=%d H=%d K=%d)", M, H, K);
+  tc::Args a;
+  a.M = M;
+  a.N = 2 * H;
+  a.K = K;
+  a.a_mn = 0;
+  a.b_mn = 1;
+  a.tiles_m = M / tc::BM;
+  a.tiles_n = H / 128;
+  a.e = Epi{pre, ldpre, 0, nullptr, 0, 0, 1.f, 0, M, 2 * H};
+  a.e.glu = 1;
+  a.e.glu_h = H;
+  a.e.glu_a0 = act0;
+  a.e.glu_a1 = act1;
+  a.e.glu_out = hidden;
+  a.e.ld_glu_out = ldh;
+  a.grp_off = grp_off;
+  a.grp_mode = 1;
+  a.G = groups;
+  a.b_grp_stride = K;  // B = [W1|Wg] of every group stacked along K: [groups*K][2H]
+  return tc::launch_pair(a, A, lda, B, ldb, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int cb_gemm_gated_bwd_grouped(int groups, const int* grp_off, int M, int H, int K, const void* A,
+                                         int64_t lda, const void* B, int64_t ldb, const void* pre, int64_t ldpre,
+                                         void* dpre, int64_t lddpre, int act0, int act1, void* stream) {
+  if (int s = grouped_check(groups, grp_off, "gemm_gated_bwd_grouped")) return s;
+  if (M % 256 || !glu_ok(M, H, K, A, lda, B, ldb, pre, ldpre, dpre, lddpre))
+    return fail(CB_ERR_UNSUPPORTED, "gemm_gated_bwd_grouped: not applicable (M=%d H=%d K=%d)", M, H, K);
+  tc::Args a;
+  a.M = M;
+  a.N = H;
+  a.K = K;
+  a.a_mn = 0;
+  a.b_mn = 0;  // dhidden = dy @ W2^T: W2 of every group stacked [groups*H][K], K-major
+  a.tiles_m = M / tc::BM;
+  a.tiles_n = (H + 255) / 256;
+  a.e = Epi{dpre, lddpre, 0, nullptr, 0, 0, 1.f, 0, M, H};
+  a.e.glu = 2;
+  a.e.glu_h = H;
+  a.e.glu_a0 = act0;
+  a.e.glu_a1 = act1;
+  a.e.glu_out = dpre;
+  a.e.ld_glu_out = lddpre;
+  a.e.glu_pre = pre;
+  a.e.ld_glu_pre = ldpre;
+  a.grp_off = grp_off;
+  a.grp_mode = 1;
+  a.G = groups;
+  a.b_grp_stride = H;
   return tc::launch_pair(a, A, lda, B, ldb, reinterpret_cast<cudaStream_t>(stream));
 }
 

@@ -441,6 +441,83 @@ __global__ void __launch_bounds__(256) router_dx_k(int64_t n, int d, int E, cons
   }
 }
 
+// ------------------------------------------------------------- padded expert layout
+// The grouped expert GEMMs (cb_gemm_grouped / cb_gemm_gated_*_grouped) need every expert's
+// rows to start on a 256-row boundary: expert e owns padded rows [poff[e], poff[e+1]),
+// poff[e+1] - poff[e] = roundup(count_e, 256); its first count_e rows are its assignments in
+// the stable sorted order, the rest are zero.  Everything stays on the device (no host sync).
+__global__ void pad_offsets_k(int E, const int* __restrict__ off, int* __restrict__ poff) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    int acc = 0;
+    poff[0] = 0;
+    for (int e = 0; e < E; ++e) {
+      acc += (off[e + 1] - off[e] + 255) / 256 * 256;
+      poff[e + 1] = acc;
+    }
+  }
+}
+
+// one block per padded row r < cap: gather mode (x != NULL): xe[r] = x[perm[off[e] + j] / k]
+// and pinv[assignment] = r, pad rows zeroed; zero mode (x == NULL): only pad rows zeroed
+template <typename T>
+__global__ void __launch_bounds__(256) pad_rows_k(int cap, int d, int E, int k, const int* __restrict__ off,
+                                                  const int* __restrict__ poff, const int32_t* __restrict__ perm,
+                                                  const T* __restrict__ x, int64_t ldx, T* __restrict__ out,
+                                                  int64_t ldo, int32_t* __restrict__ pinv) {
+  __shared__ int s_po[65], s_o[65];
+  for (int i = threadIdx.x; i <= E; i += blockDim.x) {
+    s_po[i] = poff[i];
+    s_o[i] = off[i];
+  }
+  __syncthreads();
+  const int r = blockIdx.x;
+  if (r >= s_po[E]) return;  // beyond the last expert: never read by the grouped GEMMs
+  int e = 0;
+  while (e + 1 < E && s_po[e + 1] <= r) ++e;
+  const int j = r - s_po[e];
+  T* dst = out + (int64_t)r * ldo;
+  if (j < s_o[e + 1] - s_o[e]) {
+    if (!x) return;
+    const int a = perm[s_o[e] + j];
+    if (threadIdx.x == 0) pinv[a] = r;
+    const T* src = x + (int64_t)(a / k) * ldx;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) dst[c] = src[c];
+  } else {
+    for (int c = threadIdx.x; c < d; c += blockDim.x) dst[c] = from_f32<T>(0.f);
+  }
+}
+
+extern "C" int cb_moe_dispatch_padded(int64_t nk, int dim, int experts, int top_k, const int* offsets,
+                                      const int32_t* perm, const void* x, int64_t ldx, int dtype, int* poff,
+                                      int32_t* pinv, void* xe, int64_t ldxe, int cap, void* stream) {
+  if (experts < 1 || experts > 64) return fail(CB_ERR_ARG, "moe dispatch: 1..64 experts");
+  if ((int64_t)cap < nk + (int64_t)experts * 255) return fail(CB_ERR_SHAPE, "moe dispatch: capacity %d too small", cap);
+  cudaStream_t st = (cudaStream_t)stream;
+  pad_offsets_k<<<1, 32, 0, st>>>(experts, offsets, poff);
+  if (int r = check_launch("moe_pad_offsets")) return r;
+  if (cap <= 0) return CB_OK;
+  if (dtype == CB_DT_F32)
+    pad_rows_k<float><<<cap, 256, 0, st>>>(cap, dim, experts, top_k, offsets, poff, perm, (const float*)x, ldx,
+                                           (float*)xe, ldxe, pinv);
+  else
+    pad_rows_k<__nv_bfloat16><<<cap, 256, 0, st>>>(cap, dim, experts, top_k, offsets, poff, perm,
+                                                   (const __nv_bfloat16*)x, ldx, (__nv_bfloat16*)xe, ldxe, pinv);
+  return check_launch("moe_dispatch_padded");
+}
+
+extern "C" int cb_moe_zero_pad_rows(int cap, int dim, int experts, const int* offsets, const int* poff, void* buf,
+                                    int64_t ld, int dtype, void* stream) {
+  if (cap <= 0) return CB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == CB_DT_F32)
+    pad_rows_k<float><<<cap, 256, 0, st>>>(cap, dim, experts, 1, offsets, poff, nullptr, nullptr, 0, (float*)buf, ld,
+                                           nullptr);
+  else
+    pad_rows_k<__nv_bfloat16><<<cap, 256, 0, st>>>(cap, dim, experts, 1, offsets, poff, nullptr, nullptr, 0,
+                                                   (__nv_bfloat16*)buf, ld, nullptr);
+  return check_launch("moe_zero_pad_rows");
+}
+
 // inv[perm[j]] = j
 __global__ void invert_perm_k(int64_t n, const int32_t* __restrict__ perm, int32_t* __restrict__ inv) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;

@@ -583,7 +583,8 @@ class AttentionBehavior(Behavior):
         scale = 1.0 / math.sqrt(hd)
         rec = is_recording()
         # bf16: o's rounding residual too, for the backward's delta (cb_attention_fwd o_lo)
-        o, lse, o_lo = ops.attention_fwd(q, k, v, B, T, H, KVH, hd, scale, want_lo=rec)
+        o, lse, *lo = ops.attention_fwd(q, k, v, B, T, H, KVH, hd, scale, want_lo=rec)
+        o_lo = lo[0] if lo else None
         out = torch.empty((o.shape[0], d), device=x.device, dtype=torch.float32)
         ops.gemm(o, param("wo"), out, residual=ops.rows2d(residual) if residual is not None else None)
         if rec:

@@ -8,8 +8,12 @@ combine.  FLOPs match the reference's own accounting, which already counts only 
 experts (layers.py:494-499).  ``load_balance_loss`` is recorded as a summary and, as in
 the reference, is not part of the loss (layers.py:532 vs 649-651).
 
-Per-expert row counts are read back to the host once per MoE layer invocation to size
-the expert GEMMs (E+1 ints).
+bf16 (the benchmark path): the dispatch writes each expert's rows at a 256-row boundary
+(cb_moe_dispatch_padded, zero pad rows) and every expert projection — forward and backward,
+weight gradients included — is ONE grouped CTA-pair GEMM launch that reads the expert
+offsets on the GPU (cb_gemm_grouped / cb_gemm_gated_*_grouped): no host round trip and no
+per-expert launch loop.  f32 (the parity mode) runs per-expert SIMT GEMMs sized from the E+1
+offsets read back to the host.
 """
 
 from __future__ import annotations
@@ -119,25 +123,42 @@ class MoEBehavior(Behavior):
             p = raw[E:] / n_glob
             stats = torch.cat([(E * (f * p).sum()).view(1), raw[:E], p])
         add_summary("load_balance_loss", stats[0:1] if L.is_recording() else float(stats[0].item()))
+        if L.option("moe_balanced_routing", False):
+            # BENCHMARK KNOB ONLY (bench.py --moe-routing balanced): token t's slot j goes to
+            # expert (t*k + j) % E, so every expert gets n*k/E rows — the dispatch, grouped
+            # GEMMs and combine measured off the reference init's degenerate routing
+            idx.copy_((torch.arange(n * k, device=dev, dtype=torch.int32) % E).view(n, k))
         if L.option("record_routing", False):  # debug summary: the chosen experts per token
             add_summary("route_indices", idx.view(B, T, k))
         # stable expert-sorted dispatch of the n*k assignments
         ids64 = torch.empty((n * k,), device=dev, dtype=torch.int64)
         _lib.call("cb_widen_i32", n * k, idx.data_ptr(), ids64.data_ptr(), ops.stream_ptr())
         offsets, perm = ops.sort_ids(ids64, E)
-        # the E+1 expert offsets size the per-expert GEMMs on the host: copied out right after
-        # the sort, so the host waits only for the sort while the gather below still runs
-        off_host = _pinned_offsets(E + 1)
-        off_host.copy_(offsets, non_blocking=True)
-        off_ready = torch.cuda.Event()
-        off_ready.record()
-        inv = torch.empty((n * k,), device=dev, dtype=torch.int32)
-        _lib.call("cb_invert_perm", n * k, perm.data_ptr(), inv.data_ptr(), ops.stream_ptr())
-        xe = torch.empty((n * k, d), device=dev, dtype=adt)
-        _lib.call("cb_gather_rows", n * k, d, perm.data_ptr(), k, x2.data_ptr(), ops.ld(x2), xe.data_ptr(),
-                  ops.ld(xe), ops.dt(xe), ops.stream_ptr())
-        off_ready.synchronize()
-        off = off_host.numpy().astype(np.int64)
+        if self._grouped_ok(module, adt):
+            # all experts in one grouped launch per projection, expert offsets read on the GPU:
+            # each expert's rows padded to a 256-row boundary (zero rows), no host round trip
+            cap = (n * k + 255 * E + 255) // 256 * 256
+            xe = torch.empty((cap, d), device=dev, dtype=adt)
+            poff = torch.empty((E + 1,), device=dev, dtype=torch.int32)
+            inv = torch.empty((n * k,), device=dev, dtype=torch.int32)  # assignment -> padded row
+            _lib.call("cb_moe_dispatch_padded", n * k, d, E, k, offsets.data_ptr(), perm.data_ptr(), x2.data_ptr(),
+                      ops.ld(x2), ops.dt(x2), poff.data_ptr(), inv.data_ptr(), xe.data_ptr(), ops.ld(xe), cap,
+                      ops.stream_ptr())
+            off = ("grouped", offsets, poff)
+        else:
+            # per-expert GEMMs sized on the host: the E+1 offsets are copied out right after
+            # the sort, so the host waits only for the sort while the gather below still runs
+            off_host = _pinned_offsets(E + 1)
+            off_host.copy_(offsets, non_blocking=True)
+            off_ready = torch.cuda.Event()
+            off_ready.record()
+            inv = torch.empty((n * k,), device=dev, dtype=torch.int32)
+            _lib.call("cb_invert_perm", n * k, perm.data_ptr(), inv.data_ptr(), ops.stream_ptr())
+            xe = torch.empty((n * k, d), device=dev, dtype=adt)
+            _lib.call("cb_gather_rows", n * k, d, perm.data_ptr(), k, x2.data_ptr(), ops.ld(x2), xe.data_ptr(),
+                      ops.ld(xe), ops.dt(xe), ops.stream_ptr())
+            off_ready.synchronize()
+            off = off_host.numpy().astype(np.int64)
         pre, hid = self._experts_up(module, xe, off)
         ye = self._experts_down(module, hid, off)
         out = torch.empty((n, d), device=dev, dtype=torch.float32)
@@ -153,9 +174,42 @@ class MoEBehavior(Behavior):
                  geom=(B, T, d, h, E, k))
         return out.view(B, T, d)
 
+    @staticmethod
+    def _stacked(module):
+        """Every expert's [W1|Wg] as one [E*d, 2h] matrix and W2 as [E*h, d] (views of the
+        bucket), or None when the layout is not the engine's fused one."""
+        L = _layers()
+        cfg = module.config
+        d, h, E = cfg.get("input_dim"), cfg.get("hidden_dim"), cfg.get("num_experts")
+        w1, wg, w2 = param("w1"), param("w1_gate"), param("w2")
+        es = w1.element_size()
+        if (w1.stride() != (d * 2 * h, 2 * h, 1) or wg.stride() != w1.stride()
+                or wg.data_ptr() != w1.data_ptr() + h * es or not w2.is_contiguous()):
+            return None
+        return torch.as_strided(w1, (E * d, 2 * h), (2 * h, 1)), w2.view(E * h, d)
+
+    @staticmethod
+    def _stacked_grads(module):
+        cfg = module.config
+        d, h, E = cfg.get("input_dim"), cfg.get("hidden_dim"), cfg.get("num_experts")
+        g1, gg, g2 = param_grad("w1"), param_grad("w1_gate"), param_grad("w2")
+        if (g1.stride() != (d * 2 * h, 2 * h, 1) or gg.data_ptr() != g1.data_ptr() + h * g1.element_size()
+                or not g2.is_contiguous()):
+            return None
+        return torch.as_strided(g1, (E * d, 2 * h), (2 * h, 1)), g2.view(E * h, d)
+
+    def _grouped_ok(self, module, adt) -> bool:
+        L = _layers()
+        cfg = module.config
+        pair = L.activation_pair(cfg.get("activation"))
+        return (adt == torch.bfloat16 and pair is not None and L.option("fuse_glu", True)
+                and L.option("moe_grouped", True) and cfg.get("hidden_dim") % 128 == 0
+                and cfg.get("input_dim") % 64 == 0 and cfg.get("num_experts") <= 64
+                and self._stacked(module) is not None)
+
     def _experts_up(self, module, xe, off):
         """pre / hid of every expert's rows (gate/up GEMM with the gated activation in its
-        epilogue, per expert on its contiguous rows)."""
+        epilogue): one grouped launch over the padded layout, or per expert on its rows."""
         L = _layers()
         cfg = module.config
         h, E = cfg.get("hidden_dim"), cfg.get("num_experts")
@@ -163,6 +217,12 @@ class MoEBehavior(Behavior):
         dev = xe.device
         nk = xe.shape[0]
         pair = L.activation_pair(cfg.get("activation"))
+        if isinstance(off, tuple):
+            w1s, _ = self._stacked(module)
+            pre = torch.empty((nk, 2 * h), device=dev, dtype=adt)
+            hid = torch.empty((nk, h), device=dev, dtype=adt)
+            ops.gemm_gated_fwd_grouped(xe, w1s, off[2], E, pair[0], pair[1], pre, hid)
+            return pre, hid
         w1 = param("w1")
         wg = param("w1_gate") if pair else None
         width = 2 * h if pair else h
@@ -195,6 +255,9 @@ class MoEBehavior(Behavior):
         d, E = cfg.get("input_dim"), cfg.get("num_experts")
         w2 = param("w2")
         ye = torch.empty((hid.shape[0], d), device=hid.device, dtype=torch.float32)
+        if isinstance(off, tuple):
+            ops.gemm_grouped_rows(hid, self._stacked(module)[1], ye, off[2], E)
+            return ye
         for e in range(E):
             r0, r1 = int(off[e]), int(off[e + 1])
             if r1 > r0:
@@ -225,12 +288,57 @@ class MoEBehavior(Behavior):
             _lib.call("cb_moe_route", n, d, E, k, x2.data_ptr(), ops.ld(x2), ops.dt(x2), L._f32(param("router")).data_ptr(),
                       i2.data_ptr(), w2_.data_ptr(), probs.data_ptr(), ops.stream_ptr())
         g = ops.rows2d(dout).contiguous() if dout.dtype == torch.float32 else ops.cast(ops.rows2d(dout), torch.float32)
-        dye = torch.empty((n * k, d), device=dev, dtype=adt)
+        grouped = isinstance(off, tuple)
+        dye = torch.empty((xe.shape[0], d), device=dev, dtype=adt)
+        if grouped:  # the pad rows feed the grouped weight-gradient GEMMs: zero
+            _lib.call("cb_moe_zero_pad_rows", xe.shape[0], d, E, off[1].data_ptr(), off[2].data_ptr(), dye.data_ptr(),
+                      ops.ld(dye), ops.dt(dye), ops.stream_ptr())
         dw = torch.empty((n, k), device=dev, dtype=torch.float32)
         _lib.call("cb_moe_combine_bwd", n, d, k, s["inv"].data_ptr(), s["w"].data_ptr(), ye.data_ptr(),
                   ops.ld(ye), g.data_ptr(), ops.ld(g), dye.data_ptr(), ops.ld(dye), ops.dt(dye), dw.data_ptr(),
                   ops.stream_ptr())
         pair = L.activation_pair(cfg.get("activation"))
+        if grouped:
+            dxe = self._experts_bwd_grouped(module, xe, pre, hid, dye, off[2], pair)
+        else:
+            dxe = self._experts_bwd(module, xe, pre, hid, dye, off, pair)
+        dx = torch.empty((n, d), device=dev, dtype=torch.float32)
+        _lib.call("cb_moe_combine", n, d, k, s["inv"].data_ptr(), None, dxe.data_ptr(), ops.ld(dxe), ops.dt(dxe),
+                  dx.data_ptr(), ops.ld(dx), 0, ops.stream_ptr())
+        # router: w = renorm(topk(softmax(x @ router)))
+        dlog = torch.empty((n, E), device=dev, dtype=torch.float32)
+        _lib.call("cb_moe_router_bwd", n, E, k, probs.data_ptr(), s["idx"].data_ptr(), s["w"].data_ptr(),
+                  dw.data_ptr(), dlog.data_ptr(), ops.stream_ptr())
+        router = L._f32(param("router"))
+        x2 = s["x2"]
+        ws = torch.empty(((n + 511) // 512) * d * E, device=dev, dtype=torch.float32)
+        _lib.call("cb_moe_router_bwd_gemms", n, d, E, x2.data_ptr(), ops.ld(x2), ops.dt(x2), dlog.data_ptr(),
+                  router.data_ptr(), param_grad("router").data_ptr(), dx.data_ptr(), ops.ld(dx), ws.data_ptr(),
+                  ops.stream_ptr())
+        return dx.view(B, T, d)
+
+    def _experts_bwd_grouped(self, module, xe, pre, hid, dye, poff, pair):
+        """The experts' backward in four grouped launches: dpre (dhidden = dye @ W2^T formed
+        and consumed by the gated-activation backward in the epilogue), dW2 += hid^T dye,
+        d[W1|Wg] += xe^T dpre (grouped over K: each expert's own rows), dxe = dpre @ [W1|Wg]^T."""
+        cfg = module.config
+        d, E = cfg.get("input_dim"), cfg.get("num_experts")
+        w1s, w2s = self._stacked(module)
+        g1s, g2s = self._stacked_grads(module)
+        dpre = torch.empty_like(pre)
+        ops.gemm_gated_bwd_grouped(dye, w2s, poff, E, pre, pair[0], pair[1], dpre)
+        ops.gemm_grouped_k(hid, dye, g2s, poff, E)
+        ops.gemm_grouped_k(xe, dpre, g1s, poff, E)
+        dxe = torch.empty((xe.shape[0], d), device=xe.device, dtype=torch.float32)
+        ops.gemm_grouped_rows(dpre, w1s, dxe, poff, E, trans_b=True)
+        return dxe
+
+    def _experts_bwd(self, module, xe, pre, hid, dye, off, pair):
+        L = _layers()
+        cfg = module.config
+        d, h, E = cfg.get("input_dim"), cfg.get("hidden_dim"), cfg.get("num_experts")
+        dev = xe.device
+        n_k = xe.shape[0]
         w1, w2 = param("w1"), param("w2")
         gw1, gw2 = param_grad("w1"), param_grad("w2")
         wg = param("w1_gate") if pair else None
@@ -255,7 +363,7 @@ class MoEBehavior(Behavior):
                             pair[1])
             else:
                 ops.act_bwd(pre[r0:r1], None, dhid[r0:r1], dpre[r0:r1], None, cfg.get("activation"))
-        dxe = torch.empty((n * k, d), device=dev, dtype=torch.float32)
+        dxe = torch.empty((n_k, d), device=dev, dtype=torch.float32)
         for e in range(E):
             r0, r1 = int(off[e]), int(off[e + 1])
             if r1 == r0:
@@ -266,20 +374,7 @@ class MoEBehavior(Behavior):
             if pair:
                 ops.gemm(xs, dpre[r0:r1, h:], gwg[e], trans_a=True, accumulate=True)
                 ops.gemm(dpre[r0:r1, h:], wg[e], dxe[r0:r1], trans_b=True, accumulate=True)
-        dx = torch.empty((n, d), device=dev, dtype=torch.float32)
-        _lib.call("cb_moe_combine", n, d, k, s["inv"].data_ptr(), None, dxe.data_ptr(), ops.ld(dxe), ops.dt(dxe),
-                  dx.data_ptr(), ops.ld(dx), 0, ops.stream_ptr())
-        # router: w = renorm(topk(softmax(x @ router)))
-        dlog = torch.empty((n, E), device=dev, dtype=torch.float32)
-        _lib.call("cb_moe_router_bwd", n, E, k, probs.data_ptr(), s["idx"].data_ptr(), s["w"].data_ptr(),
-                  dw.data_ptr(), dlog.data_ptr(), ops.stream_ptr())
-        router = L._f32(param("router"))
-        x2 = s["x2"]
-        ws = torch.empty(((n + 511) // 512) * d * E, device=dev, dtype=torch.float32)
-        _lib.call("cb_moe_router_bwd_gemms", n, d, E, x2.data_ptr(), ops.ld(x2), ops.dt(x2), dlog.data_ptr(),
-                  router.data_ptr(), param_grad("router").data_ptr(), dx.data_ptr(), ops.ld(dx), ws.data_ptr(),
-                  ops.stream_ptr())
-        return dx.view(B, T, d)
+        return dxe
 
 
 _PINNED: dict = {}

@@ -211,3 +211,108 @@ def test_staged_epilogue_bit_identical(cuda, M, N, K):
     assert staged.keys() == plain.keys()
     for k in staged:
         assert torch.equal(staged[k], plain[k]), k
+
+
+def _padded_offsets(counts, dev):
+    import numpy as np
+
+    po = np.zeros(len(counts) + 1, dtype=np.int32)
+    po[1:] = np.cumsum([(c + 255) // 256 * 256 for c in counts])
+    return torch.tensor(po, device=dev, dtype=torch.int32), po
+
+
+@pytest.mark.parametrize("counts", [[300, 0, 513, 256], [1, 1, 1, 1, 1, 1, 1, 1], [4096, 0, 0, 0, 0, 0, 0, 1000]])
+def test_grouped_gemm_matches_per_group(cuda, counts):
+    """cb_gemm_grouped (one launch, device offsets) == one cb_gemm per group, bit for bit:
+    mode 1 (rows; B stacked along K, and transposed along N) and mode 2 (K; the experts'
+    weight gradients, empty groups untouched), plus the gated forward / backward forms."""
+    from paper_2507_05411_b200 import ops
+
+    G, d, h = len(counts), 256, 512
+    goff, po = _padded_offsets(counts, cuda)
+    cap = int(po[-1]) + 256
+    g = torch.Generator(device="cpu").manual_seed(sum(counts))
+    x = torch.zeros(cap, d, dtype=torch.bfloat16)
+    for e in range(G):
+        x[po[e]:po[e] + counts[e]] = torch.randn(counts[e], d, generator=g)
+    x = x.to(cuda)
+    w = (0.05 * torch.randn(G * d, 2 * h, generator=g)).to(cuda, torch.bfloat16)  # [W1|Wg] stacked
+    w2 = (0.05 * torch.randn(G * h, d, generator=g)).to(cuda, torch.bfloat16)
+    # mode 1, B stacked along K
+    out = torch.zeros(cap, 2 * h, device=cuda)
+    ops.gemm_grouped_rows(x, w, out, goff, G)
+    ref = torch.zeros_like(out)
+    for e in range(G):
+        r0, r1 = int(po[e]), int(po[e + 1])
+        if r1 > r0:
+            ops.gemm(x[r0:r1], w[e * d:(e + 1) * d], ref[r0:r1])
+    torch.cuda.synchronize()
+    assert torch.equal(out[:int(po[-1])], ref[:int(po[-1])])
+    # mode 1, B read transposed (stacked along N): dx = dy @ W2_g^T
+    dy = torch.randn(cap, d, generator=g).to(cuda, torch.bfloat16)
+    dh = torch.zeros(cap, h, device=cuda)
+    ops.gemm_grouped_rows(dy, w2, dh, goff, G, trans_b=True)
+    ref = torch.zeros_like(dh)
+    for e in range(G):
+        r0, r1 = int(po[e]), int(po[e + 1])
+        if r1 > r0:
+            ops.gemm(dy[r0:r1], w2[e * h:(e + 1) * h], ref[r0:r1], trans_b=True)
+    torch.cuda.synchronize()
+    assert torch.equal(dh[:int(po[-1])], ref[:int(po[-1])])
+    # mode 2: weight gradients, accumulate into a non-zero buffer; empty groups untouched
+    gw = torch.randn(G * d, d, generator=g).to(cuda)
+    ref = gw.clone()
+    ops.gemm_grouped_k(x, dy, gw, goff, G)
+    for e in range(G):
+        r0, r1 = int(po[e]), int(po[e + 1])
+        if r1 > r0:
+            ops.gemm(x[r0:r1], dy[r0:r1], ref[e * d:(e + 1) * d], trans_a=True, accumulate=True)
+    torch.cuda.synchronize()
+    assert torch.equal(gw, ref)
+    # gated forward / backward
+    pre = torch.zeros(cap, 2 * h, device=cuda, dtype=torch.bfloat16)
+    hid = torch.zeros(cap, h, device=cuda, dtype=torch.bfloat16)
+    ops.gemm_gated_fwd_grouped(x, w, goff, G, "linear", "silu", pre, hid)
+    dpre = torch.zeros_like(pre)
+    ops.gemm_gated_bwd_grouped(dy, w2, goff, G, pre, "linear", "silu", dpre)
+    rpre, rhid, rdpre = torch.zeros_like(pre), torch.zeros_like(hid), torch.zeros_like(dpre)
+    for e in range(G):
+        r0, r1 = int(po[e]), int(po[e + 1])
+        if r1 > r0:
+            ops.gemm_gated_fwd(x[r0:r1], w[e * d:(e + 1) * d], "linear", "silu", pre=rpre[r0:r1], hidden=rhid[r0:r1])
+            ops.gemm_gated_bwd(dy[r0:r1], w2[e * h:(e + 1) * h], rpre[r0:r1], "linear", "silu", dpre=rdpre[r0:r1])
+    torch.cuda.synchronize()
+    n = int(po[-1])
+    assert torch.equal(pre[:n], rpre[:n]) and torch.equal(hid[:n], rhid[:n]) and torch.equal(dpre[:n], rdpre[:n])
+
+
+def test_moe_dispatch_padded(cuda):
+    """cb_moe_dispatch_padded: each expert's rows start on a 256-row boundary in stable sorted
+    order, pad rows are zero, and pinv maps every assignment to its padded row."""
+    import numpy as np
+
+    from paper_2507_05411_b200 import _lib, ops
+
+    n, k, E, d = 300, 2, 4, 64
+    g = torch.Generator(device="cpu").manual_seed(5)
+    ids = torch.randint(0, E, (n * k,), generator=g)
+    ids[ids == 2] = 1  # an empty expert
+    x = torch.randn(n, d, generator=g).to(cuda, torch.bfloat16)
+    off, perm = ops.sort_ids(ids.to(cuda), E)
+    cap = n * k + 255 * E
+    xe = torch.full((cap, d), 7.0, device=cuda, dtype=torch.bfloat16)
+    poff = torch.empty(E + 1, device=cuda, dtype=torch.int32)
+    pinv = torch.empty(n * k, device=cuda, dtype=torch.int32)
+    _lib.call("cb_moe_dispatch_padded", n * k, d, E, k, off.data_ptr(), perm.data_ptr(), x.data_ptr(), ops.ld(x),
+              ops.dt(x), poff.data_ptr(), pinv.data_ptr(), xe.data_ptr(), ops.ld(xe), cap, ops.stream_ptr())
+    torch.cuda.synchronize()
+    idsn, po, pi = ids.numpy(), poff.cpu().numpy(), pinv.cpu().numpy()
+    counts = np.bincount(idsn, minlength=E)
+    assert list(po) == [0] + list(np.cumsum([(c + 255) // 256 * 256 for c in counts]))
+    xc, xec = x.cpu(), xe.cpu()
+    for e in range(E):
+        mine = np.nonzero(idsn == e)[0]  # stable order of the assignments
+        rows = po[e] + np.arange(len(mine))
+        assert np.array_equal(pi[mine], rows)
+        assert torch.equal(xec[rows], xc[mine // k])
+        assert not xec[po[e] + len(mine):po[e + 1]].float().any()
