@@ -411,7 +411,7 @@ class TrainEngine:
         seen, total = set(), 0
         tensors = [t for rec in self.bufs for t in rec.values() if isinstance(t, torch.Tensor)]
         tensors += [t for t in (getattr(self, "_rs_stage", None),) if t is not None]
-        tensors += [t for t in getattr(self, "_grad_ring", []) if isinstance(t, torch.Tensor)]
+        tensors += list(getattr(self, "_gring", [])) + list(getattr(self, "_wring", []))
         for t in tensors:
             key = t.untyped_storage().data_ptr()
             if key not in seen:
