@@ -221,10 +221,17 @@ def cupti_attribution(fn) -> tuple[dict, float]:
     out: dict = {}
     if not ks:
         return out, 0.0
+    names: dict = {}
+    for e in prof.events():
+        if e.device_type == torch.autograd.DeviceType.CUDA and "cb::" not in e.name:
+            names[e.name[:60]] = names.get(e.name[:60], 0.0) + e.time_range.elapsed_us() / 1e3
     for s0, e0, k in ks:
         d = out.setdefault(k, {"launches": 0, "busy_ms": 0.0, "attributed_ms": 0.0})
         d["launches"] += 1
         d["busy_ms"] += (e0 - s0) / 1e3
+    for k in out:
+        if k.startswith("foreign"):
+            out[k]["top"] = sorted(names.items(), key=lambda kv: -kv[1])[:3]
     # sweep line over the start/end points of every kernel (all streams)
     pts = sorted({t for s0, e0, _ in ks for t in (s0, e0)})
     idx = {t: i for i, t in enumerate(pts)}
@@ -391,6 +398,8 @@ def main():
     for k, v in sorted(cupti.items(), key=lambda kv: -kv[1]["attributed_ms"]):
         row = {"launches_per_step": v["launches"] / nprof, "busy_ms_per_step": v["busy_ms"] / nprof,
                "attributed_ms_per_step": v["attributed_ms"] / nprof}
+        if "top" in v:
+            row["top_ms"] = [(n, round(t / nprof, 2)) for n, t in v["top"]]
         if flops_by_kind.get(k):
             row["tflops"] = flops_by_kind[k] / (v["busy_ms"] / 1e3) / 1e12
         kernels[k] = row

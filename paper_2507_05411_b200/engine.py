@@ -738,7 +738,7 @@ class FSDPProvider(ParamProvider):
     def _slot(self, i: int) -> int | None:
         return self.e._pos[i] % 2 if (self.e._reshard and self.e.bufs[i].get("ringed")) else None
 
-    def _ag(self, i: int) -> None:
+    def _ag(self, i: int, backward: bool = False) -> None:
         rec, b = self.e.bufs[i], self.e.buckets[i]
         if b.replicated:
             return
@@ -760,10 +760,16 @@ class FSDPProvider(ParamProvider):
                 if slot is not None:  # the own slice too (in keep mode it is already in place)
                     work[r * s:(r + 1) * s].copy_(own)
                 # pull every peer's shard over NVLink with the copy engines (no SMs taken from
-                # the compute kernels).  The first barrier: each peer's AdamW of this bucket,
-                # earlier on its comm stream, has written its shard; the second: every peer has
-                # read this rank's shard before the next AdamW overwrites it.
-                h.barrier(channel=0, timeout_ms=_BARRIER_TIMEOUT_MS)
+                # the compute kernels).  Ordering with the shards' writers, the AdamW updates:
+                # * forward gather: one barrier — each peer's AdamW of this bucket (previous
+                #   step, earlier on its comm stream) has written its shard;
+                # * backward (re-)gather: none — no AdamW of this bucket can run anywhere before
+                #   every rank has passed this bucket's reduce-scatter barrier, i.e. finished
+                #   its backward of it, which comes after this gather;
+                # * no barrier after the reads: a rank's next AdamW of this bucket waits for the
+                #   same reduce-scatter barrier, which every reader passes only after its reads.
+                if not backward:
+                    h.barrier(channel=0, timeout_ms=_BARRIER_TIMEOUT_MS)
                 for k in range(1, N):
                     p = (r + k) % N
                     if slot is not None:
@@ -771,7 +777,6 @@ class FSDPProvider(ParamProvider):
                     else:
                         src = h.get_buffer(p, (rec["total"],), work.dtype)[p * s:(p + 1) * s]
                     work[p * s:(p + 1) * s].copy_(src)
-                h.barrier(channel=0, timeout_ms=_BARRIER_TIMEOUT_MS)
             done = torch.cuda.Event()
             done.record(self.comm)
         self.gathered[i] = done
@@ -850,9 +855,12 @@ class FSDPProvider(ParamProvider):
         if pos is None:
             return
         if self.e._reshard:
-            self._use(i)
+            self._ag(i, backward=True)
+            ev = self.gathered.get(i)
+            if ev is not None:
+                self.compute.wait_event(ev)
             if pos > 0:
-                self._ag(self.layer_order[pos - 1])
+                self._ag(self.layer_order[pos - 1], backward=True)
         if self.e._grad_ring:
             ev = self.gslot_free.pop(pos % 2, None)
             if ev is not None:

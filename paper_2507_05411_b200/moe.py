@@ -144,7 +144,7 @@ class MoEBehavior(Behavior):
             _lib.call("cb_moe_dispatch_padded", n * k, d, E, k, offsets.data_ptr(), perm.data_ptr(), x2.data_ptr(),
                       ops.ld(x2), ops.dt(x2), poff.data_ptr(), inv.data_ptr(), xe.data_ptr(), ops.ld(xe), cap,
                       ops.stream_ptr())
-            off = ("grouped", offsets, poff)
+            off = ("grouped", offsets, poff, n * k)
         else:
             # per-expert GEMMs sized on the host: the E+1 offsets are copied out right after
             # the sort, so the host waits only for the sort while the gather below still runs
@@ -221,7 +221,7 @@ class MoEBehavior(Behavior):
             w1s, _ = self._stacked(module)
             pre = torch.empty((nk, 2 * h), device=dev, dtype=adt)
             hid = torch.empty((nk, h), device=dev, dtype=adt)
-            ops.gemm_gated_fwd_grouped(xe, w1s, off[2], E, pair[0], pair[1], pre, hid)
+            ops.gemm_gated_fwd_grouped(xe, w1s, off[2], E, pair[0], pair[1], pre, hid, rows=off[3])
             return pre, hid
         w1 = param("w1")
         wg = param("w1_gate") if pair else None
@@ -256,7 +256,7 @@ class MoEBehavior(Behavior):
         w2 = param("w2")
         ye = torch.empty((hid.shape[0], d), device=hid.device, dtype=torch.float32)
         if isinstance(off, tuple):
-            ops.gemm_grouped_rows(hid, self._stacked(module)[1], ye, off[2], E)
+            ops.gemm_grouped_rows(hid, self._stacked(module)[1], ye, off[2], E, rows=off[3])
             return ye
         for e in range(E):
             r0, r1 = int(off[e]), int(off[e + 1])
@@ -299,7 +299,7 @@ class MoEBehavior(Behavior):
                   ops.stream_ptr())
         pair = L.activation_pair(cfg.get("activation"))
         if grouped:
-            dxe = self._experts_bwd_grouped(module, xe, pre, hid, dye, off[2], pair)
+            dxe = self._experts_bwd_grouped(module, xe, pre, hid, dye, off[2], pair, off[3])
         else:
             dxe = self._experts_bwd(module, xe, pre, hid, dye, off, pair)
         dx = torch.empty((n, d), device=dev, dtype=torch.float32)
@@ -317,7 +317,7 @@ class MoEBehavior(Behavior):
                   ops.stream_ptr())
         return dx.view(B, T, d)
 
-    def _experts_bwd_grouped(self, module, xe, pre, hid, dye, poff, pair):
+    def _experts_bwd_grouped(self, module, xe, pre, hid, dye, poff, pair, rows):
         """The experts' backward in four grouped launches: dpre (dhidden = dye @ W2^T formed
         and consumed by the gated-activation backward in the epilogue), dW2 += hid^T dye,
         d[W1|Wg] += xe^T dpre (grouped over K: each expert's own rows), dxe = dpre @ [W1|Wg]^T."""
@@ -326,11 +326,11 @@ class MoEBehavior(Behavior):
         w1s, w2s = self._stacked(module)
         g1s, g2s = self._stacked_grads(module)
         dpre = torch.empty_like(pre)
-        ops.gemm_gated_bwd_grouped(dye, w2s, poff, E, pre, pair[0], pair[1], dpre)
-        ops.gemm_grouped_k(hid, dye, g2s, poff, E)
-        ops.gemm_grouped_k(xe, dpre, g1s, poff, E)
+        ops.gemm_gated_bwd_grouped(dye, w2s, poff, E, pre, pair[0], pair[1], dpre, rows=rows)
+        ops.gemm_grouped_k(hid, dye, g2s, poff, E, rows=rows)
+        ops.gemm_grouped_k(xe, dpre, g1s, poff, E, rows=rows)
         dxe = torch.empty((xe.shape[0], d), device=xe.device, dtype=torch.float32)
-        ops.gemm_grouped_rows(dpre, w1s, dxe, poff, E, trans_b=True)
+        ops.gemm_grouped_rows(dpre, w1s, dxe, poff, E, trans_b=True, rows=rows)
         return dxe
 
     def _experts_bwd(self, module, xe, pre, hid, dye, off, pair):

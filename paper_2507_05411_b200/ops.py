@@ -174,48 +174,50 @@ _GEMM_WS: dict = {}
 
 # --------------------------------------------------------------------- grouped GEMMs
 def gemm_grouped_rows(a: torch.Tensor, b_stacked: torch.Tensor, out: torch.Tensor, grp_off: torch.Tensor,
-                      groups: int, trans_b: bool = False, accumulate: bool = False, alpha: float = 1.0):
+                      groups: int, trans_b: bool = False, accumulate: bool = False, alpha: float = 1.0,
+                      rows: int = 0):
     """out[rows of g] = a[rows of g] @ op(B_g) for all groups in one launch (cb_gemm_grouped
-    mode 1); B_g = block g of b_stacked ([G*K, N], or [G*N, K] read transposed)."""
+    mode 1); B_g = block g of b_stacked ([G*K, N], or [G*N, K] read transposed).  rows: the
+    real (unpadded) row count, for the algorithmic FLOP tally only."""
     M, K = a.shape
     N = b_stacked.shape[0] // groups if trans_b else b_stacked.shape[1]
     if tuple(out.shape) != (M, N):
         raise ShapeError(f"gemm_grouped: out shape {tuple(out.shape)} != {(M, N)}")
-    _profiled("gemm_bf16", 0, _lib.call, "cb_gemm_grouped", 1, groups, grp_off.data_ptr(), M, N, K, a.data_ptr(),
+    _profiled("gemm_bf16", 2 * rows * N * K, _lib.call, "cb_gemm_grouped", 1, groups, grp_off.data_ptr(), M, N, K, a.data_ptr(),
               ld(a, "A"), 0, b_stacked.data_ptr(), ld(b_stacked, "B"), int(trans_b), out.data_ptr(), ld(out, "D"),
               dt(out), float(alpha), int(accumulate), stream_ptr())
     return out
 
 
 def gemm_grouped_k(a: torch.Tensor, b: torch.Tensor, out_stacked: torch.Tensor, grp_off: torch.Tensor, groups: int,
-                   accumulate: bool = True):
+                   accumulate: bool = True, rows: int = 0):
     """out_g (+)= a[rows of g]^T @ b[rows of g] for all groups in one launch (cb_gemm_grouped
     mode 2, the experts' weight gradients); out_g = rows [g*M, (g+1)*M) of out_stacked."""
     Kcap, M = a.shape
     N = b.shape[1]
     if tuple(out_stacked.shape) != (groups * M, N):
         raise ShapeError("gemm_grouped_k: out must be [groups * M, N]")
-    _profiled("gemm_bf16", 0, _lib.call, "cb_gemm_grouped", 2, groups, grp_off.data_ptr(), M, N, Kcap, a.data_ptr(),
+    _profiled("gemm_bf16", 2 * rows * M * N, _lib.call, "cb_gemm_grouped", 2, groups, grp_off.data_ptr(), M, N, Kcap, a.data_ptr(),
               ld(a, "A"), 1, b.data_ptr(), ld(b, "B"), 0, out_stacked.data_ptr(), ld(out_stacked, "D"),
               dt(out_stacked), 1.0, int(accumulate), stream_ptr())
     return out_stacked
 
 
 def gemm_gated_fwd_grouped(x: torch.Tensor, wcat_stacked: torch.Tensor, grp_off: torch.Tensor, groups: int,
-                           act0: str, act1: str, pre: torch.Tensor, hidden: torch.Tensor):
+                           act0: str, act1: str, pre: torch.Tensor, hidden: torch.Tensor, rows: int = 0):
     M, K = x.shape
     H = wcat_stacked.shape[1] // 2
-    _profiled("gemm_bf16", 0, _lib.call, "cb_gemm_gated_fwd_grouped", groups, grp_off.data_ptr(), M, H, K,
+    _profiled("gemm_bf16", 2 * rows * 2 * H * K, _lib.call, "cb_gemm_gated_fwd_grouped", groups, grp_off.data_ptr(), M, H, K,
               x.data_ptr(), ld(x, "A"), wcat_stacked.data_ptr(), ld(wcat_stacked, "B"), pre.data_ptr(), ld(pre),
               hidden.data_ptr(), ld(hidden), ACT_IDS[act0], ACT_IDS[act1], stream_ptr())
     return pre, hidden
 
 
 def gemm_gated_bwd_grouped(dy: torch.Tensor, w2_stacked: torch.Tensor, grp_off: torch.Tensor, groups: int,
-                           pre: torch.Tensor, act0: str, act1: str, dpre: torch.Tensor):
+                           pre: torch.Tensor, act0: str, act1: str, dpre: torch.Tensor, rows: int = 0):
     M, K = dy.shape
     H = w2_stacked.shape[0] // groups
-    _profiled("gemm_bf16", 0, _lib.call, "cb_gemm_gated_bwd_grouped", groups, grp_off.data_ptr(), M, H, K,
+    _profiled("gemm_bf16", 2 * rows * H * K, _lib.call, "cb_gemm_gated_bwd_grouped", groups, grp_off.data_ptr(), M, H, K,
               dy.data_ptr(), ld(dy, "A"), w2_stacked.data_ptr(), ld(w2_stacked, "B"), pre.data_ptr(), ld(pre),
               dpre.data_ptr(), ld(dpre), ACT_IDS[act0], ACT_IDS[act1], stream_ptr())
     return dpre

@@ -15,7 +15,8 @@ and gradient rings, copy-engine collectives between symmetric-memory barriers â€
 --steps steps, and compares every step's loss, the last step's gradients, and the final
 parameters and AdamW moments with the oracle's chained train_step.  f32 tensors are held to
 1e-5, or to 3x the error of the same steps computed by a plain fp32 restatement where fp32
-itself cannot meet 1e-5 (tests/test_step_gpu.py:fp32_oracle_errors); bf16 to 2e-2.
+itself cannot meet 1e-5 (tests/test_step_gpu.py:fp32_oracle_errors); bf16 to 2e-2, or to 1.5x
+the error of the oracle with bf16-rounded GEMM operands where that is larger.
 --mode decomposed drives compute_grads() + apply_update() (the round-1 check).
 --collectives both runs the step twice, with the copy-engine collectives (CB_FSDP_CE_*=1)
 and with NCCL (=0), both against the oracle and against each other.
@@ -50,7 +51,7 @@ def build(config):
     return build_experiment(config)
 
 
-def oracle_run(cfg, B, T, steps, precision, dtype):
+def oracle_run(cfg, B, T, steps, precision, dtype, bf16_operands=False):
     """The oracle's chained train_step on the global batches (dtype=float32: the plain fp32
     restatement used as the fp32 error yardstick)."""
     from oracle import decoder_oracle as O
@@ -62,9 +63,12 @@ def oracle_run(cfg, B, T, steps, precision, dtype):
     V = m.config.get("model.vocab_size")
     mm = vv = None
     losses, summs, grads = [], [], None
+    import contextlib
+
     for step in range(steps):
         toks = synthetic_batch(0, step, B, T, V)["tokens"]
-        lo, go, st, mm, vv, osum = O.train_step(st, toks, spec, O.AdamW(lr=1e-3), mm, vv, step + 1, dtype=dtype)
+        with (O.bf16_operands() if bf16_operands else contextlib.nullcontext()):
+            lo, go, st, mm, vv, osum = O.train_step(st, toks, spec, O.AdamW(lr=1e-3), mm, vv, step + 1, dtype=dtype)
         losses.append(lo)
         summs.append(osum)
         grads = go
@@ -137,7 +141,12 @@ def main():
         pb = {k: max(tol, 3 * _rel(p32[k], po[k])) for k in po}
         mb = {k: max(tol, 3 * _rel(m32[k], mo[k])) for k in mo}
     else:
-        gb = pb = mb = {k: tol for k in go}
+        # bf16: 1.5x the error of the oracle with only its GEMM operands rounded to bf16 (the
+        # least rounding any bf16 path does) where that exceeds tol / 1.5 (tests/test_step_gpu.py)
+        _, _, gq, pq, mq = oracle_run(cfg, B, T, args.steps, args.precision, torch.float64, bf16_operands=True)
+        gb = {k: max(tol, 1.5 * _rel(gq[k], go[k])) for k in go}
+        pb = {k: max(tol, 1.5 * _rel(pq[k], po[k])) for k in po}
+        mb = {k: max(tol, 1.5 * _rel(mq[k], mo[k])) for k in mo}
     out = {"world": world, "precision": args.precision, "config": args.config, "mode": args.mode,
            "steps": args.steps, "runs": {}}
     ok = True
