@@ -186,7 +186,8 @@ CB_API int cb_attention_bwd_rope(int batch, int seq_len, int heads, int kv_heads
                                  int64_t lddv, float scale, const float* cos_t, const float* sin_t, void* stream);
 /* 0 = automatic (tensor-core flash kernels when eligible), 1 = force SIMT (tests). */
 CB_API int cb_attention_set_path(int path);
-/* 1 (default) = use the tcgen05/TMEM forward for head_dim 128; 0 = warp-MMA flash kernel (tests). */
+/* 1 (default) = the tcgen05/TMEM kernels for bf16 head_dim 128 (the Python layer zero-pads
+ * head_dim 16/32/64 to 128 for them); 0 = the SIMT engine (tests). */
 CB_API int cb_attention_set_tc(int enable);
 
 /* ---------------------------------------------------------------------------------

@@ -1,4 +1,5 @@
-// Shared declarations of the attention engines (attn_simt.cu, attn_fa.cu, attn_api.cu).
+// Shared declarations of the attention engines (attn_tc.cu, attn_tc_bwd.cu, attn_simt.cu,
+// attn_api.cu).
 #pragma once
 #include "common.cuh"
 
@@ -24,9 +25,4 @@ int attn_fwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, 
 int attn_bwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, const void* dout, int64_t lddo,
                 const float* lse, const float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
                 int64_t lddv, cudaStream_t st, const float* rope_cos = nullptr, const float* rope_sin = nullptr);
-bool attn_fa_supported(const AttnGeom& g, int dtype, const void* q, const void* k, const void* v);
-int attn_fwd_fa(const AttnGeom& g, const void* q, const void* k, const void* v, void* o, float* lse, cudaStream_t st);
-int attn_bwd_fa(const AttnGeom& g, const void* q, const void* k, const void* v, const void* dout, int64_t lddo,
-                const float* lse, const float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
-                int64_t lddv, cudaStream_t st);
 }  // namespace cb

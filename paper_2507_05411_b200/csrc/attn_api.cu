@@ -37,7 +37,6 @@ extern "C" int cb_attention_fwd(int batch, int seq_len, int heads, int kv_heads,
                                       (size_t)batch * seq_len, st);
     if (e != cudaSuccess) return fail(CB_ERR_CUDA, "attention: o_lo memset: %s", cudaGetErrorString(e));
   }
-  if (g_attn_path == 0 && attn_fa_supported(g, dtype, q, k, v)) return attn_fwd_fa(g, q, k, v, o, lse, st);
   return attn_fwd_simt(g, dtype, q, k, v, o, lse, st);
 }
 
@@ -52,8 +51,6 @@ extern "C" int cb_attention_bwd(int batch, int seq_len, int heads, int kv_heads,
   if (int s = attn_delta(g, dtype, o, o_lo, dout, lddo, delta, st)) return s;
   if (tc_bwd_ok(g, dtype, q, k, v, lse, delta, lddo, lddq, lddk, lddv))
     return attn_bwd_tc(g, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st);
-  if (g_attn_path == 0 && attn_fa_supported(g, dtype, q, k, v))
-    return attn_bwd_fa(g, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st);
   return attn_bwd_simt(g, dtype, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st);
 }
 

@@ -10,7 +10,7 @@
 // reference's multi-head case).
 //
 // This engine serves the f32 parity mode and head dims the tensor-core kernel does not
-// instantiate; the bf16 hot path is attn_fa.cu.
+// instantiate; the bf16 hot path is the tcgen05 engine (attn_tc*.cu).
 #include "attn.cuh"
 #include "composer_b200.h"
 

@@ -237,8 +237,14 @@ def set_gemm_path(path: int) -> None:
     _lib.call("cb_gemm_set_path", int(path))
 
 
+_ATTN_PATH = 0
+
+
 def set_attention_path(path: int) -> None:
+    """0: automatic (tcgen05 kernels, head_dim < 128 zero-padded to them), 1: SIMT engine."""
+    global _ATTN_PATH
     _lib.call("cb_attention_set_path", int(path))
+    _ATTN_PATH = int(path)
 
 
 # -------------------------------------------------------------------------- RMSNorm
@@ -371,19 +377,76 @@ def zero_(t: torch.Tensor):
 
 
 # ------------------------------------------------------------------------ attention
+# head dims the tcgen05 kernels (head_dim 128) serve through zero padding: every head's hd
+# columns are copied into a 128-column slot whose other columns are zero — S = Q K^T and the
+# softmax are unchanged (the scale is passed explicitly), O / dQ / dK / dV come back in the
+# first hd columns; half the MMA work is wasted, against a SIMT fallback
+_PAD_HD = (16, 32, 64)
+_TC_HD = 128
+_pad_heads_enabled = True
+
+
+def _pad_ok(q: torch.Tensor, hd: int) -> bool:
+    return q.dtype == torch.bfloat16 and hd in _PAD_HD and _pad_heads_enabled and _ATTN_PATH == 0
+
+
+def _pad(x: torch.Tensor, nh: int, hd: int) -> torch.Tensor:
+    out = torch.empty((x.shape[0], nh * _TC_HD), device=x.device, dtype=x.dtype)
+    zero_(out)
+    for h in range(nh):
+        copy2d(x[:, h * hd:(h + 1) * hd], out[:, h * _TC_HD:h * _TC_HD + hd])
+    return out
+
+
+def _unpad(xp: torch.Tensor, out: torch.Tensor, nh: int, hd: int) -> torch.Tensor:
+    for h in range(nh):
+        copy2d(xp[:, h * _TC_HD:h * _TC_HD + hd], out[:, h * hd:(h + 1) * hd])
+    return out
+
+
 def attention_fwd(q, k, v, B, T, H, KVH, hd, scale, want_lo: bool = False):
     """Returns (o, lse) or, with want_lo (bf16), (o, lse, o_lo): o_lo = o - bf16(o) for the
     backward's delta (cb_attention_fwd)."""
     o = torch.empty((B * T, H * hd), device=q.device, dtype=q.dtype)
     lse = torch.empty((B, H, T), device=q.device, dtype=torch.float32)
     o_lo = torch.empty_like(o) if (want_lo and q.dtype == torch.bfloat16) else None
-    _profiled("attn_fwd", 4 * B * T * T * H * hd, _lib.call, "cb_attention_fwd", B, T, H, KVH, hd, dt(q),
-              q.data_ptr(), ld(q), k.data_ptr(), ld(k), v.data_ptr(), ld(v), o.data_ptr(), ld(o), _ptr(o_lo),
-              lse.data_ptr(), float(scale), stream_ptr())
+    if _pad_ok(q, hd):
+        qp, kp, vp = _pad(q, H, hd), _pad(k, KVH, hd), _pad(v, KVH, hd)
+        op = torch.empty((B * T, H * _TC_HD), device=q.device, dtype=q.dtype)
+        olp = torch.empty_like(op) if o_lo is not None else None
+        _profiled("attn_fwd", 4 * B * T * T * H * hd, _lib.call, "cb_attention_fwd", B, T, H, KVH, _TC_HD, dt(q),
+                  qp.data_ptr(), ld(qp), kp.data_ptr(), ld(kp), vp.data_ptr(), ld(vp), op.data_ptr(), ld(op),
+                  _ptr(olp), lse.data_ptr(), float(scale), stream_ptr())
+        _unpad(op, o, H, hd)
+        if o_lo is not None:
+            _unpad(olp, o_lo, H, hd)
+    else:
+        _profiled("attn_fwd", 4 * B * T * T * H * hd, _lib.call, "cb_attention_fwd", B, T, H, KVH, hd, dt(q),
+                  q.data_ptr(), ld(q), k.data_ptr(), ld(k), v.data_ptr(), ld(v), o.data_ptr(), ld(o), _ptr(o_lo),
+                  lse.data_ptr(), float(scale), stream_ptr())
     return (o, lse, o_lo) if want_lo else (o, lse)
 
 
+def _attention_bwd_padded(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, scale, o_lo):
+    qp, kp, vp, op, dop = _pad(q, H, hd), _pad(k, KVH, hd), _pad(v, KVH, hd), _pad(o, H, hd), _pad(do, H, hd)
+    olp = _pad(o_lo, H, hd) if o_lo is not None else None
+    dqp, dkp, dvp = torch.empty_like(qp), torch.empty_like(kp), torch.empty_like(vp)
+    delta = torch.empty((B, H, T), device=q.device, dtype=torch.float32)
+    _profiled("attn_bwd", 8 * B * T * T * H * hd, _lib.call, "cb_attention_bwd", B, T, H, KVH, _TC_HD, dt(q),
+              qp.data_ptr(), ld(qp), kp.data_ptr(), ld(kp), vp.data_ptr(), ld(vp), op.data_ptr(), ld(op), _ptr(olp),
+              lse.data_ptr(), dop.data_ptr(), ld(dop), delta.data_ptr(), dqp.data_ptr(), ld(dqp), dkp.data_ptr(),
+              ld(dkp), dvp.data_ptr(), ld(dvp), float(scale), stream_ptr())
+    _unpad(dqp, dq, H, hd)
+    _unpad(dkp, dk, KVH, hd)
+    _unpad(dvp, dv, KVH, hd)
+
+
 def attention_bwd_rope(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, scale, cos_t, sin_t, o_lo=None):
+    if _pad_ok(q, hd):
+        _attention_bwd_padded(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, scale, o_lo)
+        rope_(dq, T, H, hd, cos_t, sin_t, inverse=True)
+        rope_(dk, T, KVH, hd, cos_t, sin_t, inverse=True)
+        return
     delta = torch.empty((B, H, T), device=q.device, dtype=torch.float32)
     # algorithmic FLOPs: 2x forward (dP, dV, dQ, dK), the reference's backward_multiplier (mesh.py:644)
     _profiled("attn_bwd", 8 * B * T * T * H * hd, _lib.call, "cb_attention_bwd_rope", B, T, H, KVH, hd, dt(q),
@@ -393,6 +456,8 @@ def attention_bwd_rope(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, scale,
 
 
 def attention_bwd(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, scale, o_lo=None):
+    if _pad_ok(q, hd):
+        return _attention_bwd_padded(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, scale, o_lo)
     delta = torch.empty((B, H, T), device=q.device, dtype=torch.float32)
     _profiled("attn_bwd", 8 * B * T * T * H * hd, _lib.call, "cb_attention_bwd", B, T, H, KVH, hd, dt(q),
               q.data_ptr(), ld(q), k.data_ptr(), ld(k), v.data_ptr(), ld(v), o.data_ptr(), ld(o), _ptr(o_lo),

@@ -23,6 +23,7 @@ and with NCCL (=0), both against the oracle and against each other.
 """
 
 import argparse
+import contextlib
 import json
 import os
 import sys
@@ -63,8 +64,6 @@ def oracle_run(cfg, B, T, steps, precision, dtype, bf16_operands=False):
     V = m.config.get("model.vocab_size")
     mm = vv = None
     losses, summs, grads = [], [], None
-    import contextlib
-
     for step in range(steps):
         toks = synthetic_batch(0, step, B, T, V)["tokens"]
         with (O.bf16_operands() if bf16_operands else contextlib.nullcontext()):

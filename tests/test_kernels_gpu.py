@@ -65,9 +65,10 @@ def test_xent_matches_torch(cuda, V, scale, gdt):
     (1, 100, 4, 2, 16, torch.float32, 1),
     (2, 256, 8, 8, 128, torch.bfloat16, 0),
     (1, 384, 8, 2, 128, torch.bfloat16, 0),
-    (2, 128, 4, 4, 64, torch.bfloat16, 0),
+    (2, 128, 4, 4, 64, torch.bfloat16, 0),   # head_dim 64: zero-padded onto the tcgen05 kernels
+    (2, 128, 4, 2, 32, torch.bfloat16, 0),   # head_dim 32: same
     (2, 200, 4, 2, 128, torch.bfloat16, 0),  # ragged T: masked key tiles + rows crossing into the next sequence
-    (2, 200, 4, 2, 128, torch.bfloat16, 2),  # same, warp-MMA flash forward instead of tcgen05
+    (2, 200, 4, 2, 128, torch.bfloat16, 2),  # same, tcgen05 disabled: the SIMT engine
     (4, 128, 2, 2, 128, torch.bfloat16, 0),  # single key tile; second query tile of the CTA is padding
     (4, 128, 2, 2, 128, torch.bfloat16, 2),
     (3, 64, 2, 1, 128, torch.bfloat16, 0),   # T < tile
@@ -77,8 +78,8 @@ def test_attention_fwd_bwd(cuda, B, T, H, KVH, hd, dt, path):
     from paper_2507_05411_b200 import _lib, ops
 
     g = torch.Generator().manual_seed(T + hd)
-    warp_mma = path == 2
-    if warp_mma:
+    tc_off = path == 2
+    if tc_off:
         _lib.call("cb_attention_set_tc", 0)
         path = 0
     d, kvd = H * hd, KVH * hd
@@ -116,7 +117,7 @@ def test_attention_fwd_bwd(cuda, B, T, H, KVH, hd, dt, path):
         # o_lo: the forward's bf16 rounding residual; o + o_lo carries ~16 significant bits on
         # the tcgen05 path (zero from the other engines), and the backward with it agrees
         ops.set_attention_path(path)
-        if warp_mma:
+        if tc_off:
             _lib.call("cb_attention_set_tc", 0)
         try:
             o2, _, o_lo = ops.attention_fwd(q, k, v, B, T, H, KVH, hd, scale, want_lo=True)
@@ -129,7 +130,7 @@ def test_attention_fwd_bwd(cuda, B, T, H, KVH, hd, dt, path):
         torch.cuda.synchronize()
         assert torch.equal(o2, o)
         full = (o2.double() + o_lo.double()).view(B, T, H, hd).transpose(1, 2)
-        if hd == 128 and path == 0 and not warp_mma:  # tcgen05 forward: the residual is real
+        if path == 0 and not tc_off:  # tcgen05 forward: the residual is real
             # o + o_lo is the kernel's f32 output: at least as close to the f64 reference as o
             # (its own error is P's bf16 rounding inside the forward)
             o_ref = O.detach()
