@@ -208,6 +208,12 @@ CB_API int cb_xent_fwd_bwd(int batch, int seq_len, int vocab, const void* logits
 CB_API int cb_adamw(int64_t n, float* param, const float* grad, float* exp_avg, float* exp_avg_sq, void* param_bf16,
                     float lr, float beta1, float beta2, float eps, float weight_decay, int step, float grad_scale,
                     void* stream);
+/* AdamW on the FSDP reduce-scatter's parts: grad = scale * (parts[0] + parts[1] + ...) summed in
+ * list order (cb_sum_parts' arithmetic, so bit-identical to cb_sum_parts + cb_adamw) without the
+ * summed gradient's HBM round trip; grad_out (nullable) still receives it.  n % 4 == 0. */
+CB_API int cb_adamw_parts(int64_t n, int nparts, const void* parts, float scale, float* grad_out, float* param,
+                          float* exp_avg, float* exp_avg_sq, void* param_bf16, float lr, float beta1, float beta2,
+                          float eps, float weight_decay, int step, void* stream);
 
 /* ---------------------------------------------------------------------------------
  * MoE (layers.py:422-533).  cb_moe_route: probs = softmax(x @ router) in f64 per token,

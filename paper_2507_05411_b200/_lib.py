@@ -66,6 +66,7 @@ SIGNATURES: dict[str, list] = {
     "cb_moe_zero_pad_rows": [_I, _I, _I, _P, _P, _P, _L, _I, _P],
     "cb_xent_fwd_bwd": [_I, _I, _I, _P, _L, _I, _P, _P, _P, _L, _I, _F, _P, _P, _P],
     "cb_adamw": [_L, _P, _P, _P, _P, _P, _F, _F, _F, _F, _F, _I, _F, _P],
+    "cb_adamw_parts": [_L, _I, _P, _F, _P, _P, _P, _P, _P, _F, _F, _F, _F, _F, _I, _P],
     "cb_moe_route": [_L, _I, _I, _I, _P, _L, _I, _P, _P, _P, _P, _P],
     "cb_moe_stats": [_L, _I, _I, _P, _P, _P, _P],
     "cb_gather_rows": [_L, _I, _P, _I, _P, _L, _P, _L, _I, _P],

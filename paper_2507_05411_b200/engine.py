@@ -262,6 +262,10 @@ class TrainEngine:
         self.eps, self.weight_decay = eps, weight_decay
         self.seed = seed
         self.step_count = 0
+        # FSDP + copy-engine reduce-scatter: step() sums the gradient slices inside AdamW; set
+        # True to also store the summed gradient shards (grads_numpy() after step())
+        self.keep_grad_shards = False
+        self._grad_shards_stale = False
         self.d = _Dist(group)
         self.buckets = build_layout(self.module)
         self._alloc()
@@ -582,6 +586,11 @@ class TrainEngine:
     def grads_numpy(self) -> dict:
         """Global-batch gradients of the last step (under FSDP: the gathered reduce-scattered
         shards; replicated buckets were all-reduced in the step)."""
+        if self._grad_shards_stale:
+            from .errors import ComposerError
+
+            raise ComposerError("step() fused the gradient reduce-scatter into AdamW without storing the gradient "
+                                "shards: set engine.keep_grad_shards = True before the step to read gradients")
         return self._export("grad")
 
     # -------------------------------------------------------------------- step
@@ -636,6 +645,7 @@ class TrainEngine:
         toks = self.upload_tokens(tokens)
         if key is None:
             key = self.step_key(self.step_count)
+        self._grad_shards_stale = False
         if update:
             self.step_count += 1
         if self.d.world > 1:
@@ -691,12 +701,22 @@ class TrainEngine:
             ev.record(self._wgrad_stream)
             stream.wait_event(ev)
 
-    def _adamw_bucket(self, i: int) -> None:
+    def _adamw_bucket(self, i: int, parts: list | None = None, scale: float = 1.0) -> None:
+        """AdamW on bucket i's shard; with `parts` the gradient is scale * their in-order sum
+        (the copy-engine reduce-scatter's slices, cb_adamw_parts), stored to the gradient shard
+        only when keep_grad_shards is set."""
         rec = self.bufs[i]
         wshard = rec["wshard"]
         bf = wshard if (wshard.dtype == torch.bfloat16) else None
-        ops.adamw(rec["master"], rec["grad_shard"], rec["m"], rec["v"], bf, self.lr, self.beta1, self.beta2,
-                  self.eps, self.weight_decay, self.step_count)
+        if parts is not None:
+            ops.adamw_parts(parts, scale, rec["grad_shard"] if self.keep_grad_shards else None, rec["master"],
+                            rec["m"], rec["v"], bf, self.lr, self.beta1, self.beta2, self.eps, self.weight_decay,
+                            self.step_count)
+            if not self.keep_grad_shards:
+                self._grad_shards_stale = True
+        else:
+            ops.adamw(rec["master"], rec["grad_shard"], rec["m"], rec["v"], bf, self.lr, self.beta1, self.beta2,
+                      self.eps, self.weight_decay, self.step_count)
         if bf is None and wshard.data_ptr() != rec["master"].data_ptr():
             ops.copy2d(rec["master"].view(1, -1), wshard.view(1, -1))
 
@@ -796,6 +816,7 @@ class FSDPProvider(ParamProvider):
         ready.record(self.compute)
         ring = self.e._grad_ring and rec.get("ringed")
         gslot = self.e._pos[i] % 2 if ring else None
+        fused = False
         with torch.cuda.stream(self.comm):
             self.comm.wait_event(ready)
             self.e._join_wgrad(self.comm)
@@ -820,7 +841,11 @@ class FSDPProvider(ParamProvider):
                         parts.append(slot)
                         j += 1
                 h.barrier(channel=0, timeout_ms=_BARRIER_TIMEOUT_MS)
-                ops.sum_parts(parts, rec["grad_shard"], 1.0 / N)
+                if self.update:  # the in-order sum fused into AdamW (no summed-gradient round trip)
+                    self.e._adamw_bucket(i, parts=parts, scale=1.0 / N)
+                    fused = True
+                else:
+                    ops.sum_parts(parts, rec["grad_shard"], 1.0 / N)
             else:
                 self.dist.reduce_scatter_tensor(rec["grad_shard"], rec["grad"], op=self.dist.ReduceOp.AVG,
                                                 group=self.group)
@@ -829,7 +854,7 @@ class FSDPProvider(ParamProvider):
                 ev = torch.cuda.Event()
                 ev.record(self.comm)
                 self.gslot_free[gslot] = ev
-            if self.update:
+            if self.update and not fused:
                 self.e._adamw_bucket(i)
 
     def start_step(self) -> None:

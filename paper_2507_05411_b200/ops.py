@@ -482,3 +482,19 @@ def adamw(param, grad, m, v, param_bf16, lr, beta1, beta2, eps, weight_decay, st
     _lib.call("cb_adamw", n, param.data_ptr(), grad.data_ptr(), m.data_ptr(), v.data_ptr(), _ptr(param_bf16),
               float(lr), float(beta1), float(beta2), float(eps), float(weight_decay), int(step), float(grad_scale),
               stream_ptr())
+
+
+def adamw_parts(parts: list, scale: float, grad_out, param, m, v, param_bf16, lr, beta1, beta2, eps, weight_decay,
+                step):
+    """AdamW with grad = scale * sum(parts) in list order (cb_adamw_parts: bit-identical to
+    sum_parts + adamw, without the summed gradient's HBM round trip)."""
+    import ctypes
+
+    n = param.numel()
+    for t in parts:
+        if t.dtype != torch.float32 or t.numel() != n:
+            raise ShapeError("adamw_parts: f32 parts of the parameter's size expected")
+    ptrs = (ctypes.c_void_p * len(parts))(*[t.data_ptr() for t in parts])
+    _lib.call("cb_adamw_parts", n, len(parts), ctypes.addressof(ptrs), float(scale), _ptr(grad_out), param.data_ptr(),
+              m.data_ptr(), v.data_ptr(), _ptr(param_bf16), float(lr), float(beta1), float(beta2), float(eps),
+              float(weight_decay), int(step), stream_ptr())

@@ -85,6 +85,7 @@ def engine_run(cfg, precision, B, T, steps, mode, ce):
     world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", rank)))
     eng = TrainEngine(set_dtype_policy(cfg, precision), device=dev)
+    eng.keep_grad_shards = True  # the last step's gradients are compared with the oracle's
     V = eng.cfg.get("model.vocab_size")
     per = B // world
     losses, summs = [], []

@@ -315,3 +315,30 @@ def test_linear_with_bias_matches_reference(cuda, precision):
                            ("x[1, 2, 9]", gx[1, 2, 9], gx)):
         scale = abs(fd[key]) if precision == "f32" else float(np.sqrt(np.mean(full ** 2)))
         assert abs(got - fd[key]) <= 1e-6 + tol * scale, key
+
+
+@pytest.mark.parametrize("nparts", [1, 2, 4, 8])
+def test_adamw_parts_is_sum_parts_then_adamw(cuda, nparts):
+    """cb_adamw_parts (FSDP: the reduce-scatter's in-order sum fused into AdamW) is bit-identical
+    to cb_sum_parts followed by cb_adamw, bf16 working copy included."""
+    from paper_2507_05411_b200 import ops
+
+    n = 4096 * 3
+    g = torch.Generator(device="cpu").manual_seed(nparts)
+    parts = [torch.randn(n, generator=g).to(cuda) * 1e-3 for _ in range(nparts)]
+    p0, m0, v0 = (torch.randn(n, generator=g).to(cuda) for _ in range(3))
+    v0 = v0.abs()
+    outs = []
+    for fused in (False, True):
+        p, m, v = p0.clone(), m0.clone(), v0.clone()
+        bf = torch.empty(n, device=cuda, dtype=torch.bfloat16)
+        gs = torch.empty(n, device=cuda)
+        if fused:
+            ops.adamw_parts(parts, 1.0 / nparts, gs, p, m, v, bf, 1e-3, 0.9, 0.999, 1e-8, 0.01, 3)
+        else:
+            ops.sum_parts(parts, gs, 1.0 / nparts)
+            ops.adamw(p, gs, m, v, bf, 1e-3, 0.9, 0.999, 1e-8, 0.01, 3)
+        outs.append((p, m, v, bf, gs))
+    torch.cuda.synchronize()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
