@@ -14,6 +14,16 @@
 
 namespace cb {
 
+// One element's update, with explicitly rounded operations so every kernel that calls it
+// (adamw_k, adamw_parts_k) produces bit-identical results regardless of FMA contraction.
+__device__ __forceinline__ void adam_elem(float& p, float g, float& m, float& v, float lr, float b1, float b2,
+                                          float eps, float wd, float bc1, float bc2) {
+  m = __fmaf_rn(b1, m, __fmul_rn(1.f - b1, g));
+  v = __fmaf_rn(b2, v, __fmul_rn(__fmul_rn(1.f - b2, g), g));
+  const float upd = __fdiv_rn(__fdiv_rn(m, bc1), __fadd_rn(__fsqrt_rn(__fdiv_rn(v, bc2)), eps));
+  p = __fsub_rn(p, __fmul_rn(lr, __fadd_rn(upd, __fmul_rn(wd, p))));
+}
+
 __global__ void __launch_bounds__(256) adamw_k(int64_t n, float* __restrict__ p, const float* __restrict__ g,
                                                float* __restrict__ m, float* __restrict__ v,
                                                __nv_bfloat16* __restrict__ pbf, float lr, float b1, float b2,
@@ -30,13 +40,7 @@ __global__ void __launch_bounds__(256) adamw_k(int64_t n, float* __restrict__ p,
     float* mm = &M.x;
     float* vv = &V.x;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float gj = gg[j] * gs;
-      mm[j] = b1 * mm[j] + (1.f - b1) * gj;
-      vv[j] = b2 * vv[j] + (1.f - b2) * gj * gj;
-      const float upd = (mm[j] / bc1) / (sqrtf(vv[j] / bc2) + eps);
-      pp[j] = pp[j] - lr * (upd + wd * pp[j]);
-    }
+    for (int j = 0; j < 4; ++j) adam_elem(pp[j], __fmul_rn(gg[j], gs), mm[j], vv[j], lr, b1, b2, eps, wd, bc1, bc2);
     reinterpret_cast<float4*>(p)[i] = P;
     reinterpret_cast<float4*>(m)[i] = M;
     reinterpret_cast<float4*>(v)[i] = V;
@@ -50,12 +54,12 @@ __global__ void __launch_bounds__(256) adamw_k(int64_t n, float* __restrict__ p,
   }
   // tail
   for (int64_t i = (n4 << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-    const float gj = g[i] * gs;
-    m[i] = b1 * m[i] + (1.f - b1) * gj;
-    v[i] = b2 * v[i] + (1.f - b2) * gj * gj;
-    const float upd = (m[i] / bc1) / (sqrtf(v[i] / bc2) + eps);
-    p[i] = p[i] - lr * (upd + wd * p[i]);
-    if (pbf) pbf[i] = __float2bfloat16_rn(p[i]);
+    float pi = p[i], mi = m[i], vi = v[i];
+    adam_elem(pi, __fmul_rn(g[i], gs), mi, vi, lr, b1, b2, eps, wd, bc1, bc2);
+    p[i] = pi;
+    m[i] = mi;
+    v[i] = vi;
+    if (pbf) pbf[i] = __float2bfloat16_rn(pi);
   }
 }
 
@@ -95,13 +99,7 @@ __global__ void __launch_bounds__(256) adamw_parts_k(int64_t n4, Parts s, int np
     float* mm = &M.x;
     float* vv = &V.x;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float gj = gg[j] * 1.f;
-      mm[j] = b1 * mm[j] + (1.f - b1) * gj;
-      vv[j] = b2 * vv[j] + (1.f - b2) * gj * gj;
-      const float upd = (mm[j] / bc1) / (sqrtf(vv[j] / bc2) + eps);
-      pp[j] = pp[j] - lr * (upd + wd * pp[j]);
-    }
+    for (int j = 0; j < 4; ++j) adam_elem(pp[j], __fmul_rn(gg[j], 1.f), mm[j], vv[j], lr, b1, b2, eps, wd, bc1, bc2);
     reinterpret_cast<float4*>(p)[i] = P;
     reinterpret_cast<float4*>(m)[i] = M;
     reinterpret_cast<float4*>(v)[i] = V;
