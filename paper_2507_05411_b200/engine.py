@@ -732,6 +732,75 @@ class TrainEngine:
         return self.compute_grads(tokens, update=True)
 
 
+class GatherPlan:
+    """Host-side plan of the parameter all-gathers of one FSDP step (pure Python: which bucket
+    is gathered where and when, with or without the ordering barrier); FSDPProvider executes
+    it on the comm stream.  tests/test_fsdp.py checks its invariants on CPU.
+
+    Under ZeRO-3 (reshard) layer position p lives in gather slot p % 2: gathered before its
+    forward (prefetched while position p - 1 computes) and again before its backward unless it
+    is still resident (the forward's last two positions), prefetched while position p + 1's
+    backward runs.  Without resharding every bucket has its own full buffer and is gathered once
+    per step.  A forward gather carries the barrier that orders it after the peers' AdamW of the
+    bucket (previous step); a backward re-gather needs none (see FSDPProvider._ag)."""
+
+    def __init__(self, layer_order: list, reshard: bool):
+        self.order = list(layer_order)
+        self.pos = {b: p for p, b in enumerate(self.order)}
+        self.reshard = reshard
+        self.holder: dict[int, int] = {}  # slot -> bucket it holds
+        self.done: set[int] = set()       # keep mode: buckets gathered this step
+
+    def slot(self, b: int):
+        return self.pos[b] % 2 if (self.reshard and b in self.pos) else None
+
+    def _need(self, b: int) -> bool:
+        s = self.slot(b)
+        return (b not in self.done) if s is None else (self.holder.get(s) != b)
+
+    def _take(self, b: int, backward: bool, out: list) -> None:
+        if not self._need(b):
+            return
+        s = self.slot(b)
+        if s is None:
+            self.done.add(b)
+        else:
+            self.holder[s] = b
+        out.append((b, s, not backward))
+
+    def start(self, root: int) -> list:
+        """Gathers issued at the start of the step: the root bucket, then the first layer."""
+        out: list = []
+        self._take(root, False, out)
+        if self.order:
+            self._take(self.order[0], False, out)
+        return out
+
+    def forward(self, b: int) -> list:
+        """Gathers issued just before bucket b's forward: b (if not prefetched) and the next layer."""
+        out: list = []
+        self._take(b, False, out)
+        p = self.pos.get(b)
+        if p is not None and p + 1 < len(self.order):
+            self._take(self.order[p + 1], False, out)
+        return out
+
+    def backward(self, b: int) -> list:
+        """Gathers issued just before bucket b's backward (ZeRO-3 only): b if no longer resident
+        and the previous layer."""
+        out: list = []
+        p = self.pos.get(b)
+        if not self.reshard or p is None:
+            return out
+        self._take(b, True, out)
+        if p > 0:
+            self._take(self.order[p - 1], True, out)
+        return out
+
+    def resident(self, b: int) -> bool:
+        return not self._need(b)
+
+
 class FSDPProvider(ParamProvider):
     """Per-layer parameter all-gather (prefetched one layer ahead) and gradient
     reduce-scatter on a side (comm) stream: copy-engine peer reads of symmetric memory, or
@@ -752,20 +821,18 @@ class FSDPProvider(ParamProvider):
         self.index = {b.name: i for i, b in enumerate(eng.buckets)}
         self.layer_order = eng.layer_order
         self.gathered: dict[int, torch.cuda.Event] = {}  # bucket -> gather-done event (this step)
-        self.holder: dict[int, int] = {}  # ring slot -> bucket whose gathered copy it holds
+        self.plan = GatherPlan(self.layer_order, eng._reshard)
         self.gslot_free: dict[int, torch.cuda.Event] = {}  # grad ring slot -> cleared event
 
-    def _slot(self, i: int) -> int | None:
-        return self.e._pos[i] % 2 if (self.e._reshard and self.e.bufs[i].get("ringed")) else None
+    def _run(self, actions: list) -> None:
+        for i, slot, barrier in actions:
+            self._ag(i, slot, barrier)
 
-    def _ag(self, i: int, backward: bool = False) -> None:
+    def _ag(self, i: int, slot, barrier: bool) -> None:
+        """Gathers bucket i (into ring slot `slot`, or its own full buffer when None) on the comm
+        stream; `barrier`: order the reads after every peer's AdamW of the bucket."""
         rec, b = self.e.bufs[i], self.e.buckets[i]
         if b.replicated:
-            return
-        slot = self._slot(i)
-        if slot is None and i in self.gathered:
-            return
-        if slot is not None and self.holder.get(slot) == i:
             return
         ready = torch.cuda.Event()
         ready.record(self.compute)  # the compute stream is done with the slot's previous layer
@@ -788,7 +855,7 @@ class FSDPProvider(ParamProvider):
                 #   its backward of it, which comes after this gather;
                 # * no barrier after the reads: a rank's next AdamW of this bucket waits for the
                 #   same reduce-scatter barrier, which every reader passes only after its reads.
-                if not backward:
+                if barrier:
                     h.barrier(channel=0, timeout_ms=_BARRIER_TIMEOUT_MS)
                 for k in range(1, N):
                     p = (r + k) % N
@@ -800,12 +867,9 @@ class FSDPProvider(ParamProvider):
             done = torch.cuda.Event()
             done.record(self.comm)
         self.gathered[i] = done
-        if slot is not None:
-            self.holder[slot] = i
 
-    def _use(self, i: int) -> None:
-        """Bucket i is about to be read on the compute stream: gathered, and waited for."""
-        self._ag(i)
+    def _wait(self, i: int) -> None:
+        """The compute stream waits for bucket i's most recent gather."""
         ev = self.gathered.get(i)
         if ev is not None:
             self.compute.wait_event(ev)
@@ -858,18 +922,15 @@ class FSDPProvider(ParamProvider):
                 self.e._adamw_bucket(i)
 
     def start_step(self) -> None:
-        self._use(0)
-        if self.layer_order:
-            self._ag(self.layer_order[0])
+        self._run(self.plan.start(0))
+        self._wait(0)
 
     def before_forward(self, path: str) -> None:
         i = self.index.get(path)
         if i is None:
             return
-        self._use(i)
-        pos = self.e._pos.get(i)
-        if pos is not None and pos + 1 < len(self.layer_order):
-            self._ag(self.layer_order[pos + 1])
+        self._run(self.plan.forward(i))
+        self._wait(i)
 
     def before_backward(self, path: str) -> None:
         _wait_grads_zeroed(self)
@@ -880,12 +941,8 @@ class FSDPProvider(ParamProvider):
         if pos is None:
             return
         if self.e._reshard:
-            self._ag(i, backward=True)
-            ev = self.gathered.get(i)
-            if ev is not None:
-                self.compute.wait_event(ev)
-            if pos > 0:
-                self._ag(self.layer_order[pos - 1], backward=True)
+            self._run(self.plan.backward(i))
+            self._wait(i)
         if self.e._grad_ring:
             ev = self.gslot_free.pop(pos % 2, None)
             if ev is not None:

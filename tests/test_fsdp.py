@@ -169,3 +169,58 @@ def test_fsdp_four_gpus_step_matches_oracle(precision):
     cannot meet 1e-5; bf16 2e-2)."""
     _fsdp_check(4, "--precision", precision, "--config", "mid", "--seq", "128", "--steps", "3", "--mode", "step",
                 "--collectives", "both")
+
+
+@pytest.mark.parametrize("layers", [1, 2, 3, 8, 32])
+@pytest.mark.parametrize("reshard", [True, False])
+def test_gather_plan_invariants(layers, reshard):
+    """The host-side FSDP gather plan (engine.GatherPlan, executed by FSDPProvider) on a
+    simulated step — forward over the layers, head, backward in reverse — for several steps:
+    every layer is resident in its slot when its forward / backward reads it; a slot is never
+    re-gathered while its previous holder still has a pending read; forward gathers carry the
+    AdamW-ordering barrier and backward re-gathers do not; ZeRO-3 gathers 2L-2 layer buckets per
+    step (the last two stay resident across the forward/backward turn), full buffers L."""
+    from paper_2507_05411_b200.engine import GatherPlan
+
+    root, order = 0, list(range(1, layers + 1))
+    for _ in range(3):  # a fresh plan per step, as FSDPProvider makes one per call
+        plan = GatherPlan(order, reshard)
+        log = []  # (event, bucket, slot, barrier)
+
+        def issue(actions, phase):
+            for b, s, barrier in actions:
+                assert barrier == (phase != "bwd")
+                if s is not None:
+                    assert s == plan.slot(b)
+                log.append(("gather", b, s, barrier))
+
+        def read(b):
+            assert plan.resident(b), f"bucket {b} read while not resident"
+            log.append(("read", b, plan.slot(b), None))
+
+        issue(plan.start(root), "start")
+        read(root)
+        for b in order:
+            issue(plan.forward(b), "fwd")
+            read(b)
+        read(root)  # head
+        for b in reversed(order):
+            issue(plan.backward(b), "bwd")
+            read(b)
+        read(root)  # embedding backward
+        # a gather into a slot happens only after the slot's previous holder's last pending read
+        if reshard:
+            for idx, (ev, b, s, _) in enumerate(log):
+                if ev != "gather" or s is None:
+                    continue
+                prev = [e for e in log[:idx] if e[0] == "gather" and e[2] == s]
+                if prev:
+                    old = prev[-1][1]
+                    for e in log[idx:]:  # until `old` is gathered again, nobody may read it
+                        if e[0] == "gather" and e[1] == old:
+                            break
+                        assert not (e[0] == "read" and e[1] == old), f"slot {s}: {old} read after {b} replaced it"
+        n_layer_gathers = sum(1 for e in log if e[0] == "gather" and e[1] != root)
+        expect = (2 * layers - min(layers, 2)) if reshard else layers
+        assert n_layer_gathers == expect, (n_layer_gathers, expect)
+        assert sum(1 for e in log if e[0] == "gather" and e[1] == root) == 1
