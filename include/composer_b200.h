@@ -169,6 +169,9 @@ CB_API int cb_sum_parts(int nparts, int64_t n, const void* parts, void* out, flo
  * o_lo (bf16 only, nullable, o's layout): the forward writes o - bf16(o), and the backward
  * forms delta = rowsum(dO * (o + o_lo)) — the flash backward's delta at ~16 significant bits
  * instead of bf16 o's 8 (it multiplies every dS = P (dP - delta) entry).
+ * ds_ws (nullable, >= B*H*T*T bf16): with it and T % 128 == 0 the tcgen05 backward stores dS^T
+ * from the dK/dV sweep and forms dQ as a GEMM over it (dq_gemm_k) instead of the dQ sweep that
+ * recomputes S and dP (7 -> 5 MMA units per tile pair); without it, the two-sweep backward.
  * ------------------------------------------------------------------------------- */
 CB_API int cb_attention_fwd(int batch, int seq_len, int heads, int kv_heads, int head_dim, int dtype, const void* q,
                             int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv, void* o, int64_t ldo,
@@ -177,13 +180,14 @@ CB_API int cb_attention_bwd(int batch, int seq_len, int heads, int kv_heads, int
                             int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv, const void* o,
                             int64_t ldo, const void* o_lo, const float* lse, const void* dout, int64_t lddo,
                             float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv,
-                            float scale, void* stream);
+                            float scale, void* ds_ws, int64_t ds_bytes, void* stream);
 /* Backward for q/k rotated by cb_gemm_rope: dq/dk are returned un-rotated (the RoPE backward). */
 CB_API int cb_attention_bwd_rope(int batch, int seq_len, int heads, int kv_heads, int head_dim, int dtype,
                                  const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
                                  const void* o, int64_t ldo, const void* o_lo, const float* lse, const void* dout,
                                  int64_t lddo, float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
-                                 int64_t lddv, float scale, const float* cos_t, const float* sin_t, void* stream);
+                                 int64_t lddv, float scale, const float* cos_t, const float* sin_t, void* ds_ws,
+                                 int64_t ds_bytes, void* stream);
 /* 0 = automatic (tensor-core flash kernels when eligible), 1 = force SIMT (tests). */
 CB_API int cb_attention_set_path(int path);
 /* 1 (default) = the tcgen05/TMEM kernels for bf16 head_dim 128 (the Python layer zero-pads

@@ -24,5 +24,6 @@ int attn_fwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, 
                 cudaStream_t st);
 int attn_bwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, const void* dout, int64_t lddo,
                 const float* lse, const float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
-                int64_t lddv, cudaStream_t st, const float* rope_cos = nullptr, const float* rope_sin = nullptr);
+                int64_t lddv, cudaStream_t st, const float* rope_cos = nullptr, const float* rope_sin = nullptr,
+                void* ds_ws = nullptr);
 }  // namespace cb

@@ -18,6 +18,15 @@ static bool tc_bwd_ok(const AttnGeom& g, int dtype, const void* q, const void* k
   return g.T % 4 == 0 && ((reinterpret_cast<uintptr_t>(lse) | reinterpret_cast<uintptr_t>(delta)) & 15) == 0;
 }
 
+// the optional dS^T workspace of the tcgen05 backward: B*H*T*T bf16, 16-byte aligned
+static int ds_check(const AttnGeom& g, const void* ds_ws, int64_t ds_bytes) {
+  if (!ds_ws) return CB_OK;
+  const int64_t need = (int64_t)g.B * g.H * g.T * g.T * 2;
+  if (ds_bytes < need || (reinterpret_cast<uintptr_t>(ds_ws) & 15))
+    return fail(CB_ERR_ARG, "attention bwd: dS workspace needs %lld aligned bytes", (long long)need);
+  return CB_OK;
+}
+
 extern "C" int cb_attention_set_path(int path) {
   if (path < 0 || path > 1) return fail(CB_ERR_ARG, "attention path must be 0 (auto) or 1 (simt)");
   g_attn_path = path;
@@ -44,13 +53,14 @@ extern "C" int cb_attention_bwd(int batch, int seq_len, int heads, int kv_heads,
                                 const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
                                 const void* o, int64_t ldo, const void* o_lo, const float* lse, const void* dout,
                                 int64_t lddo, float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
-                                int64_t lddv, float scale, void* stream) {
+                                int64_t lddv, float scale, void* ds_ws, int64_t ds_bytes, void* stream) {
   AttnGeom g{batch, seq_len, heads, kv_heads, head_dim, ldq, ldk, ldv, ldo, scale};
   if (int s = check_geom(g)) return s;
   cudaStream_t st = (cudaStream_t)stream;
+  if (int s = ds_check(g, ds_ws, ds_bytes)) return s;
   if (int s = attn_delta(g, dtype, o, o_lo, dout, lddo, delta, st)) return s;
   if (tc_bwd_ok(g, dtype, q, k, v, lse, delta, lddo, lddq, lddk, lddv))
-    return attn_bwd_tc(g, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st);
+    return attn_bwd_tc(g, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st, nullptr, nullptr, ds_ws);
   return attn_bwd_simt(g, dtype, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st);
 }
 
@@ -63,16 +73,17 @@ extern "C" int cb_attention_bwd_rope(int batch, int seq_len, int heads, int kv_h
                                      int64_t ldv, const void* o, int64_t ldo, const void* o_lo, const float* lse,
                                      const void* dout, int64_t lddo, float* delta, void* dq, int64_t lddq, void* dk,
                                      int64_t lddk, void* dv, int64_t lddv, float scale, const float* cos_t,
-                                     const float* sin_t, void* stream) {
+                                     const float* sin_t, void* ds_ws, int64_t ds_bytes, void* stream) {
   AttnGeom g{batch, seq_len, heads, kv_heads, head_dim, ldq, ldk, ldv, ldo, scale};
   if (int s = check_geom(g)) return s;
   cudaStream_t st = (cudaStream_t)stream;
+  if (int s = ds_check(g, ds_ws, ds_bytes)) return s;
   if (tc_bwd_ok(g, dtype, q, k, v, lse, delta, lddo, lddq, lddk, lddv)) {
     if (int s = attn_delta(g, dtype, o, o_lo, dout, lddo, delta, st)) return s;
-    return attn_bwd_tc(g, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st, cos_t, sin_t);
+    return attn_bwd_tc(g, q, k, v, dout, lddo, lse, delta, dq, lddq, dk, lddk, dv, lddv, st, cos_t, sin_t, ds_ws);
   }
   if (int s = cb_attention_bwd(batch, seq_len, heads, kv_heads, head_dim, dtype, q, ldq, k, ldk, v, ldv, o, ldo, o_lo,
-                               lse, dout, lddo, delta, dq, lddq, dk, lddk, dv, lddv, scale, stream))
+                               lse, dout, lddo, delta, dq, lddq, dk, lddk, dv, lddv, scale, nullptr, 0, stream))
     return s;
   const int64_t rows = (int64_t)batch * seq_len;
   if (int s = cb_rope(rows, seq_len, heads, head_dim, dq, lddq, dtype, cos_t, sin_t, 1, stream)) return s;

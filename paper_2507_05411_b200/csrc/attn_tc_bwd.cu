@@ -216,11 +216,18 @@ __device__ __forceinline__ uint32_t packed_colq(int k) {
   return (uint32_t)((k * 16 / W) * W + ((k * 16) % W) / 2);
 }
 
-// NQ column groups -> 4 NQ compute warps (warps 4 .. 4 + 4 NQ), 128 + 128 NQ threads
-template <int NQ>
+// NQ column groups -> 4 NQ compute warps (warps 4 .. 4 + 4 NQ), 128 + 128 NQ threads.
+// DS: also store dS^T (bf16, exactly the dK MMA's operand) to global memory — row
+// (b*H + h)*T + key, column query — for the dQ GEMM (dq_gemm_k) that then replaces dq_k's
+// S / dP recomputation.  Each compute warp stages its [32 keys][64 queries] block in shared
+// memory (128-byte swizzle) and issues its own TMA store; the Q ring drops to two slots to
+// make room for the 32 KB stage.
+template <int NQ, bool DS>
 __global__ void __launch_bounds__(128 + 128 * NQ, 1)
     dkdv_k(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-           const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmG, const Params p) {
+           const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmG,
+           const __grid_constant__ CUtensorMap tmS, const Params p) {
+  constexpr int kQSlots = DS ? 2 : tcb::kQSlots;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if (smem_u32(smem) & 1023) __trap();  // see kSmemDkdv
@@ -229,8 +236,9 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
   uint8_t* sV = smem + kTile;
   uint8_t* sQ = smem + 2 * kTile;                               // [kQSlots]
   uint8_t* sG = sQ + kQSlots * kTile;                           // [kGSlots]
-  float* sLD = reinterpret_cast<float*>(sG + kGSlots * kTile);  // [2] x {lse[128], delta[128]}
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sG + kGSlots * kTile + 2048);
+  uint8_t* sStage = sG + kGSlots * kTile;                       // DS: [NQ][128 keys][64 queries]
+  float* sLD = reinterpret_cast<float*>(sG + (kGSlots + (DS ? 1 : 0)) * kTile);  // [2] x {lse, delta}
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sLD) + 2048);
   uint64_t* kv_full = bars;
   uint64_t* q_full = bars + 1;     // [3]
   uint64_t* q_empty = bars + 4;    // [3]
@@ -461,6 +469,13 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
         // dS^T next to it, in two halves (ds_part after the first) when a half fills whole
         // 16-column TMEM stores
         constexpr int kParts = NP >= 32 ? 2 : 1;
+        // DS: this warp's stage block (32 key rows x 128 bytes); its previous TMA store has
+        // finished reading it before it is overwritten
+        uint8_t* stg = sStage + grp * (128 * 128) + q * (32 * 128);
+        if (DS) {
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+        }
 #pragma unroll
         for (int part = 0; part < kParts; ++part) {
           float2 ds[NP / kParts];
@@ -473,11 +488,34 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
                 fmul2(pr[c2i + 1], ffma2(make_float2(d4.z, d4.w), make_float2(-1.f, -1.f), colp(dv, c2i + 1)));
           }
           pack_storeN<NP / kParts>(tmem + lo + cP + col + NP + part * (NP / kParts), ds);
+          if (DS) {  // the same bf16 pairs, 16-byte chunks at their 128B-swizzled positions
+            constexpr int kChunks = NP / kParts / 4;
+#pragma unroll
+            for (int c = 0; c < kChunks; ++c) {
+              const int lc = part * kChunks + c;
+              uint4 v;
+              v.x = pack2(ds[4 * c].x, ds[4 * c].y);
+              v.y = pack2(ds[4 * c + 1].x, ds[4 * c + 1].y);
+              v.z = pack2(ds[4 * c + 2].x, ds[4 * c + 2].y);
+              v.w = pack2(ds[4 * c + 3].x, ds[4 * c + 3].y);
+              *reinterpret_cast<uint4*>(stg + lane * 128 + ((lc ^ (lane & 7)) << 4)) = v;
+            }
+          }
           if (part == 0) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(ds_part);
           }
+        }
+      }
+      if (DS) {
+        fence_async_smem();  // the stage's generic-proxy writes, visible to the TMA store
+        __syncwarp();
+        if (lane == 0) {
+          const int hq = kvh * group + u / nq, qs = (u % nq) * BT;
+          tma_store_2d(&tmS, sStage + grp * (128 * 128) + q * (32 * 128), qs + grp * W,
+                       (b * p.H + hq) * p.T + k0 + q * 32);
+          bulk_commit();
         }
       }
       tc_fence_before();
@@ -488,6 +526,7 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
         mbar_arrive(&ld_empty[u & 1]);
       }
     }
+    if (DS && lane == 0) bulk_wait0();  // every dS^T store has landed before the CTA exits
     mbar_wait(mma_done, 0);
     tc_fence_after();
     const int krow = k0 + t;
@@ -742,30 +781,146 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ============================================================ dQ as a GEMM over stored dS
+// dQ[q, :] = scale * sum_key dS[q, key] K[key, :] for one (128-query tile, head, batch) per
+// CTA, reading the dS^T the DS variant of dkdv_k stored (row (b*H + h)*T + key, column query:
+// an MN-major A operand) and K (MN-major B), 64 keys per stage through a 6-deep TMA ring;
+// tcgen05 accumulator in TMEM; inverse RoPE + bf16 store in the epilogue.  Deterministic
+// (one CTA per dQ tile, keys in order).  Requires T % 128 == 0.
+constexpr int kGStages = 6;
+constexpr int kGThreads = 256;
+constexpr int kSmemDqGemm = kGStages * 2 * kBox + 1024 + 256;
+
+__global__ void __launch_bounds__(kGThreads, 1)
+    dq_gemm_k(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmK, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;                    // [kGStages] dS^T box pairs: 64 keys x 128 queries
+  uint8_t* sB = smem + kGStages * kBox;  // [kGStages] K box pairs: 64 keys x 128 head dims
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kGStages * 2 * kBox);
+  uint64_t* empty = full + kGStages;
+  uint64_t* done = empty + kGStages;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int kvh = h / (p.H / p.KVH);
+  const int q0 = qt * BT, nkb = p.T / 64;
+  const int srow = (b * p.H + h) * p.T, krow = b * p.T;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmS);
+    tma_prefetch_desc(&tmK);
+    for (int s = 0; s < kGStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(slot, 128);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *slot;
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int st = kb % kGStages;
+        mbar_wait(&empty[st], ((kb / kGStages) & 1) ^ 1);
+        mbar_expect_tx(&full[st], 4 * (kBox / 2));
+        uint8_t* a = sA + st * kBox;
+        uint8_t* bb = sB + st * kBox;
+        // [64 keys][64 cols] boxes: two query halves of dS^T, two head-dim halves of K
+        tma_load_2d(a, &tmS, &full[st], q0, srow + kb * 64);
+        tma_load_2d(a + kBox / 2, &tmS, &full[st], q0 + 64, srow + kb * 64);
+        tma_load_2d(bb, &tmK, &full[st], kvh * HD, krow + kb * 64);
+        tma_load_2d(bb + kBox / 2, &tmK, &full[st], kvh * HD + 64, krow + kb * 64);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    const uint32_t idesc = idesc_bf16_f32(128, 128, 1, 1);  // MN-major A and B
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int st = kb % kGStages;
+      mbar_wait(&full[st], (kb / kGStages) & 1);
+      tc_fence_after();
+      const uint64_t ad = sw128_desc(smem_u32(sA + st * kBox), kBox / 2, 1024);
+      const uint64_t bd = sw128_desc(smem_u32(sB + st * kBox), kBox / 2, 1024);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)  // K = 16 keys per MMA: +2048 bytes of the MN-major boxes
+          umma_f16_ss(tmem, ad + (uint64_t)(kk * 128), bd + (uint64_t)(kk * 128), idesc, (kb | kk) != 0);
+        umma_commit(&empty[st]);
+      }
+      __syncwarp();
+    }
+    if (elect_one()) umma_commit(done);
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int qd = warp & 3;
+    const int qrow = q0 + qd * 32 + lane;
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const float* rc = p.rope_cos ? p.rope_cos + (int64_t)qrow * (HD / 2) : nullptr;
+    const float* rs = p.rope_sin ? p.rope_sin + (int64_t)qrow * (HD / 2) : nullptr;
+    store_row(tmem + ((uint32_t)(qd * 32) << 16), p.o0 + ((int64_t)krow + qrow) * p.ld0 + (int64_t)h * HD, p.scale,
+              qrow < p.T, rc, rs, HD / 32);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 128);
+  }
+}
+
 }  // namespace tcb
 
 int attn_bwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, const void* dout, int64_t lddo,
                 const float* lse, const float* delta, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
-                int64_t lddv, cudaStream_t st, const float* rope_cos, const float* rope_sin) {
+                int64_t lddv, cudaStream_t st, const float* rope_cos, const float* rope_sin, void* ds_ws) {
   using namespace tcb;
   if ((lddo | lddq | lddk | lddv) & 7) return fail(CB_ERR_ARG, "tc attention bwd: strides must be 16-byte aligned");
-  CUtensorMap mq, mk, mv, mg;
+  CUtensorMap mq, mk, mv, mg, ms, mk64;
   const uint64_t rows = (uint64_t)g.B * g.T;
   int s;
   if ((s = make_tmap_2d_bf16(&mq, q, rows, (uint64_t)g.H * HD, g.ldq, 128, 64))) return s;
   if ((s = make_tmap_2d_bf16(&mk, k, rows, (uint64_t)g.KVH * HD, g.ldk, 128, 64))) return s;
   if ((s = make_tmap_2d_bf16(&mv, v, rows, (uint64_t)g.KVH * HD, g.ldv, 128, 64))) return s;
   if ((s = make_tmap_2d_bf16(&mg, dout, rows, (uint64_t)g.H * HD, lddo, 128, 64))) return s;
+  // dS path (a caller-provided dS^T workspace, T a multiple of 128): dK/dV sweep storing dS^T,
+  // then dQ as a GEMM over it instead of the dQ sweep's S / dP recomputation
+  const bool use_ds = ds_ws != nullptr && g.T % 128 == 0;
+  if (use_ds) {
+    if ((s = make_tmap_2d_bf16(&ms, ds_ws, (uint64_t)g.B * g.H * g.T, (uint64_t)g.T, (uint64_t)g.T, 32, 64))) return s;
+    CUtensorMap ms64;
+    if ((s = make_tmap_2d_bf16(&ms64, ds_ws, (uint64_t)g.B * g.H * g.T, (uint64_t)g.T, (uint64_t)g.T, 64, 64)))
+      return s;
+    if ((s = make_tmap_2d_bf16(&mk64, k, rows, (uint64_t)g.KVH * HD, g.ldk, 64, 64))) return s;
+    static bool attr_ds = false;
+    if (!attr_ds) {
+      cudaFuncSetAttribute(dkdv_k<kDkdvGroups, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDkdv);
+      cudaFuncSetAttribute(dq_gemm_k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDqGemm);
+      attr_ds = true;
+    }
+    Params pk{g.T, g.H, g.KVH, g.B, g.scale, lse, delta, (__nv_bfloat16*)dk, lddk, (__nv_bfloat16*)dv, lddv,
+              rope_cos, rope_sin};
+    dkdv_k<kDkdvGroups, true><<<dim3(g.T / BT, g.KVH, g.B), 128 + 128 * kDkdvGroups, kSmemDkdv, st>>>(mq, mk, mv,
+                                                                                                   mg, ms, pk);
+    if (int e = check_launch("flash_bwd_dkdv_ds_tc")) return e;
+    Params pq{g.T, g.H, g.KVH, g.B, g.scale, lse, delta, (__nv_bfloat16*)dq, lddq, nullptr, 0, rope_cos, rope_sin};
+    dq_gemm_k<<<dim3(g.T / BT, g.H, g.B), kGThreads, kSmemDqGemm, st>>>(ms64, mk64, pq);
+    return check_launch("flash_bwd_dq_gemm_tc");
+  }
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(dkdv_k<kDkdvGroups>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDkdv);
+    cudaFuncSetAttribute(dkdv_k<kDkdvGroups, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDkdv);
     cudaFuncSetAttribute(dq_k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDq);
     attr = true;
   }
   Params pk{g.T, g.H, g.KVH, g.B, g.scale, lse, delta, (__nv_bfloat16*)dk, lddk, (__nv_bfloat16*)dv, lddv,
             rope_cos, rope_sin};
-  dkdv_k<kDkdvGroups><<<dim3((g.T + BT - 1) / BT, g.KVH, g.B), 128 + 128 * kDkdvGroups, kSmemDkdv, st>>>(mq, mk, mv,
-                                                                                                      mg, pk);
+  dkdv_k<kDkdvGroups, false><<<dim3((g.T + BT - 1) / BT, g.KVH, g.B), 128 + 128 * kDkdvGroups, kSmemDkdv, st>>>(
+      mq, mk, mv, mg, mg, pk);
   if (int e = check_launch("flash_bwd_dkdv_tc")) return e;
   Params pq{g.T, g.H, g.KVH, g.B, g.scale, lse, delta, (__nv_bfloat16*)dq, lddq, nullptr, 0, rope_cos, rope_sin};
   dq_k<<<dim3((g.T + BT - 1) / BT, g.H, g.B), kThreads, kSmemDq, st>>>(mq, mk, mv, mg, pq);

@@ -676,11 +676,19 @@ class TrainEngine:
             provider.start_step()
         if self.device.type == "cuda":
             # bytes the forward leaves allocated for the backward (saved activations, logits,
-            # gathered copies) — compared with aot_analyze's saved_activation_bytes in bench.py
+            # gathered copies) — compared with aot_analyze's saved_activation_bytes in bench.py.
+            # (a weak reference: a closure over self in self.options would make a reference
+            # cycle that keeps a dropped engine's HBM alive until the next gc pass)
+            import weakref
+
             base = torch.cuda.memory_allocated(self.device)
+            ref = weakref.ref(self)
+            dev = self.device
 
             def forward_done():
-                self.last_forward_bytes = torch.cuda.memory_allocated(self.device) - base
+                eng = ref()
+                if eng is not None:
+                    eng.last_forward_bytes = torch.cuda.memory_allocated(dev) - base
 
             self.options["forward_done"] = forward_done
         loss, col, _ = value_and_grad(self.module, self.state, self.grads, key, {"tokens": toks}, provider=provider,

@@ -432,13 +432,27 @@ def _attention_bwd_padded(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, sca
     olp = _pad(o_lo, H, hd) if o_lo is not None else None
     dqp, dkp, dvp = torch.empty_like(qp), torch.empty_like(kp), torch.empty_like(vp)
     delta = torch.empty((B, H, T), device=q.device, dtype=torch.float32)
+    ws = _ds_workspace(qp, B, T, H, _TC_HD)
     _profiled("attn_bwd", 8 * B * T * T * H * hd, _lib.call, "cb_attention_bwd", B, T, H, KVH, _TC_HD, dt(q),
               qp.data_ptr(), ld(qp), kp.data_ptr(), ld(kp), vp.data_ptr(), ld(vp), op.data_ptr(), ld(op), _ptr(olp),
               lse.data_ptr(), dop.data_ptr(), ld(dop), delta.data_ptr(), dqp.data_ptr(), ld(dqp), dkp.data_ptr(),
-              ld(dkp), dvp.data_ptr(), ld(dvp), float(scale), stream_ptr())
+              ld(dkp), dvp.data_ptr(), ld(dvp), float(scale), _ptr(ws), ws.numel() * 2 if ws is not None else 0,
+              stream_ptr())
     _unpad(dqp, dq, H, hd)
     _unpad(dkp, dk, KVH, hd)
     _unpad(dvp, dv, KVH, hd)
+
+
+# tcgen05 backward with dQ as a GEMM over the dS^T the dK/dV sweep stores (cb_attention_bwd
+# ds_ws): 5 MMA units per tile pair instead of 7; CB_ATTN_DQ_GEMM=0 keeps the dQ sweep (A/B)
+_DQ_GEMM = __import__("os").environ.get("CB_ATTN_DQ_GEMM", "1") == "1"
+
+
+def _ds_workspace(q, B, T, H, hd):
+    """The dS^T workspace (B*H*T*T bf16) when the dS path applies, else None."""
+    if not (_DQ_GEMM and q.dtype == torch.bfloat16 and hd == _TC_HD and T % 128 == 0 and _ATTN_PATH == 0):
+        return None
+    return torch.empty((B * H * T * T,), device=q.device, dtype=torch.bfloat16)
 
 
 def attention_bwd_rope(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, scale, cos_t, sin_t, o_lo=None):
@@ -448,21 +462,24 @@ def attention_bwd_rope(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, scale,
         rope_(dk, T, KVH, hd, cos_t, sin_t, inverse=True)
         return
     delta = torch.empty((B, H, T), device=q.device, dtype=torch.float32)
+    ws = _ds_workspace(q, B, T, H, hd)
     # algorithmic FLOPs: 2x forward (dP, dV, dQ, dK), the reference's backward_multiplier (mesh.py:644)
     _profiled("attn_bwd", 8 * B * T * T * H * hd, _lib.call, "cb_attention_bwd_rope", B, T, H, KVH, hd, dt(q),
               q.data_ptr(), ld(q), k.data_ptr(), ld(k), v.data_ptr(), ld(v), o.data_ptr(), ld(o), _ptr(o_lo),
               lse.data_ptr(), do.data_ptr(), ld(do), delta.data_ptr(), dq.data_ptr(), ld(dq), dk.data_ptr(), ld(dk),
-              dv.data_ptr(), ld(dv), float(scale), cos_t.data_ptr(), sin_t.data_ptr(), stream_ptr())
+              dv.data_ptr(), ld(dv), float(scale), cos_t.data_ptr(), sin_t.data_ptr(), _ptr(ws),
+              ws.numel() * 2 if ws is not None else 0, stream_ptr())
 
 
 def attention_bwd(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, scale, o_lo=None):
     if _pad_ok(q, hd):
         return _attention_bwd_padded(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, scale, o_lo)
     delta = torch.empty((B, H, T), device=q.device, dtype=torch.float32)
+    ws = _ds_workspace(q, B, T, H, hd)
     _profiled("attn_bwd", 8 * B * T * T * H * hd, _lib.call, "cb_attention_bwd", B, T, H, KVH, hd, dt(q),
               q.data_ptr(), ld(q), k.data_ptr(), ld(k), v.data_ptr(), ld(v), o.data_ptr(), ld(o), _ptr(o_lo),
               lse.data_ptr(), do.data_ptr(), ld(do), delta.data_ptr(), dq.data_ptr(), ld(dq), dk.data_ptr(), ld(dk),
-              dv.data_ptr(), ld(dv), float(scale), stream_ptr())
+              dv.data_ptr(), ld(dv), float(scale), _ptr(ws), ws.numel() * 2 if ws is not None else 0, stream_ptr())
 
 
 def xent(logits2d: torch.Tensor, tokens: torch.Tensor, dlogits: torch.Tensor | None, grad_scale: float):

@@ -342,3 +342,50 @@ def test_adamw_parts_is_sum_parts_then_adamw(cuda, nparts):
     torch.cuda.synchronize()
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("B,T,H,KVH,rope", [(2, 256, 4, 4, False), (1, 384, 8, 2, True), (1, 1152, 4, 4, False),
+                                           (2, 512, 4, 1, True)])
+def test_attention_dq_gemm_matches_sweep(cuda, B, T, H, KVH, rope):
+    """The dS path of the tcgen05 backward (dK/dV sweep storing dS^T + dQ as a GEMM over it,
+    dq_gemm_k) against the two-sweep path on the same inputs: dK / dV bit-identical (the same
+    sweep), dQ equal up to the rounding of dS to bf16 in one kernel or the other, and both
+    against fp64 at the kernel tolerance; deterministic reruns."""
+    from paper_2507_05411_b200 import ops
+    from paper_2507_05411_b200.layers import rope_tables
+
+    hd = 128
+    g = torch.Generator().manual_seed(T * H + B)
+    d, kvd = H * hd, KVH * hd
+    qkv = torch.randn(B * T, d + 2 * kvd, generator=g).to(cuda, torch.bfloat16)
+    q, k, v = qkv[:, :d], qkv[:, d:d + kvd], qkv[:, d + kvd:]
+    do = torch.randn(B * T, d, generator=g).to(cuda, torch.bfloat16)
+    scale = 1 / math.sqrt(hd)
+    cs, sn = rope_tables(T, hd, 10000.0, cuda)
+    o, lse, o_lo = ops.attention_fwd(q, k, v, B, T, H, KVH, hd, scale, want_lo=True)
+    outs = []
+    for dq_gemm in (True, True, False):
+        ops._DQ_GEMM = dq_gemm
+        try:
+            dqkv = torch.empty_like(qkv)
+            args = (q, k, v, o, lse, do, dqkv[:, :d], dqkv[:, d:d + kvd], dqkv[:, d + kvd:], B, T, H, KVH, hd, scale)
+            if rope:
+                ops.attention_bwd_rope(*args, cs, sn, o_lo=o_lo)
+            else:
+                ops.attention_bwd(*args, o_lo=o_lo)
+        finally:
+            ops._DQ_GEMM = True
+        outs.append(dqkv)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])  # deterministic
+    gemm, sweep = outs[0], outs[2]
+    assert torch.equal(gemm[:, d:], sweep[:, d:])  # dK, dV: the same sweep
+    assert _rel(gemm[:, :d], sweep[:, :d]) < 2e-3
+    if not rope:
+        Q = q.double().view(B, T, H, hd).transpose(1, 2).requires_grad_(True)
+        K = k.double().view(B, T, KVH, hd).transpose(1, 2)
+        Vv = v.double().view(B, T, KVH, hd).transpose(1, 2)
+        rep = H // KVH
+        P = torch.softmax(Q @ K.repeat_interleave(rep, 1).transpose(-1, -2) * scale, -1)
+        (P @ Vv.repeat_interleave(rep, 1)).backward(do.double().view(B, T, H, hd).transpose(1, 2))
+        assert _rel(gemm[:, :d].view(B, T, H, hd).transpose(1, 2), Q.grad) < 5e-3

@@ -502,10 +502,14 @@ def test_full_size_step_properties(cuda, name, B):
 
     from paper_2507_05411_b200 import BENCH_CONFIGS, TrainEngine, synthetic_batch
 
+    import gc
+
     cfg = BENCH_CONFIGS[name](batch=B, dtype="bf16")
     toks = synthetic_batch(0, 0, B, 4096, 32000)["tokens"]
     runs = []
     for _ in range(2):
+        gc.collect()
+        torch.cuda.empty_cache()
         eng = TrainEngine(cfg, device=cuda)
         losses = [float(eng.step(toks)[0].item()) for _ in range(3)]
         sums = [float(rec["master"].double().sum().item()) for rec in eng.bufs]
