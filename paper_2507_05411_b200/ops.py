@@ -444,8 +444,11 @@ def _attention_bwd_padded(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, sca
 
 
 # tcgen05 backward with dQ as a GEMM over the dS^T the dK/dV sweep stores (cb_attention_bwd
-# ds_ws): 5 MMA units per tile pair instead of 7; CB_ATTN_DQ_GEMM=0 keeps the dQ sweep (A/B)
-_DQ_GEMM = __import__("os").environ.get("CB_ATTN_DQ_GEMM", "1") == "1"
+# ds_ws): 5 MMA units per tile pair instead of 7.  Measured no faster (7B 1693 vs 1693 us,
+# 1B 3532 vs 3230 us, profiles/r02_attn_dq_gemm_ab.log): staging dS^T through shared memory
+# costs the already shared-memory-bound dK/dV sweep +28-43%, and the dQ GEMM streams dS at
+# ~4.2 TB/s.  Opt-in with CB_ATTN_DQ_GEMM=1 (tested either way).
+_DQ_GEMM = __import__("os").environ.get("CB_ATTN_DQ_GEMM", "0") == "1"
 
 
 def _ds_workspace(q, B, T, H, hd):

@@ -364,6 +364,7 @@ def test_attention_dq_gemm_matches_sweep(cuda, B, T, H, KVH, rope):
     cs, sn = rope_tables(T, hd, 10000.0, cuda)
     o, lse, o_lo = ops.attention_fwd(q, k, v, B, T, H, KVH, hd, scale, want_lo=True)
     outs = []
+    default = ops._DQ_GEMM
     for dq_gemm in (True, True, False):
         ops._DQ_GEMM = dq_gemm
         try:
@@ -374,7 +375,7 @@ def test_attention_dq_gemm_matches_sweep(cuda, B, T, H, KVH, rope):
             else:
                 ops.attention_bwd(*args, o_lo=o_lo)
         finally:
-            ops._DQ_GEMM = True
+            ops._DQ_GEMM = default
         outs.append(dqkv)
     torch.cuda.synchronize()
     assert torch.equal(outs[0], outs[1])  # deterministic
