@@ -190,10 +190,17 @@ def run_reference(args) -> None:
 
 
 # ------------------------------------------------------------------ kernel attribution
+_FOREIGN = ("at::", "c10d::", "c10::", "cub::", "cutlass::", "flash", "Memset", "Memcpy")
+
+
 def kernel_kind(name: str) -> str:
+    """Kind of a CUPTI kernel record: this library's kernels by name (most live in namespace
+    cb::; a few helpers are at file scope), everything from torch / NCCL / the driver as foreign."""
     n = name
-    if "cb::" not in n:
-        return "foreign (" + ("nccl" if "nccl" in n.lower() else "torch") + ")"
+    if "nccl" in n.lower():
+        return "foreign (nccl)"
+    if any(f in n for f in _FOREIGN):
+        return "foreign (torch)"
     if "gemm" in n:
         return "gemm"
     if "tca::" in n or "fa::fwd" in n or "attn_fwd" in n:
@@ -203,6 +210,8 @@ def kernel_kind(name: str) -> str:
     for key in ("xent", "adamw", "rmsnorm", "embed", "moe", "router", "sum_parts", "init"):
         if key in n:
             return key
+    if any(k in n for k in ("pad_rows", "zero_pad", "pad_offsets", "combine", "gather_rows", "sort_ids")):
+        return "moe"
     return "other_cb"
 
 
