@@ -160,6 +160,11 @@ CB_API int cb_memset_zero(void* ptr, int64_t bytes, void* stream);
  * local half of the FSDP gradient reduce-scatter (replaces the reduce in NCCL's
  * reduce_scatter_tensor(AVG); the reference has no distributed step). */
 CB_API int cb_sum_parts(int nparts, int64_t n, const void* parts, void* out, float scale, void* stream);
+/* f32 -> x1 + x2 + x3, three bf16 terms (relative remainder ~2^-24): the operand split of the f32
+ * parity mode's GEMMs on the tcgen05 engine (ops.gemm: six bf16 products accumulated in f32, the
+ * BF16x6 FP32 emulation).  src: [rows][cols] with row stride ld; outputs contiguous. */
+CB_API int cb_split_bf16x3(int64_t rows, int cols, const float* src, int64_t ld, void* d1, void* d2, void* d3,
+                           void* stream);
 
 /* ---------------------------------------------------------------------------------
  * Attention (layers.py:282-348), unmasked, flash-style (P never stored).  q/k/v/o

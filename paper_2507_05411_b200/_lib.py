@@ -48,6 +48,7 @@ SIGNATURES: dict[str, list] = {
     "cb_copy2d": [_L, _I, _P, _L, _I, _P, _L, _I, _F, _I, _P],
     "cb_memset_zero": [_P, _L, _P],
     "cb_sum_parts": [_I, _L, _P, _P, _F, _P],
+    "cb_split_bf16x3": [_L, _I, _P, _L, _P, _P, _P, _P],
     "cb_attention_fwd": [_I, _I, _I, _I, _I, _I, _P, _L, _P, _L, _P, _L, _P, _L, _P, _P, _F, _P],
     "cb_attention_bwd": [_I, _I, _I, _I, _I, _I, _P, _L, _P, _L, _P, _L, _P, _L, _P, _P, _P, _L, _P, _P, _L, _P,
                          _L, _P, _L, _F, _P, _L, _P],

@@ -355,3 +355,34 @@ extern "C" int cb_sum_parts(int nparts, int64_t n, const void* parts, void* out,
   sum_parts_k<<<blocks, 256, 0, (cudaStream_t)stream>>>(s, nparts, n4, (float*)out, scale);
   return check_launch("sum_parts");
 }
+
+// f32 -> three bf16 terms x = x1 + x2 + x3 (+ O(2^-24 |x|)): the operand split of the f32 parity
+// mode's GEMMs on the tcgen05 engine (six bf16 products, the "BF16x6" FP32 emulation).
+// src is a row-major [rows][cols] view with row stride ld; the three outputs are contiguous.
+__global__ void __launch_bounds__(256) split_bf16x3_k(int64_t rows, int cols, const float* __restrict__ src,
+                                                      int64_t ld, __nv_bfloat16* __restrict__ d1,
+                                                      __nv_bfloat16* __restrict__ d2, __nv_bfloat16* __restrict__ d3) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols;
+    const float x = src[r * ld + (i - r * cols)];
+    const __nv_bfloat16 a = __float2bfloat16_rn(x);
+    const float r1 = x - __bfloat162float(a);
+    const __nv_bfloat16 b = __float2bfloat16_rn(r1);
+    const float r2 = r1 - __bfloat162float(b);
+    d1[i] = a;
+    d2[i] = b;
+    d3[i] = __float2bfloat16_rn(r2);
+  }
+}
+
+extern "C" int cb_split_bf16x3(int64_t rows, int cols, const float* src, int64_t ld, void* d1, void* d2, void* d3,
+                               void* stream) {
+  if (rows <= 0 || cols <= 0) return CB_OK;
+  if (ld < cols) return fail(CB_ERR_SHAPE, "split_bf16x3: ld %lld < cols %d", (long long)ld, cols);
+  const int64_t n = rows * cols;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  split_bf16x3_k<<<blocks, 256, 0, (cudaStream_t)stream>>>(rows, cols, src, ld, (__nv_bfloat16*)d1,
+                                                           (__nv_bfloat16*)d2, (__nv_bfloat16*)d3);
+  return check_launch("split_bf16x3");
+}

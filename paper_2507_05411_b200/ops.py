@@ -112,10 +112,44 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, trans_a: bool = Fa
         if tuple(residual.shape) != (M, N):
             raise ShapeError("gemm: residual shape mismatch")
         ldr = ld(residual, "residual")
+    if _f32_on_tc(a, b, out, M, N, K):
+        return _gemm_bf16x6(a, b, out, trans_a, trans_b, alpha, accumulate, residual)
     kind = "gemm_bf16" if a.dtype == torch.bfloat16 else "gemm_f32"
     _profiled(kind, 2 * M * N * K, _lib.call, "cb_gemm", M, N, K, dt(a), a.data_ptr(), ld(a, "A"), int(trans_a),
               b.data_ptr(), ld(b, "B"), int(trans_b), out.data_ptr(), ld(out, "out"), dt(out), _ptr(residual), ldr,
               dt(residual) if residual is not None else 0, float(alpha), int(accumulate), stream_ptr())
+    return out
+
+
+# f32 parity mode on the tensor cores: an f32 GEMM large enough for the tcgen05 engine runs as
+# six bf16 products of the operands' three-term bf16 splits (cb_split_bf16x3), accumulated in
+# the f32 output by the same CTA-pair / 1-CTA kernels and epilogues the bf16 step uses — the
+# "BF16x6" FP32 emulation, ~fp32-accurate (the dropped terms are O(2^-24)).  CB_F32_TC=0 keeps
+# these GEMMs on the SIMT engine.
+_F32_TC = __import__("os").environ.get("CB_F32_TC", "1") == "1"
+_F32_TC_MIN_WORK = 1 << 22  # the tcgen05 dispatch threshold of cb_gemm (gemm_impl)
+# products x_i * y_j of the splits, smallest first so the f32 accumulation adds small to small
+_BF16X6_TERMS = ((2, 0), (0, 2), (1, 1), (1, 0), (0, 1), (0, 0))
+
+
+def _f32_on_tc(a, b, out, M, N, K) -> bool:
+    return (_F32_TC and a.dtype == torch.float32 and b.dtype == torch.float32 and out.dtype == torch.float32
+            and M * N * K >= _F32_TC_MIN_WORK and _GEMM_PATH == 0)
+
+
+def _split3(x: torch.Tensor):
+    x2 = rows2d(x)
+    parts = [torch.empty(x2.shape, device=x.device, dtype=torch.bfloat16) for _ in range(3)]
+    _lib.call("cb_split_bf16x3", x2.shape[0], x2.shape[1], x2.data_ptr(), ld(x2), parts[0].data_ptr(),
+              parts[1].data_ptr(), parts[2].data_ptr(), stream_ptr())
+    return parts
+
+
+def _gemm_bf16x6(a, b, out, trans_a, trans_b, alpha, accumulate, residual):
+    sa, sb = _split3(a), _split3(b)
+    for n, (i, j) in enumerate(_BF16X6_TERMS):
+        gemm(sa[i], sb[j], out, trans_a=trans_a, trans_b=trans_b, alpha=alpha,
+             accumulate=accumulate if n == 0 else True, residual=residual if n == 0 else None)
     return out
 
 
@@ -126,6 +160,10 @@ def gemm_rope(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, seq_len: int,
     N = b.shape[1]
     if b.shape[0] != K or tuple(out.shape) != (M, N):
         raise ShapeError("gemm_rope: shape mismatch")
+    if _f32_on_tc(a, b, out, M, N, K):  # six accumulated products, then the rotation
+        _gemm_bf16x6(a, b, out, False, False, 1.0, False, None)
+        rope_(out[:, :rope_cols], seq_len, rope_cols // head_dim, head_dim, cos_t, sin_t)
+        return out
     _profiled("gemm_bf16" if a.dtype == torch.bfloat16 else "gemm_f32", 2 * M * N * K, _lib.call, "cb_gemm_rope",
               M, N, K, dt(a), a.data_ptr(), ld(a, "A"), 0, b.data_ptr(), ld(b, "B"), 0, out.data_ptr(),
               ld(out, "out"), dt(out), int(seq_len), int(head_dim), int(rope_cols), cos_t.data_ptr(),
@@ -233,8 +271,14 @@ def ensure_gemm_workspace(device, nbytes: int = 256 << 20) -> None:
     _lib.call("cb_gemm_set_workspace", buf.data_ptr(), buf.numel() * 4)
 
 
+_GEMM_PATH = 0
+
+
 def set_gemm_path(path: int) -> None:
+    """0: automatic, 1: SIMT engine only (f32 GEMMs then stay f32 SIMT), 2: tcgen05 only."""
+    global _GEMM_PATH
     _lib.call("cb_gemm_set_path", int(path))
+    _GEMM_PATH = int(path)
 
 
 _ATTN_PATH = 0

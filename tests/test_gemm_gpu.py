@@ -56,10 +56,41 @@ def test_gemm_simt_f32(cuda, M, N, K, ta, tb):
 
     a, b = _operands(M, N, K, ta, tb, torch.float32, cuda)
     out = torch.empty(M, N, device=cuda, dtype=torch.float32)
-    ops.gemm(a, b, out, trans_a=ta, trans_b=tb)
+    ops.set_gemm_path(1)  # the SIMT engine itself (large f32 GEMMs otherwise take the BF16x6 path)
+    try:
+        ops.gemm(a, b, out, trans_a=ta, trans_b=tb)
+    finally:
+        ops.set_gemm_path(0)
     ref = _ref(a.double(), b.double(), ta, tb).float()
     rel = (out - ref).norm() / ref.norm()
     assert rel < 1e-6, f"rel err {rel}"
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 512, 256), (264, 520, 200), (1024, 768, 2048), (512, 256, 4096)])
+@pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False)])
+def test_gemm_f32_bf16x6_on_tcgen05(cuda, M, N, K, ta, tb):
+    """f32 GEMMs of the parity mode on the tcgen05 engine: six bf16 products of the operands'
+    three-term splits accumulated in f32 (the BF16x6 FP32 emulation) agree with an fp64 GEMM to
+    fp32 accuracy, alpha / accumulate / residual included, and with the SIMT f32 engine."""
+    from paper_2507_05411_b200 import ops
+
+    a, b = _operands(M, N, K, ta, tb, torch.float32, cuda)
+    g = torch.Generator(device="cpu").manual_seed(K)
+    res = torch.randn(M, N, generator=g).to(cuda)
+    out0 = torch.randn(M, N, generator=g).to(cuda)
+    out = out0.clone()
+    ops.gemm(a, b, out, trans_a=ta, trans_b=tb, alpha=0.5, accumulate=True, residual=res)
+    torch.cuda.synchronize()
+    ref = 0.5 * _ref(a.double(), b.double(), ta, tb) + out0.double() + res.double()
+    assert ((out.double() - ref).norm() / ref.norm()).item() < 1e-6
+    simt = out0.clone()
+    ops.set_gemm_path(1)
+    try:
+        ops.gemm(a, b, simt, trans_a=ta, trans_b=tb, alpha=0.5, accumulate=True, residual=res)
+    finally:
+        ops.set_gemm_path(0)
+    torch.cuda.synchronize()
+    assert ((out - simt).norm() / simt.norm()).item() < 2e-6
 
 
 def test_gemm_epilogues(cuda):
