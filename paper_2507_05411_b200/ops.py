@@ -145,11 +145,24 @@ def _split3(x: torch.Tensor):
     return parts
 
 
+# K per pass: the tensor core's f32 accumulation inside one GEMM loses ~2^-24 per K=16 step
+# (measured: ~1e-5 relative at K = 4096), so K is cut into 256-long chunks whose results are
+# added in the epilogue's round-to-nearest f32 adds
+_BF16X6_KCHUNK = 256
+
+
 def _gemm_bf16x6(a, b, out, trans_a, trans_b, alpha, accumulate, residual):
     sa, sb = _split3(a), _split3(b)
-    for n, (i, j) in enumerate(_BF16X6_TERMS):
-        gemm(sa[i], sb[j], out, trans_a=trans_a, trans_b=trans_b, alpha=alpha,
-             accumulate=accumulate if n == 0 else True, residual=residual if n == 0 else None)
+    K = a.shape[0] if trans_a else a.shape[1]
+    n = 0
+    for k0 in range(0, K, _BF16X6_KCHUNK):
+        k1 = min(K, k0 + _BF16X6_KCHUNK)
+        for i, j in _BF16X6_TERMS:
+            ai = sa[i][k0:k1] if trans_a else sa[i][:, k0:k1]
+            bj = sb[j][:, k0:k1] if trans_b else sb[j][k0:k1]
+            gemm(ai, bj, out, trans_a=trans_a, trans_b=trans_b, alpha=alpha,
+                 accumulate=accumulate if n == 0 else True, residual=residual if n == 0 else None)
+            n += 1
     return out
 
 
