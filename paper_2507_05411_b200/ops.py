@@ -146,9 +146,9 @@ def _split3(x: torch.Tensor):
 
 
 # K per pass: the tensor core's f32 accumulation inside one GEMM loses ~2^-24 per K=16 step
-# (measured: ~1e-5 relative at K = 4096), so K is cut into 256-long chunks whose results are
+# (measured: ~1e-5 relative at K = 4096, ~1e-6 at 256), so K is cut into 128-long chunks whose results are
 # added in the epilogue's round-to-nearest f32 adds
-_BF16X6_KCHUNK = 256
+_BF16X6_KCHUNK = 128
 
 
 def _gemm_bf16x6(a, b, out, trans_a, trans_b, alpha, accumulate, residual):
