@@ -79,10 +79,15 @@ def test_gemm_f32_bf16x6_on_tcgen05(cuda, M, N, K, ta, tb):
     res = torch.randn(M, N, generator=g).to(cuda)
     out0 = torch.randn(M, N, generator=g).to(cuda)
     out = out0.clone()
-    ops.gemm(a, b, out, trans_a=ta, trans_b=tb, alpha=0.5, accumulate=True, residual=res)
+    ops.set_f32_tc(True)
+    try:
+        ops.gemm(a, b, out, trans_a=ta, trans_b=tb, alpha=0.5, accumulate=True, residual=res)
+    finally:
+        ops.set_f32_tc(False)
     torch.cuda.synchronize()
     ref = 0.5 * _ref(a.double(), b.double(), ta, tb) + out0.double() + res.double()
-    assert ((out.double() - ref).norm() / ref.norm()).item() < 1e-6
+    # fp32-level: ~1e-7 per 128-long K chunk, ~sqrt(passes) * 2^-24 from the epilogue adds
+    assert ((out.double() - ref).norm() / ref.norm()).item() < 2e-6
     simt = out0.clone()
     ops.set_gemm_path(1)
     try:

@@ -217,8 +217,19 @@ def test_fast_path_step_bf16(cuda, hd):
     run_parity(_mid(hd), "bf16", 4, 256, 2e-2)
 
 
+@pytest.fixture(params=[False, True], ids=["simt_gemm", "tcgen05_bf16x6"])
+def f32_tc(request):
+    """The f32 parity mode's GEMMs on the SIMT engine, or on the tcgen05 engine as six bf16
+    products of three-term operand splits (ops.set_f32_tc)."""
+    from paper_2507_05411_b200 import ops
+
+    ops.set_f32_tc(request.param)
+    yield request.param
+    ops.set_f32_tc(False)
+
+
 @pytest.mark.parametrize("hd", [64, 128])
-def test_fast_path_shape_f32(cuda, hd):
+def test_fast_path_shape_f32(cuda, hd, f32_tc):
     run_parity(_mid(hd), "f32", 2, 128, 1e-5)
 
 
@@ -232,7 +243,7 @@ def test_fast_path_moe_bf16(cuda):
     run_parity(_mid(128, "MoE"), "bf16", 4, 128, 2e-2)
 
 
-def test_moe_f32_unforced_routing_t256(cuda):
+def test_moe_f32_unforced_routing_t256(cuda, f32_tc):
     """f32 MoE at T=256 with the GPU's OWN routing: the top-2 expert choices of every token equal
     the f64 oracle's bit for bit (reference route_tokens, layers.py:432-443: stable argsort,
     ties -> lowest id), and every tensor is held to the f32 contract."""
@@ -256,7 +267,9 @@ def _gqa(hd: int, heads: int, kv_heads: int, layers: int = 2):
 
 @pytest.mark.parametrize("hd,heads,kv", [(64, 4, 1), (64, 8, 2), (128, 4, 1), (128, 4, 2), (128, 8, 2)])
 @pytest.mark.parametrize("precision", ["f32", "bf16"])
-def test_gqa_engine_step(cuda, hd, heads, kv, precision):
+def test_gqa_engine_step(cuda, hd, heads, kv, precision, f32_tc):
+    if f32_tc and precision == "bf16":
+        pytest.skip("the f32 GEMM switch does not apply to bf16")
     """N1: the GQA kind through TrainEngine against the oracle (which repeats each kv head over
     its group of query heads, oracle/decoder_oracle.py attention)."""
     T = 128 if precision == "f32" else 256
