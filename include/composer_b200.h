@@ -166,6 +166,13 @@ CB_API int cb_sum_parts(int nparts, int64_t n, const void* parts, void* out, flo
 CB_API int cb_split_bf16x3(int64_t rows, int cols, const float* src, int64_t ld, void* d1, void* d2, void* d3,
                            void* stream);
 
+/* Stream memory operations for cross-GPU ordering without a kernel (FSDP barriers,
+ * CB_FSDP_MEMOP_BARRIER): cb_stream_signal writes `epoch` to each of n 32-bit slots (peers'
+ * signal slots through the symmetric-memory mapping; a memory barrier first orders the stream's
+ * earlier writes); cb_stream_wait blocks the stream until each slot is >= epoch. */
+CB_API int cb_stream_signal(void* const* slots, int n, uint32_t epoch, void* stream);
+CB_API int cb_stream_wait(void* const* slots, int n, uint32_t epoch, void* stream);
+
 /* ---------------------------------------------------------------------------------
  * Attention (layers.py:282-348), unmasked, flash-style (P never stored).  q/k/v/o
  * rows are tokens (b*T + t), head h at columns [h*hd, (h+1)*hd).  lse/delta are f32

@@ -86,3 +86,52 @@ extern "C" const char* cb_last_error(void) { return cb::g_last_error; }
 extern "C" int cb_abi_version(void) { return 1; }
 // Number of kernels this library has launched in this process (all threads).
 extern "C" long long cb_launch_count(void) { return cb::g_launches.load(std::memory_order_relaxed); }
+
+// ---------------------------------------------------------------- stream memory operations
+// Cross-GPU ordering without a kernel: the FSDP collectives' barriers as stream memory
+// operations executed by the GPU front end (no SM spins while a peer is late).  A rank posts
+// an epoch into each peer's signal slot (cuStreamWriteValue32 through the peer mapping of
+// symmetric memory, after a memory barrier that makes its earlier writes visible) and waits
+// until its own slots reach the epoch (cuStreamWaitValue32, GEQ).
+namespace cb {
+typedef CUresult (*PFN_streamValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PFN_streamValue32 g_write32 = nullptr, g_wait32 = nullptr;
+static std::once_flag g_memop_once;
+
+static int memops() {
+  std::call_once(g_memop_once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_write32 = reinterpret_cast<PFN_streamValue32>(p);
+    p = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_wait32 = reinterpret_cast<PFN_streamValue32>(p);
+  });
+  if (!g_write32 || !g_wait32) return fail(CB_ERR_UNSUPPORTED, "stream memory operations unavailable from the driver");
+  return CB_OK;
+}
+}  // namespace cb
+
+using namespace cb;
+
+extern "C" int cb_stream_signal(void* const* slots, int n, uint32_t epoch, void* stream) {
+  if (int s = memops()) return s;
+  for (int i = 0; i < n; ++i) {
+    // default flags: a memory barrier orders the stream's earlier writes before the value
+    CUresult r = g_write32((CUstream)stream, (CUdeviceptr)slots[i], epoch, 0);
+    if (r != CUDA_SUCCESS) return fail(CB_ERR_CUDA, "cuStreamWriteValue32 failed: %d", (int)r);
+  }
+  return CB_OK;
+}
+
+extern "C" int cb_stream_wait(void* const* slots, int n, uint32_t epoch, void* stream) {
+  if (int s = memops()) return s;
+  for (int i = 0; i < n; ++i) {
+    CUresult r = g_wait32((CUstream)stream, (CUdeviceptr)slots[i], epoch, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) return fail(CB_ERR_CUDA, "cuStreamWaitValue32 failed: %d", (int)r);
+  }
+  return CB_OK;
+}

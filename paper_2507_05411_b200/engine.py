@@ -393,6 +393,8 @@ class TrainEngine:
                 if self._ce_reduce and not (self._grad_ring and rec["ringed"]):
                     rec["gsymm"] = _symm_mem().rendezvous(rec["grad"], group)
             self._gring_symm = [_symm_mem().rendezvous(g, group) for g in self._gring] if self._ce_reduce else []
+            if os.environ.get("CB_FSDP_MEMOP_BARRIER", "0") == "1":
+                self._memop_barrier = _MemopBarrier(self, group)
             if self._ce_reduce:  # the peers' slices of one bucket's gradient, read before the sum
                 big = max(r["shard"] for b, r in zip(self.buckets, self.bufs) if not b.replicated)
                 self._rs_stage = torch.empty((N - 1) * big, device=dev, dtype=torch.float32)
@@ -402,6 +404,17 @@ class TrainEngine:
             for e in b.entries:
                 _tree_set(self.state, e.path, e.name, _view(rec["work"], e))
                 _tree_set(self.grads, e.path, e.name, _view(rec["grad"], e))
+
+    def _barrier(self, h) -> None:
+        """A cross-rank barrier on the current (comm) stream: torch symmetric memory's barrier
+        kernel on handle h (bounded by CB_SYMM_BARRIER_TIMEOUT_MS), or — CB_FSDP_MEMOP_BARRIER=1 —
+        stream memory operations on the engine's own signal slots (cb_stream_signal / _wait: the
+        GPU front end waits, no SM spins while a peer is late; no timeout)."""
+        mb = getattr(self, "_memop_barrier", None)
+        if mb is not None:
+            mb()
+        else:
+            h.barrier(channel=0, timeout_ms=_BARRIER_TIMEOUT_MS)
 
     def _refresh_work(self, i: int) -> None:
         """This rank's slice of bucket i's working copy <- its f32 master shard."""
@@ -864,7 +877,7 @@ class FSDPProvider(ParamProvider):
                 # * no barrier after the reads: a rank's next AdamW of this bucket waits for the
                 #   same reduce-scatter barrier, which every reader passes only after its reads.
                 if barrier:
-                    h.barrier(channel=0, timeout_ms=_BARRIER_TIMEOUT_MS)
+                    self.e._barrier(h)
                 for k in range(1, N):
                     p = (r + k) % N
                     if slot is not None:
@@ -902,7 +915,7 @@ class FSDPProvider(ParamProvider):
                 # has read this rank's slices before they are cleared for the next use
                 grad, stage = rec["grad"], self.e._rs_stage
                 hn = self.e._gring[0].numel() if ring else rec["total"]  # size of the mapped buffer
-                h.barrier(channel=0, timeout_ms=_BARRIER_TIMEOUT_MS)
+                self.e._barrier(h)
                 parts, j = [], 0
                 for q in range(N):
                     if q == r:
@@ -912,7 +925,7 @@ class FSDPProvider(ParamProvider):
                         slot.copy_(h.get_buffer(q, (hn,), torch.float32)[r * s:(r + 1) * s])
                         parts.append(slot)
                         j += 1
-                h.barrier(channel=0, timeout_ms=_BARRIER_TIMEOUT_MS)
+                self.e._barrier(h)
                 if self.update:  # the in-order sum fused into AdamW (no summed-gradient round trip)
                     self.e._adamw_bucket(i, parts=parts, scale=1.0 / N)
                     fused = True
@@ -1009,6 +1022,35 @@ class LocalUpdateProvider(ParamProvider):
         fin = torch.cuda.Event()
         fin.record(self.side)
         self.compute.wait_event(fin)
+
+
+class _MemopBarrier:
+    """Barrier of all ranks from stream memory operations: the engine's int32 signal slots in
+    symmetric memory (slot q on rank p = the last epoch rank q posted to p); every call posts
+    the next epoch to its slot on each peer and waits for each peer's post on its own slots.
+    All ranks issue barriers in the same program order on their comm streams, so epochs match."""
+
+    def __init__(self, eng, group):
+        import ctypes
+
+        N, r = eng.d.world, eng.d.rank
+        self.buf = _symm_mem().empty(N, dtype=torch.int32, device=eng.device).zero_()
+        self.h = _symm_mem().rendezvous(self.buf, group)
+        peers = [p for p in range(N) if p != r]
+        self.views = [self.h.get_buffer(p, (N,), torch.int32) for p in peers]
+        self.remote = (ctypes.c_void_p * len(peers))(*[v[r:r + 1].data_ptr() for v in self.views])
+        self.local = (ctypes.c_void_p * len(peers))(*[self.buf[p:p + 1].data_ptr() for p in peers])
+        self.n = len(peers)
+        self.epoch = 0
+        torch.cuda.synchronize(eng.device)
+        eng.d.dist.barrier(group=group)  # every rank's slots are zero before the first post
+
+    def __call__(self) -> None:
+        import ctypes
+
+        self.epoch += 1
+        _lib.call("cb_stream_signal", ctypes.addressof(self.remote), self.n, self.epoch, ops.stream_ptr())
+        _lib.call("cb_stream_wait", ctypes.addressof(self.local), self.n, self.epoch, ops.stream_ptr())
 
 
 # symmetric-memory barriers time out (the kernel traps) instead of spinning forever when a
