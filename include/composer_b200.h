@@ -55,6 +55,9 @@ CB_API int cb_gemm_set_path(int path);
    tiles); 2 = cluster pairs sharing the B tile via TMA multicast; 3 = CTA pair; 0 = one CTA
    per 128-row tile. */
 CB_API int cb_gemm_set_multicast(int mode);
+/* Raster group height of the persistent GEMMs' tile order (tile rows that share each N step;
+ * default 16; A/B of the L2 reuse pattern, no effect on results). */
+CB_API int cb_gemm_set_raster(int group_m);
 /* The CTA-pair GEMM's epilogues move their rows through a per-warp shared-memory stage so
  * global accesses are coalesced.  Bit mask: 1 bf16 outputs, 2 gated-activation backward;
  * 1 = both (default); 0 = per-lane row stores everywhere (A/B and tests). */

@@ -49,6 +49,7 @@ SIGNATURES: dict[str, list] = {
     "cb_memset_zero": [_P, _L, _P],
     "cb_sum_parts": [_I, _L, _P, _P, _F, _P],
     "cb_split_bf16x3": [_L, _I, _P, _L, _P, _P, _P, _P],
+    "cb_gemm_set_raster": [_I],
     "cb_stream_signal": [_P, _I, ctypes.c_uint32, _P],
     "cb_stream_wait": [_P, _I, ctypes.c_uint32, _P],
     "cb_attention_fwd": [_I, _I, _I, _I, _I, _I, _P, _L, _P, _L, _P, _L, _P, _L, _P, _P, _F, _P],

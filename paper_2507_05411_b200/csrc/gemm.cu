@@ -77,6 +77,8 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle atom of bf16 along K
 constexpr int kThreads = 256;
 constexpr int kGroupM = 16;  // raster: 16 M-tiles share each N column step (L2 reuse)
+// raster group height actually used (cb_gemm_set_raster; A/B of the L2 reuse pattern)
+__constant__ int g_group_m = kGroupM;
 
 template <int BN>
 struct Cfg {
@@ -112,11 +114,12 @@ struct Args {
 constexpr int kMaxGroups = 64;
 
 __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
-  const int per_group = kGroupM * tiles_n;
+  const int gmx = g_group_m;
+  const int per_group = gmx * tiles_n;
   const int g = t / per_group;
   const int r = t - g * per_group;
-  const int gm0 = g * kGroupM;
-  const int gsz = min(kGroupM, tiles_m - gm0);
+  const int gm0 = g * gmx;
+  const int gsz = min(gmx, tiles_m - gm0);
   tm = gm0 + r % gsz;
   tn = r / gsz;
 }
@@ -1415,6 +1418,13 @@ extern "C" int cb_gemm_set_staged_epilogue(int enable) {
   const int v = enable == 1 ? 3 : enable < 0 ? 0 : enable & 3;
   if (cudaMemcpyToSymbol(tc::g_epi_staged, &v, sizeof(v)) != cudaSuccess)
     return fail(CB_ERR_CUDA, "cb_gemm_set_staged_epilogue: cudaMemcpyToSymbol failed");
+  return CB_OK;
+}
+
+extern "C" int cb_gemm_set_raster(int group_m) {
+  if (group_m < 1 || group_m > 1024) return fail(CB_ERR_ARG, "gemm raster group must be 1..1024 tile rows");
+  if (cudaMemcpyToSymbol(tc::g_group_m, &group_m, sizeof(group_m)) != cudaSuccess)
+    return fail(CB_ERR_CUDA, "cb_gemm_set_raster: cudaMemcpyToSymbol failed");
   return CB_OK;
 }
 

@@ -276,6 +276,8 @@ class TrainEngine:
         # epilogue staging mask of the CTA-pair GEMM (cb_gemm_set_staged_epilogue; A/B runs)
         if "CB_GEMM_STAGED_EPILOGUE" in os.environ and self.device.type == "cuda":
             _lib.call("cb_gemm_set_staged_epilogue", int(os.environ["CB_GEMM_STAGED_EPILOGUE"]))
+        if "CB_GEMM_RASTER" in os.environ and self.device.type == "cuda":  # raster A/B
+            _lib.call("cb_gemm_set_raster", int(os.environ["CB_GEMM_RASTER"]))
         self.options = {"precision": self.precision, "validate_ids": False,
                         "fuse_glu": os.environ.get("CB_FUSE_GLU", "1") != "0"}
         # weight-gradient GEMMs on their own stream (layers._wgrad), at most CB_WGRAD_STREAM of
