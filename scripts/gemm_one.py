@@ -8,7 +8,10 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from paper_2507_05411_b200 import ops  # noqa: E402
+from paper_2507_05411_b200 import _lib, ops  # noqa: E402
+
+if "CB_GEMM_RASTER" in os.environ:
+    _lib.call("cb_gemm_set_raster", int(os.environ["CB_GEMM_RASTER"]))
 
 # (M, N, K, out dtype): x[tokens, d] @ W[d, n] as the 7B / 1B steps issue them
 SHAPES = {"qkv7b": (8192, 12288, 4096, torch.bfloat16), "o7b": (8192, 4096, 4096, torch.float32),
