@@ -220,3 +220,24 @@ def test_memory_plan_matches_reference_aot_analyze(name, devices, policy):
     assert mine["optimizer_bytes"] == rep.optimizer_bytes
     assert mine["saved_activation_bytes"] == rep.saved_activation_bytes
     assert mine["per_device_bytes"] == rep.per_device_bytes
+
+
+def test_remat_decisions_match_reference():
+    """remat.resolve_policy / decide_tag (what every behavior's remat_decision applies) give the
+    reference's decisions (mesh.py:204-252) for its named policies and mixed exact / glob maps."""
+    _reference_package()
+    from composer.mesh import decide_tag as ref_decide
+    from composer.mesh import resolve_policy as ref_resolve
+
+    from paper_2507_05411_b200.remat import decide_tag, resolve_policy
+
+    tags = ["q_proj", "k_proj", "v_proj", "context", "o_proj", "hidden", "output", "router_logits", "expert_hidden",
+            "expert_output", "logits", "unknown_tag"]
+    policies = ["save_all", "recompute_all", "offload_dots", "save_qkvo_flash",
+                {"hidden": "recompute", "*_proj": "offload"}, {"*": "save", "expert_*": "recompute", "expert_output": "save"},
+                {"?_proj": "recompute", "*": "offload"}]
+    for pol in policies:
+        mine, ref = resolve_policy(pol), ref_resolve(pol)
+        assert mine == ref
+        for t in tags:
+            assert decide_tag(t, mine) == ref_decide(t, ref), (pol, t)
