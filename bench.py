@@ -163,27 +163,63 @@ def reference_sample(config: str) -> dict:
             "sample": out["sample"] + f"; numpy/OpenBLAS on {threads} host threads"}
 
 
+def workload_config(args, world: int) -> dict:
+    """The workload description both arms print (the reference arm runs on this arm's config)."""
+    from paper_2507_05411_b200 import BENCH_CONFIGS, instantiate
+    from paper_2507_05411_b200.module import iter_param_specs
+
+    cfg = BENCH_CONFIGS[args.config](batch=args.batch, seq=args.seq)
+    params = sum(int(np.prod(shape)) for _, _, _, shape in iter_param_specs(instantiate(cfg)))
+    out = {"workload": args.config, "global_batch": world * args.batch, "per_gpu_batch": args.batch,
+           "seq_len": args.seq, "d_model": cfg.get("model.dim"), "layers": len(cfg.get("model.decoder.transformer.layer")),
+           "vocab": cfg.get("model.vocab_size"), "params": params, "parallelism": f"fsdp{world}", "remat": args.remat,
+           "l2": ("tiny parity-size config: L2-resident, not flushed (not a bench line)" if args.config == "tiny"
+                  else "inputs larger than L2 (bf16 params + activations >> 126 MB)")}
+    if args.config == "moe":
+        out["moe_routing"] = args.moe_routing
+    return out
+
+
 def run_reference(args) -> None:
+    """The reference arm: rank 0 alone times the reference's own CPU step on this arm's config.
+    A step is one bounded sample of the workload — one reference TransformerLayer invoke at the
+    config's layer shape (oracle/ref_step.py; 8.5 s for the 7B layer on 16 threads) — so the
+    K timed steps run K samples; the head (embedding, norm, tied head, loss) is timed once with
+    the warm-up sample (numpy has no warm-up state: one warm-up sample is run, not W)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2507_05411_b200 import BENCH_CONFIGS
+    from oracle import ref_step
 
-    # a 7B sample is ~40 s of CPU work (1B ~14 s): no warm-up (numpy has nothing to warm)
-    # and at most 3 timed samples, so any --steps / --warmup the driver passes ends within a
-    # few minutes
-    vals = [reference_sample(args.config) for _ in range(max(1, min(args.steps, 3)))]
-    v = statistics.median(x["value"] for x in vals)
-    cfg = BENCH_CONFIGS[args.config](batch=args.batch, seq=args.seq)
+    world = args.gpus
+    if not ref_step.available():  # the oracle port, as round 1 (each step one port sample)
+        vals = [cpu_sample(args.config) for _ in range(max(1, min(args.steps, 3)))]
+        v = statistics.median(x["value"] for x in vals)
+        base = {**vals[-1], "value": v, "samples_timed": len(vals)}
+        base["sample"] = "oracle/_ref missing: " + base["sample"]
+        ms = 1000.0 * args.batch * args.seq / v
+    else:
+        r = ref_step.ReferenceStep(args.config)
+        t_head = r.head()
+        r.layer()  # the one warm-up sample
+        layers = [r.layer() for _ in range(max(1, args.steps))]
+        t_layer = statistics.median(layers)
+        v = r.rate(t_head, t_layer)
+        ms = 1000.0 * statistics.mean(layers)  # what one timed step (sample) took
+        threads = os.cpu_count() or 1
+        base = {"value": v, "unit": "tokens/s", "cores": threads, "kind": "reference",
+                "sample": r.describe(t_head, t_layer) + f"; median of {len(layers)} layer samples; numpy/OpenBLAS "
+                          f"on {threads} host threads",
+                "samples_timed": len(layers), "warmup_samples_run": 1}
     line = {
         "impl": "reference",
         "metric": "train tokens/sec and MFU per B200, decoder step",
         "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * args.batch * args.seq / v, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "global_batch": args.batch * args.gpus, "seq_len": args.seq,
-                   "d_model": cfg.get("model.dim"), "layers": len(cfg.get("model.decoder.transformer.layer"))},
-        "cpu_baseline": {**vals[-1], "value": v, "samples_timed": len(vals)},
+        "ms_per_step": ms, "ms_per_step_note": "wall time of one timed sample (a reference TransformerLayer invoke); "
+                                               "value extrapolates the sample to the configured depth",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, world),
+        "cpu_baseline": base,
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -420,15 +456,12 @@ def main():
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
         "data": "synthetic (reference synthetic_batch token stream; reference init_state weights)",
-        "config": {"workload": args.config, "global_batch": world * B, "per_gpu_batch": B, "seq_len": T,
-                   "d_model": eng.cfg.get("model.dim"), "layers": len(eng.cfg.get("model.decoder.transformer.layer")),
-                   "vocab": V, "params": eng.param_count(), "parallelism": f"fsdp{world}", "remat": args.remat,
-                   **({"moe_routing": args.moe_routing} if args.config == "moe" else {}),
-                   "collectives": ("none" if world == 1 else
-                                   ("all-gather " + ("copy-engine/symm-mem" if eng._ce_gather else "nccl")
-                                    + ", reduce-scatter " + ("copy-engine/symm-mem + cb_sum_parts"
-                                                             if eng._ce_reduce else "nccl"))),
-                   "l2": "inputs larger than L2 (bf16 params + activations >> 126 MB)"},
+        "config": workload_config(args, world),
+        "setup": {"collectives": ("none" if world == 1 else
+                                  ("all-gather " + ("copy-engine/symm-mem" if eng._ce_gather else "nccl")
+                                   + ", reduce-scatter " + ("copy-engine/symm-mem, sum fused into AdamW"
+                                                            if eng._ce_reduce else "nccl"))),
+                  "zero3": {"resharded_params": eng._reshard, "gradient_ring": eng._grad_ring}},
         "mfu": value * fpt / (world * NOMINAL_BF16_PFLOPS),
         "model_flops_per_token": fpt,
         "loss": final_loss,

@@ -89,33 +89,60 @@ def time_invoke(c, module, state, key, *args) -> float:
     return time.perf_counter() - t0
 
 
-def reference_sample(config: str) -> dict:
-    """One bounded sample of the reference's CPU step at `config`: returns tokens/s and the
-    description (see module docstring)."""
-    c = load()
-    sh = SHAPES[config]
-    B, T = sh["batch"], sh["seq"]
-    root = c.root_key(0)
-    key = c.child_key(root, "step", 0)
-    from composer.experiments import synthetic_batch
+class ReferenceStep:
+    """The reference's CPU step at `config`, prepared once (modules, init_state, inputs) so
+    samples time only `invoke`: `layer()` times one TransformerLayer invoke, `head()` the 0-layer
+    Trainer invoke, and `rate(t_head, t_layer)` extrapolates tokens/s for the full depth."""
 
-    toks = synthetic_batch(0, 0, B, T, sh["vocab"])
-    if config == "tiny":  # the full reference step
-        m = c.instantiate(_trainer_cfg(c, sh, sh["layers"]))
-        st = c.init_state(m, root)
-        t = time_invoke(c, m, st, key, toks)
-        return {"value": B * T / t, "t_step_s": t, "sample": f"reference invoke: full tiny step, {B}x{T} tokens, {t:.2f} s"}
-    lm = c.instantiate(_layer_cfg(c, sh))
-    lst = c.init_state(lm, root)
-    x = np.random.default_rng(0).standard_normal((B, T, sh["dim"]))
-    t_layer = time_invoke(c, lm, lst, key, x)
-    hm = c.instantiate(_trainer_cfg(c, sh, 0))
-    hst = c.init_state(hm, root)
-    t_head = time_invoke(c, hm, hst, key, toks)
-    t_step = t_head + sh["layers"] * t_layer
-    kind = "MoE" if sh.get("experts") else ("MHA (the reference has no GQA)" if config == "70b_layer" else "MHA")
-    return {"value": B * T / t_step, "t_step_s": t_step, "t_layer_s": t_layer, "t_head_s": t_head,
-            "sample": (f"reference composer.invoke (forward + loss; the reference has no backward/optimizer): one "
-                       f"{config} TransformerLayer ({kind}, d={sh['dim']}) at batch {B}, seq {T}: {t_layer:.2f} s; "
-                       f"0-layer Trainer (embedding, output norm, tied head V={sh['vocab']}, loss): {t_head:.2f} s; "
-                       f"step = head + {sh['layers']} x layer = {t_step:.1f} s per {B * T} tokens")}
+    def __init__(self, config: str):
+        c = self.c = load()
+        sh = self.sh = SHAPES[config]
+        self.config = config
+        B, T = sh["batch"], sh["seq"]
+        root = c.root_key(0)
+        self.key = c.child_key(root, "step", 0)
+        from composer.experiments import synthetic_batch
+
+        self.toks = synthetic_batch(0, 0, B, T, sh["vocab"])
+        if config == "tiny":  # the full reference step
+            self.full = c.instantiate(_trainer_cfg(c, sh, sh["layers"]))
+            self.full_state = c.init_state(self.full, root)
+            return
+        self.lm = c.instantiate(_layer_cfg(c, sh))
+        self.lst = c.init_state(self.lm, root)
+        self.x = np.random.default_rng(0).standard_normal((B, T, sh["dim"]))
+        self.hm = c.instantiate(_trainer_cfg(c, sh, 0))
+        self.hst = c.init_state(self.hm, root)
+
+    def layer(self) -> float:
+        if self.config == "tiny":
+            return time_invoke(self.c, self.full, self.full_state, self.key, self.toks)
+        return time_invoke(self.c, self.lm, self.lst, self.key, self.x)
+
+    def head(self) -> float:
+        return 0.0 if self.config == "tiny" else time_invoke(self.c, self.hm, self.hst, self.key, self.toks)
+
+    def rate(self, t_head: float, t_layer: float) -> float:
+        sh = self.sh
+        t_step = t_layer if self.config == "tiny" else t_head + sh["layers"] * t_layer
+        return sh["batch"] * sh["seq"] / t_step
+
+    def describe(self, t_head: float, t_layer: float) -> str:
+        sh = self.sh
+        if self.config == "tiny":
+            return f"reference invoke: full tiny step, {sh['batch']}x{sh['seq']} tokens, {t_layer:.2f} s"
+        kind = "MoE" if sh.get("experts") else ("MHA (the reference has no GQA)" if self.config == "70b_layer" else "MHA")
+        t_step = t_head + sh["layers"] * t_layer
+        return (f"reference composer.invoke (forward + loss; the reference has no backward/optimizer): one "
+                f"{self.config} TransformerLayer ({kind}, d={sh['dim']}) at batch {sh['batch']}, seq {sh['seq']}: "
+                f"{t_layer:.2f} s; 0-layer Trainer (embedding, output norm, tied head V={sh['vocab']}, loss): "
+                f"{t_head:.2f} s; step = head + {sh['layers']} x layer = {t_step:.1f} s per {sh['batch'] * sh['seq']} "
+                f"tokens")
+
+
+def reference_sample(config: str) -> dict:
+    """One bounded sample of the reference's CPU step at `config` (a head and a layer invoke)."""
+    r = ReferenceStep(config)
+    t_head, t_layer = r.head(), r.layer()
+    return {"value": r.rate(t_head, t_layer), "t_layer_s": t_layer, "t_head_s": t_head,
+            "sample": r.describe(t_head, t_layer)}
