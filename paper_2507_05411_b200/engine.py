@@ -339,6 +339,15 @@ class TrainEngine:
         self._pos = {i: p for p, i in enumerate(self.layer_order)}
         self._reshard = N > 1 and bool(self.layer_order) and os.environ.get("CB_FSDP_RESHARD", "1") == "1"
         self._grad_ring = N > 1 and bool(self.layer_order) and os.environ.get("CB_FSDP_GRAD_RING", "1") == "1"
+        # one GPU: the same two-slot gradient ring when the layers' full f32 gradients would be
+        # large (> CB_GRAD_RING_MIN_GB, default 8: the 7B step's 26 GB, not the 1B step's 3.5 GB) —
+        # each layer's AdamW runs right after its backward, so only two layers' gradients are ever
+        # live; CB_GRAD_RING=0 / 1 forces it off / on
+        if N == 1 and self.layer_order and self.device.type == "cuda":
+            gbytes = 4 * sum(_align(self.buckets[i].numel) for i in self.layer_order)
+            flag = os.environ.get("CB_GRAD_RING", "auto")
+            self._grad_ring = flag == "1" or (flag == "auto" and gbytes > float(
+                os.environ.get("CB_GRAD_RING_MIN_GB", "8")) * 1e9)
         ring_total = max([_align(self.buckets[i].numel, ALIGN * N) for i in self.layer_order] or [0])
 
         def symm_or_zeros(n, dtype, symm):
@@ -373,7 +382,9 @@ class TrainEngine:
                     work = symm_or_zeros(total, self.work_dtype, self._ce_gather)
                     wshard = work[r0:r0 + shard]
                 if N == 1:
-                    grad = grad_shard = torch.zeros(total, device=dev, dtype=torch.float32)
+                    grad = (self._gring[self._pos[i] % 2][:total] if (self._grad_ring and ringed)
+                            else torch.zeros(total, device=dev, dtype=torch.float32))
+                    grad_shard = grad
                 else:
                     grad = (self._gring[self._pos[i] % 2][:total] if (self._grad_ring and ringed)
                             else symm_or_zeros(total, torch.float32, self._ce_reduce))
@@ -604,8 +615,9 @@ class TrainEngine:
         if self._grad_shards_stale:
             from .errors import ComposerError
 
-            raise ComposerError("step() fused the gradient reduce-scatter into AdamW without storing the gradient "
-                                "shards: set engine.keep_grad_shards = True before the step to read gradients")
+            raise ComposerError("step() did not keep the gradients (FSDP: the reduce-scatter's sum is fused into "
+                                "AdamW — set engine.keep_grad_shards = True; one GPU with the gradient ring — set "
+                                "CB_GRAD_RING=0) before the step to read them")
         return self._export("grad")
 
     # -------------------------------------------------------------------- step
@@ -666,6 +678,12 @@ class TrainEngine:
         if self.d.world > 1:
             provider = FSDPProvider(self, update=update)
         else:
+            if self._grad_ring and not update:
+                from .errors import ComposerError
+
+                raise ComposerError("this engine keeps single-GPU gradients in a two-layer ring (the model's "
+                                    "gradients exceed CB_GRAD_RING_MIN_GB): compute_grads(update=False) cannot keep "
+                                    "every layer's gradient; set CB_GRAD_RING=0 before building the engine")
             provider = LocalUpdateProvider(self) if update else None
         if provider is not None and self.device.type == "cuda":
             # the gradient buffers are cleared on a side stream while the forward runs (nothing
@@ -998,18 +1016,32 @@ class LocalUpdateProvider(ParamProvider):
         self.side = eng._opt_stream
         self.index = {b.name: i for i, b in enumerate(eng.buckets)}
         self.done: set[int] = set()
+        self.gslot_free: dict[int, torch.cuda.Event] = {}  # gradient ring slot -> cleared event
 
     def _update(self, i: int) -> None:
         ready = torch.cuda.Event()
         ready.record(self.compute)
+        rec = self.e.bufs[i]
         with torch.cuda.stream(self.side):
             self.side.wait_event(ready)
             self.e._join_wgrad(self.side)
             self.e._adamw_bucket(i)
+            if self.e._grad_ring and rec.get("ringed"):
+                # the gradient slot is consumed: clear it for the layer two positions further on
+                ops.zero_(rec["grad"])
+                ev = torch.cuda.Event()
+                ev.record(self.side)
+                self.gslot_free[self.e._pos[i] % 2] = ev
+                self.e._grad_shards_stale = True  # the layer gradients are gone after the step
         self.done.add(i)
 
     def before_backward(self, path: str) -> None:
         _wait_grads_zeroed(self)
+        i = self.index.get(path)
+        if self.e._grad_ring and i is not None and i in self.e._pos:
+            ev = self.gslot_free.pop(self.e._pos[i] % 2, None)
+            if ev is not None:
+                self.compute.wait_event(ev)
 
     def after_backward(self, path: str) -> None:
         i = self.index.get(path)

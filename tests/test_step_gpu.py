@@ -533,3 +533,28 @@ def test_full_size_step_properties(cuda, name, B):
     losses = runs[0][0]
     assert abs(losses[0] - math.log(32000)) < 1.5
     assert losses[2] < losses[0]
+
+
+def test_single_gpu_grad_ring_is_exact(cuda, monkeypatch):
+    """The one-GPU two-slot gradient ring (CB_GRAD_RING; automatic above CB_GRAD_RING_MIN_GB, e.g.
+    the 7B step) gives bit-identical losses and parameters to full per-layer gradient buffers,
+    with less engine state; reading gradients after such a step raises instead of returning
+    stale values."""
+    from paper_2507_05411_b200 import TrainEngine, set_dtype_policy, synthetic_batch
+    from paper_2507_05411_b200.errors import ComposerError
+
+    cfg = set_dtype_policy(_mid(128), "bf16")
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("CB_GRAD_RING", flag)
+        eng = TrainEngine(cfg, device="cuda:0")
+        assert eng._grad_ring == (flag == "1")
+        losses = [float(eng.step(synthetic_batch(0, s, 4, 256, 512)["tokens"])[0].item()) for s in range(3)]
+        outs.append((losses, dict(_leaves(eng.state_numpy())), eng.state_bytes()))
+        if flag == "1":
+            with pytest.raises(ComposerError):
+                eng.grads_numpy()
+    assert outs[0][0] == outs[1][0]
+    for k in outs[0][1]:
+        assert np.array_equal(outs[0][1][k], outs[1][1][k]), k
+    assert outs[1][2] < outs[0][2]
