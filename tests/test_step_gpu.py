@@ -543,7 +543,12 @@ def test_single_gpu_grad_ring_is_exact(cuda, monkeypatch):
     from paper_2507_05411_b200 import TrainEngine, set_dtype_policy, synthetic_batch
     from paper_2507_05411_b200.errors import ComposerError
 
-    cfg = set_dtype_policy(_mid(128), "bf16")
+    from paper_2507_05411_b200.experiments import transformer_trainer
+
+    cfg = transformer_trainer(256, 5, ("linear", "silu"), pos_kind="RoPE", heads=2, vocab=512)
+    for i in range(5):  # five layers: both ring slots are reused within a step
+        cfg = cfg.set(f"model.decoder.transformer.layer[{i}].feed_forward.hidden_dim", 768)
+    cfg = set_dtype_policy(cfg, "bf16")
     outs = []
     for flag in ("0", "1"):
         monkeypatch.setenv("CB_GRAD_RING", flag)
