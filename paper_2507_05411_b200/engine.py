@@ -406,7 +406,7 @@ class TrainEngine:
                 if self._ce_reduce and not (self._grad_ring and rec["ringed"]):
                     rec["gsymm"] = _symm_mem().rendezvous(rec["grad"], group)
             self._gring_symm = [_symm_mem().rendezvous(g, group) for g in self._gring] if self._ce_reduce else []
-            if os.environ.get("CB_FSDP_MEMOP_BARRIER", "0") == "1":
+            if os.environ.get("CB_FSDP_MEMOP_BARRIER", "1") == "1":
                 self._memop_barrier = _MemopBarrier(self, group)
             if self._ce_reduce:  # the peers' slices of one bucket's gradient, read before the sum
                 big = max(r["shard"] for b, r in zip(self.buckets, self.bufs) if not b.replicated)
@@ -419,10 +419,12 @@ class TrainEngine:
                 _tree_set(self.grads, e.path, e.name, _view(rec["grad"], e))
 
     def _barrier(self, h) -> None:
-        """A cross-rank barrier on the current (comm) stream: torch symmetric memory's barrier
-        kernel on handle h (bounded by CB_SYMM_BARRIER_TIMEOUT_MS), or — CB_FSDP_MEMOP_BARRIER=1 —
-        stream memory operations on the engine's own signal slots (cb_stream_signal / _wait: the
-        GPU front end waits, no SM spins while a peer is late; no timeout)."""
+        """A cross-rank barrier on the current (comm) stream: by default stream memory operations
+        on the engine's own signal slots (cb_stream_signal / _wait: the GPU front end waits, no
+        SM spins while a peer is late — 70B layer at 4 GPUs +1.5%, profiles/r02_memop_barrier_4gpu;
+        a dead peer is caught by the NCCL watchdog on the step's loss all-reduce), or —
+        CB_FSDP_MEMOP_BARRIER=0 — torch symmetric memory's barrier kernel on handle h, bounded by
+        CB_SYMM_BARRIER_TIMEOUT_MS."""
         mb = getattr(self, "_memop_barrier", None)
         if mb is not None:
             mb()
