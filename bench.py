@@ -10,7 +10,8 @@ steps, then K steps bracketed by barrier + synchronize, CUDA events on the compu
 stream, max over ranks.  Rank 0 prints one JSON line.
 
 The default workload is BASELINE.json configs[2], the Llama2-7B-shaped step (the
-north-star config; 2 x 4096 tokens per GPU); --config 1b selects configs[1].
+north-star config; 3 x 4096 tokens per GPU — the largest per-GPU batch that fits in HBM
+with the one-GPU gradient ring); --config 1b selects configs[1].
 
 --impl reference times the REFERENCE's own CPU step — ``composer.invoke`` (forward +
 loss; the reference has no backward or optimizer) of the unmodified reference installed
@@ -318,7 +319,7 @@ def main():
                          "save_qkvo_flash for 70b_layer (BASELINE configs[4]: FSDP + rematerialisation; the "
                          "policy of the reference's gpu-H100 mesh rule, experiments.py:49), none otherwise")
     args = ap.parse_args()
-    defaults = {"tiny": (8, 256), "1b": (8, 4096), "7b": (2, 4096), "moe": (4, 4096), "70b_layer": (2, 4096)}
+    defaults = {"tiny": (8, 256), "1b": (8, 4096), "7b": (3, 4096), "moe": (4, 4096), "70b_layer": (2, 4096)}
     if args.remat is None:
         args.remat = "save_qkvo_flash" if args.config == "70b_layer" else "save_all"
     args.batch = args.batch or defaults[args.config][0]
