@@ -267,17 +267,20 @@ def cupti_attribution(fn) -> tuple[dict, float]:
     out: dict = {}
     if not ks:
         return out, 0.0
-    names: dict = {}
+    names: dict = {}  # per kind: kernel name -> busy ms (the top three are reported)
     for e in prof.events():
-        if e.device_type == torch.autograd.DeviceType.CUDA and "cb::" not in e.name:
-            names[e.name[:60]] = names.get(e.name[:60], 0.0) + e.time_range.elapsed_us() / 1e3
+        if (e.device_type == torch.autograd.DeviceType.CUDA and e.time_range.elapsed_us() > 0
+                and "memcpy" not in e.name.lower() and "memset" not in e.name.lower()):
+            nm = names.setdefault(kernel_kind(e.name), {})
+            key = e.name.split("(")[0][:60]
+            nm[key] = nm.get(key, 0.0) + e.time_range.elapsed_us() / 1e3
     for s0, e0, k in ks:
         d = out.setdefault(k, {"launches": 0, "busy_ms": 0.0, "attributed_ms": 0.0})
         d["launches"] += 1
         d["busy_ms"] += (e0 - s0) / 1e3
     for k in out:
-        if k.startswith("foreign"):
-            out[k]["top"] = sorted(names.items(), key=lambda kv: -kv[1])[:3]
+        if len(names.get(k, {})) > 1:
+            out[k]["top"] = sorted(names[k].items(), key=lambda kv: -kv[1])[:3]
     # sweep line over the start/end points of every kernel (all streams)
     pts = sorted({t for s0, e0, _ in ks for t in (s0, e0)})
     idx = {t: i for i, t in enumerate(pts)}
@@ -436,7 +439,7 @@ def main():
     if os.path.exists(tpath):
         with open(tpath) as fh:
             tj = json.load(fh)
-        if tj.get("workload") == args.config:
+        if tj.get("workload") == args.config and tj.get("per_gpu_batch", args.batch) == args.batch:
             traffic = tj.get("bytes_per_launch")
     flops_by_kind = {"gemm": gflops, "attn_fwd": tally.get("attn_fwd", {}).get("flops", 0),
                      "attn_bwd": tally.get("attn_bwd", {}).get("flops", 0)}

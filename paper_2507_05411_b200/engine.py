@@ -340,14 +340,15 @@ class TrainEngine:
         self._reshard = N > 1 and bool(self.layer_order) and os.environ.get("CB_FSDP_RESHARD", "1") == "1"
         self._grad_ring = N > 1 and bool(self.layer_order) and os.environ.get("CB_FSDP_GRAD_RING", "1") == "1"
         # one GPU: the same two-slot gradient ring when the layers' full f32 gradients would be
-        # large (> CB_GRAD_RING_MIN_GB, default 8: the 7B step's 26 GB, not the 1B step's 3.5 GB) —
+        # large (> CB_GRAD_RING_MIN_GB, default 16: the 7B step's 26 GB; not the 1B, MoE or 70B-layer
+        # steps' 3.5 / 9.7 / 14.7 GB, which fit comfortably and run ~1% faster without it) —
         # each layer's AdamW runs right after its backward, so only two layers' gradients are ever
         # live; CB_GRAD_RING=0 / 1 forces it off / on
         if N == 1 and self.layer_order and self.device.type == "cuda":
             gbytes = 4 * sum(_align(self.buckets[i].numel) for i in self.layer_order)
             flag = os.environ.get("CB_GRAD_RING", "auto")
             self._grad_ring = flag == "1" or (flag == "auto" and gbytes > float(
-                os.environ.get("CB_GRAD_RING_MIN_GB", "8")) * 1e9)
+                os.environ.get("CB_GRAD_RING_MIN_GB", "16")) * 1e9)
         ring_total = max([_align(self.buckets[i].numel, ALIGN * N) for i in self.layer_order] or [0])
 
         def symm_or_zeros(n, dtype, symm):

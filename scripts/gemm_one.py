@@ -1,6 +1,6 @@
 """One step-shaped CTA-pair GEMM launch (after a warm-up launch), for ncu --set full captures.
 
-    python scripts/gemm_one.py [qkv7b|o7b|up7b|down7b|qkv1b]
+    python scripts/gemm_one.py [qkv7b|qkv7b3|o7b|up7b|down7b|qkv1b]   (qkv7b3: 3 sequences per GPU)
 """
 import os
 import sys
@@ -14,7 +14,7 @@ if "CB_GEMM_RASTER" in os.environ:
     _lib.call("cb_gemm_set_raster", int(os.environ["CB_GEMM_RASTER"]))
 
 # (M, N, K, out dtype): x[tokens, d] @ W[d, n] as the 7B / 1B steps issue them
-SHAPES = {"qkv7b": (8192, 12288, 4096, torch.bfloat16), "o7b": (8192, 4096, 4096, torch.float32),
+SHAPES = {"qkv7b": (8192, 12288, 4096, torch.bfloat16), "qkv7b3": (12288, 12288, 4096, torch.bfloat16), "o7b": (8192, 4096, 4096, torch.float32),
           "up7b": (8192, 22016, 4096, torch.bfloat16), "down7b": (8192, 4096, 11008, torch.float32),
           "qkv1b": (32768, 6144, 2048, torch.bfloat16)}
 M, N, K, odt = SHAPES[sys.argv[1] if len(sys.argv) > 1 else "qkv7b"]
