@@ -127,12 +127,14 @@ CB_API int cb_col_reduce(int nparts, int dim, const float* partial, float* out, 
 
 /* ---------------------------------------------------------------------------------
  * Embedding (layers.py:199-229): out[i] = table[ids[i]].  The backward is
- * deterministic: cb_sort_ids groups positions by id (stable counting sort, one CTA;
- * offsets int32[vocab+1], cursor int32[vocab] scratch, perm int32[n]), then
+ * deterministic: cb_sort_ids groups positions by id (stable counting sort: one CTA, or
+ * per-1024-position chunks for vocab <= 64 such as the MoE expert ids; offsets
+ * int32[vocab+1], cursor int32[cb_sort_ids_scratch(n, vocab)] scratch, perm int32[n]), then
  * cb_embedding_bwd adds each id's rows, in position order, into dtable (f32).
  * ------------------------------------------------------------------------------- */
 CB_API int cb_embedding_fwd(int64_t n, int dim, const int64_t* ids, const void* table, int64_t ldt, int t_dtype,
                             void* out, int64_t ldo, int o_dtype, void* stream);
+CB_API int64_t cb_sort_ids_scratch(int n, int vocab);
 CB_API int cb_sort_ids(int n, int vocab, const int64_t* ids, int* offsets, int* cursor, int* perm, void* stream);
 CB_API int cb_embedding_bwd(int vocab, int dim, const int* offsets, const int* perm, const void* dout, int64_t ldo,
                             int g_dtype, float* dtable, int64_t ldt, void* stream);
@@ -256,7 +258,7 @@ CB_API int cb_moe_combine_bwd(int64_t n, int dim, int top_k, const int32_t* inv,
 CB_API int cb_moe_router_bwd(int64_t n, int experts, int top_k, const float* probs, const int32_t* idx,
                              const float* weights, const float* dweights, float* dlogits, void* stream);
 /* Router backward products (x @ router, layers.py:516): drouter (+)= x^T dlogits (fixed token
- * blocks + ordered reduction; workspace ceil(n/512)*dim*experts floats) and
+ * blocks + ordered reduction; workspace ceil(n/128)*dim*experts floats) and
  * dx += dlogits router^T. */
 CB_API int cb_moe_router_bwd_gemms(int64_t n, int dim, int experts, const void* x, int64_t ldx, int x_dtype,
                                    const float* dlogits, const float* router, float* drouter, float* dx,

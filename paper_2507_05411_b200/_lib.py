@@ -28,7 +28,8 @@ _L = ctypes.c_int64
 _F = ctypes.c_float
 _D = ctypes.c_double
 
-# name -> argtypes; the return type is always int (status) except where noted.
+# name -> argtypes; the return type is always int (status) except those in RESTYPES.
+RESTYPES = {"cb_sort_ids_scratch": ctypes.c_int64}
 SIGNATURES: dict[str, list] = {
     "cb_abi_version": [],
     "cb_gemm_set_path": [_I],
@@ -40,6 +41,7 @@ SIGNATURES: dict[str, list] = {
     "cb_rmsnorm_bwd": [_I, _I, _P, _L, _I, _P, _P, _P, _L, _I, _P, _L, _P, _L, _P, _L, _P, _P, _P],
     "cb_col_reduce": [_I, _I, _P, _P, _I, _P],
     "cb_embedding_fwd": [_L, _I, _P, _P, _L, _I, _P, _L, _I, _P],
+    "cb_sort_ids_scratch": [_I, _I],
     "cb_sort_ids": [_I, _I, _P, _P, _P, _P, _P],
     "cb_embedding_bwd": [_I, _I, _P, _P, _P, _L, _I, _P, _L, _P],
     "cb_rope": [_L, _I, _I, _I, _P, _L, _I, _P, _P, _I, _P],
@@ -110,7 +112,7 @@ def load():
         except AttributeError:
             raise MissingExtensionError(f"kernel library lacks symbol {name}") from None
         fn.argtypes = argtypes
-        fn.restype = ctypes.c_int
+        fn.restype = RESTYPES.get(name, ctypes.c_int)
     lib.cb_last_error.argtypes = []
     lib.cb_last_error.restype = ctypes.c_char_p
     lib.cb_launch_count.argtypes = []

@@ -72,6 +72,91 @@ __global__ void __launch_bounds__(1024) sort_ids_k(int n, int vocab, const int64
   }
 }
 
+// Multi-CTA stable counting sort for few keys (vocab <= kSortSmallVocab: the MoE dispatch's
+// expert ids), the single-CTA kernel's warp-serial scatter being the MoE forward's longest
+// serial step.  Chunks of 1024 positions, one per CTA:
+//   sort_count_k:   cnt[chunk][v] = occurrences of v in the chunk
+//   sort_scatter_k: base[v] = (positions of every key < v) + (occurrences of v in earlier
+//                   chunks); within the chunk a position's rank among equal ids is its rank
+//                   in its warp (__match_any_sync) plus the counts of that id in earlier warps.
+// The output (offsets, perm) is identical to sort_ids_k's: positions grouped by id, in
+// position order within an id.
+constexpr int kSortChunk = 1024;
+constexpr int kSortSmallVocab = 64;
+
+__global__ void __launch_bounds__(kSortChunk) sort_count_k(int n, int vocab, const int64_t* __restrict__ ids,
+                                                          int* __restrict__ cnt) {
+  __shared__ int c[kSortSmallVocab];
+  if (threadIdx.x < vocab) c[threadIdx.x] = 0;
+  __syncthreads();
+  const int pos = blockIdx.x * kSortChunk + threadIdx.x;
+  if (pos < n) atomicAdd(&c[(int)ids[pos]], 1);
+  __syncthreads();
+  if (threadIdx.x < vocab) cnt[blockIdx.x * vocab + threadIdx.x] = c[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kSortChunk) sort_scatter_k(int n, int vocab, const int64_t* __restrict__ ids,
+                                                            const int* __restrict__ cnt, int* __restrict__ offsets,
+                                                            int* __restrict__ perm) {
+  __shared__ int base[kSortSmallVocab];
+  __shared__ int wcnt[kSortChunk / 32][kSortSmallVocab];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int chunks = gridDim.x, me = blockIdx.x;
+  for (int i = tid; i < (kSortChunk / 32) * kSortSmallVocab; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+  if (warp == 0) {
+    // lane v (and v + 32): total and earlier-chunk counts of key v, then an exclusive scan of
+    // the totals across keys
+    int tot[2] = {0, 0}, pre[2] = {0, 0};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int v = lane + 32 * h;
+      if (v < vocab)
+        for (int b = 0; b < chunks; ++b) {
+          const int x = cnt[b * vocab + v];
+          tot[h] += x;
+          pre[h] += b < me ? x : 0;
+        }
+    }
+    int run = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      int inc = tot[h];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const int v = lane + 32 * h;
+      const int excl = run + inc - tot[h];
+      if (v < vocab) {
+        base[v] = excl + pre[h];
+        if (me == 0) offsets[v] = excl;
+      }
+      run += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (me == 0 && lane == 0) offsets[vocab] = n;
+  }
+  __syncthreads();
+  const int pos = me * kSortChunk + tid;
+  const bool valid = pos < n;
+  const int id = valid ? (int)ids[pos] : -1 - lane;
+  const unsigned peers = __match_any_sync(0xffffffffu, id);
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int rank = __popc(peers & lt_mask);
+  if (valid && (peers & lt_mask) == 0) wcnt[warp][id] = __popc(peers);
+  __syncthreads();
+  if (tid < vocab) {  // exclusive prefix of this key's per-warp counts
+    int run = 0;
+    for (int w = 0; w < kSortChunk / 32; ++w) {
+      const int c = wcnt[w][tid];
+      wcnt[w][tid] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  if (valid) perm[base[id] + wcnt[warp][id] + rank] = pos;
+}
+
 template <typename TG>
 __global__ void __launch_bounds__(256) embed_bwd_k(int dim, const int* __restrict__ offsets, const int* __restrict__ perm,
                                                    const TG* __restrict__ dout, int64_t ldo, float* __restrict__ dtable,
@@ -107,10 +192,23 @@ extern "C" int cb_embedding_fwd(int64_t n, int dim, const int64_t* ids, const vo
   return check_launch("embedding_fwd");
 }
 
-// offsets: int32[vocab+1] (out), cursor: int32[vocab] (scratch), perm: int32[n] (out)
+// scratch (the `cursor` argument of cb_sort_ids) in int32 elements
+extern "C" int64_t cb_sort_ids_scratch(int n, int vocab) {
+  if (vocab <= kSortSmallVocab && n > kSortChunk) return (int64_t)((n + kSortChunk - 1) / kSortChunk) * vocab;
+  return vocab;
+}
+
+// offsets: int32[vocab+1] (out), cursor: int32[cb_sort_ids_scratch(n, vocab)] (scratch), perm: int32[n] (out)
 extern "C" int cb_sort_ids(int n, int vocab, const int64_t* ids, int* offsets, int* cursor, int* perm, void* stream) {
   if (n < 0 || vocab <= 0) return fail(CB_ERR_SHAPE, "sort_ids: bad extents");
-  sort_ids_k<<<1, 1024, 0, (cudaStream_t)stream>>>(n, vocab, ids, offsets, cursor, perm);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (vocab <= kSortSmallVocab && n > kSortChunk) {
+    const int chunks = (n + kSortChunk - 1) / kSortChunk;
+    sort_count_k<<<chunks, kSortChunk, 0, st>>>(n, vocab, ids, cursor);
+    sort_scatter_k<<<chunks, kSortChunk, 0, st>>>(n, vocab, ids, cursor, offsets, perm);
+    return check_launch("sort_ids");
+  }
+  sort_ids_k<<<1, 1024, 0, st>>>(n, vocab, ids, offsets, cursor, perm);
   return check_launch("sort_ids");
 }
 

@@ -74,94 +74,129 @@ __global__ void __launch_bounds__(128) moe_route_k(int64_t n, int d, int E, int 
   }
 }
 
-// E <= 8 experts, bf16 x: the router matrix staged once per CTA in shared memory (f32,
-// zero-padded to 8 experts, split into two [d] float4 planes), one warp per token with every lane accumulating all experts over
-// its columns (stride 32), lanes summed by a fixed-order f64 butterfly; softmax / stable
-// top-k / renormalisation as moe_route_k.  Grid-stride over tokens.
+// E <= 8 experts, bf16 x, d % 256 == 0: the router matrix widened to f64 once per CTA into
+// shared memory (128 KB at d = 2048), one warp per group of kRouteTok tokens.  Lane l owns
+// columns 256 i + 8 l + u (u < 8): a 16-byte load brings 8 of a token's bf16 values, and the
+// router is stored as [i][u][expert pair][lane] (16 B per entry) so every shared-memory read of
+// a warp is 512 contiguous bytes (conflict-free).  Each lane accumulates a fixed-order f64 fma
+// chain over its columns, then a fixed-order f64 butterfly across lanes — the same logits on
+// every run; top-k bit-exactness against the reference holds as for any f64 summation order
+// (ties resolved on identical logits).  The one-token-per-warp f32-staged form spent 9 f32->f64
+// conversions and a 2-byte load per 8 DFMA.  Softmax / stable top-k / renormalisation as
+// moe_route_k.  Grid-stride over token groups, one CTA per SM.
 constexpr int kRouteWarps = 8;
+constexpr int kRouteTok = 4;
+
+__device__ __forceinline__ void route_finish(double (&acc)[8], int64_t t, int E, int k, int lane,
+                                             int32_t* __restrict__ idx, float* __restrict__ w,
+                                             float* __restrict__ probs) {
+  double logit = -INFINITY;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+    if (lane == e && e < E) logit = acc[e];
+  }
+  double mx = logit;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const double ex = lane < E ? exp(logit - mx) : 0.0;
+  double sum = ex;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const double pr = ex / sum;
+  if (lane < E) probs[t * E + lane] = (float)pr;
+  // stable top-k: repeatedly take (max prob, lowest id); k <= 8
+  bool taken = lane >= E;
+  double picked[8];
+  int pid[8];
+  double psum = 0.0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (j >= k) break;
+    double bv = taken ? -1.0 : pr;
+    int bi = taken ? 1 << 30 : lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == bi) taken = true;
+    picked[j] = bv;
+    pid[j] = bi;
+    psum += bv;
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j >= k) break;
+      idx[t * k + j] = pid[j];
+      w[t * k + j] = (float)(picked[j] / psum);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kRouteWarps * 32) moe_route8_k(int64_t n, int d, int E, int k,
                                                                   const __nv_bfloat16* __restrict__ x, int64_t ldx,
                                                                   const float* __restrict__ router,
                                                                   int32_t* __restrict__ idx, float* __restrict__ w,
                                                                   float* __restrict__ probs) {
-  extern __shared__ float4 rsm4[];  // [2][d] float4: experts 0-3 of column c, then experts 4-7
-  float* rsm = reinterpret_cast<float*>(rsm4);
-  for (int i = threadIdx.x; i < d * 8; i += blockDim.x) {
-    const int c = i >> 3, e = i & 7;
-    rsm[(e >> 2) * d * 4 + c * 4 + (e & 3)] = e < E ? router[(int64_t)c * E + e] : 0.f;
+  extern __shared__ double2 rsm2[];  // [d/256][8 u][4 expert pairs][32 lanes]
+  for (int i = threadIdx.x; i < d * 4; i += blockDim.x) {
+    const int c = i >> 2, ep = i & 3;  // column, expert pair
+    const int blk = c >> 8, l = (c >> 3) & 31, u = c & 7;
+    const int e0 = 2 * ep, e1 = e0 + 1;
+    rsm2[((blk * 8 + u) * 4 + ep) * 32 + l] =
+        make_double2(e0 < E ? (double)router[(int64_t)c * E + e0] : 0.0, e1 < E ? (double)router[(int64_t)c * E + e1] : 0.0);
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int64_t t = (int64_t)blockIdx.x * kRouteWarps + warp; t < n; t += (int64_t)gridDim.x * kRouteWarps) {
-    const __nv_bfloat16* xr = x + t * ldx;
-    double acc[8];
+  const int nblk = d >> 8;
+  const int64_t groups = (n + kRouteTok - 1) / kRouteTok;
+  for (int64_t g = (int64_t)blockIdx.x * kRouteWarps + warp; g < groups; g += (int64_t)gridDim.x * kRouteWarps) {
+    const int64_t t0 = g * kRouteTok;
+    const int nt = (int)min((int64_t)kRouteTok, n - t0);
+    const uint4* xr[kRouteTok];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
-    // lane l takes columns l, l + 32, ... so a warp reads 32 consecutive router rows (1 KB,
-    // bank-conflict free) per step
-#pragma unroll 4
-    for (int c = lane; c < d; c += 32) {
-      {
-        const float4 r0 = rsm4[c], r1 = rsm4[d + c];
-        const double xd = (double)__bfloat162float(xr[c]);
-        acc[0] = fma(xd, (double)r0.x, acc[0]);
-        acc[1] = fma(xd, (double)r0.y, acc[1]);
-        acc[2] = fma(xd, (double)r0.z, acc[2]);
-        acc[3] = fma(xd, (double)r0.w, acc[3]);
-        acc[4] = fma(xd, (double)r1.x, acc[4]);
-        acc[5] = fma(xd, (double)r1.y, acc[5]);
-        acc[6] = fma(xd, (double)r1.z, acc[6]);
-        acc[7] = fma(xd, (double)r1.w, acc[7]);
-      }
-    }
-    double logit = -INFINITY;
+    for (int q = 0; q < kRouteTok; ++q)  // tail: re-read token t0
+      xr[q] = reinterpret_cast<const uint4*>(x + (t0 + (q < nt ? q : 0)) * ldx) + lane;
+    double acc[kRouteTok][8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
+    for (int q = 0; q < kRouteTok; ++q)
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
-      if (lane == e && e < E) logit = acc[e];
-    }
-    double mx = logit;
+      for (int e = 0; e < 8; ++e) acc[q][e] = 0.0;
+#pragma unroll 1
+    for (int blk = 0; blk < nblk; ++blk) {
+      uint4 xv[kRouteTok];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const double ex = lane < E ? exp(logit - mx) : 0.0;
-    double sum = ex;
+      for (int q = 0; q < kRouteTok; ++q) xv[q] = xr[q][blk * 32];
+      const double2* rb = rsm2 + blk * 8 * 4 * 32 + lane;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    const double pr = ex / sum;
-    if (lane < E) probs[t * E + lane] = (float)pr;
-    // stable top-k: repeatedly take (max prob, lowest id); k <= 8
-    bool taken = lane >= E;
-    double picked[8];
-    int pid[8];
-    double psum = 0.0;
+      for (int u = 0; u < 8; ++u) {
+        const double2 r01 = rb[(u * 4 + 0) * 32], r23 = rb[(u * 4 + 1) * 32];
+        const double2 r45 = rb[(u * 4 + 2) * 32], r67 = rb[(u * 4 + 3) * 32];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (j >= k) break;
-      double bv = taken ? -1.0 : pr;
-      int bi = taken ? 1 << 30 : lane;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > bv || (ov == bv && oi < bi)) {
-          bv = ov;
-          bi = oi;
+        for (int q = 0; q < kRouteTok; ++q) {
+          const uint32_t word = (&xv[q].x)[u >> 1];
+          const double xd = (double)__uint_as_float((u & 1) ? (word & 0xffff0000u) : (word << 16));
+          acc[q][0] = fma(xd, r01.x, acc[q][0]);
+          acc[q][1] = fma(xd, r01.y, acc[q][1]);
+          acc[q][2] = fma(xd, r23.x, acc[q][2]);
+          acc[q][3] = fma(xd, r23.y, acc[q][3]);
+          acc[q][4] = fma(xd, r45.x, acc[q][4]);
+          acc[q][5] = fma(xd, r45.y, acc[q][5]);
+          acc[q][6] = fma(xd, r67.x, acc[q][6]);
+          acc[q][7] = fma(xd, r67.y, acc[q][7]);
         }
       }
-      if (lane == bi) taken = true;
-      picked[j] = bv;
-      pid[j] = bi;
-      psum += bv;
     }
-    if (lane == 0) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (j >= k) break;
-        idx[t * k + j] = pid[j];
-        w[t * k + j] = (float)(picked[j] / psum);
-      }
-    }
+    for (int q = 0; q < kRouteTok; ++q)
+      if (q < nt) route_finish(acc[q], t0 + q, E, k, lane, idx, w, probs);
   }
 }
 
@@ -283,6 +318,11 @@ __device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* dst, float4
   *reinterpret_cast<uint2*>(dst) = u;
 }
 
+// One warp per token; the token's dout row is read once for all k slots (k <= 8), in chunks of
+// kCbChunk float4 per lane whose loads are all issued before their use (the one-float4-at-a-
+// time loop was load-latency bound at ~3.4 TB/s).  Each dw[t,j] still accumulates over the
+// columns in ascending order, as in the scalar kernel.
+constexpr int kCbChunk = 8;
 template <typename TG>
 __global__ void __launch_bounds__(256) combine_bwd_v4_k(int64_t n, int d4, int k, const int32_t* __restrict__ inv,
                                                         const float* __restrict__ w, const float* __restrict__ y,
@@ -291,18 +331,45 @@ __global__ void __launch_bounds__(256) combine_bwd_v4_k(int64_t n, int d4, int k
   const int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= n) return;
   const int lane = threadIdx.x & 31;
-  for (int j = 0; j < k; ++j) {
-    const int64_t r = inv[t * k + j];
-    const float wj = w[t * k + j];
-    float dot = 0.f;
-    for (int c = lane; c < d4; c += 32) {
-      const float4 g = reinterpret_cast<const float4*>(dout + t * lddo)[c];
-      const float4 v = reinterpret_cast<const float4*>(y + r * ldy)[c];
-      store4<TG>(dy + r * lddy + 4 * c, make_float4(wj * g.x, wj * g.y, wj * g.z, wj * g.w));
-      dot = fmaf(g.x, v.x, fmaf(g.y, v.y, fmaf(g.z, v.z, fmaf(g.w, v.w, dot))));
+  const float4* g4 = reinterpret_cast<const float4*>(dout + t * lddo);
+  float dot[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) dot[j] = 0.f;
+  for (int c0 = 0; c0 < d4; c0 += 32 * kCbChunk) {
+    float4 g[kCbChunk];
+#pragma unroll
+    for (int i = 0; i < kCbChunk; ++i) {
+      const int c = c0 + i * 32 + lane;
+      g[i] = c < d4 ? g4[c] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    dot = warp_sum(dot);
-    if (lane == 0) dw[t * k + j] = dot;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j >= k) break;
+      const int64_t r = inv[t * k + j];
+      const float wj = w[t * k + j];
+      const float4* y4 = reinterpret_cast<const float4*>(y + r * ldy);
+      float4 v[kCbChunk];
+#pragma unroll
+      for (int i = 0; i < kCbChunk; ++i) {
+        const int c = c0 + i * 32 + lane;
+        v[i] = c < d4 ? y4[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int i = 0; i < kCbChunk; ++i) {
+        const int c = c0 + i * 32 + lane;
+        if (c < d4) {
+          store4<TG>(dy + r * lddy + 4 * c, make_float4(wj * g[i].x, wj * g[i].y, wj * g[i].z, wj * g[i].w));
+          dot[j] = fmaf(g[i].x, v[i].x, fmaf(g[i].y, v[i].y, fmaf(g[i].z, v[i].z, fmaf(g[i].w, v[i].w, dot[j]))));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (j < k) {
+      const float s = warp_sum(dot[j]);
+      if (lane == 0) dw[t * k + j] = s;
+    }
   }
 }
 
@@ -357,16 +424,16 @@ extern "C" int cb_moe_route(int64_t n, int dim, int experts, int top_k, const vo
   if (top_k < 1 || top_k > experts) return fail(CB_ERR_SHAPE, "top_k=%d must lie in [1, %d]", top_k, experts);
   if (n <= 0) return CB_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t rsm_bytes = (size_t)dim * 8 * sizeof(float);
-  if (x_dtype == CB_DT_BF16 && experts <= 8 && dim % 8 == 0 && ldx % 8 == 0 &&
+  const size_t rsm_bytes = (size_t)dim * 8 * sizeof(double);
+  if (x_dtype == CB_DT_BF16 && experts <= 8 && dim % 256 == 0 && ldx % 8 == 0 &&
       (reinterpret_cast<uintptr_t>(x) & 15) == 0 && rsm_bytes <= 200 * 1024) {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(moe_route8_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr = true;
     }
-    const int64_t need = (n + kRouteWarps - 1) / kRouteWarps;
-    const int blocks8 = (int)std::min<int64_t>(need, 2 * kNumSMs);
+    const int64_t need = (n + kRouteWarps * kRouteTok - 1) / (kRouteWarps * kRouteTok);
+    const int blocks8 = (int)std::min<int64_t>(need, kNumSMs);
     moe_route8_k<<<blocks8, kRouteWarps * 32, rsm_bytes, st>>>(n, dim, experts, top_k, (const __nv_bfloat16*)x, ldx,
                                                                router, idx, weights, probs);
     return check_launch("moe_route8");
@@ -424,7 +491,7 @@ extern "C" int cb_moe_combine_bwd(int64_t n, int dim, int top_k, const int32_t* 
                                   int dy_dtype, float* dweights, void* stream) {
   if (n <= 0) return CB_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  const bool v4 = dim % 4 == 0 && ((ldy | lddo | lddy) & 3) == 0 &&
+  const bool v4 = top_k <= 8 && dim % 4 == 0 && ((ldy | lddo | lddy) & 3) == 0 &&
                   !((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(dout) |
                      reinterpret_cast<uintptr_t>(dy)) & (dy_dtype == CB_DT_F32 ? 15 : 7)) &&
                   !(reinterpret_cast<uintptr_t>(y) & 15) && !(reinterpret_cast<uintptr_t>(dout) & 15);
@@ -527,6 +594,47 @@ __global__ void __launch_bounds__(256) router_dx_k(int64_t n, int d, int E, cons
         if (e < E) s = fmaf(g[e], router[(int64_t)c * E + e], s);
     }
     dx[t * lddx + c] += s;
+  }
+}
+
+// E == 8, d % 4 == 0, 16-byte aligned rows: a thread owns 4 columns (their 32 router values in
+// registers) for a block of tokens, so the router is read once per block instead of once per
+// token and column; each element's sum is the same e-ordered fma chain as router_dx_k.
+constexpr int kRouterDxTok = 64;
+__global__ void __launch_bounds__(256) router_dx_v4_k(int64_t n, int d, const float* __restrict__ dlog,
+                                                      const float* __restrict__ router, float* __restrict__ dx,
+                                                      int64_t lddx) {
+  const int c = (blockIdx.y * 256 + threadIdx.x) * 4;
+  if (c >= d) return;
+  float r[4][8];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float4 a = *reinterpret_cast<const float4*>(router + (int64_t)(c + q) * 8);
+    const float4 b = *reinterpret_cast<const float4*>(router + (int64_t)(c + q) * 8 + 4);
+    r[q][0] = a.x, r[q][1] = a.y, r[q][2] = a.z, r[q][3] = a.w;
+    r[q][4] = b.x, r[q][5] = b.y, r[q][6] = b.z, r[q][7] = b.w;
+  }
+  const int64_t t0 = (int64_t)blockIdx.x * kRouterDxTok, t1 = min(n, t0 + kRouterDxTok);
+#pragma unroll 2
+  for (int64_t t = t0; t < t1; ++t) {
+    const float4 g0 = *reinterpret_cast<const float4*>(dlog + t * 8);
+    const float4 g1 = *reinterpret_cast<const float4*>(dlog + t * 8 + 4);
+    const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    float4* o = reinterpret_cast<float4*>(dx + t * lddx + c);
+    float4 v = *o;
+    float sq[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float acc = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc = fmaf(g[e], r[q][e], acc);
+      sq[q] = acc;
+    }
+    v.x += sq[0];
+    v.y += sq[1];
+    v.z += sq[2];
+    v.w += sq[3];
+    *o = v;
   }
 }
 
@@ -652,14 +760,14 @@ extern "C" int cb_widen_i32(int64_t n, const int32_t* a, int64_t* b, void* strea
 }
 
 // drouter (+)= x^T dlog (deterministic: fixed token blocks + ordered column reduction);
-// dx += dlog router^T.  workspace: ceil(n / 512) * dim * experts floats.
+// dx += dlog router^T.  workspace: ceil(n / 128) * dim * experts floats.
 extern "C" int cb_moe_router_bwd_gemms(int64_t n, int dim, int experts, const void* x, int64_t ldx, int x_dtype,
                                        const float* dlogits, const float* router, float* drouter, float* dx,
                                        int64_t lddx, float* workspace, void* stream) {
   if (experts < 1 || experts > kMaxExperts) return fail(CB_ERR_UNSUPPORTED, "moe: experts must be in [1, %d]", kMaxExperts);
   if (n <= 0) return CB_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  const int tpb = 512;
+  const int tpb = 128;  // tokens per block: 4x the blocks of 512 for load-latency hiding
   const int nblk = (int)((n + tpb - 1) / tpb);
   dim3 grid(nblk, (dim + 255) / 256);
   const bool small = experts <= 8;
@@ -681,7 +789,11 @@ extern "C" int cb_moe_router_bwd_gemms(int64_t n, int dim, int experts, const vo
   if (int s = check_launch("moe_router_wgrad")) return s;
   if (int s = cb_col_reduce(nblk, dim * experts, workspace, drouter, 1, stream)) return s;
   const bool vec = experts == 8 && (reinterpret_cast<uintptr_t>(router) & 15) == 0;
-  if (vec)
+  if (vec && dim % 4 == 0 && lddx % 4 == 0 && !(reinterpret_cast<uintptr_t>(dx) & 15) &&
+      !(reinterpret_cast<uintptr_t>(dlogits) & 15)) {
+    dim3 g2((unsigned)((n + kRouterDxTok - 1) / kRouterDxTok), (unsigned)((dim + 1023) / 1024));
+    router_dx_v4_k<<<g2, 256, 0, st>>>(n, dim, dlogits, router, dx, lddx);
+  } else if (vec)
     router_dx_k<8><<<(int)n, 256, 0, st>>>(n, dim, experts, dlogits, router, dx, lddx);
   else
     router_dx_k<kMaxExperts><<<(int)n, 256, 0, st>>>(n, dim, experts, dlogits, router, dx, lddx);

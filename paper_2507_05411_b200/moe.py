@@ -311,7 +311,7 @@ class MoEBehavior(Behavior):
                   dw.data_ptr(), dlog.data_ptr(), ops.stream_ptr())
         router = L._f32(param("router"))
         x2 = s["x2"]
-        ws = torch.empty(((n + 511) // 512) * d * E, device=dev, dtype=torch.float32)
+        ws = torch.empty(((n + 127) // 128) * d * E, device=dev, dtype=torch.float32)
         _lib.call("cb_moe_router_bwd_gemms", n, d, E, x2.data_ptr(), ops.ld(x2), ops.dt(x2), dlog.data_ptr(),
                   router.data_ptr(), param_grad("router").data_ptr(), dx.data_ptr(), ops.ld(dx), ws.data_ptr(),
                   ops.stream_ptr())

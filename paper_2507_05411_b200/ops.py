@@ -358,7 +358,7 @@ def sort_ids(ids: torch.Tensor, vocab: int):
     flat = ids.reshape(-1)
     n = flat.numel()
     offsets = torch.empty((vocab + 1,), device=ids.device, dtype=torch.int32)
-    cursor = torch.empty((vocab,), device=ids.device, dtype=torch.int32)
+    cursor = torch.empty((int(_lib.load().cb_sort_ids_scratch(n, vocab)),), device=ids.device, dtype=torch.int32)
     perm = torch.empty((max(n, 1),), device=ids.device, dtype=torch.int32)
     _lib.call("cb_sort_ids", n, vocab, flat.data_ptr(), offsets.data_ptr(), cursor.data_ptr(), perm.data_ptr(),
               stream_ptr())

@@ -43,6 +43,15 @@ def test_signature_table_matches_header():
     assert set(_lib.SIGNATURES) | special == declared
 
 
+def test_sort_scratch_sizes():
+    """cb_sort_ids' scratch: one count per key and 1024-position chunk for the multi-CTA
+    small-vocabulary sort (MoE expert ids), else one cursor per key (host-only query)."""
+    lib = _lib.load()
+    assert lib.cb_sort_ids_scratch(32768, 8) == 32 * 8
+    assert lib.cb_sort_ids_scratch(1000, 8) == 8
+    assert lib.cb_sort_ids_scratch(32768, 32000) == 32000
+
+
 def test_status_mapping():
     _lib.load()
     with pytest.raises(ShapeError):

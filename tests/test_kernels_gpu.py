@@ -237,6 +237,108 @@ def test_moe_router_topk_bit_exact(cuda):
     assert np.allclose(w.cpu().numpy(), rw.numpy(), atol=1e-6)
 
 
+@pytest.mark.parametrize("n,vocab", [(1024, 8), (1025, 8), (32768, 8), (50001, 33), (40000, 64), (3000, 500)])
+def test_sort_ids_matches_stable_argsort(cuda, n, vocab):
+    """cb_sort_ids (single CTA, or the chunked multi-CTA sort for <= 64 keys) = numpy's stable
+    argsort: positions grouped by id in position order, offsets = the ids' exclusive counts."""
+    from paper_2507_05411_b200 import ops
+
+    rng = np.random.default_rng(n + vocab)
+    ids = rng.integers(0, vocab, n)
+    ids[: n // 3] = rng.integers(0, 2, n // 3)  # skewed like the init routing
+    off, perm = ops.sort_ids(torch.tensor(ids, device=cuda), vocab)
+    assert np.array_equal(perm.cpu().numpy()[:n], np.argsort(ids, kind="stable"))
+    ref_off = np.concatenate([[0], np.cumsum(np.bincount(ids, minlength=vocab))])
+    assert np.array_equal(off.cpu().numpy(), ref_off)
+
+
+def test_moe_router_bf16_topk_bit_exact(cuda):
+    """The bf16-input router (several tokens per warp, d = 2048 as in the MoE config): the
+    reference's stable top-k on the f64 logits of the same bf16 inputs, ties and a ragged tail
+    of tokens included."""
+    from oracle import decoder_oracle as O
+    from paper_2507_05411_b200 import _lib, ops
+
+    n, d, E, k = 4099, 2048, 8, 2
+    rng = np.random.default_rng(4)
+    xb = torch.tensor(rng.standard_normal((n, d)), dtype=torch.float32).bfloat16()
+    router = rng.standard_normal((d, E)).astype(np.float32) * 0.02
+    router[:, 6] = router[:, 1]  # exact ties between experts 1 and 6
+    xt, rt = xb.to(cuda), torch.tensor(router, device=cuda)
+    idx = torch.empty(n, k, dtype=torch.int32, device=cuda)
+    w = torch.empty(n, k, device=cuda)
+    probs = torch.empty(n, E, device=cuda)
+    _lib.call("cb_moe_route", n, d, E, k, xt.data_ptr(), d, 1, rt.data_ptr(), idx.data_ptr(), w.data_ptr(),
+              probs.data_ptr(), ops.stream_ptr())
+    p64 = torch.softmax(xb.double() @ torch.tensor(router, dtype=torch.float64), -1)
+    ridx, rw, _, _ = O.route_tokens(p64, k)
+    assert np.array_equal(idx.cpu().numpy(), ridx.numpy())
+    assert np.allclose(w.cpu().numpy(), rw.numpy(), atol=1e-6)
+    assert np.allclose(probs.cpu().numpy(), p64.numpy(), atol=1e-6)
+
+
+@pytest.mark.parametrize("k,dy_bf16", [(2, True), (3, False), (1, True)])
+def test_moe_combine_fwd_bwd(cuda, k, dy_bf16):
+    """cb_moe_combine: out[t] = sum_j w[t,j] y[inv[t,j]] (slot order, layers.py:529-531) and its
+    backward dy[inv[t,j]] = w[t,j] dout[t], dw[t,j] = dout[t] . y[inv[t,j]], against fp64 torch
+    on rows scattered through a padded expert layout."""
+    from paper_2507_05411_b200 import _lib, ops
+
+    n, d = 3001, 512
+    cap = n * k + 997  # padded expert layout: more rows than assignments
+    g = torch.Generator().manual_seed(k)
+    inv = torch.randperm(cap, generator=g)[: n * k].to(torch.int32)
+    w = torch.rand(n, k, generator=g)
+    y = torch.randn(cap, d, generator=g)
+    dout = torch.randn(n, d, generator=g)
+    Inv, W, Y, Dout = inv.to(cuda), w.to(cuda), y.to(cuda), dout.to(cuda)
+    out = torch.empty(n, d, device=cuda)
+    _lib.call("cb_moe_combine", n, d, k, Inv.data_ptr(), W.data_ptr(), Y.data_ptr(), d, 0, out.data_ptr(), d, 0,
+              ops.stream_ptr())
+    rows = y.double()[inv.long()].view(n, k, d)
+    ref = (w.double().unsqueeze(-1) * rows).sum(1)
+    assert _rel(out.cpu(), ref) < 1e-6
+    dy = torch.zeros(cap, d, device=cuda, dtype=torch.bfloat16 if dy_bf16 else torch.float32)
+    dw = torch.empty(n, k, device=cuda)
+    _lib.call("cb_moe_combine_bwd", n, d, k, Inv.data_ptr(), W.data_ptr(), Y.data_ptr(), d, Dout.data_ptr(), d,
+              dy.data_ptr(), d, ops.dt(dy), dw.data_ptr(), ops.stream_ptr())
+    ref_dy = torch.zeros(cap, d, dtype=torch.float64)
+    ref_dy[inv.long()] = (w.double().unsqueeze(-1) * dout.double().unsqueeze(1)).reshape(n * k, d)
+    assert _rel(dy.cpu(), ref_dy) < (4e-3 if dy_bf16 else 1e-6)
+    ref_dw = (rows * dout.double().unsqueeze(1)).sum(-1)
+    assert _rel(dw.cpu(), ref_dw) < 1e-5
+
+
+@pytest.mark.parametrize("E,bf16_x", [(8, True), (8, False), (4, True)])
+def test_moe_router_bwd_gemms(cuda, E, bf16_x):
+    """cb_moe_router_bwd_gemms: drouter += x^T dlogits (fixed token blocks, ordered reduction)
+    and dx += dlogits router^T, against fp64 torch; bit-identical on a rerun."""
+    from paper_2507_05411_b200 import _lib, ops
+
+    n, d = 1000, 512
+    g = torch.Generator().manual_seed(E)
+    x = torch.randn(n, d, generator=g)
+    if bf16_x:
+        x = x.bfloat16()
+    dlog = torch.randn(n, E, generator=g)
+    router = torch.randn(d, E, generator=g) * 0.1
+    dx0 = torch.randn(n, d, generator=g)
+    X, Dl, R = x.to(cuda), dlog.to(cuda), router.to(cuda)
+    outs = []
+    for _ in range(2):
+        dr = torch.full((d, E), 0.5, device=cuda)
+        dx = dx0.to(cuda)
+        ws = torch.empty(((n + 127) // 128) * d * E, device=cuda)
+        _lib.call("cb_moe_router_bwd_gemms", n, d, E, X.data_ptr(), d, ops.dt(X), Dl.data_ptr(), R.data_ptr(),
+                  dr.data_ptr(), dx.data_ptr(), d, ws.data_ptr(), ops.stream_ptr())
+        outs.append((dr.cpu(), dx.cpu()))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    ref_dr = 0.5 + x.double().t() @ dlog.double()
+    ref_dx = dx0.double() + dlog.double() @ router.double().t()
+    assert _rel(outs[0][0], ref_dr) < 1e-5
+    assert _rel(outs[0][1], ref_dx) < 1e-6
+
+
 def test_adamw_kernel(cuda):
     from oracle import decoder_oracle as O
     from paper_2507_05411_b200 import ops
