@@ -252,6 +252,12 @@ CB_API int cb_gather_rows(int64_t n, int dim, const int32_t* perm, int div, cons
 /* out[t] (+)= sum_j w[t,j] * y[inv[t*k+j]]  (weights == NULL -> 1), slot order (layers.py:529-531). */
 CB_API int cb_moe_combine(int64_t n, int dim, int top_k, const int32_t* inv, const float* weights, const void* y,
                           int64_t ldy, int y_dtype, float* out, int64_t ldo, int accumulate, void* stream);
+/* out[t] = res[t] + sum_j w[t,j] * y[inv[t*k+j]]: the MoE block output with the pre-norm residual
+ * add of TransformerLayer (layers.py:539-551) fused; f32 y/res/out, 16-byte aligned rows,
+ * dim % 4 == 0 (else CB_ERR_UNSUPPORTED, nothing launched). */
+CB_API int cb_moe_combine_residual(int64_t n, int dim, int top_k, const int32_t* inv, const float* weights,
+                                   const float* y, int64_t ldy, const float* res, int64_t ldr, float* out,
+                                   int64_t ldo, void* stream);
 CB_API int cb_moe_combine_bwd(int64_t n, int dim, int top_k, const int32_t* inv, const float* weights, const float* y,
                               int64_t ldy, const float* dout, int64_t lddo, void* dy, int64_t lddy, int dy_dtype,
                               float* dweights, void* stream);

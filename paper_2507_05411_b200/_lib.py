@@ -76,6 +76,7 @@ SIGNATURES: dict[str, list] = {
     "cb_moe_route": [_L, _I, _I, _I, _P, _L, _I, _P, _P, _P, _P, _P],
     "cb_moe_stats": [_L, _I, _I, _P, _P, _P, _P],
     "cb_gather_rows": [_L, _I, _P, _I, _P, _L, _P, _L, _I, _P],
+    "cb_moe_combine_residual": [_L, _I, _I, _P, _P, _P, _L, _P, _L, _P, _L, _P],
     "cb_moe_combine": [_L, _I, _I, _P, _P, _P, _L, _I, _P, _L, _I, _P],
     "cb_moe_combine_bwd": [_L, _I, _I, _P, _P, _P, _L, _P, _L, _P, _L, _I, _P, _P],
     "cb_moe_router_bwd": [_L, _I, _I, _P, _P, _P, _P, _P, _P],

@@ -303,6 +303,31 @@ __global__ void __launch_bounds__(256) combine_v4_k(int64_t n, int d4, int k, co
   }
 }
 
+// out[t] = res[t] + sum_j w[t,j] * y[inv[t*k+j]]: the MoE block's residual add fused into the
+// combine (one pass over the residual instead of a combine pass plus an add pass); the same
+// bits as combine then add (float addition commutes)
+__global__ void __launch_bounds__(256) combine_res_v4_k(int64_t n, int d4, int k, const int32_t* __restrict__ inv,
+                                                        const float* __restrict__ w, const float* __restrict__ y,
+                                                        int64_t ldy, const float* __restrict__ res, int64_t ldr,
+                                                        float* __restrict__ out, int64_t ldo) {
+  const int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (t >= n) return;
+  const int lane = threadIdx.x & 31;
+  for (int c = lane; c < d4; c += 32) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < k; ++j) {
+      const float wj = w[t * k + j];
+      const float4 v = reinterpret_cast<const float4*>(y + (int64_t)inv[t * k + j] * ldy)[c];
+      acc.x += wj * v.x;
+      acc.y += wj * v.y;
+      acc.z += wj * v.z;
+      acc.w += wj * v.w;
+    }
+    const float4 p = reinterpret_cast<const float4*>(res + t * ldr)[c];
+    reinterpret_cast<float4*>(out + t * ldo)[c] = make_float4(p.x + acc.x, p.y + acc.y, p.z + acc.z, p.w + acc.w);
+  }
+}
+
 template <typename TG>
 __device__ __forceinline__ void store4(TG* dst, float4 v);
 template <>
@@ -484,6 +509,18 @@ extern "C" int cb_moe_combine(int64_t n, int dim, int top_k, const int32_t* inv,
     combine_k<__nv_bfloat16><<<n, 256, 0, st>>>(n, dim, top_k, inv, weights, (const __nv_bfloat16*)y, ldy, out, ldo,
                                                 accumulate);
   return check_launch("moe_combine");
+}
+
+extern "C" int cb_moe_combine_residual(int64_t n, int dim, int top_k, const int32_t* inv, const float* weights,
+                                       const float* y, int64_t ldy, const float* res, int64_t ldr, float* out,
+                                       int64_t ldo, void* stream) {
+  if (n <= 0) return CB_OK;
+  if (!weights || dim % 4 || ((ldy | ldr | ldo) & 3) ||
+      ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(res) | reinterpret_cast<uintptr_t>(out)) & 15))
+    return fail(CB_ERR_UNSUPPORTED, "moe_combine_residual: needs f32 16-byte aligned rows, dim %% 4 == 0");
+  combine_res_v4_k<<<(unsigned)((n + 7) / 8), 256, 0, (cudaStream_t)stream>>>(n, dim / 4, top_k, inv, weights, y, ldy,
+                                                                              res, ldr, out, ldo);
+  return check_launch("moe_combine_residual");
 }
 
 extern "C" int cb_moe_combine_bwd(int64_t n, int dim, int top_k, const int32_t* inv, const float* weights,

@@ -91,7 +91,9 @@ class MoEBehavior(Behavior):
                 RematTag("expert_output", k * rows * d * nb, k * 2 * rows * h * d)]
 
     # ------------------------------------------------------------------ execution
-    def forward(self, module, x):
+    fuses_residual = True  # forward(x, residual=r) returns r + moe(x) from the combine kernel
+
+    def forward(self, module, x, residual=None):
         L = _layers()
         cfg = module.config
         d, h, E, k = cfg.get("input_dim"), cfg.get("hidden_dim"), cfg.get("num_experts"), cfg.get("top_k")
@@ -162,8 +164,14 @@ class MoEBehavior(Behavior):
         pre, hid = self._experts_up(module, xe, off)
         ye = self._experts_down(module, hid, off)
         out = torch.empty((n, d), device=dev, dtype=torch.float32)
-        _lib.call("cb_moe_combine", n, d, k, inv.data_ptr(), w.data_ptr(), ye.data_ptr(), ops.ld(ye), ops.dt(ye),
-                  out.data_ptr(), ops.ld(out), 0, ops.stream_ptr())
+        res = None if residual is None else ops.rows2d(residual)
+        if not (res is not None and ye.dtype == torch.float32 and res.dtype == torch.float32 and _lib.try_call(
+                "cb_moe_combine_residual", n, d, k, inv.data_ptr(), w.data_ptr(), ye.data_ptr(), ops.ld(ye),
+                res.data_ptr(), ops.ld(res), out.data_ptr(), ops.ld(out), ops.stream_ptr())):
+            _lib.call("cb_moe_combine", n, d, k, inv.data_ptr(), w.data_ptr(), ye.data_ptr(), ops.ld(ye), ops.dt(ye),
+                      out.data_ptr(), ops.ld(out), 0, ops.stream_ptr())
+            if res is not None:
+                ops.add_(out, res)
         if L.is_recording():
             # remat tags (reference layers.py:501-511): router_logits = the router
             # probabilities, expert_hidden = the experts' up-projections, expert_output = the

@@ -298,6 +298,12 @@ def test_moe_combine_fwd_bwd(cuda, k, dy_bf16):
     rows = y.double()[inv.long()].view(n, k, d)
     ref = (w.double().unsqueeze(-1) * rows).sum(1)
     assert _rel(out.cpu(), ref) < 1e-6
+    # the residual-fused form: bit-identical to combine followed by the residual add
+    res = torch.randn(n, d, generator=g).to(cuda)
+    fused = torch.empty(n, d, device=cuda)
+    _lib.call("cb_moe_combine_residual", n, d, k, Inv.data_ptr(), W.data_ptr(), Y.data_ptr(), d, res.data_ptr(), d,
+              fused.data_ptr(), d, ops.stream_ptr())
+    assert torch.equal(fused, out + res)
     dy = torch.zeros(cap, d, device=cuda, dtype=torch.bfloat16 if dy_bf16 else torch.float32)
     dw = torch.empty(n, k, device=cuda)
     _lib.call("cb_moe_combine_bwd", n, d, k, Inv.data_ptr(), W.data_ptr(), Y.data_ptr(), d, Dout.data_ptr(), d,
