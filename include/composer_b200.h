@@ -49,6 +49,16 @@ CB_API long long cb_launch_count(void);
 CB_API int cb_gemm(int M, int N, int K, int in_dtype, const void* A, int64_t lda, int trans_a, const void* B,
                    int64_t ldb, int trans_b, void* D, int64_t ldd, int d_dtype, const void* R, int64_t ldr,
                    int r_dtype, float alpha, int accumulate, void* stream);
+/* The AdamW update (fn:adamw, layers.py:657-663; cb_adamw below) fused into a weight-gradient
+ * GEMM whose product alpha * op(A) @ op(B) is the whole gradient of the output elements this
+ * step: the epilogue updates param / exp_avg / exp_avg_sq (f32) and writes param_bf16
+ * (optional) at D's positions; D (the gradient buffer's view, row stride ldd) is an address
+ * frame only, never read or written.  Same engines as cb_gemm; bit-identical to cb_gemm
+ * accumulating into a zeroed D followed by cb_adamw on D. */
+CB_API int cb_gemm_adamw(int M, int N, int K, int in_dtype, const void* A, int64_t lda, int trans_a, const void* B,
+                         int64_t ldb, int trans_b, void* D, int64_t ldd, float alpha, float* param, float* exp_avg,
+                         float* exp_avg_sq, void* param_bf16, float lr, float beta1, float beta2, float eps,
+                         float weight_decay, int step, void* stream);
 /* 0 = automatic engine choice, 1 = force SIMT, 2 = force tcgen05 (tests only). */
 CB_API int cb_gemm_set_path(int path);
 /* Cluster mode of the tcgen05 engine: 1 (default) = CTA-pair MMA (cta_group::2, 256x256

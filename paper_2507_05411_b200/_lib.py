@@ -36,6 +36,8 @@ SIGNATURES: dict[str, list] = {
     "cb_gemm_set_multicast": [_I],
     "cb_gemm_set_staged_epilogue": [_I],
     "cb_gemm": [_I, _I, _I, _I, _P, _L, _I, _P, _L, _I, _P, _L, _I, _P, _L, _I, _F, _I, _P],
+    "cb_gemm_adamw": [_I, _I, _I, _I, _P, _L, _I, _P, _L, _I, _P, _L, _F, _P, _P, _P, _P, _F, _F, _F, _F, _F, _I,
+                      _P],
     "cb_rmsnorm_fwd": [_I, _I, _P, _L, _I, _P, _F, _P, _L, _I, _P, _P],
     "cb_rmsnorm_bwd_workspace": [_I, _I, ctypes.POINTER(ctypes.c_int64)],
     "cb_rmsnorm_bwd": [_I, _I, _P, _L, _I, _P, _P, _P, _L, _I, _P, _L, _P, _L, _P, _L, _P, _P, _P],

@@ -14,16 +14,6 @@
 
 namespace cb {
 
-// One element's update, with explicitly rounded operations so every kernel that calls it
-// (adamw_k, adamw_parts_k) produces bit-identical results regardless of FMA contraction.
-__device__ __forceinline__ void adam_elem(float& p, float g, float& m, float& v, float lr, float b1, float b2,
-                                          float eps, float wd, float bc1, float bc2) {
-  m = __fmaf_rn(b1, m, __fmul_rn(1.f - b1, g));
-  v = __fmaf_rn(b2, v, __fmul_rn(__fmul_rn(1.f - b2, g), g));
-  const float upd = __fdiv_rn(__fdiv_rn(m, bc1), __fadd_rn(__fsqrt_rn(__fdiv_rn(v, bc2)), eps));
-  p = __fsub_rn(p, __fmul_rn(lr, __fadd_rn(upd, __fmul_rn(wd, p))));
-}
-
 __global__ void __launch_bounds__(256) adamw_k(int64_t n, float* __restrict__ p, const float* __restrict__ g,
                                                float* __restrict__ m, float* __restrict__ v,
                                                __nv_bfloat16* __restrict__ pbf, float lr, float b1, float b2,

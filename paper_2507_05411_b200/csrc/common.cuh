@@ -31,6 +31,18 @@ static constexpr int kNumSMs = 148;
 // ------------------------------------------------------------------------------------
 // small device helpers
 // ------------------------------------------------------------------------------------
+// One AdamW element update (adamw.cu; reference layers.py:657-663), with explicitly rounded
+// operations so every kernel that calls it — adamw_k, adamw_parts_k and the GEMM epilogue
+// that fuses the update into a weight-gradient GEMM (cb_gemm_adamw) — produces bit-identical
+// results regardless of FMA contraction.
+__device__ __forceinline__ void adam_elem(float& p, float g, float& m, float& v, float lr, float b1, float b2,
+                                          float eps, float wd, float bc1, float bc2) {
+  m = __fmaf_rn(b1, m, __fmul_rn(1.f - b1, g));
+  v = __fmaf_rn(b2, v, __fmul_rn(__fmul_rn(1.f - b2, g), g));
+  const float upd = __fdiv_rn(__fdiv_rn(m, bc1), __fadd_rn(__fsqrt_rn(__fdiv_rn(v, bc2)), eps));
+  p = __fsub_rn(p, __fmul_rn(lr, __fadd_rn(upd, __fmul_rn(wd, p))));
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -47,13 +47,50 @@ struct Epi {
   int64_t ld_glu_out = 0;
   const void* glu_pre = nullptr;
   int64_t ld_glu_pre = 0;
+  // AdamW fused into a weight-gradient GEMM (cb_gemm_adamw): the accumulator is the whole
+  // gradient of the output elements (D is only the address frame, never read or written); the
+  // epilogue applies the update to the f32 master / m / v and writes the bf16 working copy,
+  // all laid out like D (same row stride).  g = fma(acc, alpha, 0) — the value the unfused
+  // path stores into a cleared gradient buffer — then adam_elem exactly as cb_adamw.
+  float* ad_p = nullptr;
+  float* ad_m = nullptr;
+  float* ad_v = nullptr;
+  __nv_bfloat16* ad_bf = nullptr;
+  float ad_lr = 0.f, ad_b1 = 0.f, ad_b2 = 0.f, ad_eps = 0.f, ad_wd = 0.f, ad_bc1 = 1.f, ad_bc2 = 1.f;
 };
+
+// L2 prefetch of one output row's optimizer state (master / m / v) over a tile's columns: the
+// fused-AdamW epilogue issues it for the next tile while the current one drains, so the
+// epilogue's loads hit L2 instead of waiting on HBM with only 4 warps of loads in flight.
+__device__ __forceinline__ void epi_adam_prefetch(const Epi& e, int row, int col0, int ncols) {
+  if (!e.ad_p || row >= e.M) return;
+  const int64_t base = (int64_t)row * e.ldd + col0;
+  for (int c = 0; c < ncols && col0 + c < e.N; c += 32) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(e.ad_p + base + c));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(e.ad_m + base + c));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(e.ad_v + base + c));
+  }
+}
+
+__device__ __forceinline__ void epi_adam1(const Epi& e, int64_t di, float acc) {
+  float p = e.ad_p[di], m = e.ad_m[di], v = e.ad_v[di];
+  adam_elem(p, __fmul_rn(__fmaf_rn(acc, e.alpha, 0.f), 1.f), m, v, e.ad_lr, e.ad_b1, e.ad_b2, e.ad_eps, e.ad_wd,
+            e.ad_bc1, e.ad_bc2);
+  e.ad_p[di] = p;
+  e.ad_m[di] = m;
+  e.ad_v[di] = v;
+  if (e.ad_bf) e.ad_bf[di] = __float2bfloat16_rn(p);
+}
 
 __device__ __forceinline__ float epi_load(const void* p, int64_t idx, int f32) {
   return f32 ? reinterpret_cast<const float*>(p)[idx] : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[idx]);
 }
 
 __device__ __forceinline__ void epi_store1(const Epi& e, int r, int c, float v) {
+  if (e.ad_p) {
+    epi_adam1(e, (int64_t)r * e.ldd + c, v);
+    return;
+  }
   v *= e.alpha;
   const int64_t di = (int64_t)r * e.ldd + c;
   if (e.accumulate) v += epi_load(e.D, di, e.d_f32);
@@ -148,6 +185,51 @@ __device__ __forceinline__ void epi_chunk(const Epi& e, uint32_t (&v)[32], int r
     }
   }
   const bool full_chunk = col0 + 32 <= e.N;
+  if (e.ad_p) {
+    const int64_t di = (int64_t)row * e.ldd + col0;
+    const bool v4 = full_chunk && (e.ldd & 7) == 0 &&
+                    !((reinterpret_cast<uintptr_t>(e.ad_p) | reinterpret_cast<uintptr_t>(e.ad_m) |
+                       reinterpret_cast<uintptr_t>(e.ad_v)) & 15) && !(reinterpret_cast<uintptr_t>(e.ad_bf) & 15);
+    if (v4) {
+#pragma unroll
+      for (int g8 = 0; g8 < 4; ++g8) {
+        const int64_t i = di + g8 * 8;
+        float4 P[2], Mv[2], V[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          P[h] = reinterpret_cast<const float4*>(e.ad_p + i)[h];
+          Mv[h] = reinterpret_cast<const float4*>(e.ad_m + i)[h];
+          V[h] = reinterpret_cast<const float4*>(e.ad_v + i)[h];
+        }
+        float* pp = &P[0].x;
+        float* mm = &Mv[0].x;
+        float* vv = &V[0].x;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          adam_elem(pp[j], __fmul_rn(__fmaf_rn(__uint_as_float(v[g8 * 8 + j]), e.alpha, 0.f), 1.f), mm[j], vv[j],
+                    e.ad_lr, e.ad_b1, e.ad_b2, e.ad_eps, e.ad_wd, e.ad_bc1, e.ad_bc2);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          reinterpret_cast<float4*>(e.ad_p + i)[h] = P[h];
+          reinterpret_cast<float4*>(e.ad_m + i)[h] = Mv[h];
+          reinterpret_cast<float4*>(e.ad_v + i)[h] = V[h];
+        }
+        if (e.ad_bf) {
+          uint4 t;
+          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&t);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) h2[j] = __floats2bfloat162_rn(pp[2 * j], pp[2 * j + 1]);
+          *reinterpret_cast<uint4*>(e.ad_bf + i) = t;
+        }
+      }
+    } else {
+      const int lim = min(32, e.N - col0);
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < lim) epi_adam1(e, di + j, __uint_as_float(v[j]));
+    }
+    return;
+  }
   const bool fast = full_chunk && !e.accumulate && !e.R && e.alpha == 1.f && !e.d_f32 && ((e.ldd & 7) == 0) &&
                     ((reinterpret_cast<uintptr_t>(e.D) & 15) == 0);
   const bool vec = full_chunk && ((e.ldd & 7) == 0) && ((reinterpret_cast<uintptr_t>(e.D) & 31) == 0) &&
@@ -391,6 +473,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const Epi& e = args.e;
     int it = 0;
+    if (e.ad_p && unit0 < num_units) {
+      int tm, tn;
+      coords(unit0, tm, tn);
+      epi_adam_prefetch(e, tm * BM + q * 32 + lane, tn * BN, BN);
+    }
     for (int u = unit0; u < num_units; u += unit_stride, ++it) {
       int tm, tn;
       coords(u, tm, tn);
@@ -398,6 +485,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (e.ad_p && u + unit_stride < num_units) {  // the next tile's optimizer state into L2
+        int tm2, tn2;
+        coords(u + unit_stride, tm2, tn2);
+        epi_adam_prefetch(e, tm2 * BM + q * 32 + lane, tn2 * BN, BN);
+      }
       const int row = tm * BM + q * 32 + lane;
       const bool row_ok = row < e.M;
 #pragma unroll 1
@@ -924,6 +1016,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                             (e0.ld_glu_out & 7) == 0 && (reinterpret_cast<uintptr_t>(e0.glu_pre) & 15) == 0 &&
                             (reinterpret_cast<uintptr_t>(e0.glu_out) & 15) == 0;
     int it = 0;
+    const bool adam_pf = e0.ad_p && gm == 0;
+    if (adam_pf && unit0 < num_units) {
+      int tm, tn, g;
+      coords(unit0, tm, tn, g);
+      epi_adam_prefetch(e0, tm * BM + q * 32 + lane, tn * BN, BN);
+    }
     for (int u = unit0; u < num_units; u += unit_stride) {
       int tm, tn, g;
       coords(u, tm, tn, g);
@@ -936,6 +1034,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++it;
       mbar_wait(&tfull[acc], ((it - 1) >> 1) & 1);
       tc_fence_after();
+      if (adam_pf && u + unit_stride < num_units) {  // the next tile's optimizer state into L2
+        int tm2, tn2, g2;
+        coords(u + unit_stride, tm2, tn2, g2);
+        epi_adam_prefetch(e0, tm2 * BM + q * 32 + lane, tn2 * BN, BN);
+      }
       Epi eg = e0;
       if (gm == 2)  // group g's rows of the stacked output
         eg.D = reinterpret_cast<char*>(eg.D) + (int64_t)g * eg.M * eg.ldd * (eg.d_f32 ? 4 : 2);
@@ -1452,6 +1555,33 @@ extern "C" int cb_gemm(int M, int N, int K, int in_dtype, const void* A, int64_t
   Epi e{D, ldd, d_dtype == CB_DT_F32, R, ldr, r_dtype == CB_DT_F32, alpha, accumulate, M, N};
   return gemm_impl(M, N, K, in_dtype, A, lda, trans_a, B, ldb, trans_b, D, ldd, d_dtype, R, ldr, r_dtype, alpha,
                    accumulate, reinterpret_cast<cudaStream_t>(stream), e);
+}
+
+// AdamW fused into a weight-gradient GEMM: the update of the parameters whose gradient is
+// alpha * op(A) @ op(B) (their whole gradient this step); D frames the addresses (the
+// gradient buffer's view, never read or written), param / exp_avg / exp_avg_sq (f32) and
+// param_bf16 (optional) share D's layout.  Bit-identical to cb_gemm(accumulate into a zeroed
+// D) followed by cb_adamw on D.
+extern "C" int cb_gemm_adamw(int M, int N, int K, int in_dtype, const void* A, int64_t lda, int trans_a, const void* B,
+                             int64_t ldb, int trans_b, void* D, int64_t ldd, float alpha, float* param, float* exp_avg,
+                             float* exp_avg_sq, void* param_bf16, float lr, float beta1, float beta2, float eps,
+                             float weight_decay, int step, void* stream) {
+  if (step < 1) return fail(CB_ERR_ARG, "gemm_adamw: step must be >= 1");
+  if (!param || !exp_avg || !exp_avg_sq) return fail(CB_ERR_ARG, "gemm_adamw: null optimizer buffer");
+  Epi e{D, ldd, 1, nullptr, 0, 0, alpha, 0, M, N};
+  e.ad_p = param;
+  e.ad_m = exp_avg;
+  e.ad_v = exp_avg_sq;
+  e.ad_bf = reinterpret_cast<__nv_bfloat16*>(param_bf16);
+  e.ad_lr = lr;
+  e.ad_b1 = beta1;
+  e.ad_b2 = beta2;
+  e.ad_eps = eps;
+  e.ad_wd = weight_decay;
+  e.ad_bc1 = (float)(1.0 - pow((double)beta1, step));  // as cb_adamw
+  e.ad_bc2 = (float)(1.0 - pow((double)beta2, step));
+  return gemm_impl(M, N, K, in_dtype, A, lda, trans_a, B, ldb, trans_b, D, ldd, CB_DT_F32, nullptr, 0, 0, alpha, 0,
+                   reinterpret_cast<cudaStream_t>(stream), e);
 }
 
 // D = op(A) @ op(B) with RoPE applied to output columns [0, rope_cols) (the q|k part of a

@@ -619,8 +619,9 @@ class TrainEngine:
             from .errors import ComposerError
 
             raise ComposerError("step() did not keep the gradients (FSDP: the reduce-scatter's sum is fused into "
-                                "AdamW — set engine.keep_grad_shards = True; one GPU with the gradient ring — set "
-                                "CB_GRAD_RING=0) before the step to read them")
+                                "AdamW; one GPU: AdamW fused into the weight-gradient GEMMs, or the gradient ring "
+                                "— set engine.keep_grad_shards = True, and CB_GRAD_RING=0 for the ring, before the "
+                                "step to read them)")
         return self._export("grad")
 
     # -------------------------------------------------------------------- step
@@ -696,10 +697,11 @@ class TrainEngine:
                 self._zero_stream = torch.cuda.Stream(self.device)
             ready = torch.cuda.Event()
             ready.record(cur)
+            fused = provider.fused if isinstance(provider, LocalUpdateProvider) else {}
             with torch.cuda.stream(self._zero_stream):
                 self._zero_stream.wait_event(ready)
-                for rec in self.bufs:
-                    if not (self._grad_ring and rec.get("ringed")):
+                for i, rec in enumerate(self.bufs):
+                    if not (self._grad_ring and rec.get("ringed")) and i not in fused:
                         ops.zero_(rec["grad"])
                 zeroed = torch.cuda.Event()
                 zeroed.record(self._zero_stream)
@@ -744,6 +746,36 @@ class TrainEngine:
             ev = torch.cuda.Event()
             ev.record(self._wgrad_stream)
             stream.wait_event(ev)
+
+    # layer-bucket parameters whose whole gradient is one accumulating weight-gradient GEMM per
+    # step (ops.gemm), so their AdamW can run in that GEMM's epilogue
+    _FUSABLE = {("Attention", "wq"), ("Attention", "wk"), ("Attention", "wv"), ("Attention", "wo"),
+                ("GroupedQueryAttention", "wq"), ("GroupedQueryAttention", "wk"),
+                ("GroupedQueryAttention", "wv"), ("GroupedQueryAttention", "wo"),
+                ("FeedForward", "w1"), ("FeedForward", "w1_gate"), ("FeedForward", "w2")}
+
+    def fused_update_buckets(self) -> dict[int, int]:
+        """{bucket index: parameter count} of the buckets whose AdamW the single-GPU step runs in
+        the weight-gradient GEMMs' epilogues (cb_gemm_adamw): opt-in (CB_FUSED_ADAMW=1), one
+        GPU, bf16 working copy, layer buckets holding only attention / dense-FFN projection
+        weights (a MoE expert with no routed rows has no GEMM but still a momentum update),
+        gradients not kept for reading (keep_grad_shards).
+
+        Off by default: measured, the update does not hide in the epilogue.  The weight-gradient
+        GEMMs are bound by L2->SM operand traffic, and the epilogue's 24 bytes of optimizer
+        state per element queue behind it — each 7B wgrad GEMM grows by the separate AdamW
+        kernel's whole duration (QKV 0.88 -> 1.12 ms vs 0.25 ms of AdamW), the 7B step is 1.5%
+        slower and the 1B step 0.8% faster (profiles/r02_fused_adamw_ab.txt)."""
+        if (self.d.world > 1 or self.keep_grad_shards or os.environ.get("CB_FUSED_ADAMW", "0") != "1"
+                or self.device.type != "cuda"):
+            return {}
+        out = {}
+        for i, b in enumerate(self.buckets):
+            if b.name == "root" or b.replicated or self.bufs[i]["wshard"].dtype != torch.bfloat16:
+                continue
+            if all((e.module_kind, e.name) in self._FUSABLE and len(e.shape) == 2 for e in b.entries):
+                out[i] = sum(int(np.prod(e.shape)) for e in b.entries)
+        return out
 
     def _adamw_bucket(self, i: int, parts: list | None = None, scale: float = 1.0) -> None:
         """AdamW on bucket i's shard; with `parts` the gradient is scale * their in-order sum
@@ -1020,6 +1052,8 @@ class LocalUpdateProvider(ParamProvider):
         self.index = {b.name: i for i, b in enumerate(eng.buckets)}
         self.done: set[int] = set()
         self.gslot_free: dict[int, torch.cuda.Event] = {}  # gradient ring slot -> cleared event
+        self.fused = eng.fused_update_buckets()
+        self.cur = None
 
     def _update(self, i: int) -> None:
         ready = torch.cuda.Event()
@@ -1028,6 +1062,14 @@ class LocalUpdateProvider(ParamProvider):
         with torch.cuda.stream(self.side):
             self.side.wait_event(ready)
             self.e._join_wgrad(self.side)
+            if i in self.fused:
+                # master / m / v were updated by the weight-gradient GEMMs' epilogues (the
+                # gradient never reached HBM); the bf16 working copy is refreshed here, after
+                # every data-gradient GEMM of the layer has read the old one
+                ops.copy2d(rec["master"].view(1, -1), rec["wshard"].view(1, -1))
+                self.e._grad_shards_stale = True
+                self.done.add(i)
+                return
             self.e._adamw_bucket(i)
             if self.e._grad_ring and rec.get("ringed"):
                 # the gradient slot is consumed: clear it for the layer two positions further on
@@ -1045,10 +1087,23 @@ class LocalUpdateProvider(ParamProvider):
             ev = self.gslot_free.pop(self.e._pos[i] % 2, None)
             if ev is not None:
                 self.compute.wait_event(ev)
+        if i in self.fused:
+            rec, e = self.e.bufs[i], self.e
+            self.cur = (i, ops.FusedUpdate(rec["grad"], rec["master"], rec["m"], rec["v"], None, e.lr, e.beta1,
+                                           e.beta2, e.eps, e.weight_decay, e.step_count))
+            ops.set_fused_update(self.cur[1])
 
     def after_backward(self, path: str) -> None:
         i = self.index.get(path)
         if i is not None:
+            if self.cur is not None and self.cur[0] == i:
+                ops.set_fused_update(None)
+                fu, self.cur = self.cur[1], None
+                if fu.covered != self.fused[i]:
+                    from .errors import KernelError
+
+                    raise KernelError(f"fused AdamW: the weight-gradient GEMMs of {self.e.buckets[i].name} covered "
+                                      f"{fu.covered} of its {self.fused[i]} parameters")
             self._update(i)
 
     def finish_backward(self) -> None:

@@ -115,10 +115,48 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, trans_a: bool = Fa
     if _f32_on_tc(a, b, out, M, N, K):
         return _gemm_bf16x6(a, b, out, trans_a, trans_b, alpha, accumulate, residual)
     kind = "gemm_bf16" if a.dtype == torch.bfloat16 else "gemm_f32"
+    fu = _FUSED_UPDATE
+    if fu is not None and accumulate and residual is None and out.dtype == torch.float32 and (
+            fu.lo <= out.data_ptr() < fu.hi):
+        # the whole gradient of these elements: the bucket's AdamW runs in this GEMM's epilogue
+        off = (out.data_ptr() - fu.lo) // 4
+        last = off + (M - 1) * ld(out, "out") + N
+        if last > fu.numel:
+            raise ShapeError("gemm: fused-update output leaves its bucket")
+        fu.covered += M * N
+        _profiled(kind, 2 * M * N * K, _lib.call, "cb_gemm_adamw", M, N, K, dt(a), a.data_ptr(), ld(a, "A"),
+                  int(trans_a), b.data_ptr(), ld(b, "B"), int(trans_b), out.data_ptr(), ld(out, "out"), float(alpha),
+                  fu.master + 4 * off, fu.m + 4 * off, fu.v + 4 * off, (fu.bf + 2 * off) if fu.bf else None,
+                  fu.lr, fu.beta1, fu.beta2, fu.eps, fu.wd, fu.step, stream_ptr())
+        return out
     _profiled(kind, 2 * M * N * K, _lib.call, "cb_gemm", M, N, K, dt(a), a.data_ptr(), ld(a, "A"), int(trans_a),
               b.data_ptr(), ld(b, "B"), int(trans_b), out.data_ptr(), ld(out, "out"), dt(out), _ptr(residual), ldr,
               dt(residual) if residual is not None else 0, float(alpha), int(accumulate), stream_ptr())
     return out
+
+
+class FusedUpdate:
+    """A bucket whose AdamW runs in its weight-gradient GEMMs' epilogues (cb_gemm_adamw): any
+    accumulating f32 GEMM into [lo, hi) — the bucket's gradient buffer — becomes the update of
+    those elements of master / m / v / bf16 copy (same flat layout).  `covered` counts the
+    elements updated, which the engine checks against the bucket's parameter count."""
+
+    def __init__(self, grad, master, m, v, bf, lr, beta1, beta2, eps, wd, step):
+        self.lo, self.numel = grad.data_ptr(), grad.numel()
+        self.hi = self.lo + 4 * self.numel
+        self.master, self.m, self.v = master.data_ptr(), m.data_ptr(), v.data_ptr()
+        self.bf = bf.data_ptr() if bf is not None else 0
+        self.lr, self.beta1, self.beta2, self.eps, self.wd = (float(x) for x in (lr, beta1, beta2, eps, wd))
+        self.step = int(step)
+        self.covered = 0
+
+
+_FUSED_UPDATE: FusedUpdate | None = None
+
+
+def set_fused_update(fu: FusedUpdate | None) -> None:
+    global _FUSED_UPDATE
+    _FUSED_UPDATE = fu
 
 
 # f32 parity mode on the tensor cores: an f32 GEMM large enough for the tcgen05 engine runs as

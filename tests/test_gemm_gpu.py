@@ -352,3 +352,52 @@ def test_moe_dispatch_padded(cuda):
         assert np.array_equal(pi[mine], rows)
         assert torch.equal(xec[rows], xc[mine // k])
         assert not xec[po[e] + len(mine):po[e + 1]].float().any()
+
+
+@pytest.mark.parametrize("M,N,K,ldd,path", [
+    (2048, 3072, 1024, 3072, 0),   # CTA-pair engine, whole chunks
+    (512, 384, 768, 1024, 0),      # a column block of a wider buffer (fused wq|wk|wv slice)
+    (520, 200, 264, 200, 0),       # ragged tails: per-element epilogue
+    (256, 96, 512, 96, 0),         # N <= 128 engine
+    (96, 80, 64, 80, 0),           # below the tcgen05 work threshold: SIMT epilogue
+    (256, 512, 256, 512, 1),       # forced SIMT
+    (128, 256, 0, 256, 0),         # K = 0: the zero gradient's update (momentum only)
+])
+def test_gemm_adamw_matches_gemm_then_adamw(cuda, M, N, K, ldd, path):
+    """cb_gemm_adamw (AdamW in the weight-gradient GEMM's epilogue) = cb_gemm accumulating
+    into a zeroed gradient followed by cb_adamw, bit for bit, on every engine and epilogue path;
+    the gradient buffer itself is never written."""
+    from paper_2507_05411_b200 import _lib, ops
+
+    g = torch.Generator(device="cpu").manual_seed(M + N + K)
+    x = torch.randn(max(K, 1), M, generator=g).to(cuda, torch.bfloat16)[:K]  # A = x^T (trans_a)
+    dy = torch.randn(max(K, 1), N, generator=g).to(cuda, torch.bfloat16)[:K]
+    rows = M * ldd
+    p0 = torch.randn(rows, generator=g).to(cuda)
+    m0 = torch.randn(rows, generator=g).to(cuda) * 1e-3
+    v0 = torch.rand(rows, generator=g).to(cuda) * 1e-6
+    hyper = (1e-3, 0.9, 0.999, 1e-8, 0.01, 3)
+    ops.set_gemm_path(path)
+    try:
+        # unfused: gradient into a zeroed buffer, then AdamW over the whole buffer
+        grad = torch.zeros(rows, device=cuda)
+        gv = grad.view(M, ldd)[:, :N]
+        ops.gemm(x, dy, gv, trans_a=True, accumulate=True, alpha=0.5)
+        p1, m1, v1 = p0.clone(), m0.clone(), v0.clone()
+        bf1 = torch.empty(rows, device=cuda, dtype=torch.bfloat16)
+        ops.adamw(p1, grad, m1, v1, bf1, *hyper)
+        # fused: only the GEMM's own elements are touched
+        p2, m2, v2 = p0.clone(), m0.clone(), v0.clone()
+        sentinel = torch.full((rows,), 7.0, device=cuda)
+        sv = sentinel.view(M, ldd)[:, :N]
+        _lib.call("cb_gemm_adamw", M, N, K, ops.dt(x), x.data_ptr(), M, 1, dy.data_ptr(), N, 0, sv.data_ptr(), ldd,
+                  0.5, p2.data_ptr(), m2.data_ptr(), v2.data_ptr(), None, *[float(h) for h in hyper[:5]], hyper[5],
+                  ops.stream_ptr())
+    finally:
+        ops.set_gemm_path(0)
+    assert torch.equal(sentinel, torch.full_like(sentinel, 7.0))
+    sel = torch.zeros(M, ldd, dtype=torch.bool, device=cuda)
+    sel[:, :N] = True
+    sel = sel.view(-1)
+    assert torch.equal(p2[sel], p1[sel]) and torch.equal(m2[sel], m1[sel]) and torch.equal(v2[sel], v1[sel])
+    assert torch.equal(p2[~sel], p0[~sel]) and torch.equal(m2[~sel], m0[~sel])

@@ -586,3 +586,37 @@ def test_single_gpu_grad_ring_is_exact(cuda, monkeypatch):
     for k in outs[0][1]:
         assert np.array_equal(outs[0][1][k], outs[1][1][k]), k
     assert outs[1][2] < outs[0][2]
+
+
+@pytest.mark.parametrize("kind", ["swiglu_5l", "gqa"])
+def test_fused_adamw_in_wgrad_gemm_is_exact(cuda, monkeypatch, kind):
+    """One-GPU step with AdamW fused into the weight-gradient GEMMs' epilogues (cb_gemm_adamw,
+    opt-in CB_FUSED_ADAMW=1) against the separate AdamW kernel: bit-identical losses, parameters and
+    AdamW moments over three steps, with and without the gradient ring; every layer bucket of
+    these dense configs takes the fused path."""
+    from paper_2507_05411_b200 import TrainEngine, set_dtype_policy, synthetic_batch
+    from paper_2507_05411_b200.experiments import _llama_trainer, transformer_trainer
+
+    if kind == "gqa":
+        cfg = _llama_trainer(256, 2, 4, 768, 512, 4, 256, kv_heads=2)
+    else:
+        cfg = transformer_trainer(256, 5, ("linear", "silu"), pos_kind="RoPE", heads=2, vocab=512)
+        for i in range(5):
+            cfg = cfg.set(f"model.decoder.transformer.layer[{i}].feed_forward.hidden_dim", 768)
+    cfg = set_dtype_policy(cfg, "bf16")
+    outs = []
+    for fused, ring in (("0", "0"), ("1", "0"), ("1", "1")):
+        monkeypatch.setenv("CB_FUSED_ADAMW", fused)
+        monkeypatch.setenv("CB_GRAD_RING", ring)
+        eng = TrainEngine(cfg, device="cuda:0")
+        nf = len(eng.fused_update_buckets())
+        assert nf == (0 if fused == "0" else len(eng.layer_order))
+        losses = [float(eng.step(synthetic_batch(0, s, 4, 256, 512)["tokens"])[0].item()) for s in range(3)]
+        opt = eng.opt_state_numpy()
+        outs.append((losses, dict(_leaves(eng.state_numpy())), dict(_leaves(opt["m"])), dict(_leaves(opt["v"]))))
+        del eng
+    for o in outs[1:]:
+        assert o[0] == outs[0][0]
+        for j in (1, 2, 3):
+            for k in outs[0][j]:
+                assert np.array_equal(o[j][k], outs[0][j][k]), k
