@@ -1048,7 +1048,9 @@ class LocalUpdateProvider(ParamProvider):
         self.compute = torch.cuda.current_stream(eng.device)
         if not hasattr(eng, "_opt_stream"):
             eng._opt_stream = torch.cuda.Stream(eng.device, priority=_side_priority())
-        self.side = eng._opt_stream
+        # CB_ADAMW_INLINE=1: each layer's AdamW on the compute stream between the layers'
+        # backward kernels instead of beside them
+        self.side = self.compute if os.environ.get("CB_ADAMW_INLINE", "0") == "1" else eng._opt_stream
         self.index = {b.name: i for i, b in enumerate(eng.buckets)}
         self.done: set[int] = set()
         self.gslot_free: dict[int, torch.cuda.Event] = {}  # gradient ring slot -> cleared event
