@@ -697,11 +697,11 @@ class TrainEngine:
                 self._zero_stream = torch.cuda.Stream(self.device)
             ready = torch.cuda.Event()
             ready.record(cur)
-            fused = provider.fused if isinstance(provider, LocalUpdateProvider) else {}
+            written = set(provider.fused) | set(provider.overwrite)  # gradients never accumulated
             with torch.cuda.stream(self._zero_stream):
                 self._zero_stream.wait_event(ready)
                 for i, rec in enumerate(self.bufs):
-                    if not (self._grad_ring and rec.get("ringed")) and i not in fused:
+                    if not (self._grad_ring and rec.get("ringed")) and i not in written:
                         ops.zero_(rec["grad"])
                 zeroed = torch.cuda.Event()
                 zeroed.record(self._zero_stream)
@@ -754,6 +754,29 @@ class TrainEngine:
                 ("GroupedQueryAttention", "wv"), ("GroupedQueryAttention", "wo"),
                 ("FeedForward", "w1"), ("FeedForward", "w1_gate"), ("FeedForward", "w2")}
 
+    def dense_layer_buckets(self) -> dict[int, int]:
+        """{bucket index: parameter count} of the layer buckets (bf16 working copy) holding only
+        attention / dense-FFN projection weights, each of whose elements gets exactly one
+        accumulating weight-gradient GEMM (ops.gemm) per backward — a MoE expert with no routed
+        rows gets none, the tied embedding two, so their buckets are excluded."""
+        out = {}
+        if self.device.type != "cuda":
+            return out
+        for i, b in enumerate(self.buckets):
+            if b.name == "root" or b.replicated or self.bufs[i]["wshard"].dtype != torch.bfloat16:
+                continue
+            if all((e.module_kind, e.name) in self._FUSABLE and len(e.shape) == 2 for e in b.entries):
+                out[i] = sum(int(np.prod(e.shape)) for e in b.entries)
+        return out
+
+    def overwrite_buckets(self) -> dict[int, int]:
+        """The dense layer buckets whose weight-gradient GEMMs write their gradient instead of
+        adding it to a cleared buffer (ops.Overwrite): no clearing pass over those gradients
+        (the 7B step: 26 GB of memset per step).  CB_WGRAD_OVERWRITE=0 turns it off."""
+        if os.environ.get("CB_WGRAD_OVERWRITE", "1") == "0":
+            return {}
+        return self.dense_layer_buckets()
+
     def fused_update_buckets(self) -> dict[int, int]:
         """{bucket index: parameter count} of the buckets whose AdamW the single-GPU step runs in
         the weight-gradient GEMMs' epilogues (cb_gemm_adamw): opt-in (CB_FUSED_ADAMW=1), one
@@ -766,16 +789,9 @@ class TrainEngine:
         state per element queue behind it — each 7B wgrad GEMM grows by the separate AdamW
         kernel's whole duration (QKV 0.88 -> 1.12 ms vs 0.25 ms of AdamW), the 7B step is 1.5%
         slower and the 1B step 0.8% faster (profiles/r02_fused_adamw_ab.txt)."""
-        if (self.d.world > 1 or self.keep_grad_shards or os.environ.get("CB_FUSED_ADAMW", "0") != "1"
-                or self.device.type != "cuda"):
+        if self.d.world > 1 or self.keep_grad_shards or os.environ.get("CB_FUSED_ADAMW", "0") != "1":
             return {}
-        out = {}
-        for i, b in enumerate(self.buckets):
-            if b.name == "root" or b.replicated or self.bufs[i]["wshard"].dtype != torch.bfloat16:
-                continue
-            if all((e.module_kind, e.name) in self._FUSABLE and len(e.shape) == 2 for e in b.entries):
-                out[i] = sum(int(np.prod(e.shape)) for e in b.entries)
-        return out
+        return self.dense_layer_buckets()
 
     def _adamw_bucket(self, i: int, parts: list | None = None, scale: float = 1.0) -> None:
         """AdamW on bucket i's shard; with `parts` the gradient is scale * their in-order sum
@@ -899,6 +915,9 @@ class FSDPProvider(ParamProvider):
         self.gathered: dict[int, torch.cuda.Event] = {}  # bucket -> gather-done event (this step)
         self.plan = GatherPlan(self.layer_order, eng._reshard)
         self.gslot_free: dict[int, torch.cuda.Event] = {}  # grad ring slot -> cleared event
+        self.fused = {}
+        self.overwrite = eng.overwrite_buckets()
+        self.ow_cur = None
 
     def _run(self, actions: list) -> None:
         for i, slot, barrier in actions:
@@ -990,7 +1009,8 @@ class FSDPProvider(ParamProvider):
                 self.dist.reduce_scatter_tensor(rec["grad_shard"], rec["grad"], op=self.dist.ReduceOp.AVG,
                                                 group=self.group)
             if ring:  # the slot is free for the layer two positions further in the backward
-                ops.zero_(rec["grad"])
+                if i not in self.overwrite:  # (cleared unless that layer's GEMMs overwrite it)
+                    ops.zero_(rec["grad"])
                 ev = torch.cuda.Event()
                 ev.record(self.comm)
                 self.gslot_free[gslot] = ev
@@ -1023,10 +1043,12 @@ class FSDPProvider(ParamProvider):
             ev = self.gslot_free.pop(pos % 2, None)
             if ev is not None:
                 self.compute.wait_event(ev)
+        _begin_overwrite(self, i)
 
     def after_backward(self, path: str) -> None:
         i = self.index.get(path)
         if i is not None:
+            _end_overwrite(self, i)
             self._rs(i)
 
     def finish_backward(self) -> None:
@@ -1040,22 +1062,27 @@ class FSDPProvider(ParamProvider):
 
 
 class LocalUpdateProvider(ParamProvider):
-    """Single-GPU step: AdamW of each layer bucket on a side stream right after that layer's
-    backward (the root and replicated buckets, whose gradients complete last, at the end)."""
+    """Single-GPU step: AdamW of each layer bucket right after that layer's backward, on the
+    compute stream (the root and replicated buckets, whose gradients complete last, at the
+    end)."""
 
     def __init__(self, eng: TrainEngine):
         self.e = eng
         self.compute = torch.cuda.current_stream(eng.device)
         if not hasattr(eng, "_opt_stream"):
             eng._opt_stream = torch.cuda.Stream(eng.device, priority=_side_priority())
-        # CB_ADAMW_INLINE=1: each layer's AdamW on the compute stream between the layers'
-        # backward kernels instead of beside them
-        self.side = self.compute if os.environ.get("CB_ADAMW_INLINE", "0") == "1" else eng._opt_stream
+        # each layer's AdamW on the compute stream, between the layers' backward kernels: run
+        # beside them (CB_ADAMW_INLINE=0, the comm stream) its HBM/L2 traffic slowed the backward
+        # GEMMs by more than its own duration — inline is +1.0% (7B), +1.8% (1B), +1.2% (MoE)
+        # per step (profiles/r02_adamw_inline_ab.txt)
+        self.side = self.compute if os.environ.get("CB_ADAMW_INLINE", "1") == "1" else eng._opt_stream
         self.index = {b.name: i for i, b in enumerate(eng.buckets)}
         self.done: set[int] = set()
         self.gslot_free: dict[int, torch.cuda.Event] = {}  # gradient ring slot -> cleared event
         self.fused = eng.fused_update_buckets()
+        self.overwrite = {i: n for i, n in eng.overwrite_buckets().items() if i not in self.fused}
         self.cur = None
+        self.ow_cur = None
 
     def _update(self, i: int) -> None:
         ready = torch.cuda.Event()
@@ -1075,7 +1102,9 @@ class LocalUpdateProvider(ParamProvider):
             self.e._adamw_bucket(i)
             if self.e._grad_ring and rec.get("ringed"):
                 # the gradient slot is consumed: clear it for the layer two positions further on
-                ops.zero_(rec["grad"])
+                # (unless that layer's GEMMs overwrite it)
+                if i not in self.overwrite:
+                    ops.zero_(rec["grad"])
                 ev = torch.cuda.Event()
                 ev.record(self.side)
                 self.gslot_free[self.e._pos[i] % 2] = ev
@@ -1094,6 +1123,7 @@ class LocalUpdateProvider(ParamProvider):
             self.cur = (i, ops.FusedUpdate(rec["grad"], rec["master"], rec["m"], rec["v"], None, e.lr, e.beta1,
                                            e.beta2, e.eps, e.weight_decay, e.step_count))
             ops.set_fused_update(self.cur[1])
+        _begin_overwrite(self, i)
 
     def after_backward(self, path: str) -> None:
         i = self.index.get(path)
@@ -1106,6 +1136,7 @@ class LocalUpdateProvider(ParamProvider):
 
                     raise KernelError(f"fused AdamW: the weight-gradient GEMMs of {self.e.buckets[i].name} covered "
                                       f"{fu.covered} of its {self.fused[i]} parameters")
+            _end_overwrite(self, i)
             self._update(i)
 
     def finish_backward(self) -> None:
@@ -1156,6 +1187,28 @@ def _symm_mem():
     import torch.distributed._symmetric_memory as symm_mem
 
     return symm_mem
+
+
+def _begin_overwrite(provider, i) -> None:
+    """Layer bucket i's backward starts: its weight-gradient GEMMs write its gradient buffer."""
+    if i in provider.overwrite:
+        provider.ow_cur = (i, ops.Overwrite(provider.e.bufs[i]["grad"]))
+        ops.set_overwrite(provider.ow_cur[1])
+
+
+def _end_overwrite(provider, i) -> None:
+    """Layer bucket i's backward is done: every one of its parameters must have been written
+    (a gradient element no GEMM wrote would hold another layer's value — fail loudly)."""
+    cur = getattr(provider, "ow_cur", None)
+    if cur is None or cur[0] != i:
+        return
+    ops.set_overwrite(None)
+    provider.ow_cur = None
+    if cur[1].covered != provider.overwrite[i]:
+        from .errors import KernelError
+
+        raise KernelError(f"weight-gradient overwrite: the GEMMs of {provider.e.buckets[i].name} wrote "
+                          f"{cur[1].covered} of its {provider.overwrite[i]} gradient elements")
 
 
 def _wait_grads_zeroed(provider) -> None:

@@ -115,9 +115,14 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, trans_a: bool = Fa
     if _f32_on_tc(a, b, out, M, N, K):
         return _gemm_bf16x6(a, b, out, trans_a, trans_b, alpha, accumulate, residual)
     kind = "gemm_bf16" if a.dtype == torch.bfloat16 else "gemm_f32"
+    wgrad = accumulate and residual is None and out.dtype == torch.float32  # a weight-gradient-style GEMM
+    ow = _OVERWRITE
+    if ow is not None and wgrad and ow.lo <= out.data_ptr() < ow.hi:
+        # the whole gradient of these elements: written, not added to a cleared buffer
+        accumulate = False
+        ow.covered += M * N
     fu = _FUSED_UPDATE
-    if fu is not None and accumulate and residual is None and out.dtype == torch.float32 and (
-            fu.lo <= out.data_ptr() < fu.hi):
+    if fu is not None and wgrad and fu.lo <= out.data_ptr() < fu.hi:
         # the whole gradient of these elements: the bucket's AdamW runs in this GEMM's epilogue
         off = (out.data_ptr() - fu.lo) // 4
         last = off + (M - 1) * ld(out, "out") + N
@@ -152,6 +157,26 @@ class FusedUpdate:
 
 
 _FUSED_UPDATE: FusedUpdate | None = None
+
+
+class Overwrite:
+    """A layer's gradient buffer [lo, hi) whose every element gets exactly one weight-gradient
+    GEMM per step: an accumulating GEMM into it writes instead (the same values as adding to a
+    cleared buffer, up to the sign of zero), so the buffer is never cleared.  `covered` counts
+    the elements written, which the engine checks against the bucket's parameter count."""
+
+    def __init__(self, grad):
+        self.lo = grad.data_ptr()
+        self.hi = self.lo + 4 * grad.numel()
+        self.covered = 0
+
+
+_OVERWRITE: Overwrite | None = None
+
+
+def set_overwrite(ow: Overwrite | None) -> None:
+    global _OVERWRITE
+    _OVERWRITE = ow
 
 
 def set_fused_update(fu: FusedUpdate | None) -> None:

@@ -591,9 +591,11 @@ def test_single_gpu_grad_ring_is_exact(cuda, monkeypatch):
 @pytest.mark.parametrize("kind", ["swiglu_5l", "gqa"])
 def test_fused_adamw_in_wgrad_gemm_is_exact(cuda, monkeypatch, kind):
     """One-GPU step with AdamW fused into the weight-gradient GEMMs' epilogues (cb_gemm_adamw,
-    opt-in CB_FUSED_ADAMW=1) against the separate AdamW kernel: bit-identical losses, parameters and
-    AdamW moments over three steps, with and without the gradient ring; every layer bucket of
-    these dense configs takes the fused path."""
+    opt-in CB_FUSED_ADAMW=1), and with the weight-gradient GEMMs overwriting instead of
+    accumulating into cleared buffers (CB_WGRAD_OVERWRITE, default on), against the separate
+    AdamW kernel on cleared, accumulated gradients: bit-identical losses, parameters and AdamW
+    moments over three steps, with and without the gradient ring; every layer bucket of these
+    dense configs takes the fused / overwrite path."""
     from paper_2507_05411_b200 import TrainEngine, set_dtype_policy, synthetic_batch
     from paper_2507_05411_b200.experiments import _llama_trainer, transformer_trainer
 
@@ -605,9 +607,10 @@ def test_fused_adamw_in_wgrad_gemm_is_exact(cuda, monkeypatch, kind):
             cfg = cfg.set(f"model.decoder.transformer.layer[{i}].feed_forward.hidden_dim", 768)
     cfg = set_dtype_policy(cfg, "bf16")
     outs = []
-    for fused, ring in (("0", "0"), ("1", "0"), ("1", "1")):
+    for fused, ring, ow in (("0", "0", "0"), ("0", "0", "1"), ("0", "1", "1"), ("1", "0", "1"), ("1", "1", "1")):
         monkeypatch.setenv("CB_FUSED_ADAMW", fused)
         monkeypatch.setenv("CB_GRAD_RING", ring)
+        monkeypatch.setenv("CB_WGRAD_OVERWRITE", ow)
         eng = TrainEngine(cfg, device="cuda:0")
         nf = len(eng.fused_update_buckets())
         assert nf == (0 if fused == "0" else len(eng.layer_order))
