@@ -1,5 +1,6 @@
-"""Times every GEMM shape of one 1B decoder layer (forward, dgrad, wgrad) on the default
-engine: TFLOP/s per shape, with and without the split-K workspace (interleaved, same box)."""
+"""Times every GEMM shape of one 1B (default) or 7B decoder layer (forward, dgrad, wgrad) on the
+default engine: TFLOP/s per shape, with and without the split-K workspace (interleaved, same
+box).   python scripts/gemm_shapes.py [--7b] [shape names...]"""
 import json
 import os
 import sys
@@ -10,7 +11,7 @@ import torch
 from paper_2507_05411_b200 import _lib, ops
 
 dev = torch.device("cuda")
-T, d, qkv, ffn = 32768, 2048, 6144, 5632
+T, d, qkv, ffn = (12288, 4096, 12288, 11008) if "--7b" in sys.argv else (32768, 2048, 6144, 5632)
 # (name, M, N, K, trans_a, trans_b, out f32, accumulate)
 shapes = [
     ("fwd_qkv", T, qkv, d, 0, 0, 0, 0), ("fwd_o", T, d, d, 0, 0, 1, 0), ("fwd_up", T, 2 * ffn, d, 0, 0, 0, 0),
