@@ -185,7 +185,7 @@ def run_reference(args) -> None:
     """The reference arm: rank 0 alone times the reference's own CPU step on this arm's config.
     A step is one bounded sample of the workload — one reference TransformerLayer invoke at the
     config's layer shape (oracle/ref_step.py; 8.5 s for the 7B layer on 16 threads) — so the
-    K timed steps run K samples; the head (embedding, norm, tied head, loss) is timed once with
+    K timed steps run min(K, 10) samples; the head (embedding, norm, tied head, loss) is timed once with
     the warm-up sample (numpy has no warm-up state: one warm-up sample is run, not W)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -203,7 +203,9 @@ def run_reference(args) -> None:
         r = ref_step.ReferenceStep(args.config)
         t_head = r.head()
         r.layer()  # the one warm-up sample
-        layers = [r.layer() for _ in range(max(1, args.steps))]
+        # at most 10 timed samples (~8 s each at the 7B shape): the arm stays within a few minutes
+        # whatever --steps the driver passes
+        layers = [r.layer() for _ in range(max(1, min(args.steps, 10)))]
         t_layer = statistics.median(layers)
         v = r.rate(t_head, t_layer)
         ms = 1000.0 * statistics.mean(layers)  # what one timed step (sample) took
