@@ -17,6 +17,7 @@ from paper_2507_05411_b200 import BENCH_CONFIGS, TrainEngine, synthetic_batch
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="1b")
 ap.add_argument("--steps", type=int, default=2)
+ap.add_argument("--batch", type=int, default=None)
 args = ap.parse_args()
 world = int(os.environ.get("WORLD_SIZE", "1"))
 rank = int(os.environ.get("RANK", "0"))
@@ -27,10 +28,10 @@ if world > 1:  # under torchrun: FSDP over the ranks, rank 0 reports
     import torch.distributed as dist
 
     dist.init_process_group("nccl", device_id=dev)
-cfg = BENCH_CONFIGS[args.config](dtype="bf16")
+B, T = args.batch or BENCH_CONFIGS[args.config].__defaults__[0], BENCH_CONFIGS[args.config].__defaults__[1]
+cfg = BENCH_CONFIGS[args.config](batch=B, dtype="bf16")
 eng = TrainEngine(cfg, device=dev)
 V = eng.cfg.get("model.vocab_size")
-B, T = BENCH_CONFIGS[args.config].__defaults__[0], BENCH_CONFIGS[args.config].__defaults__[1]
 toks = [eng.upload_tokens(synthetic_batch(0, s, B, T, V)["tokens"]) for s in range(3 + args.steps)]
 for s in range(3):
     eng.step(toks[s])
@@ -39,8 +40,6 @@ with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) a
     for s in range(args.steps):
         eng.step(toks[3 + s])
     torch.cuda.synchronize()
-if rank != 0:
-    sys.exit(0)
 evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA and e.time_range.elapsed_us() > 0
        and "memcpy" not in e.name.lower() and "memset" not in e.name.lower()]
 by_stream = {}
@@ -59,7 +58,7 @@ for e in evs:
     else:
         cur_e = max(cur_e, en)
 busy += cur_e - cur_s
-print(f"{args.config}: {args.steps} steps, span {(t1 - t0) / 1e3:.2f} ms, GPU busy {busy / 1e3:.2f} ms "
+print(f"rank {rank} {args.config}: {args.steps} steps, span {(t1 - t0) / 1e3:.2f} ms, GPU busy {busy / 1e3:.2f} ms "
       f"({100 * busy / (t1 - t0):.1f}%), {len(evs)} kernels")
 gaps = []
 end = evs[0].time_range.end
@@ -70,6 +69,6 @@ for e in evs[1:]:
     if e.time_range.end > end:
         end, prev = e.time_range.end, e
 gaps.sort(reverse=True)
-print(f"idle total {sum(g[0] for g in gaps) / 1e3:.2f} ms in {len(gaps)} gaps; largest:")
-for g, a, b in gaps[:15]:
+print(f"rank {rank} idle total {sum(g[0] for g in gaps) / 1e3:.2f} ms in {len(gaps)} gaps; largest:")
+for g, a, b in gaps[:15 if rank == 0 else 5]:
     print(f"  {g:8.1f} us  after {a}  before {b}")
