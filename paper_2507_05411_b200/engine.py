@@ -729,8 +729,14 @@ class TrainEngine:
                     eng.last_forward_bytes = torch.cuda.memory_allocated(dev) - base
 
             self.options["forward_done"] = forward_done
-        loss, col, _ = value_and_grad(self.module, self.state, self.grads, key, {"tokens": toks}, provider=provider,
-                                      options=self.options)
+        try:
+            loss, col, _ = value_and_grad(self.module, self.state, self.grads, key, {"tokens": toks},
+                                          provider=provider, options=self.options)
+        finally:
+            # a backward that raised must not leave a gradient region marked for overwrite /
+            # fused update (a later buffer at the same address would be treated as one)
+            ops.set_overwrite(None)
+            ops.set_fused_update(None)
         if provider:
             provider.finish_backward()
         if self._wgrad_stream is not None:
