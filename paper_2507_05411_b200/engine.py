@@ -7,15 +7,19 @@
   tensors (norm scales, MoE router).  Inside a bucket an attention block's wq|wk|wv and a
   gated FFN's w1|w1_gate are laid out as column slices of one matrix so the behaviors
   issue one wide GEMM; every block is 64-element aligned (TMA needs 16 B).
-* per bucket: f32 master shard, bf16 (or f32) working copy of the full bucket, f32 grad
-  buffer, AdamW m/v shards.  With world size 1 the shard is the whole bucket.
-* **FSDP** (world size N > 1, one process per GPU, NCCL over NVLink): the working copy of
-  layer i+1 is all-gathered on a side stream while layer i computes; each layer's
-  gradient is reduce-scattered (mean over ranks) on the side stream right after that
-  layer's backward; AdamW runs on local shards and refreshes the local slice of the
-  working copy.  Sequences are independent, so the data path is plain data parallelism
-  over the batch and the loss is the all-reduced mean (reference SPEC.md:445: numerics
-  do not depend on partitioning).
+* per bucket: f32 master shard, bf16 (or f32) working copy, f32 gradient, AdamW m/v shards.
+  With world size 1 the shard is the whole bucket; large models keep the layers' gradients in
+  a two-slot ring (``CB_GRAD_RING``), each layer updated right after its backward, inline on
+  the compute stream.  Dense layers' weight-gradient GEMMs write their gradient buffers instead
+  of accumulating into cleared ones (``overwrite_buckets``).
+* **FSDP / ZeRO-3** (world size N > 1, one process per GPU, single node): parameters,
+  gradients and optimizer state sharded 1/N; layer p's working copy is gathered into ring slot
+  p % 2 on the comm stream (copy-engine reads of the peers' symmetric-memory shards, or NCCL)
+  while the previous layer computes, again before its backward; its gradient is
+  reduce-scattered right after its backward and AdamW runs on the in-order sum of the slices
+  (``cb_adamw_parts``).  Sequences are independent, so the data path is plain data parallelism
+  over the batch and the loss is the all-reduced mean (reference SPEC.md:445: numerics do not
+  depend on partitioning).
 
 The step itself is ``module.value_and_grad`` over the behaviors in ``layers.py``: no
 PyTorch arithmetic, only C-ABI kernel launches.  PyTorch provides memory, streams and
@@ -669,9 +673,8 @@ class TrainEngine:
         """Forward + backward; gradients land in the (sharded) grad buffers.  Returns (loss, collection).
 
         update=True also applies AdamW (step counter advanced first): each layer bucket is
-        updated on a side stream as soon as its gradient is final (right after that layer's
-        backward, or its reduce-scatter under FSDP), overlapping the HBM-bound optimizer with
-        the backward GEMMs of earlier layers.
+        updated as soon as its gradient is final — right after that layer's backward, inline on
+        the compute stream (one GPU), or after its reduce-scatter on the comm stream (FSDP).
         """
         toks = self.upload_tokens(tokens)
         if key is None:
