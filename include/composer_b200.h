@@ -220,6 +220,9 @@ CB_API int cb_attention_set_path(int path);
 /* 1 (default) = the tcgen05/TMEM kernels for bf16 head_dim 128 (the Python layer zero-pads
  * head_dim 16/32/64 to 128 for them); 0 = the SIMT engine (tests). */
 CB_API int cb_attention_set_tc(int enable);
+/* 1 (default) = the backward's dQ sweep on CTA pairs (cta_group::2 MMAs over 256 query rows;
+ * needs seq_len % 256 == 0, else the single-CTA sweep runs); 0 = single-CTA sweep.  Same bits. */
+CB_API int cb_attention_set_dq_pair(int enable);
 
 /* ---------------------------------------------------------------------------------
  * Next-token cross-entropy (TrainerBehavior.forward, layers.py:638-651) fused with its

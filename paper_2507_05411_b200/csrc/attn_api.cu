@@ -27,6 +27,16 @@ static int ds_check(const AttnGeom& g, const void* ds_ws, int64_t ds_bytes) {
   return CB_OK;
 }
 
+namespace cb {
+namespace tcb {
+extern int g_dq_pair;
+}
+}  // namespace cb
+extern "C" int cb_attention_set_dq_pair(int enable) {
+  cb::tcb::g_dq_pair = enable ? 1 : 0;
+  return CB_OK;
+}
+
 extern "C" int cb_attention_set_path(int path) {
   if (path < 0 || path > 1) return fail(CB_ERR_ARG, "attention path must be 0 (auto) or 1 (simt)");
   g_attn_path = path;

@@ -781,6 +781,282 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// 1 (default): the dQ sweep on CTA pairs (dq_pair_k) when T % 256 == 0 (cb_attention_set_dq_pair)
+int g_dq_pair = 1;
+
+// ============================================================ dQ sweep on CTA pairs
+// The dQ sweep with cta_group::2 MMAs: a cluster of two CTAs owns 256 query rows (128 each);
+// every MMA is one pair instruction (M = 256) issued by the leader, each CTA supplying its own
+// 128 rows of A (Q, dO, or dS from its TMEM) and half of B:
+//   S  = Q K_j^T  : B = its 64 keys of K_j (all 128 head dims)     [64 x 128, K-major]
+//   dP = dO V_j^T : B = its 64 keys of V_j                          [64 x 128, K-major]
+//   dQ += dS K_j  : B = all 128 keys of K_j, its 64 head-dim columns [128 x 64, MN-major]
+// so each SM reads 160 KB of shared memory per key tile instead of the single-CTA sweep's
+// 224 KB (which bounds that kernel above its 1536-cycle MMA time).  The pair instruction runs
+// at the single-CTA per-SM rate at N = 128 (profiles/r02_ubench_mma_pair.txt).  TMA loads of
+// both CTAs complete on the leader's barriers; MMA completions are multicast to both CTAs; the
+// compute warps of both CTAs signal dP-consumed / dS-ready on the leader's barriers with
+// relaxed cluster arrives (the tcgen05 fences order the TMEM accesses; a release at cluster
+// scope cost ~1300 cycles per signal on the critical chain).  Same arithmetic and order as
+// dq_k.  Requires T % 256 == 0 (else dq_k runs).
+constexpr int kBoxH = 64 * 64 * 2;  // one [64 rows][64 cols] bf16 box (8 KB)
+constexpr int kSmemDqPair = 2 * kTile + kKSlots * (2 * kBoxH + kBox) + kVSlots * (2 * kBoxH) + 1024 + 256;
+
+// descriptor offset of the kk-th K=16 step of a K-major [64][128] half tile (two 64-col boxes)
+__device__ __forceinline__ uint64_t koff64(int kk) { return (uint64_t)(((kk >> 2) * kBoxH + (kk & 3) * 32) >> 4); }
+
+__device__ __forceinline__ void umma_f16_ts_pair(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    dq_pair_k(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+              const __grid_constant__ CUtensorMap tmK64, const __grid_constant__ CUtensorMap tmV64,
+              const __grid_constant__ CUtensorMap tmG, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sG = smem + kTile;
+  uint8_t* sKs = smem + 2 * kTile;                 // [kKSlots] this CTA's 64 keys of K_j (S operand)
+  uint8_t* sKq = sKs + kKSlots * 2 * kBoxH;        // [kKSlots] K_j's 128 keys x this CTA's 64 dims
+  uint8_t* sV = sKq + kKSlots * kBox;              // [kVSlots] this CTA's 64 keys of V_j
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kVSlots * 2 * kBoxH);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;   // [3]  (leader's copy counts both CTAs' loads)
+  uint64_t* k_empty = bars + 4;  // [3]  (multicast by the leader's MMA commits)
+  uint64_t* v_full = bars + 7;   // [2]
+  uint64_t* v_empty = bars + 9;  // [2]
+  uint64_t* s_full = bars + 11;  // [2]
+  uint64_t* dp_full = bars + 13;
+  uint64_t* ds_ready = bars + 14;  // leader: 16 arrivals (8 compute warps x 2 CTAs)
+  uint64_t* mma_done = bars + 15;
+  uint64_t* ds_part = bars + 16;
+  uint64_t* dp_free = bars + 17;  // leader: 16 arrivals — dP(j) is in the compute warps' registers
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 18);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int kvh = h / (p.H / p.KVH);
+  const int nk = p.T / BT;
+  const int row0 = b * p.T, q0 = (blockIdx.x >> 1) * 2 * BT + (int)rank * BT;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmK64);
+    tma_prefetch_desc(&tmV64);
+    tma_prefetch_desc(&tmG);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < kKSlots; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+    }
+    mbar_init(dp_full, 1);
+    mbar_init(ds_ready, 16);
+    mbar_init(ds_part, 16);
+    mbar_init(dp_free, 16);
+    mbar_init(mma_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_pair(slot, kCols);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *slot;
+  const uint32_t cP = 256, cQ = 384;  // S buffers at (j & 1) * 128
+
+  if (warp == 0) {
+    // producer A (both CTAs): own Q, dO rows once, then per key tile its 64 keys of K_j (two
+    // [64][64] boxes) and K_j's 128 keys x its 64 head dims; completions on the leader's barriers
+    if (elect_one()) {
+      const uint32_t fq = leader_addr(q_full);
+      if (leader) mbar_expect_tx(q_full, 2 * 2 * kTile);
+      tma_load_2d_pair(sQ, &tmQ, fq, h * HD, row0 + q0);
+      tma_load_2d_pair(sQ + kBox, &tmQ, fq, h * HD + 64, row0 + q0);
+      tma_load_2d_pair(sG, &tmG, fq, h * HD, row0 + q0);
+      tma_load_2d_pair(sG + kBox, &tmG, fq, h * HD + 64, row0 + q0);
+      for (int j = 0; j < nk; ++j) {
+        const int st = j % kKSlots;
+        mbar_wait(&k_empty[st], ((j / kKSlots) & 1) ^ 1);
+        BWD_TRACE(16, j);
+        const uint32_t fk = leader_addr(&k_full[st]);
+        if (leader) mbar_expect_tx(&k_full[st], 2 * (2 * kBoxH + kBox));
+        const int krow = row0 + j * BT;
+        tma_load_2d_pair(sKs + st * 2 * kBoxH, &tmK64, fk, kvh * HD, krow + (int)rank * 64);
+        tma_load_2d_pair(sKs + st * 2 * kBoxH + kBoxH, &tmK64, fk, kvh * HD + 64, krow + (int)rank * 64);
+        tma_load_2d_pair(sKq + st * kBox, &tmK, fk, kvh * HD + (int)rank * 64, krow);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 3) {
+    // producer B (both CTAs): its 64 keys of V_j
+    if (elect_one()) {
+      for (int j = 0; j < nk; ++j) {
+        const int st = j & 1;
+        mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        BWD_TRACE(17, j);
+        const uint32_t fv = leader_addr(&v_full[st]);
+        if (leader) mbar_expect_tx(&v_full[st], 2 * 2 * kBoxH);
+        const int krow = row0 + j * BT + (int)rank * 64;
+        tma_load_2d_pair(sV + st * 2 * kBoxH, &tmV64, fv, kvh * HD, krow);
+        tma_load_2d_pair(sV + st * 2 * kBoxH + kBoxH, &tmV64, fv, kvh * HD + 64, krow);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (leader) {
+      const uint32_t id_s = idesc_bf16_f32(256, 128, 0, 0);
+      const uint32_t id_acc = idesc_bf16_f32(256, 128, 0, 1);
+      const uint64_t dQd = sw128_desc(smem_u32(sQ), 16, 1024), dGd = sw128_desc(smem_u32(sG), 16, 1024);
+      auto issue_s = [&](int j) {
+        const int ks = j % kKSlots;
+        BWD_TRACE(18, j);
+        mbar_wait(&k_full[ks], (j / kKSlots) & 1);
+        tc_fence_after();
+        BWD_TRACE(10, j);
+        const uint64_t dKj = sw128_desc(smem_u32(sKs + ks * 2 * kBoxH), 16, 1024);
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk)
+            umma_f16_ss_pair(tmem + (j & 1) * 128u, dQd + koff(kk), dKj + koff64(kk), id_s, kk > 0);
+          umma_commit_pair_mc(&s_full[j & 1], 0x3);
+        }
+        __syncwarp();
+      };
+      auto issue_dp = [&](int j) {
+        mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+        tc_fence_after();
+        BWD_TRACE(12, j);
+        const uint64_t dVj = sw128_desc(smem_u32(sV + (j & 1) * 2 * kBoxH), 16, 1024);
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk)
+            umma_f16_ss_pair(tmem + cP, dGd + koff(kk), dVj + koff64(kk), id_s, kk > 0);
+          umma_commit_pair_mc(dp_full, 0x3);
+          umma_commit_pair_mc(&v_empty[j & 1], 0x3);
+        }
+        __syncwarp();
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      issue_dp(0);
+      for (int j = 0; j < nk; ++j) {
+        const int st = j & 1;
+        if (j + 1 < nk) issue_s(j + 1);
+        // dP(j+1) as soon as both CTAs' compute warps hold dP(j) in registers (the cross-SM
+        // signal latency then overlaps tile j's dS pass instead of following it)
+        if (j + 1 < nk) {
+          mbar_wait(dp_free, j & 1);
+          tc_fence_after();
+          issue_dp(j + 1);
+        }
+        // B: K_j's 128 keys x this CTA's 64 head dims, MN-major (one 64-column atom)
+        const uint64_t mK = sw128_desc(smem_u32(sKq + (j % kKSlots) * kBox), kBox, 1024);
+        mbar_wait(ds_part, j & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < BT / 16; ++k)
+            if ((k & 3) < 2)
+              umma_f16_ts_pair(tmem + cQ, tmem + st * 128u + packed_col(k), mK + (uint64_t)(k * 128), id_acc,
+                               (j | k) != 0);
+        }
+        __syncwarp();
+        mbar_wait(ds_ready, j & 1);
+        tc_fence_after();
+        BWD_TRACE(11, j);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < BT / 16; ++k)
+            if ((k & 3) >= 2)
+              umma_f16_ts_pair(tmem + cQ, tmem + st * 128u + packed_col(k), mK + (uint64_t)(k * 128), id_acc, 1);
+          umma_commit_pair_mc(&k_empty[j % kKSlots], 0x3);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) umma_commit_pair_mc(mma_done, 0x3);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int ch = (warp - 4) >> 2;  // key-column half of each tile
+    const int t = q * 32 + lane;
+    const uint32_t lo = (uint32_t)(q * 32) << 16;
+    const float c = p.scale * kLog2e;
+    const int qrow = q0 + t;
+    const int64_t li = ((int64_t)b * p.H + h) * p.T + qrow;
+    const float L = p.lse[li] * kLog2e;
+    const float D = p.delta[li];
+    const float2 c2 = make_float2(c, c), nl2 = make_float2(-L, -L), nd2 = make_float2(-D, -D);
+    const uint32_t ds_part_l = leader_addr(ds_part), ds_ready_l = leader_addr(ds_ready);
+    const uint32_t dp_free_l = leader_addr(dp_free);
+    for (int j = 0; j < nk; ++j) {
+      const int st = j & 1;
+      mbar_wait(&s_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      if (warp == 4) BWD_TRACE(13, j);
+      float2 pr[32];
+      {
+        uint32_t sv[2][32];
+        ld64(tmem + lo + st * 128u + ch * 64, sv);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pr[i] = exp2_pair(ffma2(col2(sv, i), c2, nl2), i);
+      }
+      mbar_wait(dp_full, j & 1);
+      tc_fence_after();
+      if (warp == 4) BWD_TRACE(14, j);
+      {
+        uint32_t dv[2][32];
+        ld64(tmem + lo + cP + ch * 64, dv);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster_relaxed(dp_free_l);
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float2 d = fmul2(pr[16 * part + i], fadd2(col2(dv, 16 * part + i), nd2));
+            pk[i] = pack2(d.x, d.y);
+          }
+          tmem_st16(tmem + lo + st * 128u + ch * 64 + 16 * part, pk);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (part == 0 && lane == 0) mbar_arrive_cluster_relaxed(ds_part_l);
+        }
+      }
+      if (warp == 4) BWD_TRACE(15, j);
+      if (lane == 0) mbar_arrive_cluster_relaxed(ds_ready_l);
+    }
+    mbar_wait(mma_done, 0);
+    tc_fence_after();
+    const float* rc = p.rope_cos ? p.rope_cos + (int64_t)qrow * (HD / 2) + ch * 32 : nullptr;
+    const float* rs = p.rope_sin ? p.rope_sin + (int64_t)qrow * (HD / 2) + ch * 32 : nullptr;
+    store_row(tmem + lo + cQ + ch * 64, p.o0 + ((int64_t)row0 + qrow) * p.ld0 + (int64_t)h * HD + ch * 64, p.scale,
+              true, rc, rs, 2);
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, kCols);
+  }
+}
+
 // ============================================================ dQ as a GEMM over stored dS
 // dQ[q, :] = scale * sum_key dS[q, key] K[key, :] for one (128-query tile, head, batch) per
 // CTA, reading the dS^T the DS variant of dkdv_k stored (row (b*H + h)*T + key, column query:
@@ -923,6 +1199,18 @@ int attn_bwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, 
       mq, mk, mv, mg, mg, pk);
   if (int e = check_launch("flash_bwd_dkdv_tc")) return e;
   Params pq{g.T, g.H, g.KVH, g.B, g.scale, lse, delta, (__nv_bfloat16*)dq, lddq, nullptr, 0, rope_cos, rope_sin};
+  if (g_dq_pair && g.T % (2 * BT) == 0) {
+    CUtensorMap mk64p, mv64;
+    if ((s = make_tmap_2d_bf16(&mk64p, k, rows, (uint64_t)g.KVH * HD, g.ldk, 64, 64))) return s;
+    if ((s = make_tmap_2d_bf16(&mv64, v, rows, (uint64_t)g.KVH * HD, g.ldv, 64, 64))) return s;
+    static bool attr_pair = false;
+    if (!attr_pair) {
+      cudaFuncSetAttribute(dq_pair_k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDqPair);
+      attr_pair = true;
+    }
+    dq_pair_k<<<dim3(g.T / BT, g.H, g.B), kThreads, kSmemDqPair, st>>>(mq, mk, mk64p, mv64, mg, pq);
+    return check_launch("flash_bwd_dq_pair_tc");
+  }
   dq_k<<<dim3((g.T + BT - 1) / BT, g.H, g.B), kThreads, kSmemDq, st>>>(mq, mk, mv, mg, pq);
   return check_launch("flash_bwd_dq_tc");
 }

@@ -578,8 +578,28 @@ def _attention_bwd_padded(q, k, v, o, lse, do, dq, dk, dv, B, T, H, KVH, hd, sca
 _DQ_GEMM = __import__("os").environ.get("CB_ATTN_DQ_GEMM", "0") == "1"
 
 
+# the backward's dQ sweep on CTA pairs (cb_attention_set_dq_pair; seq_len % 256 == 0):
+# bit-identical to the single-CTA sweep and 11-14% faster in the step (profiles/r02_attn_dq_pair_ab.txt).
+# Default on; CB_ATTN_DQ_PAIR=0 restores the single-CTA sweep.  Applied on first use.
+_DQ_PAIR = __import__("os").environ.get("CB_ATTN_DQ_PAIR", "1") == "1"
+_DQ_PAIR_SET = None
+
+
+def set_dq_pair(enable: bool) -> None:
+    global _DQ_PAIR, _DQ_PAIR_SET
+    _DQ_PAIR = bool(enable)
+    _lib.call("cb_attention_set_dq_pair", int(_DQ_PAIR))
+    _DQ_PAIR_SET = _DQ_PAIR
+
+
+def _sync_dq_pair() -> None:
+    if _DQ_PAIR_SET != _DQ_PAIR:
+        set_dq_pair(_DQ_PAIR)
+
+
 def _ds_workspace(q, B, T, H, hd):
     """The dS^T workspace (B*H*T*T bf16) when the dS path applies, else None."""
+    _sync_dq_pair()
     if not (_DQ_GEMM and q.dtype == torch.bfloat16 and hd == _TC_HD and T % 128 == 0 and _ATTN_PATH == 0):
         return None
     return torch.empty((B * H * T * T,), device=q.device, dtype=torch.bfloat16)

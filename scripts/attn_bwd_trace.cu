@@ -10,7 +10,8 @@
 #include "../paper_2507_05411_b200/csrc/attn_tc.cu"
 #include "../paper_2507_05411_b200/csrc/attn_tc_bwd.cu"
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1 && argv[1][0] == 'p') cb::tcb::g_dq_pair = 1;  // "pair": the CTA-pair dQ sweep
   const int B = 8, T = 4096, H = 16, hd = 128;
   const size_t n = (size_t)B * T * H * hd;
   std::vector<__nv_bfloat16> h(n);
@@ -27,9 +28,10 @@ int main() {
   cudaMemset(delta, 0, (size_t)B * H * T * 4);
   for (void* p : {q, k, v, g}) cudaMemcpy(p, h.data(), n * 2, cudaMemcpyHostToDevice);
   cb::AttnGeom geo{B, T, H, H, hd, H * hd, H * hd, H * hd, H * hd, 0.08838834764831845f};
-  cb::attn_fwd_tc(geo, q, k, v, o, lse, 0);
+  cb::attn_fwd_tc(geo, q, k, v, o, nullptr, lse, 0);
   auto bwd = [&]() {
-    return cb::attn_bwd_tc(geo, q, k, v, g, H * hd, lse, delta, dq, H * hd, dk, H * hd, dv, H * hd, 0);
+    return cb::attn_bwd_tc(geo, q, k, v, g, H * hd, lse, delta, dq, H * hd, dk, H * hd, dv, H * hd, 0, nullptr, nullptr,
+                           nullptr);
   };
   for (int it = 0; it < 3; ++it)
     if (int s = bwd()) {

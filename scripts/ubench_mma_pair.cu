@@ -13,8 +13,17 @@
 using namespace cb;
 constexpr int kIters = 1024;
 
-// PAIR: cta_group::2 (cluster of 2, leader issues) or cta_group::1; BMN: B MN-major
-template <int PAIR, int N, int BMN>
+__device__ __forceinline__ void umma_ts_pair(uint32_t d, uint32_t a, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(bd), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// PAIR: cta_group::2 (cluster of 2, leader issues) or cta_group::1; BMN: B MN-major; TS: A from
+// TMEM (columns 256.., the accumulator at column 0)
+template <int PAIR, int N, int BMN, int TS = 0>
 __global__ void __launch_bounds__(128, 1) mma_bench(unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
@@ -47,7 +56,11 @@ __global__ void __launch_bounds__(128, 1) mma_bench(unsigned long long* out) {
     const uint64_t bd = BMN ? sw128_desc(b, 8192, 1024) : sw128_desc(b, 16, 1024);
     const unsigned long long t0 = clock64();
     for (int it = 0; it < kIters; ++it) {
-      if (PAIR)
+      if (TS && PAIR)
+        umma_ts_pair(tmem, tmem + 256, bd, idesc, it > 0);
+      else if (TS)
+        umma_f16_ts(tmem, tmem + 256, bd, idesc, it > 0);
+      else if (PAIR)
         umma_f16_ss_pair(tmem, ad, bd, idesc, it > 0);
       else
         umma_f16_ss(tmem, ad, bd, idesc, it > 0);
@@ -76,13 +89,13 @@ __global__ void __launch_bounds__(128, 1) mma_bench(unsigned long long* out) {
   }
 }
 
-template <int PAIR, int N, int BMN>
+template <int PAIR, int N, int BMN, int TS = 0>
 void run(const char* name, int ctas) {
   unsigned long long* d;
   cudaMalloc(&d, sizeof(unsigned long long) * ctas);
   cudaMemset(d, 0, sizeof(unsigned long long) * ctas);
   const int smem_bytes = 98304;
-  cudaFuncSetAttribute(mma_bench<PAIR, N, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  cudaFuncSetAttribute(mma_bench<PAIR, N, BMN, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ctas);
   cfg.blockDim = dim3(128);
@@ -95,7 +108,7 @@ void run(const char* name, int ctas) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   for (int rep = 0; rep < 2; ++rep) {
-    cudaError_t e = cudaLaunchKernelEx(&cfg, mma_bench<PAIR, N, BMN>, d);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, mma_bench<PAIR, N, BMN, TS>, d);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
       printf("%s: %s\n", name, cudaGetErrorString(e));
@@ -129,6 +142,9 @@ int main() {
     run<1, 256, 0>("pair   M256 N256 B K-major", ctas);
     run<1, 128, 1>("pair   M256 N128 B MN-major", ctas);
     run<1, 256, 1>("pair   M256 N256 B MN-major", ctas);
+    run<0, 128, 1, 1>("1-CTA  M128 N128 TS B MN-major", ctas);
+    run<1, 128, 1, 1>("pair   M256 N128 TS B MN-major", ctas);
+    run<1, 128, 0, 1>("pair   M256 N128 TS B K-major", ctas);
   }
   return 0;
 }

@@ -498,3 +498,40 @@ def test_attention_dq_gemm_matches_sweep(cuda, B, T, H, KVH, rope):
         P = torch.softmax(Q @ K.repeat_interleave(rep, 1).transpose(-1, -2) * scale, -1)
         (P @ Vv.repeat_interleave(rep, 1)).backward(do.double().view(B, T, H, hd).transpose(1, 2))
         assert _rel(gemm[:, :d].view(B, T, H, hd).transpose(1, 2), Q.grad) < 5e-3
+
+
+@pytest.mark.parametrize("B,T,H,KVH,rope", [(2, 256, 4, 4, False), (1, 512, 8, 2, True), (1, 1024, 4, 4, False),
+                                           (2, 768, 4, 1, True)])
+def test_attention_dq_pair_matches_sweep(cuda, B, T, H, KVH, rope):
+    """The dQ sweep on CTA pairs (cta_group::2 MMAs over 256 query rows, cb_attention_set_dq_pair)
+    against the single-CTA sweep on the same inputs: the same MMAs in the same order, so dQ, dK
+    and dV are bit-identical; deterministic reruns."""
+    from paper_2507_05411_b200 import ops
+    from paper_2507_05411_b200.layers import rope_tables
+
+    hd = 128
+    g = torch.Generator().manual_seed(T * H + B + 7)
+    d, kvd = H * hd, KVH * hd
+    qkv = torch.randn(B * T, d + 2 * kvd, generator=g).to(cuda, torch.bfloat16)
+    q, k, v = qkv[:, :d], qkv[:, d:d + kvd], qkv[:, d + kvd:]
+    do = torch.randn(B * T, d, generator=g).to(cuda, torch.bfloat16)
+    scale = 1 / math.sqrt(hd)
+    cs, sn = rope_tables(T, hd, 10000.0, cuda)
+    o, lse, o_lo = ops.attention_fwd(q, k, v, B, T, H, KVH, hd, scale, want_lo=True)
+    outs = []
+    default = ops._DQ_PAIR
+    for pair in (1, 1, 0):
+        ops.set_dq_pair(bool(pair))
+        try:
+            dqkv = torch.empty_like(qkv)
+            args = (q, k, v, o, lse, do, dqkv[:, :d], dqkv[:, d:d + kvd], dqkv[:, d + kvd:], B, T, H, KVH, hd, scale)
+            if rope:
+                ops.attention_bwd_rope(*args, cs, sn, o_lo=o_lo)
+            else:
+                ops.attention_bwd(*args, o_lo=o_lo)
+        finally:
+            ops.set_dq_pair(default)
+        outs.append(dqkv)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])  # deterministic
+    assert torch.equal(outs[0], outs[2])  # the single-CTA sweep's bits
