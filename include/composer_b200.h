@@ -223,6 +223,9 @@ CB_API int cb_attention_set_tc(int enable);
 /* 1 (default) = the backward's dQ sweep on CTA pairs (cta_group::2 MMAs over 256 query rows;
  * needs seq_len % 256 == 0, else the single-CTA sweep runs); 0 = single-CTA sweep.  Same bits. */
 CB_API int cb_attention_set_dq_pair(int enable);
+/* 1 = the backward's dK/dV sweep on CTA pairs (cta_group::2 MMAs over 256 keys; needs
+ * seq_len % 256 == 0, else the single-CTA sweep runs); 0 (default) = single-CTA sweep. */
+CB_API int cb_attention_set_dkdv_pair(int enable);
 
 /* ---------------------------------------------------------------------------------
  * Next-token cross-entropy (TrainerBehavior.forward, layers.py:638-651) fused with its

@@ -61,6 +61,7 @@ SIGNATURES: dict[str, list] = {
                          _L, _P, _L, _F, _P, _L, _P],
     "cb_attention_set_path": [_I],
     "cb_attention_set_dq_pair": [_I],
+    "cb_attention_set_dkdv_pair": [_I],
     "cb_gemm_rope": [_I, _I, _I, _I, _P, _L, _I, _P, _L, _I, _P, _L, _I, _I, _I, _I, _P, _P, _P],
     "cb_gemm_set_workspace": [_P, _L],
     "cb_gemm_gated_fwd": [_I, _I, _I, _P, _L, _I, _P, _L, _I, _P, _L, _P, _L, _I, _I, _P],

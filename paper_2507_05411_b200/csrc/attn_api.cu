@@ -30,10 +30,15 @@ static int ds_check(const AttnGeom& g, const void* ds_ws, int64_t ds_bytes) {
 namespace cb {
 namespace tcb {
 extern int g_dq_pair;
+extern int g_dkdv_pair;
 }
 }  // namespace cb
 extern "C" int cb_attention_set_dq_pair(int enable) {
   cb::tcb::g_dq_pair = enable ? 1 : 0;
+  return CB_OK;
+}
+extern "C" int cb_attention_set_dkdv_pair(int enable) {
+  cb::tcb::g_dkdv_pair = enable ? 1 : 0;
   return CB_OK;
 }
 

@@ -553,6 +553,335 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
   }
 }
 
+// CTA-pair (cta_group::2) helpers of the pair sweeps below
+constexpr int kBoxH = 64 * 64 * 2;  // one [64 rows][64 cols] bf16 box (8 KB)
+
+// descriptor offset of the kk-th K=16 step of a K-major [64][128] half tile (two 64-col boxes)
+__device__ __forceinline__ uint64_t koff64(int kk) { return (uint64_t)(((kk >> 2) * kBoxH + (kk & 3) * 32) >> 4); }
+
+__device__ __forceinline__ void umma_f16_ts_pair(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// ====================================================================== dK / dV on CTA pairs
+// The dK/dV sweep with cta_group::2 MMAs: a cluster of two CTAs owns 256 keys (128 each); for
+// every 128-query tile each pair MMA (M = 256, issued by the leader) takes each CTA's own 128
+// rows of A (K, V, or P^T / dS^T from its TMEM) and half of B:
+//   S^T  = K Q_u^T   : B = its 64 queries of Q_u (all head dims)      [64 x 128, K-major]
+//   dP^T = V dO_u^T  : B = its 64 queries of dO_u                     [64 x 128, K-major]
+//   dV  += P^T dO_u  : B = all 128 queries of dO_u, its 64 head dims  [128 x 64, MN-major]
+//   dK  += dS^T Q_u  : B = all 128 queries of Q_u, its 64 head dims   [128 x 64, MN-major]
+// so each SM reads ~192 KB of shared memory per tile instead of ~256 KB (the single-CTA
+// sweep's bound, at its 2048-cycle MMA time).  TMA loads of K/V, Q and dO complete on the
+// leader's barriers, MMA completions are multicast, the compute warps' signals reach the
+// leader's barriers with relaxed cluster arrives (tcgen05 fences order the TMEM accesses).
+// lse / delta rows stay per-CTA (bulk copies, local barriers).  Same arithmetic and order as
+// dkdv_k<NQ, false>.  Requires T % 256 == 0 (else dkdv_k runs).
+template <int NQ>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 128 * NQ, 1)
+    dkdv_pair_k(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQ64,
+                const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmG64, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if (smem_u32(smem) & 1023) __trap();  // see kSmemDkdv
+  uint8_t* sK = smem;
+  uint8_t* sV = smem + kTile;
+  uint8_t* sQ = smem + 2 * kTile;      // [kQSlots] {its 64 queries x 128 dims | 128 queries x its 64 dims}
+  uint8_t* sG = sQ + kQSlots * kTile;  // [kGSlots] same for dO
+  float* sLD = reinterpret_cast<float*>(sG + kGSlots * kTile);  // [2] x {lse, delta}
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sLD) + 2048);
+  uint64_t* kv_full = bars;
+  uint64_t* q_full = bars + 1;     // [3]
+  uint64_t* q_empty = bars + 4;    // [3]
+  uint64_t* g_full = bars + 7;     // [2]
+  uint64_t* g_empty = bars + 9;    // [2]
+  uint64_t* ld_full = bars + 11;   // [2] (per CTA)
+  uint64_t* ld_empty = bars + 13;  // [2] (per CTA)
+  uint64_t* s_full = bars + 15;
+  uint64_t* dp_full = bars + 16;
+  uint64_t* s_free = bars + 17;
+  uint64_t* pd_ready = bars + 18;
+  uint64_t* mma_done = bars + 19;
+  uint64_t* p_ready = bars + 20;
+  uint64_t* ds_part = bars + 21;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 22);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int kvh = blockIdx.y, b = blockIdx.z;
+  const int group = p.H / p.KVH;
+  const int nq = p.T / BT;
+  const int total = group * nq;
+  const int row0 = b * p.T, k0 = (blockIdx.x >> 1) * 2 * BT + (int)rank * BT;
+  constexpr int kSig = 2 * 4 * NQ;  // compute-warp signals per phase (both CTAs)
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmQ64);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    tma_prefetch_desc(&tmG);
+    tma_prefetch_desc(&tmG64);
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < kQSlots; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&g_full[s], 1);
+      mbar_init(&g_empty[s], 1);
+      mbar_init(&ld_full[s], 1);
+      mbar_init(&ld_empty[s], 4 * NQ);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(dp_full, 1);
+    mbar_init(s_free, kSig);
+    mbar_init(pd_ready, kSig);
+    mbar_init(p_ready, kSig);
+    mbar_init(ds_part, kSig);
+    mbar_init(mma_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_pair(slot, kCols);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *slot;
+  const uint32_t cS = 0, cP = 128, cV = 256, cK = 384;
+
+  if (warp == 0) {
+    // producer A: its K, V rows once, then per query tile its halves of Q_u
+    if (elect_one()) {
+      const uint32_t fkv = leader_addr(kv_full);
+      if (leader) mbar_expect_tx(kv_full, 2 * 2 * kTile);
+      tma_load_2d_pair(sK, &tmK, fkv, kvh * HD, row0 + k0);
+      tma_load_2d_pair(sK + kBox, &tmK, fkv, kvh * HD + 64, row0 + k0);
+      tma_load_2d_pair(sV, &tmV, fkv, kvh * HD, row0 + k0);
+      tma_load_2d_pair(sV + kBox, &tmV, fkv, kvh * HD + 64, row0 + k0);
+      for (int it = 0; it < total; ++it) {
+        const int st = it % kQSlots;
+        const int h = kvh * group + it / nq, q0 = (it % nq) * BT;
+        mbar_wait(&q_empty[st], ((it / kQSlots) & 1) ^ 1);
+        BWD_TRACE(8, it);
+        const uint32_t fq = leader_addr(&q_full[st]);
+        if (leader) mbar_expect_tx(&q_full[st], 2 * kTile);
+        uint8_t* dst = sQ + st * kTile;
+        tma_load_2d_pair(dst, &tmQ64, fq, h * HD, row0 + q0 + (int)rank * 64);
+        tma_load_2d_pair(dst + kBoxH, &tmQ64, fq, h * HD + 64, row0 + q0 + (int)rank * 64);
+        tma_load_2d_pair(dst + kBox, &tmQ, fq, h * HD + (int)rank * 64, row0 + q0);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 3) {
+    // producer B: its halves of dO_u (leader's barriers) and the lse / delta rows (its own)
+    if (elect_one()) {
+      for (int it = 0; it < total; ++it) {
+        const int st = it & 1;
+        const uint32_t ph = ((it >> 1) & 1) ^ 1;
+        const int h = kvh * group + it / nq, q0 = (it % nq) * BT;
+        mbar_wait(&g_empty[st], ph);
+        BWD_TRACE(9, it);
+        const uint32_t fg = leader_addr(&g_full[st]);
+        if (leader) mbar_expect_tx(&g_full[st], 2 * kTile);
+        uint8_t* dst = sG + st * kTile;
+        tma_load_2d_pair(dst, &tmG64, fg, h * HD, row0 + q0 + (int)rank * 64);
+        tma_load_2d_pair(dst + kBoxH, &tmG64, fg, h * HD + 64, row0 + q0 + (int)rank * 64);
+        tma_load_2d_pair(dst + kBox, &tmG, fg, h * HD + (int)rank * 64, row0 + q0);
+        const uint32_t bytes = (uint32_t)BT * 4u;
+        const int64_t li = ((int64_t)b * p.H + h) * p.T + q0;
+        mbar_wait(&ld_empty[st], ph);
+        mbar_expect_tx(&ld_full[st], 2 * bytes);
+        bulk_load(sLD + st * 256, p.lse + li, bytes, &ld_full[st]);
+        bulk_load(sLD + st * 256 + 128, p.delta + li, bytes, &ld_full[st]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (leader) {
+      const uint32_t id_s = idesc_bf16_f32(256, 128, 0, 0);    // K-major x K-major
+      const uint32_t id_acc = idesc_bf16_f32(256, 128, 0, 1);  // TMEM A x MN-major B
+      const uint64_t dK = sw128_desc(smem_u32(sK), 16, 1024), dV = sw128_desc(smem_u32(sV), 16, 1024);
+      auto tileQ = [&](int u) { return smem_u32(sQ + (u % kQSlots) * kTile); };
+      auto tileG = [&](int u) { return smem_u32(sG + (u & 1) * kTile); };
+      auto issue_s = [&](int u) {
+        mbar_wait(&q_full[u % kQSlots], (u / kQSlots) & 1);
+        tc_fence_after();
+        BWD_TRACE(1, u);
+        const uint64_t dQ = sw128_desc(tileQ(u), 16, 1024);
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk)
+            umma_f16_ss_pair(tmem + cS, dK + koff(kk), dQ + koff64(kk), id_s, kk > 0);
+          umma_commit_pair_mc(s_full, 0x3);
+        }
+        __syncwarp();
+      };
+      auto issue_dp = [&](int u) {
+        mbar_wait(&g_full[u & 1], (u >> 1) & 1);
+        tc_fence_after();
+        BWD_TRACE(3, u);
+        const uint64_t dG = sw128_desc(tileG(u), 16, 1024);
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk)
+            umma_f16_ss_pair(tmem + cP, dV + koff(kk), dG + koff64(kk), id_s, kk > 0);
+          umma_commit_pair_mc(dp_full, 0x3);
+        }
+        __syncwarp();
+      };
+      mbar_wait(kv_full, 0);
+      tc_fence_after();
+      issue_s(0);
+      issue_dp(0);
+      for (int u = 0; u < total; ++u) {
+        // B of dV / dK: all 128 queries x this CTA's 64 head dims (one MN-major atom)
+        const uint64_t mQ = sw128_desc(tileQ(u) + kBox, kBox, 1024), mG = sw128_desc(tileG(u) + kBox, kBox, 1024);
+        if (u + 1 < total) {
+          mbar_wait(s_free, u & 1);
+          tc_fence_after();
+          issue_s(u + 1);
+        }
+        mbar_wait(p_ready, u & 1);
+        tc_fence_after();
+        BWD_TRACE(0, u);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < BT / 16; ++k)
+            umma_f16_ts_pair(tmem + cV, tmem + cP + packed_colq<NQ>(k), mG + (uint64_t)(k * 128), id_acc,
+                             (u | k) != 0);
+          umma_commit_pair_mc(&g_empty[u & 1], 0x3);
+        }
+        __syncwarp();
+        constexpr int KPG = BT / 16 / NQ;
+        mbar_wait(ds_part, u & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < BT / 16; ++k)
+            if (k % KPG < KPG / 2)
+              umma_f16_ts_pair(tmem + cK, tmem + cP + 64 / NQ + packed_colq<NQ>(k), mQ + (uint64_t)(k * 128), id_acc,
+                               (u | k) != 0);
+        }
+        __syncwarp();
+        mbar_wait(pd_ready, u & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < BT / 16; ++k)
+            if (k % KPG >= KPG / 2)
+              umma_f16_ts_pair(tmem + cK, tmem + cP + 64 / NQ + packed_colq<NQ>(k), mQ + (uint64_t)(k * 128), id_acc,
+                               1);
+          umma_commit_pair_mc(&q_empty[u % kQSlots], 0x3);
+        }
+        __syncwarp();
+        BWD_TRACE(2, u);
+        if (u + 1 < total) issue_dp(u + 1);
+      }
+      if (elect_one()) umma_commit_pair_mc(mma_done, 0x3);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    constexpr int W = 128 / NQ;
+    constexpr int NP = W / 2;
+    const int q = warp & 3;
+    const int grp = (warp - 4) >> 2;
+    const int t = q * 32 + lane;
+    const uint32_t lo = (uint32_t)(q * 32) << 16;
+    const uint32_t col = (uint32_t)grp * W;
+    const float c = p.scale * kLog2e;
+    const float2 c2 = make_float2(c, c), nlog2e = make_float2(-kLog2e, -kLog2e);
+    const uint32_t s_free_l = leader_addr(s_free), p_ready_l = leader_addr(p_ready);
+    const uint32_t ds_part_l = leader_addr(ds_part), pd_ready_l = leader_addr(pd_ready);
+    for (int u = 0; u < total; ++u) {
+      mbar_wait(&ld_full[u & 1], (u >> 1) & 1);
+      const uint32_t sL = smem_u32(sLD + (u & 1) * 256 + grp * W);
+      mbar_wait(s_full, u & 1);
+      tc_fence_after();
+      if (warp == 4) BWD_TRACE(4, u);
+      float2 pr[NP];
+      {
+        uint32_t sv[W / 32][32];
+        ldW<W>(tmem + lo + cS + col, sv);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster_relaxed(s_free_l);
+#pragma unroll
+        for (int i = 0; i < NP; i += 2) {
+          const float4 l4 = lds4(sL + 8 * i);
+          pr[i] = exp2_pair(ffma2(colp(sv, i), c2, fmul2(make_float2(l4.x, l4.y), nlog2e)), i);
+          pr[i + 1] = exp2_pair(ffma2(colp(sv, i + 1), c2, fmul2(make_float2(l4.z, l4.w), nlog2e)), i + 1);
+        }
+      }
+      if (warp == 4) BWD_TRACE(5, u);
+      mbar_wait(dp_full, u & 1);
+      tc_fence_after();
+      if (warp == 4) BWD_TRACE(6, u);
+      {
+        uint32_t dv[W / 32][32];
+        ldW<W>(tmem + lo + cP + col, dv);
+        pack_storeN<NP>(tmem + lo + cP + col, pr);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster_relaxed(p_ready_l);
+        constexpr int kParts = NP >= 32 ? 2 : 1;
+#pragma unroll
+        for (int part = 0; part < kParts; ++part) {
+          float2 ds[NP / kParts];
+#pragma unroll
+          for (int i = 0; i < NP / kParts; i += 2) {
+            const int c2i = part * (NP / kParts) + i;
+            const float4 d4 = lds4(sL + 512 + 8 * c2i);
+            ds[i] = fmul2(pr[c2i], ffma2(make_float2(d4.x, d4.y), make_float2(-1.f, -1.f), colp(dv, c2i)));
+            ds[i + 1] =
+                fmul2(pr[c2i + 1], ffma2(make_float2(d4.z, d4.w), make_float2(-1.f, -1.f), colp(dv, c2i + 1)));
+          }
+          pack_storeN<NP / kParts>(tmem + lo + cP + col + NP + part * (NP / kParts), ds);
+          if (part == 0) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster_relaxed(ds_part_l);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (warp == 4) BWD_TRACE(7, u);
+      if (lane == 0) {
+        mbar_arrive_cluster_relaxed(pd_ready_l);
+        mbar_arrive(&ld_empty[u & 1]);
+      }
+    }
+    mbar_wait(mma_done, 0);
+    tc_fence_after();
+    const int krow = k0 + t;
+    constexpr int kCh = 8 / NQ;
+    const int c0 = grp * kCh * 32;
+    if (c0 < 128) {
+      const float* rc = p.rope_cos ? p.rope_cos + (int64_t)krow * (HD / 2) + c0 / 2 : nullptr;
+      const float* rs = p.rope_sin ? p.rope_sin + (int64_t)krow * (HD / 2) + c0 / 2 : nullptr;
+      store_row(tmem + lo + cK + c0, p.o0 + ((int64_t)row0 + krow) * p.ld0 + (int64_t)kvh * HD + c0, p.scale, true,
+                rc, rs, kCh);
+    } else {
+      store_row(tmem + lo + cV + (c0 - 128), p.o1 + ((int64_t)row0 + krow) * p.ld1 + (int64_t)kvh * HD + (c0 - 128),
+                1.f, true, nullptr, nullptr, kCh);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, kCols);
+  }
+}
+
 // =========================================================================== dQ
 __global__ void __launch_bounds__(kThreads, 1)
     dq_k(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -783,6 +1112,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // 1 (default): the dQ sweep on CTA pairs (dq_pair_k) when T % 256 == 0 (cb_attention_set_dq_pair)
 int g_dq_pair = 1;
+// 1: the dK/dV sweep on CTA pairs (dkdv_pair_k) when T % 256 == 0 (cb_attention_set_dkdv_pair)
+int g_dkdv_pair = 0;
 
 // ============================================================ dQ sweep on CTA pairs
 // The dQ sweep with cta_group::2 MMAs: a cluster of two CTAs owns 256 query rows (128 each);
@@ -799,21 +1130,8 @@ int g_dq_pair = 1;
 // relaxed cluster arrives (the tcgen05 fences order the TMEM accesses; a release at cluster
 // scope cost ~1300 cycles per signal on the critical chain).  Same arithmetic and order as
 // dq_k.  Requires T % 256 == 0 (else dq_k runs).
-constexpr int kBoxH = 64 * 64 * 2;  // one [64 rows][64 cols] bf16 box (8 KB)
 constexpr int kSmemDqPair = 2 * kTile + kKSlots * (2 * kBoxH + kBox) + kVSlots * (2 * kBoxH) + 1024 + 256;
 
-// descriptor offset of the kk-th K=16 step of a K-major [64][128] half tile (two 64-col boxes)
-__device__ __forceinline__ uint64_t koff64(int kk) { return (uint64_t)(((kk >> 2) * kBoxH + (kk & 3) * 32) >> 4); }
-
-__device__ __forceinline__ void umma_f16_ts_pair(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
-                                                 uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     dq_pair_k(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -1190,14 +1508,24 @@ int attn_bwd_tc(const AttnGeom& g, const void* q, const void* k, const void* v, 
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(dkdv_k<kDkdvGroups, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDkdv);
+    cudaFuncSetAttribute(dkdv_pair_k<kDkdvGroups>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDkdv);
     cudaFuncSetAttribute(dq_k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDq);
     attr = true;
   }
   Params pk{g.T, g.H, g.KVH, g.B, g.scale, lse, delta, (__nv_bfloat16*)dk, lddk, (__nv_bfloat16*)dv, lddv,
             rope_cos, rope_sin};
-  dkdv_k<kDkdvGroups, false><<<dim3((g.T + BT - 1) / BT, g.KVH, g.B), 128 + 128 * kDkdvGroups, kSmemDkdv, st>>>(
-      mq, mk, mv, mg, mg, pk);
-  if (int e = check_launch("flash_bwd_dkdv_tc")) return e;
+  if (g_dkdv_pair && g.T % (2 * BT) == 0) {
+    CUtensorMap mq64, mg64;
+    if ((s = make_tmap_2d_bf16(&mq64, q, rows, (uint64_t)g.H * HD, g.ldq, 64, 64))) return s;
+    if ((s = make_tmap_2d_bf16(&mg64, dout, rows, (uint64_t)g.H * HD, lddo, 64, 64))) return s;
+    dkdv_pair_k<kDkdvGroups><<<dim3(g.T / BT, g.KVH, g.B), 128 + 128 * kDkdvGroups, kSmemDkdv, st>>>(
+        mq, mq64, mk, mv, mg, mg64, pk);
+    if (int e = check_launch("flash_bwd_dkdv_pair_tc")) return e;
+  } else {
+    dkdv_k<kDkdvGroups, false><<<dim3((g.T + BT - 1) / BT, g.KVH, g.B), 128 + 128 * kDkdvGroups, kSmemDkdv, st>>>(
+        mq, mk, mv, mg, mg, pk);
+    if (int e = check_launch("flash_bwd_dkdv_tc")) return e;
+  }
   Params pq{g.T, g.H, g.KVH, g.B, g.scale, lse, delta, (__nv_bfloat16*)dq, lddq, nullptr, 0, rope_cos, rope_sin};
   if (g_dq_pair && g.T % (2 * BT) == 0) {
     CUtensorMap mk64p, mv64;

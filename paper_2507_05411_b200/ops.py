@@ -585,6 +585,10 @@ _DQ_PAIR = __import__("os").environ.get("CB_ATTN_DQ_PAIR", "1") == "1"
 _DQ_PAIR_SET = None
 
 
+_DKDV_PAIR = __import__("os").environ.get("CB_ATTN_DKDV_PAIR", "0") == "1"
+_DKDV_PAIR_SET = None
+
+
 def set_dq_pair(enable: bool) -> None:
     global _DQ_PAIR, _DQ_PAIR_SET
     _DQ_PAIR = bool(enable)
@@ -592,9 +596,19 @@ def set_dq_pair(enable: bool) -> None:
     _DQ_PAIR_SET = _DQ_PAIR
 
 
+def set_dkdv_pair(enable: bool) -> None:
+    """The backward's dK/dV sweep on CTA pairs (cb_attention_set_dkdv_pair; seq_len % 256 == 0)."""
+    global _DKDV_PAIR, _DKDV_PAIR_SET
+    _DKDV_PAIR = bool(enable)
+    _lib.call("cb_attention_set_dkdv_pair", int(_DKDV_PAIR))
+    _DKDV_PAIR_SET = _DKDV_PAIR
+
+
 def _sync_dq_pair() -> None:
     if _DQ_PAIR_SET != _DQ_PAIR:
         set_dq_pair(_DQ_PAIR)
+    if _DKDV_PAIR_SET != _DKDV_PAIR:
+        set_dkdv_pair(_DKDV_PAIR)
 
 
 def _ds_workspace(q, B, T, H, hd):

@@ -11,7 +11,9 @@
 #include "../paper_2507_05411_b200/csrc/attn_tc_bwd.cu"
 
 int main(int argc, char** argv) {
-  if (argc > 1 && argv[1][0] == 'p') cb::tcb::g_dq_pair = 1;  // "pair": the CTA-pair dQ sweep
+  // "single" / "pair" (dQ on pairs) / "both" (dQ and dK/dV on pairs)
+  cb::tcb::g_dq_pair = argc > 1 && (argv[1][0] == 'p' || argv[1][0] == 'b');
+  cb::tcb::g_dkdv_pair = argc > 1 && argv[1][0] == 'b';
   const int B = 8, T = 4096, H = 16, hd = 128;
   const size_t n = (size_t)B * T * H * hd;
   std::vector<__nv_bfloat16> h(n);

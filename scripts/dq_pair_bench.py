@@ -23,8 +23,9 @@ for (B, T, H, KVH) in [(8, 4096, 16, 16), (3, 4096, 32, 32), (2, 4096, 64, 8)]:
     flops = 8 * B * T * T * H * hd
     res = {}
     for rep in range(6):
-        for pair in ((0, 1) if rep % 2 == 0 else (1, 0)):
-            ops.set_dq_pair(bool(pair))
+        for pair in ((0, 1, 2) if rep % 2 == 0 else (2, 1, 0)):  # 0 single, 1 pair dQ, 2 pair dQ + dK/dV
+            ops.set_dq_pair(pair >= 1)
+            ops.set_dkdv_pair(pair >= 2)
             for _ in range(2):
                 ops.attention_bwd(*args, o_lo=o_lo)
             torch.cuda.synchronize()
@@ -36,9 +37,11 @@ for (B, T, H, KVH) in [(8, 4096, 16, 16), (3, 4096, 32, 32), (2, 4096, 64, 8)]:
             torch.cuda.synchronize()
             res.setdefault(pair, []).append(s.elapsed_time(e) / 10)
     ops.set_dq_pair(True)
+    ops.set_dkdv_pair(False)
     import statistics
 
-    t0, t1 = statistics.median(res[0]), statistics.median(res[1])
+    t0, t1, t2 = statistics.median(res[0]), statistics.median(res[1]), statistics.median(res[2])
     print(f"B={B} T={T} H={H} KVH={KVH}: backward single {t0:.3f} ms ({flops / t0 / 1e9:.0f} TF/s), "
           f"pair dQ {t1:.3f} ms ({flops / t1 / 1e9:.0f} TF/s), {100 * (t0 - t1) / t0:+.1f}% (medians of 6, "
-          f"alternating order; min {min(res[0]):.3f} / {min(res[1]):.3f})", flush=True)
+          f"alternating order; min {min(res[0]):.3f} / {min(res[1]):.3f}); pair dQ + dK/dV {t2:.3f} ms "
+          f"({flops / t2 / 1e9:.0f} TF/s), {100 * (t0 - t2) / t0:+.1f}%", flush=True)

@@ -503,9 +503,10 @@ def test_attention_dq_gemm_matches_sweep(cuda, B, T, H, KVH, rope):
 @pytest.mark.parametrize("B,T,H,KVH,rope", [(2, 256, 4, 4, False), (1, 512, 8, 2, True), (1, 1024, 4, 4, False),
                                            (2, 768, 4, 1, True)])
 def test_attention_dq_pair_matches_sweep(cuda, B, T, H, KVH, rope):
-    """The dQ sweep on CTA pairs (cta_group::2 MMAs over 256 query rows, cb_attention_set_dq_pair)
-    against the single-CTA sweep on the same inputs: the same MMAs in the same order, so dQ, dK
-    and dV are bit-identical; deterministic reruns."""
+    """The dQ and dK/dV sweeps on CTA pairs (cta_group::2 MMAs over 256 query / key rows,
+    cb_attention_set_dq_pair / _dkdv_pair) against the single-CTA sweeps on the same inputs: the
+    same MMAs in the same order, so dQ, dK and dV are bit-identical in every combination;
+    deterministic reruns."""
     from paper_2507_05411_b200 import ops
     from paper_2507_05411_b200.layers import rope_tables
 
@@ -519,9 +520,10 @@ def test_attention_dq_pair_matches_sweep(cuda, B, T, H, KVH, rope):
     cs, sn = rope_tables(T, hd, 10000.0, cuda)
     o, lse, o_lo = ops.attention_fwd(q, k, v, B, T, H, KVH, hd, scale, want_lo=True)
     outs = []
-    default = ops._DQ_PAIR
-    for pair in (1, 1, 0):
-        ops.set_dq_pair(bool(pair))
+    defaults = (ops._DQ_PAIR, ops._DKDV_PAIR)
+    for dq_pair, dkdv_pair in ((1, 1), (1, 1), (0, 0), (1, 0), (0, 1)):
+        ops.set_dq_pair(bool(dq_pair))
+        ops.set_dkdv_pair(bool(dkdv_pair))
         try:
             dqkv = torch.empty_like(qkv)
             args = (q, k, v, o, lse, do, dqkv[:, :d], dqkv[:, d:d + kvd], dqkv[:, d + kvd:], B, T, H, KVH, hd, scale)
@@ -530,8 +532,10 @@ def test_attention_dq_pair_matches_sweep(cuda, B, T, H, KVH, rope):
             else:
                 ops.attention_bwd(*args, o_lo=o_lo)
         finally:
-            ops.set_dq_pair(default)
+            ops.set_dq_pair(defaults[0])
+            ops.set_dkdv_pair(defaults[1])
         outs.append(dqkv)
     torch.cuda.synchronize()
     assert torch.equal(outs[0], outs[1])  # deterministic
-    assert torch.equal(outs[0], outs[2])  # the single-CTA sweep's bits
+    for o_ in outs[2:]:  # the single-CTA sweeps' bits, with either sweep on pairs
+        assert torch.equal(outs[0], o_)
