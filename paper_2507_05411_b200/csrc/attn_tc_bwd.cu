@@ -1152,11 +1152,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* v_empty = bars + 9;  // [2]
   uint64_t* s_full = bars + 11;  // [2]
   uint64_t* dp_full = bars + 13;
-  uint64_t* ds_ready = bars + 14;  // leader: 16 arrivals (8 compute warps x 2 CTAs)
-  uint64_t* mma_done = bars + 15;
-  uint64_t* ds_part = bars + 16;
-  uint64_t* dp_free = bars + 17;  // leader: 16 arrivals — dP(j) is in the compute warps' registers
-  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 18);
+  // leader's copies, 16 arrivals each (8 compute warps x 2 CTAs).  ds_ready / ds_part are
+  // double-buffered by tile parity: dP(j+1) is issued on dp_free(j), so a fast warp can reach
+  // tile j+1's dS signals before a slow one has given tile j's (never two tiles ahead: dP(j+2)
+  // needs every warp's dp_free(j+1)); one barrier per parity keeps the phases apart
+  uint64_t* ds_ready = bars + 14;  // [2]
+  uint64_t* mma_done = bars + 16;
+  uint64_t* ds_part = bars + 17;  // [2]
+  uint64_t* dp_free = bars + 19;  // dP(j) is in the compute warps' registers
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 20);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -1183,8 +1187,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&s_full[s], 1);
     }
     mbar_init(dp_full, 1);
-    mbar_init(ds_ready, 16);
-    mbar_init(ds_part, 16);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&ds_ready[s], 16);
+      mbar_init(&ds_part[s], 16);
+    }
     mbar_init(dp_free, 16);
     mbar_init(mma_done, 1);
     fence_mbar_init();
@@ -1283,7 +1289,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         // B: K_j's 128 keys x this CTA's 64 head dims, MN-major (one 64-column atom)
         const uint64_t mK = sw128_desc(smem_u32(sKq + (j % kKSlots) * kBox), kBox, 1024);
-        mbar_wait(ds_part, j & 1);
+        mbar_wait(&ds_part[j & 1], (j >> 1) & 1);
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
@@ -1293,7 +1299,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                (j | k) != 0);
         }
         __syncwarp();
-        mbar_wait(ds_ready, j & 1);
+        mbar_wait(&ds_ready[j & 1], (j >> 1) & 1);
         tc_fence_after();
         BWD_TRACE(11, j);
         if (elect_one()) {
@@ -1319,7 +1325,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const float L = p.lse[li] * kLog2e;
     const float D = p.delta[li];
     const float2 c2 = make_float2(c, c), nl2 = make_float2(-L, -L), nd2 = make_float2(-D, -D);
-    const uint32_t ds_part_l = leader_addr(ds_part), ds_ready_l = leader_addr(ds_ready);
+    const uint32_t ds_part_l[2] = {leader_addr(&ds_part[0]), leader_addr(&ds_part[1])};
+    const uint32_t ds_ready_l[2] = {leader_addr(&ds_ready[0]), leader_addr(&ds_ready[1])};
     const uint32_t dp_free_l = leader_addr(dp_free);
     for (int j = 0; j < nk; ++j) {
       const int st = j & 1;
@@ -1354,11 +1361,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
-          if (part == 0 && lane == 0) mbar_arrive_cluster_relaxed(ds_part_l);
+          if (part == 0 && lane == 0) mbar_arrive_cluster_relaxed(ds_part_l[st]);
         }
       }
       if (warp == 4) BWD_TRACE(15, j);
-      if (lane == 0) mbar_arrive_cluster_relaxed(ds_ready_l);
+      if (lane == 0) mbar_arrive_cluster_relaxed(ds_ready_l[st]);
     }
     mbar_wait(mma_done, 0);
     tc_fence_after();
