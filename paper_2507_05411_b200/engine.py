@@ -438,6 +438,7 @@ class TrainEngine:
 
     def _refresh_work(self, i: int) -> None:
         """This rank's slice of bucket i's working copy <- its f32 master shard."""
+        self._gather_synced = False
         rec = self.bufs[i]
         if rec["wshard"].data_ptr() != rec["master"].data_ptr():
             ops.copy2d(rec["master"].view(1, -1), rec["wshard"].view(1, -1))
@@ -462,6 +463,7 @@ class TrainEngine:
     # -------------------------------------------------------------- parameters
     def _host_bucket(self, b: Bucket, rec, values) -> None:
         """values(entry) -> np.ndarray; writes this rank's shard of the bucket's master + work."""
+        self._gather_synced = False
         host = np.zeros(rec["total"], dtype=np.float32)
         for e in b.entries:
             arr = np.asarray(values(e), dtype=np.float64)
@@ -680,10 +682,15 @@ class TrainEngine:
         if key is None:
             key = self.step_key(self.step_count)
         self._grad_shards_stale = False
+        # FSDP: were the shards last written by a step() whose AdamW finished before its loss
+        # all-reduce?  Then every peer's shards are final once that all-reduce completed, and
+        # this step's forward gathers (ordered after it on the compute stream) need no barrier
+        synced = getattr(self, "_gather_synced", False) and self.d.world > 1
+        self._gather_synced = False
         if update:
             self.step_count += 1
         if self.d.world > 1:
-            provider = FSDPProvider(self, update=update)
+            provider = FSDPProvider(self, update=update, synced=synced)
         else:
             if self._grad_ring and not update:
                 from .errors import ComposerError
@@ -747,6 +754,9 @@ class TrainEngine:
             self._wgrad_pending.clear()  # operands released after the compute stream's wait
         if self.d.world > 1:
             self.d.dist.all_reduce(loss, op=self.d.dist.ReduceOp.AVG, group=self.d.group)
+            # every rank's AdamW of this step ran on its comm stream before its compute stream's
+            # wait in finish_backward, i.e. before it joined this all-reduce
+            self._gather_synced = bool(update) and os.environ.get("CB_FSDP_FWD_BARRIER", "0") != "1"
         return loss, col
 
     def _join_wgrad(self, stream) -> None:
@@ -823,6 +833,7 @@ class TrainEngine:
 
     @_on_device
     def apply_update(self) -> None:
+        self._gather_synced = False  # the shards change after this step's loss all-reduce
         self.step_count += 1
         for i in range(len(self.buckets)):
             self._adamw_bucket(i)
@@ -910,9 +921,12 @@ class FSDPProvider(ParamProvider):
     done with the slot's previous layer, and the comm stream clears a gradient slot right
     after its reduce-scatter has been read by every peer."""
 
-    def __init__(self, eng: TrainEngine, update: bool = False):
+    def __init__(self, eng: TrainEngine, update: bool = False, synced: bool = False):
         self.e = eng
         self.update = update  # run AdamW on each bucket right after its reduce-scatter (comm stream)
+        # the peers' shards are final (written by the previous step() before its loss
+        # all-reduce): forward gathers skip their barrier
+        self.synced = synced
         self.dist = eng.d.dist
         self.group = eng.d.group
         self.compute = torch.cuda.current_stream(eng.device)
@@ -953,13 +967,16 @@ class FSDPProvider(ParamProvider):
                 # pull every peer's shard over NVLink with the copy engines (no SMs taken from
                 # the compute kernels).  Ordering with the shards' writers, the AdamW updates:
                 # * forward gather: one barrier — each peer's AdamW of this bucket (previous
-                #   step, earlier on its comm stream) has written its shard;
+                #   step, earlier on its comm stream) has written its shard — unless the previous
+                #   step() already ordered every peer's AdamW before its loss all-reduce, which
+                #   this gather follows on this rank's streams (self.synced; CB_FSDP_FWD_BARRIER=1
+                #   keeps the barrier);
                 # * backward (re-)gather: none — no AdamW of this bucket can run anywhere before
                 #   every rank has passed this bucket's reduce-scatter barrier, i.e. finished
                 #   its backward of it, which comes after this gather;
                 # * no barrier after the reads: a rank's next AdamW of this bucket waits for the
                 #   same reduce-scatter barrier, which every reader passes only after its reads.
-                if barrier:
+                if barrier and not self.synced:
                     self.e._barrier(h)
                 for k in range(1, N):
                     p = (r + k) % N
