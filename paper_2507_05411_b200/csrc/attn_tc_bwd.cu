@@ -433,6 +433,7 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
     const uint32_t col = (uint32_t)grp * W;
     const float c = p.scale * kLog2e;
     const float2 c2 = make_float2(c, c), nlog2e = make_float2(-kLog2e, -kLog2e);
+    if (warp == 4) BWD_TRACE(19, 0);  // compute warps start
     for (int u = 0; u < total; ++u) {
       mbar_wait(&ld_full[u & 1], (u >> 1) & 1);
       const uint32_t sL = smem_u32(sLD + (u & 1) * 256 + grp * W);  // lse; delta at +128 floats
@@ -529,6 +530,7 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
     if (DS && lane == 0) bulk_wait0();  // every dS^T store has landed before the CTA exits
     mbar_wait(mma_done, 0);
     tc_fence_after();
+    if (warp == 4) BWD_TRACE(20, 0);  // last MMA done: epilogue starts
     const int krow = k0 + t;
     const bool ok = krow < p.T;
     // the 256 output columns (dK | dV) split evenly over the NQ groups
@@ -543,6 +545,7 @@ __global__ void __launch_bounds__(128 + 128 * NQ, 1)
       store_row(tmem + lo + cV + (c0 - 128), p.o1 + ((int64_t)row0 + krow) * p.ld1 + (int64_t)kvh * HD + (c0 - 128),
                 1.f, ok, nullptr, nullptr, kCh);
     }
+    if (warp == 4) BWD_TRACE(21, 0);  // epilogue stores issued
   }
   tc_fence_before();
   __syncthreads();
@@ -591,6 +594,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 128 * NQ, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if (smem_u32(smem) & 1023) __trap();  // see kSmemDkdv
+  CTA_TRACE(0, 0);
   uint8_t* sK = smem;
   uint8_t* sV = smem + kTile;
   uint8_t* sQ = smem + 2 * kTile;      // [kQSlots] {its 64 queries x 128 dims | 128 queries x its 64 dims}
@@ -876,6 +880,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 128 * NQ, 1)
   }
   tc_fence_before();
   cluster_sync();
+  CTA_TRACE(0, 1);
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc_pair(tmem, kCols);
@@ -1139,6 +1144,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const __grid_constant__ CUtensorMap tmG, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  CTA_TRACE(1, 0);
   uint8_t* sQ = smem;
   uint8_t* sG = smem + kTile;
   uint8_t* sKs = smem + 2 * kTile;                 // [kKSlots] this CTA's 64 keys of K_j (S operand)
@@ -1376,6 +1382,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   cluster_sync();
+  CTA_TRACE(1, 1);
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc_pair(tmem, kCols);

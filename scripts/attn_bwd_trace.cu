@@ -80,6 +80,11 @@ int main(int argc, char** argv) {
   printf("dq: k_full wait per tile (S issue ready -> K tile present), cycles:");
   for (int j = 4; j < 12; ++j) printf(" %lld", (long long)(tr[10][j] - tr[18][j]));
   printf("\n");
+  if (tr[19][0] && tr[21][0])
+    printf("dkdv CTA (0,0,0), single-CTA sweep: compute start %lld, last tile's dV issue %lld, last MMA done %lld, "
+           "epilogue stores issued %lld (cycles from the first S)\n",
+           (long long)(tr[19][0] - t0), (long long)(tr[0][31] - t0), (long long)(tr[20][0] - t0),
+           (long long)(tr[21][0] - t0));
   printf("steady-state period (tiles 4..15): dkdv %.0f cycles, dq %.0f cycles\n", (tr[0][15] - tr[0][4]) / 11.0,
          (tr[11][15] - tr[11][4]) / 11.0);
   // per-CTA timeline of the last launch: CTA duration, gap to the next CTA on the same SM
